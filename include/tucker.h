@@ -1,0 +1,148 @@
+/*
+ * tucker.h — C-ABI of the B200-native (sm_100a) Tucker/HOSVD hot path of arXiv 1711.06874,
+ * "Tucker tensor analysis of Matérn functions in spatial statistics".
+ *
+ * Citations: "P:n" is line n of the paper's LaTeX source; "R<k>" are the readings of
+ * ambiguous passages listed in DESIGN.md §3.
+ *
+ * The path:
+ *   a-1 grid nodes             x_i = -b + (i-1)h, h = 2b/(n-1)
+ *   a-2 function-tensor fill   F[i,j,k] = C(||x_ijk||), Matérn / Slater
+ *   a-3 per-mode Gram          G_m = F_(m) F_(m)^T  (the SVD of the unfolding A_(l))
+ *   a-4 top-r eigenvectors     U_m = leading r_m eigenvectors of G_m, sigma = sqrt(lambda)
+ *   a-5 core                   beta = F x1 U1^T x2 U2^T x3 U3^T
+ *   a-6 error                  E = ||F - beta x1 U1 x2 U2 x3 U3|| / ||F||
+ *
+ * Conventions (all entry points):
+ *   - Device pointers ("dev") are CUDA device memory owned by the caller; the library never
+ *     allocates or frees caller memory.  All scratch comes from the caller's workspace `ws`
+ *     (device, >= tucker_workspace_size() bytes, 256-byte aligned).
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).  Entry points
+ *     are asynchronous unless stated; tucker_hosvd synchronises `stream` once per mode to test
+ *     eigensolver convergence.
+ *   - Tensors are FP64, C order (n1 x n2 x n3, k fastest).  Factor U_m is n_m x r_m row-major
+ *     (column c = c-th factor vector).  The core is r1 x r2 x r3 C order.
+ *   - Validation happens before any launch.  Errors are returned as TUCKER_* codes; no exception
+ *     crosses the ABI.  Functions are reentrant (no global mutable state besides a one-time
+ *     driver entry-point lookup).
+ */
+#ifndef TUCKER_B200_H
+#define TUCKER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TUCKER_API __attribute__((visibility("default")))
+#else
+#define TUCKER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Axes-parallel box prod_m [lo_m, hi_m] with n_m collocation nodes per axis.
+ * Node i of axis m (i = 0..n_m-1) is c + s*(2i-(n_m-1)), c = (lo+hi)/2, s = (hi-lo)/(2(n_m-1)):
+ * the paper's -b + (i-1)h, evaluated in a form that is bitwise mirror-exact (R2). */
+typedef struct {
+    int64_t n[3];
+    double lo[3], hi[3];
+} tucker_grid;
+
+enum { TUCKER_MATERN = 0, TUCKER_SLATER = 1 };
+
+/* Kernel parameters.
+ *   TUCKER_MATERN: C(r) = sigma2 * 2^{1-nu}/Gamma(nu) * z^nu K_nu(z), z = sqrt(2 nu) r / ell
+ *                  (eq. Matern; sigma2 per R3; C(0) = sigma2, R4).  nu in {0.5,1.5,2.5}
+ *                  (compared exactly) uses the closed forms e^{-z}, (1+z)e^{-z}, (1+z+z^2/3)e^{-z}
+ *                  unless TUCKER_FORCE_GENERAL_BESSEL is set.
+ *   TUCKER_SLATER: C(r) = sigma2 * exp(-lambda r^p), 0 < p <= 2 (eq. exp_p; p = 2 is
+ *                  the Gaussian).
+ * `flags` may hold TUCKER_FORCE_GENERAL_BESSEL. */
+typedef struct {
+    int32_t family;
+    int32_t flags;
+    double sigma2, ell, nu, lambda, p;
+} tucker_kernel;
+
+enum {
+    TUCKER_FORCE_GENERAL_BESSEL = 2, /* kernel flag: evaluate half-integer nu through K_nu */
+};
+
+enum {
+    TUCKER_OK = 0,
+    TUCKER_ERR_INVALID_ARG = 1, /* null pointer, n_m < 2, lo >= hi, bad mode                */
+    TUCKER_ERR_DOMAIN = 2,      /* sigma2<=0, ell<=0, nu<=0, lambda<=0, p not in (0,2]       */
+    TUCKER_ERR_RANK = 3,        /* r_m < 1 or r_m > n_m                                      */
+    TUCKER_ERR_SIZE = 4,        /* workspace too small / size overflow                       */
+    TUCKER_ERR_NOCONV = 5,      /* eigensolver hit its iteration cap (best iterate returned) */
+    TUCKER_ERR_CUDA = 6,        /* a CUDA runtime/driver call failed                         */
+    TUCKER_ERR_UNSUPPORTED = 7  /* e.g. r_m too large for the eigensolver block (r_m > 56)   */
+};
+
+/* Per-mode eigensolver report (host struct, optional). */
+typedef struct {
+    int32_t iters[3];     /* subspace iterations (0 = direct Jacobi on G_m)                   */
+    int32_t converged[3]; /* 1 if every leading-r_m Ritz residual met the tolerance           */
+    int32_t block[3];     /* subspace block width p_m                                          */
+    int32_t sweeps[3];    /* Jacobi sweeps of the last Rayleigh-Ritz solve                    */
+    double resid[3];      /* max_{k<=r_m} ||G v_k - theta_k v_k|| / theta_1                   */
+    double lambda1[3];    /* theta_1 (largest eigenvalue of G_m)                              */
+} tucker_info;
+
+/* Workspace bytes needed by tucker_fill / tucker_hosvd / tucker_error / tucker_gram /
+ * tucker_eig / tucker_ttm_core for this grid and ranks (r may be NULL: ranks = 64). */
+TUCKER_API size_t tucker_workspace_size(const tucker_grid* grid, const int32_t r[3]);
+
+/* a-1 + a-2: F (dev, n1*n2*n3 doubles) <- collocation tensor of `kernel` on `grid`
+ * (P:981-997).  Uses ws for the nodes and the K_nu Chebyshev table. */
+TUCKER_API int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F, void* ws,
+                size_t ws_bytes, void* stream);
+
+/* a-3: G (dev, n_m x n_m, both triangles) <- F_(m) F_(m)^T for mode m in {0,1,2}
+ * (P:555-561).  Deterministic (fixed-order split-K reduction). */
+TUCKER_API int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,
+                size_t ws_bytes, void* stream);
+
+/* a-4: leading r eigenpairs of a symmetric PSD n x n matrix G (dev): U (dev, n x r row-major,
+ * sorted by descending eigenvalue, sign rule R6), lambda (dev, r).  Synchronises `stream`.
+ * `info_mode` (host, nullable) receives {iters, converged, block, sweeps, resid, lambda1} in
+ * slot 0 of a tucker_info. */
+TUCKER_API int tucker_eig(int64_t n, const double* G, int32_t r, double* U, double* lambda, void* ws,
+               size_t ws_bytes, void* stream, tucker_info* info_mode);
+
+/* a-5: core (dev, r1*r2*r3) <- F x1 U1^T x2 U2^T x3 U3^T for given factors (dev). */
+TUCKER_API int tucker_ttm_core(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1,
+                    const double* U2, const double* U3, double* core, void* ws, size_t ws_bytes,
+                    void* stream);
+
+/* a-3..a-5: truncated HOSVD of F (dev).  Outputs (dev): U1,U2,U3 (n_m x r_m), core, and
+ * sigma_m (dev, r_m) = sqrt(max(lambda_m,0)).  `info` (host) may be NULL. */
+TUCKER_API int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1,
+                 double* U2, double* U3, double* core, double* sigma1, double* sigma2,
+                 double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
+/* a-6: out3 (dev, 3 doubles) <- {E, ||F||, ||F - Ft||} with Ft = core x1 U1 x2 U2 x3 U3
+ * (P:1016-1025).  Deterministic (fixed-order reduction, no float atomics). */
+TUCKER_API int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1,
+                 const double* U2, const double* U3, const double* core, double* out3, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* Whole path with HOST outputs (the end-to-end call a user makes): fill F into the caller's
+ * device buffer F (dev, n1*n2*n3), HOSVD, error; then copy U_m, core, sigma_m and
+ * {E, ||F||, ||F-Ft||} to the host buffers (any host memory; pinned is faster) and synchronise.
+ * Host buffers: U_h[m] (n_m*r_m), core_h (r1*r2*r3), sigma_h[m] (r_m), err_h (3). */
+TUCKER_API int tucker_approximate(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
+                       double* F, double* const U_h[3], double* core_h, double* const sigma_h[3],
+                       double* err_h, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
+/* Number of kernel launches enqueued by this thread's most recent entry-point call. */
+TUCKER_API int64_t tucker_last_launch_count(void);
+
+TUCKER_API const char* tucker_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TUCKER_B200_H */

@@ -1,0 +1,276 @@
+// api.cu — the extern "C" boundary declared in include/tucker.h: argument validation,
+// workspace planning, stage orchestration on the caller's stream.  Host C++ only; every step of
+// the numerical path runs in the kernels of fill.cu / gram.cu / eig.cu / ttm.cu.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tk {
+
+int64_t& launch_counter() {
+    static thread_local int64_t c = 0;
+    return c;
+}
+
+PFN_tmapEncodeTiled tmap_encoder() {
+    static PFN_tmapEncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_tmapEncodeTiled>(p);
+    }
+    return fn;
+}
+
+bool make_tmap_f64(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box) {
+    PFN_tmapEncodeTiled enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t d[5], s[4];
+    cuuint32_t b[5], e[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        e[i] = 1;
+    }
+    for (int i = 0; i + 1 < rank; ++i) s[i] = strides_bytes[i];
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base), d, s, b, e,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+namespace {
+
+int check_grid(const tucker_grid* g) {
+    if (!g) return TUCKER_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; ++a) {
+        if (g->n[a] < 2) return TUCKER_ERR_INVALID_ARG;
+        if (!(g->lo[a] < g->hi[a]) || !std::isfinite(g->lo[a]) || !std::isfinite(g->hi[a]))
+            return TUCKER_ERR_INVALID_ARG;
+        if (g->n[a] > (int64_t)1 << 20) return TUCKER_ERR_SIZE;
+    }
+    const double N = (double)g->n[0] * (double)g->n[1] * (double)g->n[2];
+    if (N * 8.0 > 9.0e18) return TUCKER_ERR_SIZE;
+    return TUCKER_OK;
+}
+
+int check_kernel(const tucker_kernel* k) {
+    if (!k) return TUCKER_ERR_INVALID_ARG;
+    if (!(k->sigma2 > 0.0) || !std::isfinite(k->sigma2)) return TUCKER_ERR_DOMAIN;
+    if (k->family == TUCKER_MATERN) {
+        if (!(k->nu > 0.0) || !(k->ell > 0.0) || !std::isfinite(k->nu) || !std::isfinite(k->ell))
+            return TUCKER_ERR_DOMAIN;
+        if (k->nu > 50.0) return TUCKER_ERR_DOMAIN;
+        return TUCKER_OK;
+    }
+    if (k->family == TUCKER_SLATER) {
+        if (!(k->lambda > 0.0) || !(k->p > 0.0) || !(k->p <= 2.0) || !std::isfinite(k->lambda))
+            return TUCKER_ERR_DOMAIN;
+        return TUCKER_OK;
+    }
+    return TUCKER_ERR_INVALID_ARG;
+}
+
+int check_ranks(const tucker_grid* g, const int32_t* r) {
+    if (!r) return TUCKER_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; ++a)
+        if (r[a] < 1 || r[a] > g->n[a]) return TUCKER_ERR_RANK;
+    return TUCKER_OK;
+}
+
+// Workspace layout (all 256-byte aligned):
+//   [nodes x^2 (n1+n2+n3)] [K_nu table] [G (max n_m^2)] [scratch = max(gram, eig, ttm, err)]
+//   [device outputs of tucker_approximate: U1 U2 U3 core sigma1..3 err3]
+struct Layout {
+    size_t nodes, cheb, G, scratch, outs, total;
+    size_t scratch_bytes;
+};
+
+Layout plan(const tucker_grid* g, const int32_t* rin) {
+    int32_t r[3];
+    for (int a = 0; a < 3; ++a) r[a] = rin ? rin[a] : (int32_t)std::min<int64_t>(g->n[a], 56);
+    const int64_t* n = g->n;
+    Layout L{};
+    size_t off = 0;
+    L.nodes = off;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
+    L.cheb = off;
+    off += align_up((size_t)kChebIntervals * kChebN * 8, 256);
+    L.G = off;
+    const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
+    off += align_up((size_t)nmax * nmax * 8, 256);
+    L.scratch = off;
+    size_t s = gram_ws_bytes(n);
+    for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
+    s = std::max(s, ttm_ws_bytes(n, r));
+    s = std::max(s, err_ws_bytes(n, r));
+    L.scratch_bytes = align_up(s, 256);
+    off += L.scratch_bytes;
+    L.outs = off;
+    size_t o = 0;
+    for (int a = 0; a < 3; ++a) o += align_up((size_t)n[a] * r[a] * 8, 256) + align_up((size_t)r[a] * 8, 256);
+    o += align_up((size_t)r[0] * r[1] * r[2] * 8, 256) + 256;
+    off += o;
+    L.total = off;
+    return L;
+}
+
+inline char* at(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
+
+int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* const U[3], double* core,
+               double* const sig[3], void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info) {
+    const Layout L = plan(g, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    double* G = reinterpret_cast<double*>(at(ws, L.G));
+    void* scr = at(ws, L.scratch);
+    int worst = TUCKER_OK;
+    for (int m = 0; m < 3; ++m) {
+        TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));
+        const int rc = launch_eig(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, st, info, m);
+        if (rc == TUCKER_ERR_NOCONV) worst = rc;
+        else if (rc != TUCKER_OK) return rc;
+    }
+    TK_RC(launch_ttm_core(g->n, r, F, U[0], U[1], U[2], core, scr, L.scratch_bytes, st));
+    return worst;
+}
+
+}  // namespace
+}  // namespace tk
+
+using namespace tk;
+
+extern "C" {
+
+size_t tucker_workspace_size(const tucker_grid* grid, const int32_t r[3]) {
+    if (check_grid(grid) != TUCKER_OK) return 0;
+    return plan(grid, r).total;
+}
+
+int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F, void* ws, size_t ws_bytes,
+                void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    if (!F || !ws) return TUCKER_ERR_INVALID_ARG;
+    const Layout L = plan(grid, nullptr);
+    if (ws_bytes < L.scratch) return TUCKER_ERR_SIZE;
+    return launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                       reinterpret_cast<double*>(at(ws, L.cheb)), static_cast<cudaStream_t>(stream));
+}
+
+int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws, size_t ws_bytes,
+                void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    if (mode < 0 || mode > 2 || !F || !G || !ws) return TUCKER_ERR_INVALID_ARG;
+    return launch_gram(grid->n, mode, F, G, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int tucker_eig(int64_t n, const double* G, int32_t r, double* U, double* lambda, void* ws, size_t ws_bytes,
+               void* stream, tucker_info* info_mode) {
+    launch_counter() = 0;
+    if (n < 1 || !G || !U || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (r < 1 || r > n) return TUCKER_ERR_RANK;
+    return launch_eig(n, G, r, U, lambda, nullptr, ws, ws_bytes, static_cast<cudaStream_t>(stream), info_mode, 0);
+}
+
+int tucker_ttm_core(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1,
+                    const double* U2, const double* U3, double* core, void* ws, size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    return launch_ttm_core(grid->n, r, F, U1, U2, U3, core, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1, double* U2, double* U3,
+                 double* core, double* sigma1, double* sigma2, double* sigma3, void* ws, size_t ws_bytes,
+                 void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (info) std::memset(info, 0, sizeof(*info));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    return hosvd_impl(grid, r, F, U, core, S, ws, ws_bytes, static_cast<cudaStream_t>(stream), info);
+}
+
+int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1, const double* U2,
+                 const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !out3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    return launch_error(grid->n, r, F, U1, U2, U3, core, out3, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int tucker_approximate(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F,
+                       double* const U_h[3], double* core_h, double* const sigma_h[3], double* err_h, void* ws,
+                       size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U_h || !core_h || !sigma_h || !err_h || !ws) return TUCKER_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; ++a)
+        if (!U_h[a] || !sigma_h[a]) return TUCKER_ERR_INVALID_ARG;
+    const Layout L = plan(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (info) std::memset(info, 0, sizeof(*info));
+    // device outputs live in the tail of the workspace
+    char* o = at(ws, L.outs);
+    double *Ud[3], *Sd[3];
+    for (int a = 0; a < 3; ++a) {
+        Ud[a] = reinterpret_cast<double*>(o);
+        o += align_up((size_t)grid->n[a] * r[a] * 8, 256);
+        Sd[a] = reinterpret_cast<double*>(o);
+        o += align_up((size_t)r[a] * 8, 256);
+    }
+    double* cored = reinterpret_cast<double*>(o);
+    o += align_up((size_t)r[0] * r[1] * r[2] * 8, 256);
+    double* errd = reinterpret_cast<double*>(o);
+
+    TK_RC(launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                      reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    const int64_t c0 = launch_counter();
+    const int rc = hosvd_impl(grid, r, F, Ud, cored, Sd, ws, ws_bytes, st, info);
+    if (rc != TUCKER_OK && rc != TUCKER_ERR_NOCONV) return rc;
+    const int64_t c1 = launch_counter();
+    (void)c0;
+    (void)c1;
+    TK_RC(launch_error(grid->n, r, F, Ud[0], Ud[1], Ud[2], cored, errd, at(ws, L.scratch), L.scratch_bytes, st));
+    for (int a = 0; a < 3; ++a) {
+        TK_CUDA(cudaMemcpyAsync(U_h[a], Ud[a], (size_t)grid->n[a] * r[a] * 8, cudaMemcpyDeviceToHost, st));
+        TK_CUDA(cudaMemcpyAsync(sigma_h[a], Sd[a], (size_t)r[a] * 8, cudaMemcpyDeviceToHost, st));
+    }
+    TK_CUDA(cudaMemcpyAsync(core_h, cored, (size_t)r[0] * r[1] * r[2] * 8, cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaMemcpyAsync(err_h, errd, 3 * 8, cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    return rc;
+}
+
+int64_t tucker_last_launch_count(void) { return launch_counter(); }
+
+const char* tucker_strerror(int code) {
+    switch (code) {
+        case TUCKER_OK: return "ok";
+        case TUCKER_ERR_INVALID_ARG: return "invalid argument (null pointer, n < 2, lo >= hi, bad mode)";
+        case TUCKER_ERR_DOMAIN: return "kernel parameter outside its domain";
+        case TUCKER_ERR_RANK: return "rank out of range (r < 1 or r > n)";
+        case TUCKER_ERR_SIZE: return "workspace too small or size overflow";
+        case TUCKER_ERR_NOCONV: return "eigensolver did not converge (best iterate returned)";
+        case TUCKER_ERR_CUDA: return "CUDA runtime/driver error";
+        case TUCKER_ERR_UNSUPPORTED: return "unsupported configuration";
+        default: return "unknown error code";
+    }
+}
+
+}  // extern "C"

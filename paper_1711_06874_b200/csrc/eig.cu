@@ -1,0 +1,551 @@
+// eig.cu — a-4: leading r eigenpairs of the symmetric PSD Gram matrix G_m.
+//
+// The HOSVD factor U_m is the top-r_m left singular subspace of the unfolding A_(m),
+// i.e. the top-r_m eigenvectors of G_m; sigma = sqrt(max(lambda, 0)).
+//
+// Method (B200 design; the paper names no eigensolver): block subspace iteration with
+// Rayleigh–Ritz on p = r + q columns (q = min(16, 64 - r)):
+//   V_0 = orth(G Omega), Omega a fixed counter-hash block (deterministic)
+//   repeat: W = G V (multi-CTA DFMA GEMM); H = V^T W (p x p); H = Q Theta Q^T by parallel cyclic
+//           Jacobi in shared memory (round-robin pairs, warp-parallel rotations, skip rule R7);
+//           Vr = V Q, Y = W Q; residual rho_k = ||Y_k - theta_k Vr_k||;
+//           stop when rho_k <= 1e-14 theta_1 for k < r after >= 3 iterations, else V = CGS2(Y).
+// Small matrices (n <= 96) are diagonalised directly by the same shared-memory Jacobi.
+// Outputs are sorted descending (stable) and sign-fixed by rule R6: the first entry with
+// |u_i| >= max|u|/2 is made positive.  Everything is deterministic (fixed reduction orders).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tk {
+namespace eig {
+
+constexpr int kMaxP = 64;
+constexpr int kDirectMax = 96;
+constexpr int kThreads = 1024;
+constexpr int kBatch = 8;
+constexpr int kMaxIters = 96;
+constexpr int kMinIters = 3;
+constexpr double kTol = 1e-14;
+
+struct State {  // device-side status block
+    int done;
+    int iters;
+    int converged;
+    int sweeps;
+    double resid;
+    double lambda1;
+};
+
+__device__ __forceinline__ double hash_uniform(uint64_t idx) {  // SplitMix64 finaliser -> [-1,1)
+    uint64_t z = idx * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// ---------------------------------------------------------------------- shared-memory Jacobi
+// H (p x p, leading dim p) is diagonalised in place; Q (p x p) accumulates the rotations.
+// Parallel cyclic Jacobi, round-robin ordering, rotations of Golub & Van Loan Alg. 8.4.2.
+// Returns the sweep count (negative if the cap was hit).  All threads of the block call it.
+struct JacobiScratch {
+    int* arr;       // m players
+    int* pp;        // m/2
+    int* qq;        // m/2
+    double* cs;     // m/2
+    double* sn;     // m/2
+    int* flag;      // 1
+    double* red;    // >= 33
+};
+
+__device__ int jacobi_block(double* H, double* Q, int p, JacobiScratch js, int max_sweeps) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int m = p + (p & 1), half = m / 2;
+    const double eps = 2.220446049250313e-16;
+    for (int idx = tid; idx < p * p; idx += nt) Q[idx] = (idx / p == idx % p) ? 1.0 : 0.0;
+    __syncthreads();
+    int sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        double dm = 0.0;
+        for (int i = tid; i < p; i += nt) dm = fmax(dm, fabs(H[i * p + i]));
+        // block max (reuse block_sum machinery with max): warp max then smem
+        dm = warp_max(dm);
+        if ((tid & 31) == 0) js.red[tid >> 5] = dm;
+        if (tid == 0) *js.flag = 0;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (nt + 31) / 32; ++w) t = fmax(t, js.red[w]);
+            js.red[32] = t;
+        }
+        for (int t = tid; t < m; t += nt) js.arr[t] = t;
+        __syncthreads();
+        const double floor_abs = eps * js.red[32] / (double)p;
+        for (int step = 0; step < m - 1; ++step) {
+            for (int w = tid; w < half; w += nt) {
+                int a = js.arr[w], b = js.arr[m - 1 - w];
+                if (a > b) { int t = a; a = b; b = t; }
+                double c = 1.0, s = 0.0;
+                bool rot = false;
+                if (b < p) {
+                    const double apq = H[a * p + b], app = H[a * p + a], aqq = H[b * p + b];
+                    const double thr = fmax(eps * sqrt(fabs(app * aqq)), floor_abs);
+                    if (fabs(apq) > thr) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                                      : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        rot = true;
+                    }
+                }
+                js.pp[w] = rot ? a : -1;
+                js.qq[w] = b;
+                js.cs[w] = c;
+                js.sn[w] = s;
+                if (rot) *js.flag = 1;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < half * p; idx += nt) {  // rows: H <- J^T H
+                const int w = idx / p, j = idx % p, a = js.pp[w];
+                if (a < 0) continue;
+                const int b = js.qq[w];
+                const double c = js.cs[w], s = js.sn[w];
+                const double x = H[a * p + j], y = H[b * p + j];
+                H[a * p + j] = c * x - s * y;
+                H[b * p + j] = s * x + c * y;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < half * p; idx += nt) {  // cols: H <- H J, Q <- Q J
+                const int w = idx / p, i = idx % p, a = js.pp[w];
+                if (a < 0) continue;
+                const int b = js.qq[w];
+                const double c = js.cs[w], s = js.sn[w];
+                double x = H[i * p + a], y = H[i * p + b];
+                H[i * p + a] = c * x - s * y;
+                H[i * p + b] = s * x + c * y;
+                x = Q[i * p + a];
+                y = Q[i * p + b];
+                Q[i * p + a] = c * x - s * y;
+                Q[i * p + b] = s * x + c * y;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 0; w < half; ++w)
+                    if (js.pp[w] >= 0) {
+                        H[js.pp[w] * p + js.qq[w]] = 0.0;
+                        H[js.qq[w] * p + js.pp[w]] = 0.0;
+                    }
+                const int last = js.arr[m - 1];
+                for (int t = m - 1; t > 1; --t) js.arr[t] = js.arr[t - 1];
+                if (m > 1) js.arr[1] = last;
+            }
+            __syncthreads();
+        }
+        const int any = *js.flag;
+        __syncthreads();
+        if (!any) return sweep + 1;
+    }
+    return -sweep;
+}
+
+// Stable descending order of the diagonal: order[rank] = index.
+__device__ void sort_desc(const double* H, int p, int* order) {
+    for (int k = threadIdx.x; k < p; k += blockDim.x) {
+        const double v = H[k * p + k];
+        int rank = 0;
+        for (int j = 0; j < p; ++j) {
+            const double w = H[j * p + j];
+            rank += (w > v) || (w == v && j < k);
+        }
+        order[rank] = k;
+    }
+    __syncthreads();
+}
+
+// Sign rule R6 on column vector u (n entries, stride `ld` in elements) — whole block.
+__device__ void sign_fix_block(double* u, int64_t n, int64_t ld, double* red) {
+    double mx = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, fabs(u[i * ld]));
+    mx = warp_max(mx);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t = fmax(t, red[w]);
+        red[32] = t;
+    }
+    __syncthreads();
+    const double half = 0.5 * red[32];
+    int64_t first = INT64_MAX;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (fabs(u[i * ld]) >= half) { first = i; break; }
+    // block min of `first` (as double is exact for i < 2^53)
+    double f = (double)first;
+    for (int o = 16; o > 0; o >>= 1) f = fmin(f, __shfl_xor_sync(0xffffffffu, f, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w) t = fmin(t, red[w]);
+        red[32] = t;
+    }
+    __syncthreads();
+    const int64_t istar = (int64_t)red[32];
+    const bool flip = u[istar * ld] < 0.0;
+    __syncthreads();
+    if (flip)
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) u[i * ld] = -u[i * ld];
+    __syncthreads();
+}
+
+// Two-pass classical Gram–Schmidt of the p rows of Yt (p x n) into Vt (orthonormal rows).
+__device__ void cgs2_block(const double* Yt, double* Vt, int p, int64_t n, double* red, double* h) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = (nt + 31) / 32;
+    for (int k = 0; k < p; ++k) {
+        double* v = Vt + (size_t)k * n;
+        for (int64_t i = tid; i < n; i += nt) v[i] = Yt[(size_t)k * n + i];
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            for (int pass = 0; pass < 2 && k > 0; ++pass) {
+                for (int j0 = 0; j0 < k; j0 += 8) {
+                    double part[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) part[u] = 0.0;
+                    for (int64_t i = tid; i < n; i += nt) {
+                        const double vi = v[i];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (j0 + u < k) part[u] += Vt[(size_t)(j0 + u) * n + i] * vi;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double s = warp_sum(part[u]);
+                        if (lane == 0) red[warp * 8 + u] = s;
+                    }
+                    __syncthreads();
+                    if (tid < 8 && j0 + tid < k) {
+                        double s = 0.0;
+                        for (int w = 0; w < nw; ++w) s += red[w * 8 + tid];
+                        h[j0 + tid] = s;
+                    }
+                    __syncthreads();
+                }
+                for (int64_t i = tid; i < n; i += nt) {
+                    double vi = v[i];
+                    for (int j = 0; j < k; ++j) vi -= h[j] * Vt[(size_t)j * n + i];
+                    v[i] = vi;
+                }
+            }
+            double ss = 0.0;
+            for (int64_t i = tid; i < n; i += nt) ss += v[i] * v[i];
+            ss = block_sum(ss, red);
+            if (ss > 1e-280) {
+                const double inv = 1.0 / sqrt(ss);
+                for (int64_t i = tid; i < n; i += nt) v[i] *= inv;
+                break;
+            }
+            // exactly dependent column: replace by a deterministic pseudo-random vector, retry
+            for (int64_t i = tid; i < n; i += nt) v[i] = hash_uniform(0x5eedull * (k + 1) + (uint64_t)i);
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------ kernels
+__global__ void k_omega(double* Vt, int p, int64_t n) {
+    const int64_t tot = (int64_t)p * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x)
+        Vt[t] = hash_uniform((uint64_t)t);
+}
+
+// Wt (p x n) = Vt (p x n) * G (n x n)   [= (G V)^T, G symmetric].  Tile 16 rows x 64 cols.
+__global__ void __launch_bounds__(256) k_gemm_vg(const double* __restrict__ Vt, const double* __restrict__ G,
+                                                 double* __restrict__ Wt, int p, int64_t n, const State* st) {
+    if (st && st->done) return;
+    __shared__ double sV[16][33];
+    __shared__ double sG[32][64];
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // ty 0..3 -> rows ty*4..ty*4+3
+    const int64_t col = blockIdx.x * 64 + tx;
+    const int row0 = blockIdx.y * 16;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+        for (int t = threadIdx.x; t < 16 * 32; t += 256) {
+            const int rr = t / 32, kk = t % 32;
+            sV[rr][kk] = (row0 + rr < p && k0 + kk < n) ? Vt[(size_t)(row0 + rr) * n + k0 + kk] : 0.0;
+        }
+        for (int t = threadIdx.x; t < 32 * 64; t += 256) {
+            const int kk = t / 64, cc = t % 64;
+            const int64_t gc = blockIdx.x * 64 + cc;
+            sG[kk][cc] = (k0 + kk < n && gc < n) ? G[(size_t)(k0 + kk) * n + gc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double g = sG[kk][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(sV[ty * 4 + u][kk], g, acc[u]);
+        }
+        __syncthreads();
+    }
+    if (col < n)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (row0 + ty * 4 + u < p) Wt[(size_t)(row0 + ty * 4 + u) * n + col] = acc[u];
+}
+
+__global__ void __launch_bounds__(kThreads) k_orth(const double* Yt, double* Vt, int p, int64_t n) {
+    __shared__ double red[8 * 32 + 40];
+    __shared__ double h[kMaxP];
+    cgs2_block(Yt, Vt, p, n, red, h);
+}
+
+struct RRArgs {
+    int64_t n;
+    int p, r, it, last;
+    double* Vt;
+    const double* Wt;
+    double* VrT;
+    double* YT;
+    double* U;       // n x r output
+    double* lambda;  // r (nullable)
+    double* sigma;   // r (nullable)
+    State* st;
+};
+
+// One Rayleigh–Ritz step (single CTA).
+__global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
+    if (a.st->done) return;
+    extern __shared__ double sm[];
+    const int p = a.p;
+    const int64_t n = a.n;
+    double* H = sm;
+    double* Q = H + p * p;
+    double* red = Q + p * p;          // 8*32 + 40
+    double* h = red + 8 * 32 + 40;    // kMaxP
+    double* cs = h + kMaxP;           // kMaxP/2 + 1
+    double* sn = cs + kMaxP / 2 + 1;
+    double* res = sn + kMaxP / 2 + 1;  // kMaxP
+    int* ints = reinterpret_cast<int*>(res + kMaxP);
+    int* arr = ints;                  // kMaxP + 1
+    int* pp = arr + kMaxP + 2;
+    int* qq = pp + kMaxP / 2 + 1;
+    int* order = qq + kMaxP / 2 + 1;  // kMaxP
+    int* flag = order + kMaxP;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x / 32;
+
+    // 1. H = V^T W (lower triangle, mirrored)
+    for (int pair = warp; pair < p * (p + 1) / 2; pair += nw) {
+        int aa = (int)((sqrt(8.0 * pair + 1.0) - 1.0) * 0.5);
+        while ((aa + 1) * (aa + 2) / 2 <= pair) ++aa;
+        while (aa * (aa + 1) / 2 > pair) --aa;
+        const int bb = pair - aa * (aa + 1) / 2;
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32) s += a.Vt[(size_t)aa * n + i] * a.Wt[(size_t)bb * n + i];
+        s = warp_sum(s);
+        if (lane == 0) { H[aa * p + bb] = s; H[bb * p + aa] = s; }
+    }
+    __syncthreads();
+    // 2. Jacobi
+    JacobiScratch js{arr, pp, qq, cs, sn, flag, red};
+    const int sweeps = jacobi_block(H, Q, p, js, 60);
+    sort_desc(H, p, order);
+    // 3. VrT[k] = sum_a Q[a][order[k]] Vt[a],  YT[k] = sum_a Q[a][order[k]] Wt[a]
+    for (int64_t i = tid; i < n; i += blockDim.x)
+        for (int k0 = 0; k0 < p; k0 += 8) {
+            double av[8], ay[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) av[u] = ay[u] = 0.0;
+            for (int aa = 0; aa < p; ++aa) {
+                const double v = a.Vt[(size_t)aa * n + i], w = a.Wt[(size_t)aa * n + i];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k0 + u < p) {
+                        const double qv = Q[aa * p + order[k0 + u]];
+                        av[u] = fma(qv, v, av[u]);
+                        ay[u] = fma(qv, w, ay[u]);
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < p) {
+                    a.VrT[(size_t)(k0 + u) * n + i] = av[u];
+                    a.YT[(size_t)(k0 + u) * n + i] = ay[u];
+                }
+        }
+    __syncthreads();
+    // 4. residuals rho_k = ||Y_k - theta_k Vr_k|| for k < r
+    for (int k = warp; k < a.r; k += nw) {
+        const double th = H[order[k] * p + order[k]];
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32) {
+            const double d = a.YT[(size_t)k * n + i] - th * a.VrT[(size_t)k * n + i];
+            s += d * d;
+        }
+        s = warp_sum(s);
+        if (lane == 0) res[k] = sqrt(s);
+    }
+    __syncthreads();
+    const double theta1 = H[order[0] * p + order[0]];
+    double rmax = 0.0;
+    for (int k = 0; k < a.r; ++k) rmax = fmax(rmax, res[k]);
+    const double rel = theta1 > 0.0 ? rmax / theta1 : 0.0;
+    const bool conv = (a.it + 1 >= kMinIters) && (rel <= kTol);
+    if (conv || a.last) {
+        // 5. outputs: U[:, k] = Vr_k (sign rule R6), lambda, sigma
+        for (int k = 0; k < a.r; ++k) {
+            sign_fix_block(a.VrT + (size_t)k * n, n, 1, red);
+        }
+        for (int64_t idx = tid; idx < n * a.r; idx += blockDim.x) {
+            const int64_t i = idx / a.r;
+            const int k = (int)(idx % a.r);
+            a.U[idx] = a.VrT[(size_t)k * n + i];
+        }
+        for (int k = tid; k < a.r; k += blockDim.x) {
+            const double th = H[order[k] * p + order[k]];
+            if (a.lambda) a.lambda[k] = th;
+            if (a.sigma) a.sigma[k] = sqrt(fmax(th, 0.0));
+        }
+        if (tid == 0) {
+            a.st->done = 1;
+            a.st->converged = conv ? 1 : 0;
+            a.st->iters = a.it + 1;
+            a.st->sweeps = sweeps;
+            a.st->resid = rel;
+            a.st->lambda1 = theta1;
+        }
+        return;
+    }
+    // 6. next basis V = CGS2(Y)
+    cgs2_block(a.YT, a.Vt, p, n, red, h);
+    if (tid == 0) { a.st->iters = a.it + 1; a.st->resid = rel; a.st->sweeps = sweeps; }
+}
+
+// Direct Jacobi of the whole n x n matrix (n <= kDirectMax), single CTA.
+__global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int r, double* U, double* lambda,
+                                                     double* sigma, State* st) {
+    extern __shared__ double sm[];
+    double* H = sm;
+    double* Q = H + n * n;
+    double* red = Q + n * n;
+    double* cs = red + 8 * 32 + 40;
+    double* sn = cs + kDirectMax / 2 + 1;
+    int* arr = reinterpret_cast<int*>(sn + kDirectMax / 2 + 1);
+    int* pp = arr + kDirectMax + 2;
+    int* qq = pp + kDirectMax / 2 + 1;
+    int* order = qq + kDirectMax / 2 + 1;
+    int* flag = order + kDirectMax;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) H[idx] = G[idx];
+    __syncthreads();
+    JacobiScratch js{arr, pp, qq, cs, sn, flag, red};
+    const int sweeps = jacobi_block(H, Q, n, js, 100);
+    sort_desc(H, n, order);
+    // U (n x r) <- Q[:, order[k]], then sign rule per column (in place, stride r)
+    for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
+        const int i = idx / r, k = idx % r;
+        U[idx] = Q[i * n + order[k]];
+    }
+    __syncthreads();
+    for (int k = 0; k < r; ++k) sign_fix_block(U + k, n, r, red);
+    for (int k = threadIdx.x; k < r; k += blockDim.x) {
+        const double th = H[order[k] * n + order[k]];
+        if (lambda) lambda[k] = th;
+        if (sigma) sigma[k] = sqrt(fmax(th, 0.0));
+    }
+    if (threadIdx.x == 0) {
+        st->done = 1;
+        st->converged = sweeps > 0 ? 1 : 0;
+        st->iters = 0;
+        st->sweeps = sweeps > 0 ? sweeps : -sweeps;
+        st->resid = 0.0;
+        st->lambda1 = H[order[0] * n + order[0]];
+    }
+}
+
+static int block_width(int64_t n, int r) {
+    if (n <= kDirectMax) return (int)n;
+    const int q = std::min(16, kMaxP - r);
+    return (int)std::min<int64_t>(n, r + q);
+}
+
+static size_t rr_smem(int p) {
+    return (size_t)(2 * p * p + 8 * 32 + 40 + kMaxP + 2 * (kMaxP / 2 + 1) + kMaxP) * sizeof(double) +
+           (size_t)(kMaxP + 2 + 2 * (kMaxP / 2 + 1) + kMaxP + 4) * sizeof(int);
+}
+static size_t direct_smem(int n) {
+    return (size_t)(2 * n * n + 8 * 32 + 40 + 2 * (kDirectMax / 2 + 1)) * sizeof(double) +
+           (size_t)(kDirectMax + 2 + 2 * (kDirectMax / 2 + 1) + kDirectMax + 4) * sizeof(int);
+}
+
+}  // namespace eig
+
+size_t eig_ws_bytes(int64_t n, int r) {
+    using namespace eig;
+    const int p = block_width(n, std::max(1, r));
+    return align_up(sizeof(State), 256) + 4 * align_up((size_t)p * n * sizeof(double), 256);
+}
+
+int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+               size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot) {
+    using namespace eig;
+    if (r < 1 || r > n) return TUCKER_ERR_RANK;
+    if (n > kDirectMax && r > kMaxP - 8) return TUCKER_ERR_UNSUPPORTED;
+    if (ws_bytes < eig_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
+    const int p = block_width(n, r);
+    char* w = static_cast<char*>(ws);
+    State* dst = reinterpret_cast<State*>(w);
+    w += align_up(sizeof(State), 256);
+    const size_t blk = align_up((size_t)p * n * sizeof(double), 256);
+    double* Vt = reinterpret_cast<double*>(w);
+    double* Wt = reinterpret_cast<double*>(w + blk);
+    double* VrT = reinterpret_cast<double*>(w + 2 * blk);
+    double* YT = reinterpret_cast<double*>(w + 3 * blk);
+    TK_CUDA(cudaMemsetAsync(dst, 0, sizeof(State), st));
+
+    if (n <= kDirectMax) {
+        const size_t sm = direct_smem((int)n);
+        TK_CUDA(cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_direct<<<1, kThreads, sm, st>>>(G, (int)n, r, U, lambda, sigma, dst);
+        TK_CHECK_LAUNCH();
+    } else {
+        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
+        k_omega<<<64, 256, 0, st>>>(Vt, p, n);
+        TK_CHECK_LAUNCH();
+        k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
+        TK_CHECK_LAUNCH();
+        k_orth<<<1, kThreads, 0, st>>>(Wt, Vt, p, n);
+        TK_CHECK_LAUNCH();
+        const size_t sm = rr_smem(p);
+        TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int it = 0;
+        while (true) {
+            for (int b = 0; b < kBatch && it < kMaxIters; ++b, ++it) {
+                k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
+                TK_CHECK_LAUNCH();
+                RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, Vt, Wt, VrT, YT, U, lambda, sigma, dst};
+                k_rr<<<1, kThreads, sm, st>>>(a);
+                TK_CHECK_LAUNCH();
+            }
+            State hs;
+            TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
+            TK_CUDA(cudaStreamSynchronize(st));
+            if (hs.done || it >= kMaxIters) break;
+        }
+    }
+    State hs;
+    TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
+    TK_CUDA(cudaStreamSynchronize(st));
+    if (info) {
+        info->iters[slot] = hs.iters;
+        info->converged[slot] = hs.converged;
+        info->block[slot] = p;
+        info->sweeps[slot] = hs.sweeps;
+        info->resid[slot] = hs.resid;
+        info->lambda1[slot] = hs.lambda1;
+    }
+    return hs.converged ? TUCKER_OK : TUCKER_ERR_NOCONV;
+}
+
+}  // namespace tk

@@ -1,0 +1,226 @@
+// fill.cu — a-1 grid nodes and a-2 function-tensor fill F[i,j,k] = C(||x_ijk||).
+//
+// Kernel families: Matérn eq. (Matern) P:353-358 (closed forms for nu = 1/2, 3/2, 5/2, P:365-366
+// and the half-integer K_nu), general nu through a hand-written K_nu; p-Slater eq. (exp_p)
+// P:1029-1031.
+//
+// General-nu K_nu: g(z) = e^z z^nu K_nu(z) is smooth on every dyadic
+// interval [2^j, 2^{j+1}); a per-call table of degree-20 Chebyshev coefficients of
+// pref * g (pref = sigma2 2^{1-nu}/Gamma(nu)) is built on the device from node values computed by
+// the trapezoid rule on K_nu(z) = int_0^inf e^{-z cosh t} cosh(nu t) dt with h = 1/32 — the paper's
+// own sinc-quadrature device.  Each point then costs one exp and a Clenshaw sum
+// (~21 DFMA), C = e^{-z} * cheb_j(4m - 3) where z = m 2^{j+1}, m in [1/2, 1).  Points outside the
+// table range fall back to the per-point trapezoid sum.
+//
+// Store path: on centred grids (lo = -hi on every axis) F is even in every index, so the kernel
+// evaluates one octant and writes each value to its 8 mirror images with 256-bit stores
+// (st.global.v4.f64 -> STG.E.ENL2.256); reversed positions stay inside the same cache lines.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tk {
+
+// ------------------------------------------------------------------------------------------ a-1
+__global__ void k_nodes(double c0, double s0, int64_t n0, double c1, double s1, int64_t n1,
+                        double c2, double s2, int64_t n2, double* x2) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t tot = n0 + n1 + n2;
+    if (t >= tot) return;
+    double c, s;
+    int64_t n, i;
+    if (t < n0) { c = c0; s = s0; n = n0; i = t; }
+    else if (t < n0 + n1) { c = c1; s = s1; n = n1; i = t - n0; }
+    else { c = c2; s = s2; n = n2; i = t - n0 - n1; }
+    double m = (double)(2 * i - (n - 1));
+    double x = __dadd_rn(c, __dmul_rn(s, m));  // R2: c + s (2i - (n-1)), no contraction
+    x2[t] = __dmul_rn(x, x);
+}
+
+// ------------------------------------------------------------------------- K_nu Chebyshev table
+// e^z K_nu(z) = int_0^inf exp(-2 z sinh^2(t/2)) cosh(nu t) dt, trapezoid h = 1/32.
+__device__ double scaled_besselk_trapz(double nu, double z) {
+    const double h = 1.0 / 32.0;
+    double sum = 0.5, prev = 1.0;
+    for (int k = 1; k < 200000; ++k) {
+        double t = k * h;
+        double sh = sinh(0.5 * t);
+        double f = exp(-2.0 * z * sh * sh) * cosh(nu * t);
+        sum += f;
+        if (f < prev && f < 1e-18 * sum) break;
+        prev = f;
+    }
+    return h * sum;
+}
+
+// One block per dyadic interval j = kChebJmin + blockIdx.x; thread k < 21 computes the node
+// value at x_k = cos(pi (k+1/2)/21), then thread m the coefficient
+// c_m = 2/21 sum_k g_k cos(pi m (k+1/2)/21).
+__global__ void k_cheb_table(double nu, double pref, double* table) {
+    __shared__ double g[kChebN];
+    const int j = kChebJmin + blockIdx.x;
+    const int k = threadIdx.x;
+    if (k < kChebN) {
+        double xk = cospi((k + 0.5) / kChebN);
+        double z = ldexp(1.5 + 0.5 * xk, j);
+        g[k] = pref * pow(z, nu) * scaled_besselk_trapz(nu, z);
+    }
+    __syncthreads();
+    if (k < kChebN) {
+        double c = 0.0;
+        for (int t = 0; t < kChebN; ++t) c += g[t] * cospi(k * (t + 0.5) / kChebN);
+        table[blockIdx.x * kChebN + k] = c * (2.0 / kChebN);
+    }
+}
+
+// ----------------------------------------------------------------------------- point kernels
+struct KParams {
+    int family;
+    int closed;  // 0 general, 1: nu=1/2, 2: nu=3/2, 3: nu=5/2
+    double sigma2, ell, sqrt2nu, lambda, p, nu, pref;
+};
+
+__device__ __forceinline__ double cheb_eval(const double* c, double x) {
+    // y = c0/2 + sum_{m>=1} c_m T_m(x)  (Clenshaw)
+    double b1 = 0.0, b2 = 0.0, x2 = 2.0 * x;
+#pragma unroll
+    for (int m = kChebN - 1; m >= 1; --m) {
+        double b0 = fma(x2, b1, c[m] - b2);
+        b2 = b1;
+        b1 = b0;
+    }
+    return fma(x, b1, 0.5 * c[0] - b2);
+}
+
+__device__ __forceinline__ double eval_point(const KParams& kp, const double* cheb, double r2) {
+    const double r = __dsqrt_rn(r2);
+    if (kp.family == TUCKER_SLATER) {
+        double rp = (kp.p == 1.0) ? r : (kp.p == 2.0) ? r2 : pow(r, kp.p);
+        return __dmul_rn(kp.sigma2, exp(__dmul_rn(-kp.lambda, rp)));
+    }
+    if (r == 0.0) return kp.sigma2;  // R4: C(0) = sigma^2
+    const double z = __ddiv_rn(__dmul_rn(kp.sqrt2nu, r), kp.ell);
+    const double e = exp(-z);
+    switch (kp.closed) {
+        case 1: return __dmul_rn(kp.sigma2, e);
+        case 2: return __dmul_rn(kp.sigma2, __dmul_rn(__dadd_rn(1.0, z), e));
+        case 3: {
+            double poly = __dadd_rn(__dadd_rn(1.0, z), __ddiv_rn(__dmul_rn(z, z), 3.0));
+            return __dmul_rn(kp.sigma2, __dmul_rn(poly, e));
+        }
+        default: break;
+    }
+    int ex;
+    double m = frexp(z, &ex);  // z = m 2^ex, m in [1/2,1): interval j = ex - 1
+    int j = ex - 1 - kChebJmin;
+    if (j >= 0 && j < kChebIntervals) return e * cheb_eval(cheb + j * kChebN, 4.0 * m - 3.0);
+    return e * (kp.pref * pow(z, kp.nu) * scaled_besselk_trapz(kp.nu, z));
+}
+
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+
+// Octant fill with 8-fold mirrored 256-bit stores.  Requires lo = -hi on all axes and
+// n3 % 8 == 0.  Item = (i < h1, j < h2, quad t < n3/8); 4 consecutive k per thread.
+__global__ void __launch_bounds__(256) k_fill_octant(KParams kp, const double* __restrict__ cheb_g,
+                                                     const double* __restrict__ x2,
+                                                     int64_t n1, int64_t n2, int64_t n3,
+                                                     double* __restrict__ F) {
+    __shared__ double cheb[kChebIntervals * kChebN];
+    if (kp.family == TUCKER_MATERN && kp.closed == 0)
+        for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    __syncthreads();
+    const double* xa = x2;
+    const double* xb = x2 + n1;
+    const double* xc = x2 + n1 + n2;
+    const int64_t h1 = (n1 + 1) / 2, h2 = (n2 + 1) / 2, q3 = n3 / 8;
+    const int64_t total = h1 * h2 * q3;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = it % q3;
+        const int64_t ij = it / q3;
+        const int64_t j = ij % h2, i = ij / h2;
+        const int64_t k0 = 4 * t;
+        const double s = __dadd_rn(xa[i], xb[j]);
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = eval_point(kp, cheb, __dadd_rn(s, xc[k0 + u]));
+        const int64_t rows[4] = {i * n2 + j, i * n2 + (n2 - 1 - j), (n1 - 1 - i) * n2 + j,
+                                 (n1 - 1 - i) * n2 + (n2 - 1 - j)};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            double* row = F + rows[w] * n3;
+            st_v4(row + k0, v[0], v[1], v[2], v[3]);
+            st_v4(row + (n3 - 4 - k0), v[3], v[2], v[1], v[0]);
+        }
+    }
+}
+
+// General fill: one point per thread (any grid, any n3).
+__global__ void __launch_bounds__(256) k_fill_general(KParams kp, const double* __restrict__ cheb_g,
+                                                      const double* __restrict__ x2,
+                                                      int64_t n1, int64_t n2, int64_t n3,
+                                                      double* __restrict__ F) {
+    __shared__ double cheb[kChebIntervals * kChebN];
+    if (kp.family == TUCKER_MATERN && kp.closed == 0)
+        for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    __syncthreads();
+    const int64_t N = n1 * n2 * n3;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < N;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = it % n3;
+        const int64_t ij = it / n3;
+        const int64_t j = ij % n2, i = ij / n2;
+        const double r2 = __dadd_rn(__dadd_rn(x2[i], x2[n1 + j]), x2[n1 + n2 + k]);
+        F[it] = eval_point(kp, cheb, r2);
+    }
+}
+
+// --------------------------------------------------------------------------------- launcher
+int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2,
+                double* cheb, cudaStream_t st) {
+    const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    double c[3], s[3];
+    for (int a = 0; a < 3; ++a) {  // host: exactly the oracle's expressions (R2)
+        c[a] = (g.lo[a] + g.hi[a]) * 0.5;
+        s[a] = (g.hi[a] - g.lo[a]) / (2.0 * (double)(g.n[a] - 1));
+    }
+    const int64_t tot = n1 + n2 + n3;
+    k_nodes<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(c[0], s[0], n1, c[1], s[1], n2, c[2],
+                                                          s[2], n3, nodes_x2);
+    TK_CHECK_LAUNCH();
+
+    KParams kp{};
+    kp.family = kn.family;
+    kp.sigma2 = kn.sigma2;
+    kp.ell = kn.ell;
+    kp.nu = kn.nu;
+    kp.lambda = kn.lambda;
+    kp.p = kn.p;
+    kp.sqrt2nu = sqrt(2.0 * kn.nu);
+    kp.closed = 0;
+    if (kn.family == TUCKER_MATERN && !(kn.flags & TUCKER_FORCE_GENERAL_BESSEL)) {
+        if (kn.nu == 0.5) kp.closed = 1;
+        else if (kn.nu == 1.5) kp.closed = 2;
+        else if (kn.nu == 2.5) kp.closed = 3;
+    }
+    if (kn.family == TUCKER_MATERN && kp.closed == 0) {
+        kp.pref = kn.sigma2 * (pow(2.0, 1.0 - kn.nu) / tgamma(kn.nu));
+        k_cheb_table<<<kChebIntervals, 32, 0, st>>>(kn.nu, kp.pref, cheb);
+        TK_CHECK_LAUNCH();
+    }
+    const bool centred = (g.lo[0] == -g.hi[0]) && (g.lo[1] == -g.hi[1]) && (g.lo[2] == -g.hi[2]);
+    if (centred && n3 % 8 == 0) {
+        const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 8);
+        const int64_t blocks = std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16);
+        k_fill_octant<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F);
+    } else {
+        const int64_t blocks = std::min<int64_t>(ceil_div(n1 * n2 * n3, 256), (int64_t)kNumSMs * 16);
+        k_fill_general<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F);
+    }
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+}  // namespace tk

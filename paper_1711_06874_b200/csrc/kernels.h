@@ -1,0 +1,55 @@
+// kernels.h — internal launch interfaces between api.cu and the kernel files (not exported).
+#pragma once
+
+#include <algorithm>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tucker.h"
+
+namespace tk {
+
+// K_nu Chebyshev table: dyadic intervals [2^j, 2^{j+1}), j = kChebJmin .. kChebJmin+kChebIntervals-1
+constexpr int kChebN = 21;  // degree 20
+constexpr int kChebJmin = -16;
+constexpr int kChebIntervals = 25;  // z in [2^-16, 2^9)
+
+int launch_fill(const tucker_grid& g, const tucker_kernel& k, double* F, double* nodes_x2,
+                double* cheb, cudaStream_t st);
+
+// Gram G_m (n_m x n_m, both triangles) of the mode-m unfolding of F.
+size_t gram_ws_bytes(const int64_t n[3]);
+int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
+                cudaStream_t st);
+
+// Top-r eigenpairs of a symmetric PSD n x n matrix (dev).  iters/resid/... reported in `info`
+// slot `slot`.
+size_t eig_ws_bytes(int64_t n, int r);
+int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma,
+               void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot);
+
+// Core beta = F x1 U1^T x2 U2^T x3 U3^T.
+size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]);
+int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,
+                    const double* U2, const double* U3, double* core, void* ws, size_t ws_bytes,
+                    cudaStream_t st);
+
+// Relative Frobenius error {E, ||F||, ||F-Ft||}.
+size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]);
+int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,
+                 const double* U2, const double* U3, const double* core, double* out3, void* ws,
+                 size_t ws_bytes, cudaStream_t st);
+
+// Small strided batched GEMM (DFMA): C[b](M x N) = A[b](M x K) * B[b](K x N); element strides.
+struct SmallGemm {
+    int64_t M, N, K, batch;
+    const double* A;
+    int64_t sam, sak, sab;
+    const double* B;
+    int64_t sbk, sbn, sbb;
+    double* C;
+    int64_t scm, scn, scb;
+};
+int launch_small_gemm(const SmallGemm& p, cudaStream_t st);
+
+}  // namespace tk

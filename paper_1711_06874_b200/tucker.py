@@ -1,0 +1,274 @@
+"""Thin ctypes binding of the C-ABI in include/tucker.h (argument marshalling only).
+
+Every numerical step runs in libtucker_b200.so (hand-written sm_100a CUDA).  PyTorch provides the
+device memory and the stream; there is no CPU or PyTorch fallback: if the native library is
+missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtucker_b200.so")
+
+MATERN, SLATER = 0, 1
+FORCE_GENERAL_BESSEL = 2
+ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
+          4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED"}
+EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
+           "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_last_launch_count",
+           "tucker_strerror")
+
+
+class TuckerError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {ERRORS.get(code, code)} ({_strerror(code)})")
+
+
+class CGrid(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64 * 3), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3)]
+
+
+class CKernel(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int32), ("flags", ctypes.c_int32), ("sigma2", ctypes.c_double),
+                ("ell", ctypes.c_double), ("nu", ctypes.c_double), ("lam", ctypes.c_double),
+                ("p", ctypes.c_double)]
+
+
+class CInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32 * 3), ("converged", ctypes.c_int32 * 3), ("block", ctypes.c_int32 * 3),
+                ("sweeps", ctypes.c_int32 * 3), ("resid", ctypes.c_double * 3), ("lambda1", ctypes.c_double * 3)]
+
+    def as_dict(self) -> dict:
+        return {k: list(getattr(self, k)) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the native library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"native library not built: {path} (run python -m paper_1711_06874_b200.build)")
+    lib = ctypes.CDLL(path)
+    P, vp, i32, i64, sz = ctypes.POINTER, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    pg, pk, pi = P(CGrid), P(CKernel), P(CInfo)
+    pr = P(ctypes.c_int32)
+    sig = {
+        "tucker_workspace_size": (sz, [pg, pr]),
+        "tucker_fill": (ctypes.c_int, [pg, pk, vp, vp, sz, vp]),
+        "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
+        "tucker_eig": (ctypes.c_int, [i64, vp, i32, vp, vp, vp, sz, vp, pi]),
+        "tucker_ttm_core": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "tucker_hosvd": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
+        "tucker_error": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "tucker_approximate": (ctypes.c_int, [pg, pk, pr, vp, P(vp), vp, P(vp), vp, vp, sz, vp, pi]),
+        "tucker_last_launch_count": (i64, []),
+        "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _strerror(code: int) -> str:
+    try:
+        return load().tucker_strerror(code).decode()
+    except Exception:  # pragma: no cover
+        return "?"
+
+
+def _check(code: int, where: str) -> int:
+    if code != 0:
+        raise TuckerError(code, where)
+    return code
+
+
+def cgrid(g) -> CGrid:
+    c = CGrid()
+    for a in range(3):
+        c.n[a], c.lo[a], c.hi[a] = int(g.n[a]), float(g.lo[a]), float(g.hi[a])
+    return c
+
+
+def ckernel(k) -> CKernel:
+    return CKernel(int(k.family), int(getattr(k, "flags", 0)), float(k.sigma2), float(k.ell), float(k.nu),
+                   float(k.lam), float(k.p))
+
+
+def cranks(r) -> ctypes.Array:
+    return (ctypes.c_int32 * 3)(*[int(v) for v in r])
+
+
+def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+
+
+def last_launch_count() -> int:
+    return int(load().tucker_last_launch_count())
+
+
+def workspace_bytes(grid, ranks=None) -> int:
+    lib = load()
+    g = cgrid(grid)
+    return int(lib.tucker_workspace_size(ctypes.byref(g), cranks(ranks) if ranks is not None else None))
+
+
+def workspace(grid, ranks=None, device="cuda") -> torch.Tensor:
+    return torch.empty(workspace_bytes(grid, ranks), dtype=torch.uint8, device=device)
+
+
+# -------------------------------------------------------------------------------- entry points
+def fill(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    lib = load()
+    shape = tuple(int(v) for v in grid.n)
+    if F is None:
+        F = torch.empty(shape, dtype=torch.float64, device="cuda")
+    _dev(F, "F")
+    ws = ws if ws is not None else workspace(grid)
+    g, k = cgrid(grid), ckernel(kernel)
+    _check(lib.tucker_fill(ctypes.byref(g), ctypes.byref(k), _ptr(F), _ptr(ws), ws.numel(), _stream(stream)),
+           "tucker_fill")
+    return F
+
+
+def gram(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    lib = load()
+    _dev(F, "F")
+    n = int(grid.n[mode])
+    G = torch.empty((n, n), dtype=torch.float64, device=F.device)
+    ws = ws if ws is not None else workspace(grid)
+    g = cgrid(grid)
+    _check(lib.tucker_gram(ctypes.byref(g), int(mode), _ptr(F), _ptr(G), _ptr(ws), ws.numel(), _stream(stream)),
+           "tucker_gram")
+    return G
+
+
+def eig(G: torch.Tensor, r: int, ws: torch.Tensor | None = None, stream=None, check: bool = True):
+    lib = load()
+    _dev(G, "G")
+    n = G.shape[0]
+    U = torch.empty((n, r), dtype=torch.float64, device=G.device)
+    lam = torch.empty(r, dtype=torch.float64, device=G.device)
+    if ws is None:
+        ws = workspace(type("g", (), {"n": (n, 2, 2), "lo": (-1, -1, -1), "hi": (1, 1, 1)}), (r, 1, 1))
+    info = CInfo()
+    rc = lib.tucker_eig(n, _ptr(G), int(r), _ptr(U), _ptr(lam), _ptr(ws), ws.numel(), _stream(stream),
+                        ctypes.byref(info))
+    if check and rc not in (0, 5):
+        _check(rc, "tucker_eig")
+    return U, lam, info.as_dict(), rc
+
+
+def ttm_core(grid, ranks, F, U1, U2, U3, ws=None, stream=None) -> torch.Tensor:
+    lib = load()
+    for t, nm in ((F, "F"), (U1, "U1"), (U2, "U2"), (U3, "U3")):
+        _dev(t, nm)
+    core = torch.empty(tuple(int(v) for v in ranks), dtype=torch.float64, device=F.device)
+    ws = ws if ws is not None else workspace(grid, ranks)
+    g = cgrid(grid)
+    _check(lib.tucker_ttm_core(ctypes.byref(g), cranks(ranks), _ptr(F), _ptr(U1), _ptr(U2), _ptr(U3), _ptr(core),
+                               _ptr(ws), ws.numel(), _stream(stream)), "tucker_ttm_core")
+    return core
+
+
+@dataclass
+class HosvdResult:
+    U: list
+    core: torch.Tensor
+    sigma: list
+    info: dict
+    rc: int
+
+
+def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> HosvdResult:
+    lib = load()
+    _dev(F, "F")
+    dev = F.device
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device=dev) for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device=dev) for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device=dev)
+    ws = ws if ws is not None else workspace(grid, r)
+    info = CInfo()
+    g = cgrid(grid)
+    rc = lib.tucker_hosvd(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core),
+                          _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(), _stream(stream),
+                          ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd")
+    return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+def error(grid, ranks, F, U, core, ws=None, stream=None) -> torch.Tensor:
+    lib = load()
+    out = torch.empty(3, dtype=torch.float64, device=F.device)
+    ws = ws if ws is not None else workspace(grid, ranks)
+    g = cgrid(grid)
+    _check(lib.tucker_error(ctypes.byref(g), cranks(ranks), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
+                            _ptr(core), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)), "tucker_error")
+    return out
+
+
+@dataclass
+class HostResult:
+    U: list
+    core: np.ndarray
+    sigma: list
+    err: np.ndarray
+    info: dict
+    rc: int
+
+
+class HostBuffers:
+    """Pinned host output buffers for tucker_approximate."""
+
+    def __init__(self, grid, ranks):
+        r = tuple(int(v) for v in ranks)
+        self.U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64).pin_memory() for m in range(3)]
+        self.sigma = [torch.empty(r[m], dtype=torch.float64).pin_memory() for m in range(3)]
+        self.core = torch.empty(r, dtype=torch.float64).pin_memory()
+        self.err = torch.empty(3, dtype=torch.float64).pin_memory()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 8 * (sum(u.numel() for u in self.U) + sum(s.numel() for s in self.sigma) + self.core.numel() + 3)
+
+
+def approximate(grid, kernel, ranks, F: torch.Tensor, ws: torch.Tensor, host: HostBuffers, stream=None) -> HostResult:
+    """The end-to-end call: fill + HOSVD + error on the device, factors/core/sigma/E to host."""
+    lib = load()
+    _dev(F, "F")
+    g, k = cgrid(grid), ckernel(kernel)
+    info = CInfo()
+    Uh = (ctypes.c_void_p * 3)(*[u.data_ptr() for u in host.U])
+    Sh = (ctypes.c_void_p * 3)(*[s.data_ptr() for s in host.sigma])
+    rc = lib.tucker_approximate(ctypes.byref(g), ctypes.byref(k), cranks(ranks), _ptr(F), Uh,
+                                ctypes.c_void_p(host.core.data_ptr()), Sh, ctypes.c_void_p(host.err.data_ptr()),
+                                _ptr(ws), ws.numel(), _stream(stream), ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_approximate")
+    return HostResult([u.numpy() for u in host.U], host.core.numpy(), [s.numpy() for s in host.sigma],
+                      host.err.numpy(), info.as_dict(), rc)
