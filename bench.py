@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the Tucker/HOSVD hot path of arXiv 1711.06874 on B200.
+
+One step = the whole hot path over one synthetic problem: grid nodes + fill
+of F, the three Gram matrices, the three eigensolves, the core (TTM chain) and the relative
+Frobenius error.  Workload at N=1: BASELINE.json config 5 (1024^3 on [-1,1]^3, Matérn nu=1.5,
+ell=0.2, sigma^2=1, ranks (40,40,40)).  Metric: grid points per second (whole job).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 1024] [--r 40]
+
+With --gpus N > 1 (launched by torch.distributed.run), every rank solves its own independent
+problem (weak scaling, no data-path collective); the step time is the max over ranks.
+--impl reference times the CPU oracle (oracle/, the only other program computing this path) on a
+bounded sample of the same workload on the host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Tucker HOSVD grid points/s and FP64 TFLOP/s vs peak (n=512–1024, r≤40)"
+UNIT = "grid points/s"
+FP64_PEAK_SPEC_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 TF/s: SMs x FP64 FMA/clk/SM x 2 x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--r", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-host-tensor", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ our GPU arm ----
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_06874_b200 import tucker as T
+    from tucker_inputs import GridSpec, KernelSpec
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    T.load()
+    n, rr = args.n, args.r
+    grid = GridSpec.cube(n, 1.0)
+    kern = KernelSpec.matern(1.5, 0.2)
+    ranks = (rr, rr, rr)
+    N = grid.points
+    stream = torch.cuda.current_stream()
+    F = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    ws = T.workspace(grid, ranks)
+    dev = F.device
+    U = [torch.empty((n, rr), dtype=torch.float64, device=dev) for _ in range(3)]
+    S = [torch.empty(rr, dtype=torch.float64, device=dev) for _ in range(3)]
+    G = torch.empty((n, n), dtype=torch.float64, device=dev)
+    core = torch.empty(ranks, dtype=torch.float64, device=dev)
+    out3 = torch.empty(3, dtype=torch.float64, device=dev)
+    lib = T.load()
+    import ctypes
+    g_c, k_c, r_c = T.cgrid(grid), T.ckernel(kern), T.cranks(ranks)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    wsp, wsn = ctypes.c_void_p(ws.data_ptr()), ws.numel()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+
+    def step(ev=None):
+        """One pass of the path as separate ABI calls; returns kernel launches.  ev: list of events."""
+        launches = 0
+
+        def rec(i):
+            if ev is not None:
+                ev[i].record(stream)
+
+        rec(0)
+        T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, sp), "fill")
+        launches += lib.tucker_last_launch_count()
+        rec(1)
+        for m in range(3):
+            T._check(lib.tucker_gram(ctypes.byref(g_c), m, P(F), P(G), wsp, wsn, sp), "gram")
+            launches += lib.tucker_last_launch_count()
+            rec(2 + 2 * m)
+            rc = lib.tucker_eig(n, P(G), rr, P(U[m]), P(S[m]), wsp, wsn, sp, None)  # S[m] <- lambda_m
+            if rc not in (0, 5):
+                T._check(rc, "eig")
+            launches += lib.tucker_last_launch_count()
+            rec(3 + 2 * m)
+        T._check(lib.tucker_ttm_core(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), wsp, wsn, sp),
+                 "ttm")
+        launches += lib.tucker_last_launch_count()
+        rec(8)
+        T._check(lib.tucker_error(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), P(out3), wsp,
+                                  wsn, sp), "error")
+        launches += lib.tucker_last_launch_count()
+        rec(9)
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(K):
+            launches += step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / K
+
+    # per-stage times (ms) averaged over the timed steps
+    def stage(i, j):
+        return sum(evs[k][i].elapsed_time(evs[k][j]) for k in range(K)) / K
+
+    st = {"fill": stage(0, 1), "gram": [stage(1 + 2 * m, 2 + 2 * m) for m in range(3)],
+          "eig": [stage(2 + 2 * m, 3 + 2 * m) for m in range(3)], "ttm": stage(7, 8), "error": stage(8, 9)}
+    E = out3.cpu().tolist()
+
+    # ---- roofline: dominant kernel = the Gram stage (SYRK-count flops N (n_m + 1) per launch)
+    gram_flops = [N * (n + 1) for _ in range(3)]
+    gram_ms = sum(st["gram"]) / 3
+    achieved = (sum(gram_flops) / 3) / (gram_ms * 1e-3) / 1e12
+    peak = FP64_PEAK_SPEC_TFLOPS
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gram_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    total_flops = sum(gram_flops) + 2.0 * N * rr * 2  # Gram + TTM1 + error reconstruction (algorithmic)
+    result = {
+        "metric": METRIC, "value": world * N / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2", "grid": [n, n, n], "box": [-1.0, 1.0],
+                   "kernel": {"family": "matern", "nu": 1.5, "ell": 0.2, "sigma2": 1.0}, "ranks": list(ranks),
+                   "l2": f"inputs larger than L2 (F = {8 * N / 1e9:.2f} GB per step, L2 = 126 MB)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "stages_ms": st,
+        "fp64_tflops_algorithmic": total_flops / (ms_step * 1e-3) / 1e12,
+        "roofline": {"bound": "tensor", "kernel": "k_gram_tma (+k_gram_reduce), per mode",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "peak_source": "FP64 tensor (DMMA) = FP64 FMA pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz "
+                                    "(spec-derived; MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops_per_launch": gram_flops[0]},
+        "gpu_launches": launches,
+        "error": {"E": E[0], "normF": E[1], "normDiff": E[2]},
+    }
+
+    # ---- e2e through the public call with host outputs (tucker_approximate)
+    if not args.no_e2e:
+        host = T.HostBuffers(grid, ranks)
+        for _ in range(1):
+            T.approximate(grid, kern, ranks, F, ws, host, stream)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        ke = max(1, min(K, 3))
+        for _ in range(ke):
+            T.approximate(grid, kern, ranks, F, ws, host, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = a0.elapsed_time(a1) / ke
+        if world > 1:
+            tt = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_e2e = float(tt.item())
+        param_bytes = ctypes.sizeof(g_c) + ctypes.sizeof(k_c) + ctypes.sizeof(r_c)
+        result["e2e"] = {"value": world * N / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": param_bytes,
+                         "d2h_bytes_per_step": host.d2h_bytes, "ms_per_step": ms_e2e,
+                         "call": "tucker_approximate (grid + kernel spec in, U/core/sigma/E to pinned host)"}
+        # variant: the tensor F already sampled on the host (pinned) -> H2D copy inside the timed region
+        if not args.no_host_tensor:
+            try:
+                Fh = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+                Fh.copy_(F)
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                b0.record(stream)
+                F.copy_(Fh, non_blocking=True)
+                res = T.hosvd(grid, ranks, F, ws, stream)
+                errv = T.error(grid, ranks, F, res.U, res.core, ws, stream)
+                outs = [u.cpu() for u in res.U] + [res.core.cpu(), errv.cpu()] + [s.cpu() for s in res.sigma]
+                b1.record(stream)
+                torch.cuda.synchronize()
+                ms_h = b0.elapsed_time(b1)
+                result["e2e_host_tensor"] = {"value": N / (ms_h * 1e-3), "unit": UNIT, "ms_per_step": ms_h,
+                                             "h2d_bytes_per_step": 8 * N,
+                                             "d2h_bytes_per_step": 8 * sum(o.numel() for o in outs)}
+                del Fh
+            except RuntimeError as e:  # pinned allocation failure etc.
+                result["e2e_host_tensor"] = {"unavailable": str(e)[:200]}
+    result["clocks"] = clk.summary()
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
+    if world > 1:
+        dist.destroy_process_group()
+    return result
+
+
+# ------------------------------------------------------------------------------ oracle arm ----
+def cpu_baseline(n: int, r: int, budget_s: float = 20.0) -> dict:
+    """The oracle, as it stands, on a bounded sample of the workload, scaled to points/s.
+
+    Sample: the oracle's own functions on s of the n i-slabs of the same tensor (fill, a mode-2 Gram
+    over the s*n unfolding columns those slabs hold, TTM core and reconstruction error) plus its
+    cyclic Jacobi at a reduced order; each part is scaled by its exact work ratio to the full step.
+    """
+    import numpy as np
+
+    from oracle import oracle as orc
+    orc.build()
+    threads = orc.num_threads()
+    k = orc.Kernel.matern(1.5, 0.2)
+    N = n ** 3
+    s = 16 if budget_s >= 20 else 8
+    s = min(s, n)
+    h = 2.0 / (n - 1)
+    sub = orc.Grid((s, n, n), (-1.0, -1.0, -1.0), (-1.0 + h * (s - 1), 1.0, 1.0))
+    t = time.perf_counter()
+    Fs = orc.fill(sub, k)
+    t_fill = (time.perf_counter() - t) * (n / s)
+    A = orc.unfold(Fs, 1)  # n x (s n): s n of the n^2 columns of the mode-2 unfolding
+    Ks = A.shape[1]
+    t = time.perf_counter()
+    Gs = orc.gram(A)
+    t_gram = (time.perf_counter() - t) * ((N // n) / Ks) * 3
+    ns = min(n, 160)
+    Gj = np.ascontiguousarray(Gs[:ns, :ns])
+    t = time.perf_counter()
+    orc.jacobi_eig(Gj)
+    t_eig = (time.perf_counter() - t) * (n / ns) ** 3 * 3
+    rng = np.random.default_rng(0)
+    U = [np.linalg.qr(rng.standard_normal((dim, min(r, dim))))[0] for dim in (s, n, n)]
+    t = time.perf_counter()
+    core = orc.ttm_core(Fs, *U)
+    t_ttm = (time.perf_counter() - t) * (n / s)
+    t = time.perf_counter()
+    orc.tucker_error(Fs, *U, core)
+    t_err = (time.perf_counter() - t) * (n / s)
+    total = t_fill + t_gram + t_eig + t_ttm + t_err
+    return {"value": N / total, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"oracle functions on {s} of {n} i-slabs of cfg5 ({n}^3, Matern nu=1.5 ell=0.2, r={r}): "
+                       f"fill, TTM core and error on the slabs (x{n / s:g}); Dot2 Gram over {Ks} of {N // n} "
+                       f"mode-2 unfolding columns (x{(N // n) / Ks:g}, x3 modes); cyclic Jacobi at order {ns} "
+                       f"scaled by (n/{ns})^3 (x3 modes); estimated full step {total:.1f} s"),
+            "est_seconds_per_step": total,
+            "parts_s": {"fill": t_fill, "gram": t_gram, "eig": t_eig, "ttm": t_ttm, "error": t_err}}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.n, args.r, budget_s=10.0)
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        cb = cpu_baseline(args.n, args.r, budget_s=10.0)
+        steps.append((time.perf_counter() - t, cb))
+    vals = [cb["value"] for _, cb in steps]
+    v = statistics.median(vals)
+    cb = steps[-1][1]
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * cb["est_seconds_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg5_{args.n}cube_matern_nu1.5_ell0.2", "grid": [args.n] * 3,
+                       "ranks": [args.r] * 3},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s_per_sampled_step": statistics.median([s for s, _ in steps])}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world, local)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
