@@ -14,6 +14,7 @@
 // Outputs are sorted descending (stable) and sign-fixed by rule R6: the first entry with
 // |u_i| >= max|u|/2 is made positive.  Everything is deterministic (fixed reduction orders).
 #include "common.cuh"
+#include "jacobi.cuh"
 #include "kernels.h"
 
 namespace tk {
@@ -42,125 +43,6 @@ __device__ __forceinline__ double hash_uniform(uint64_t idx) {  // SplitMix64 fi
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     z ^= z >> 31;
     return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
-}
-
-// ---------------------------------------------------------------------- shared-memory Jacobi
-// H (p x p, leading dim p) is diagonalised in place; Q (p x p) accumulates the rotations.
-// Parallel cyclic Jacobi, round-robin ordering, rotations of Golub & Van Loan Alg. 8.4.2.
-// Returns the sweep count (negative if the cap was hit).  All threads of the block call it.
-struct JacobiScratch {
-    int* arr;       // m players
-    int* pp;        // m/2
-    int* qq;        // m/2
-    double* cs;     // m/2
-    double* sn;     // m/2
-    int* flag;      // 1
-    double* red;    // >= 33
-};
-
-__device__ int jacobi_block(double* H, double* Q, int p, JacobiScratch js, int max_sweeps) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int m = p + (p & 1), half = m / 2;
-    const double eps = 2.220446049250313e-16;
-    for (int idx = tid; idx < p * p; idx += nt) Q[idx] = (idx / p == idx % p) ? 1.0 : 0.0;
-    __syncthreads();
-    int sweep = 0;
-    for (; sweep < max_sweeps; ++sweep) {
-        double dm = 0.0;
-        for (int i = tid; i < p; i += nt) dm = fmax(dm, fabs(H[i * p + i]));
-        // block max (reuse block_sum machinery with max): warp max then smem
-        dm = warp_max(dm);
-        if ((tid & 31) == 0) js.red[tid >> 5] = dm;
-        if (tid == 0) *js.flag = 0;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < (nt + 31) / 32; ++w) t = fmax(t, js.red[w]);
-            js.red[32] = t;
-        }
-        for (int t = tid; t < m; t += nt) js.arr[t] = t;
-        __syncthreads();
-        const double floor_abs = eps * js.red[32] / (double)p;
-        for (int step = 0; step < m - 1; ++step) {
-            for (int w = tid; w < half; w += nt) {
-                int a = js.arr[w], b = js.arr[m - 1 - w];
-                if (a > b) { int t = a; a = b; b = t; }
-                double c = 1.0, s = 0.0;
-                bool rot = false;
-                if (b < p) {
-                    const double apq = H[a * p + b], app = H[a * p + a], aqq = H[b * p + b];
-                    const double thr = fmax(eps * sqrt(fabs(app * aqq)), floor_abs);
-                    if (fabs(apq) > thr) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                                      : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        rot = true;
-                    }
-                }
-                js.pp[w] = rot ? a : -1;
-                js.qq[w] = b;
-                js.cs[w] = c;
-                js.sn[w] = s;
-                if (rot) *js.flag = 1;
-            }
-            __syncthreads();
-            for (int idx = tid; idx < half * p; idx += nt) {  // rows: H <- J^T H
-                const int w = idx / p, j = idx % p, a = js.pp[w];
-                if (a < 0) continue;
-                const int b = js.qq[w];
-                const double c = js.cs[w], s = js.sn[w];
-                const double x = H[a * p + j], y = H[b * p + j];
-                H[a * p + j] = c * x - s * y;
-                H[b * p + j] = s * x + c * y;
-            }
-            __syncthreads();
-            for (int idx = tid; idx < half * p; idx += nt) {  // cols: H <- H J, Q <- Q J
-                const int w = idx / p, i = idx % p, a = js.pp[w];
-                if (a < 0) continue;
-                const int b = js.qq[w];
-                const double c = js.cs[w], s = js.sn[w];
-                double x = H[i * p + a], y = H[i * p + b];
-                H[i * p + a] = c * x - s * y;
-                H[i * p + b] = s * x + c * y;
-                x = Q[i * p + a];
-                y = Q[i * p + b];
-                Q[i * p + a] = c * x - s * y;
-                Q[i * p + b] = s * x + c * y;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                for (int w = 0; w < half; ++w)
-                    if (js.pp[w] >= 0) {
-                        H[js.pp[w] * p + js.qq[w]] = 0.0;
-                        H[js.qq[w] * p + js.pp[w]] = 0.0;
-                    }
-                const int last = js.arr[m - 1];
-                for (int t = m - 1; t > 1; --t) js.arr[t] = js.arr[t - 1];
-                if (m > 1) js.arr[1] = last;
-            }
-            __syncthreads();
-        }
-        const int any = *js.flag;
-        __syncthreads();
-        if (!any) return sweep + 1;
-    }
-    return -sweep;
-}
-
-// Stable descending order of the diagonal: order[rank] = index.
-__device__ void sort_desc(const double* H, int p, int* order) {
-    for (int k = threadIdx.x; k < p; k += blockDim.x) {
-        const double v = H[k * p + k];
-        int rank = 0;
-        for (int j = 0; j < p; ++j) {
-            const double w = H[j * p + j];
-            rank += (w > v) || (w == v && j < k);
-        }
-        order[rank] = k;
-    }
-    __syncthreads();
 }
 
 // Sign rule R6 on column vector u (n entries, stride `ld` in elements) — whole block.
@@ -319,11 +201,11 @@ struct RRArgs {
 __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
     if (a.st->done) return;
     extern __shared__ double sm[];
-    const int p = a.p;
+    const int p = a.p, ld = jacobi_ld(p);
     const int64_t n = a.n;
     double* H = sm;
-    double* Q = H + p * p;
-    double* red = Q + p * p;          // 8*32 + 40
+    double* Q = H + p * ld;
+    double* red = Q + p * ld;          // 8*32 + 40
     double* h = red + 8 * 32 + 40;    // kMaxP
     double* cs = h + kMaxP;           // kMaxP/2 + 1
     double* sn = cs + kMaxP / 2 + 1;
@@ -345,13 +227,13 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
         double s = 0.0;
         for (int64_t i = lane; i < n; i += 32) s += a.Vt[(size_t)aa * n + i] * a.Wt[(size_t)bb * n + i];
         s = warp_sum(s);
-        if (lane == 0) { H[aa * p + bb] = s; H[bb * p + aa] = s; }
+        if (lane == 0) { H[aa * ld + bb] = s; H[bb * ld + aa] = s; }
     }
     __syncthreads();
     // 2. Jacobi
-    JacobiScratch js{arr, pp, qq, cs, sn, flag, red};
-    const int sweeps = jacobi_block(H, Q, p, js, 60);
-    sort_desc(H, p, order);
+    JacobiWork js{cs, sn, pp, qq, flag, red};
+    const int sweeps = jacobi_sym(H, Q, p, js, 60);
+    sort_desc_diag(H, p, order);
     // 3. VrT[k] = sum_a Q[a][order[k]] Vt[a],  YT[k] = sum_a Q[a][order[k]] Wt[a]
     for (int64_t i = tid; i < n; i += blockDim.x)
         for (int k0 = 0; k0 < p; k0 += 8) {
@@ -363,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
                     if (k0 + u < p) {
-                        const double qv = Q[aa * p + order[k0 + u]];
+                        const double qv = Q[aa * ld + order[k0 + u]];
                         av[u] = fma(qv, v, av[u]);
                         ay[u] = fma(qv, w, ay[u]);
                     }
@@ -378,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
     __syncthreads();
     // 4. residuals rho_k = ||Y_k - theta_k Vr_k|| for k < r
     for (int k = warp; k < a.r; k += nw) {
-        const double th = H[order[k] * p + order[k]];
+        const double th = H[order[k] * ld + order[k]];
         double s = 0.0;
         for (int64_t i = lane; i < n; i += 32) {
             const double d = a.YT[(size_t)k * n + i] - th * a.VrT[(size_t)k * n + i];
@@ -388,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
         if (lane == 0) res[k] = sqrt(s);
     }
     __syncthreads();
-    const double theta1 = H[order[0] * p + order[0]];
+    const double theta1 = H[order[0] * ld + order[0]];
     double rmax = 0.0;
     for (int k = 0; k < a.r; ++k) rmax = fmax(rmax, res[k]);
     const double rel = theta1 > 0.0 ? rmax / theta1 : 0.0;
@@ -404,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
             a.U[idx] = a.VrT[(size_t)k * n + i];
         }
         for (int k = tid; k < a.r; k += blockDim.x) {
-            const double th = H[order[k] * p + order[k]];
+            const double th = H[order[k] * ld + order[k]];
             if (a.lambda) a.lambda[k] = th;
             if (a.sigma) a.sigma[k] = sqrt(fmax(th, 0.0));
         }
@@ -428,8 +310,8 @@ __global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int
                                                      double* sigma, State* st) {
     extern __shared__ double sm[];
     double* H = sm;
-    double* Q = H + n * n;
-    double* red = Q + n * n;
+    double* Q = H + n * jacobi_ld(n);
+    double* red = Q + n * jacobi_ld(n);
     double* cs = red + 8 * 32 + 40;
     double* sn = cs + kDirectMax / 2 + 1;
     int* arr = reinterpret_cast<int*>(sn + kDirectMax / 2 + 1);
@@ -437,20 +319,21 @@ __global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int
     int* qq = pp + kDirectMax / 2 + 1;
     int* order = qq + kDirectMax / 2 + 1;
     int* flag = order + kDirectMax;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) H[idx] = G[idx];
+    const int ld = jacobi_ld(n);
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) H[(idx / n) * ld + idx % n] = G[idx];
     __syncthreads();
-    JacobiScratch js{arr, pp, qq, cs, sn, flag, red};
-    const int sweeps = jacobi_block(H, Q, n, js, 100);
-    sort_desc(H, n, order);
+    JacobiWork js{cs, sn, pp, qq, flag, red};
+    const int sweeps = jacobi_sym(H, Q, n, js, 100);
+    sort_desc_diag(H, n, order);
     // U (n x r) <- Q[:, order[k]], then sign rule per column (in place, stride r)
     for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
         const int i = idx / r, k = idx % r;
-        U[idx] = Q[i * n + order[k]];
+        U[idx] = Q[i * ld + order[k]];
     }
     __syncthreads();
     for (int k = 0; k < r; ++k) sign_fix_block(U + k, n, r, red);
     for (int k = threadIdx.x; k < r; k += blockDim.x) {
-        const double th = H[order[k] * n + order[k]];
+        const double th = H[order[k] * ld + order[k]];
         if (lambda) lambda[k] = th;
         if (sigma) sigma[k] = sqrt(fmax(th, 0.0));
     }
@@ -460,7 +343,7 @@ __global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int
         st->iters = 0;
         st->sweeps = sweeps > 0 ? sweeps : -sweeps;
         st->resid = 0.0;
-        st->lambda1 = H[order[0] * n + order[0]];
+        st->lambda1 = H[order[0] * ld + order[0]];
     }
 }
 
@@ -471,11 +354,11 @@ static int block_width(int64_t n, int r) {
 }
 
 static size_t rr_smem(int p) {
-    return (size_t)(2 * p * p + 8 * 32 + 40 + kMaxP + 2 * (kMaxP / 2 + 1) + kMaxP) * sizeof(double) +
+    return (size_t)(2 * p * jacobi_ld(p) + 8 * 32 + 40 + kMaxP + 2 * (kMaxP / 2 + 1) + kMaxP) * sizeof(double) +
            (size_t)(kMaxP + 2 + 2 * (kMaxP / 2 + 1) + kMaxP + 4) * sizeof(int);
 }
 static size_t direct_smem(int n) {
-    return (size_t)(2 * n * n + 8 * 32 + 40 + 2 * (kDirectMax / 2 + 1)) * sizeof(double) +
+    return (size_t)(2 * n * jacobi_ld(n) + 8 * 32 + 40 + 2 * (kDirectMax / 2 + 1)) * sizeof(double) +
            (size_t)(kDirectMax + 2 + 2 * (kDirectMax / 2 + 1) + kDirectMax + 4) * sizeof(int);
 }
 
@@ -509,6 +392,28 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
         TK_CUDA(cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_direct<<<1, kThreads, sm, st>>>(G, (int)n, r, U, lambda, sigma, dst);
         TK_CHECK_LAUNCH();
+    } else if (eig_cluster_supported(n)) {
+        // cluster path (n <= 2048): W = G V on many CTAs, Rayleigh–Ritz + CGS2 in one cluster
+        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
+        k_omega<<<64, 256, 0, st>>>(Vt, p, n);
+        TK_CHECK_LAUNCH();
+        k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
+        TK_CHECK_LAUNCH();
+        TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
+        int it = 0;
+        while (true) {
+            const int batch = it == 0 ? 4 : kBatch;
+            for (int b = 0; b < batch && it < kMaxIters; ++b, ++it) {
+                k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
+                TK_CHECK_LAUNCH();
+                TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst,
+                                        st));
+            }
+            State hs;
+            TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
+            TK_CUDA(cudaStreamSynchronize(st));
+            if (hs.done || it >= kMaxIters) break;
+        }
     } else {
         const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
         k_omega<<<64, 256, 0, st>>>(Vt, p, n);

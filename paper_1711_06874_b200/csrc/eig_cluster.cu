@@ -1,0 +1,452 @@
+// eig_cluster.cu — a-4 Rayleigh–Ritz + CGS2 step of the block subspace iteration, run by ONE
+// thread-block cluster whose CTAs each own 128 rows of the n x p basis.
+//
+// The HOSVD factor U_m is the top-r_m eigenbasis of G_m.  Per iteration (see eig.cu
+// for the driver loop):  W = G V (k_gemm_vg, many CTAs), then this kernel:
+//   H = V^T W            local 4x4-blocked partial sums over the CTA's rows, cluster-summed in
+//                        rank order through distributed shared memory (deterministic; every
+//                        CTA ends with the bitwise same H)
+//   H = Q Theta Q^T      parallel cyclic Jacobi (jacobi.cuh), redundantly in every CTA
+//   Vr = V Q, Y = W Q    in place, warp per row
+//   rho_k = ||Y_k - theta_k Vr_k||  (k < r), cluster-summed
+//   converged (rho_k <= 1e-14 theta_1 after >= 3 iterations) or last: sign rule R6 with two
+//                        cluster reductions (column max, then first index >= max/2), write U,
+//                        lambda, sigma
+//   else V <- CGS2(Y)    column by column, projections and norms cluster-summed
+// The basis never leaves shared memory inside an iteration; the only global traffic is loading
+// V, W (n x p each) and storing the next V.  A 16-CTA cluster covers n <= 2048.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "jacobi.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace tk {
+namespace eigc {
+
+constexpr int RB = 128;   // rows per CTA
+constexpr int P = 64;     // basis storage width (p <= 64)
+constexpr int NT = 512;   // threads per CTA
+constexpr int STG = 1088; // doubles per cluster-reduction stage buffer
+constexpr int kMinIters = 3;
+constexpr double kTol = 1e-14;
+
+// swizzled [RB][P] tile: conflict-free for both row-wise (fixed i) and column-wise (fixed j)
+// warp accesses
+__device__ __forceinline__ int sw(int i, int j) { return i * P + (j ^ (i & 15)); }
+
+struct Smem {
+    double H[P * (P + 1)];
+    double Q[P * (P + 1)];
+    double V[RB * P];
+    double Y[RB * P];
+    double stage[2][STG];
+    double red[64];
+    double theta[P];
+    double vec[P];    // h / residuals / column stats (cluster-reduced)
+    double tmp[16 * P];  // per-warp partials (16 warps x P)
+    double cs[P / 2], sn[P / 2];
+    int pa[P / 2], pb[P / 2];
+    int order[P];
+    int flag;
+};
+
+struct State {  // must match eig.cu
+    int done;
+    int iters;
+    int converged;
+    int sweeps;
+    double resid;
+    double lambda1;
+};
+
+struct Args {
+    int64_t n;
+    int p, r, it, last, orth_only;
+    double* Vt;        // p x n (in: V; out: next V)
+    const double* Wt;  // p x n  (G V, or G Omega when orth_only)
+    double* U;         // n x r
+    double* lambda;    // r (nullable)
+    double* sigma;     // r (nullable)
+    State* st;
+};
+
+enum { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2 };
+
+// Cluster all-reduce of `count` doubles from local smem `in` into local smem `out` (may alias).
+// Fixed rank order 0..C-1: deterministic and identical in every CTA.  Stage buffers alternate
+// by round so a buffer is rewritten only after the cluster barrier that follows its last remote
+// read.
+template <int OP>
+__device__ void cl_reduce(cg::cluster_group& cl, Smem& s, int& round, const double* in, double* out, int count) {
+    const unsigned C = cl.num_blocks();
+    for (int base = 0; base < count; base += STG) {
+        const int cnt = min(STG, count - base);
+        double* stg = s.stage[round & 1];
+        for (int x = threadIdx.x; x < cnt; x += blockDim.x) stg[x] = in[base + x];
+        cl.sync();
+        for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+            double v[16];  // independent DSMEM loads first, then the fixed-order combine
+#pragma unroll
+            for (int rk = 0; rk < 16; ++rk)
+                if (rk < (int)C) v[rk] = cl.map_shared_rank(stg, rk)[x];
+            double acc = v[0];
+#pragma unroll
+            for (int rk = 1; rk < 16; ++rk)
+                if (rk < (int)C) acc = OP == OP_SUM ? acc + v[rk] : OP == OP_MAX ? fmax(acc, v[rk]) : fmin(acc, v[rk]);
+            out[base + x] = acc;
+        }
+        ++round;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double hash_uniform(uint64_t idx) {  // SplitMix64 finaliser -> [-1,1)
+    uint64_t z = idx * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// Per-column partial sums over the CTA's rows: out[j] = sum_i f(i, j) for j < ncol, in a fixed
+// order (8 row groups of 16, then groups in order).
+template <typename Fn>
+__device__ __forceinline__ void col_partials(Smem& s, int nrows, int ncol, double* out, Fn f) {
+    const int t = threadIdx.x, j = t & (P - 1), part = t >> 6;  // 8 parts
+    double acc = 0.0;
+    if (j < ncol)
+        for (int i = part * 16; i < min(nrows, part * 16 + 16); ++i) acc += f(i, j);
+    s.tmp[part * P + j] = acc;
+    __syncthreads();
+    if (t < ncol) {
+        double a = s.tmp[t];
+        for (int q = 1; q < 8; ++q) a += s.tmp[q * P + t];
+        out[t] = a;
+    }
+    __syncthreads();
+}
+
+// Cluster sum of the per-warp partials tmp[w][0..cnt) (16 warps) into vec[0..cnt): warps summed
+// in order into the stage buffer, then the CTAs in rank order.  Deterministic, identical in every
+// CTA; one cluster barrier.
+__device__ __forceinline__ void warp_partials_cluster_sum(cg::cluster_group& cl, Smem& s, int& round, int cnt) {
+    const unsigned C = cl.num_blocks();
+    double* stg = s.stage[round & 1];
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+        double a = s.tmp[threadIdx.x];
+        for (int w = 1; w < NT / 32; ++w) a += s.tmp[w * P + threadIdx.x];
+        stg[threadIdx.x] = a;
+    }
+    cl.sync();
+    if (threadIdx.x < cnt) {
+        double v[16];
+#pragma unroll
+        for (int rk = 0; rk < 16; ++rk)
+            if (rk < (int)C) v[rk] = cl.map_shared_rank(stg, rk)[threadIdx.x];
+        double acc = v[0];
+#pragma unroll
+        for (int rk = 1; rk < 16; ++rk)
+            if (rk < (int)C) acc += v[rk];
+        s.vec[threadIdx.x] = acc;
+    }
+    ++round;
+    __syncthreads();
+}
+
+// CGS2 of the p columns of Y (in place) over the cluster's distributed rows.  Warp w owns rows
+// 8w..8w+7 for the projections; 4 lanes per row apply the update.
+__device__ void cgs2_cluster(cg::cluster_group& cl, Smem& s, int& round, int p, int nrows, int64_t i0) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int r0 = warp * 8, r1 = min(nrows, r0 + 8);
+    for (int k = 0; k < p; ++k) {
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            for (int pass = 0; pass < 2 && k > 0; ++pass) {
+                __syncwarp();  // the same warp updated these rows in the previous pass
+                double a0 = 0.0, a1 = 0.0;
+                for (int i = r0; i < r1; ++i) {
+                    const double yk = s.Y[sw(i, k)];
+                    a0 = fma(s.Y[sw(i, lane)], yk, a0);
+                    a1 = fma(s.Y[sw(i, lane + 32)], yk, a1);
+                }
+                s.tmp[warp * P + lane] = a0;
+                s.tmp[warp * P + lane + 32] = a1;
+                warp_partials_cluster_sum(cl, s, round, k);
+                {   // y_i -= sum_j h_j Y[i][j]: 4 lanes per row, j interleaved, fixed combine order
+                    const int i = t >> 2, qd = t & 3;
+                    double acc = 0.0;
+                    if (i < nrows)
+                        for (int j = qd; j < k; j += 4) acc = fma(s.vec[j], s.Y[sw(i, j)], acc);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    if (i < nrows && qd == 0) s.Y[sw(i, k)] -= acc;
+                }
+            }
+            // norm of column k (rows r0..r1 of each warp, lane-strided)
+            __syncthreads();
+            double ss = 0.0;
+            if (lane < 8 && r0 + lane < r1) {
+                const double y = s.Y[sw(r0 + lane, k)];
+                ss = y * y;
+            }
+            ss = warp_sum(ss);
+            if (lane == 0) s.tmp[warp * P] = ss;
+            warp_partials_cluster_sum(cl, s, round, 1);
+            const double tot = s.vec[0];
+            if (tot > 1e-280) {
+                const double inv = 1.0 / sqrt(tot);
+                if (t < nrows) s.Y[sw(t, k)] *= inv;
+                __syncthreads();
+                break;
+            }
+            // exactly dependent column: deterministic pseudo-random replacement, retry
+            if (t < nrows) s.Y[sw(t, k)] = hash_uniform(0x5eedull * (k + 1) + (uint64_t)(i0 + t));
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_rr_cluster(Args a) {
+    cg::cluster_group cl = cg::this_cluster();
+    if (a.st->done) return;  // uniform across the cluster (written by an earlier launch)
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);  // (no integer casts: keeps LDS/STS addressing)
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int p = a.p, ld = jacobi_ld(p);
+    const int64_t n = a.n;
+    const int64_t i0 = (int64_t)cl.block_rank() * RB;
+    const int64_t rem = n - i0;
+    const int nrows = rem <= 0 ? 0 : (rem >= RB ? RB : (int)rem);
+    int round = 0;
+
+    // load V (unless orth_only) and W rows; zero padding
+    for (int e = t; e < RB * P; e += NT) {
+        const int j = e / RB, i = e % RB;
+        const bool ok = i < nrows && j < p;
+        s.Y[sw(i, j)] = ok ? a.Wt[(size_t)j * n + i0 + i] : 0.0;
+        if (!a.orth_only) s.V[sw(i, j)] = ok ? a.Vt[(size_t)j * n + i0 + i] : 0.0;
+    }
+    __syncthreads();
+
+    if (!a.orth_only) {
+        // 1. H = V^T W: lower-triangular 4x4 blocks (bi >= bj), 136 blocks, packed 16 per block
+        double* hp = s.Q;  // scratch (2176 doubles)
+        if (t < 136) {
+            int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+            while (bi * (bi + 1) / 2 > t) --bi;
+            const int bj = t - bi * (bi + 1) / 2;
+            double acc[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+            for (int i = 0; i < nrows; ++i) {
+                double va[4], wb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) va[u] = s.V[sw(i, 4 * bi + u)];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) wb[v] = s.Y[sw(i, 4 * bj + v)];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(va[u], wb[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) hp[t * 16 + u * 4 + v] = acc[u][v];
+        }
+        __syncthreads();
+        cl_reduce<OP_SUM>(cl, s, round, hp, hp, 136 * 16);
+        for (int e = t; e < 136 * 16; e += NT) {
+            const int blk = e >> 4, u = (e >> 2) & 3, v = e & 3;
+            int bi = (int)((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
+            while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
+            while (bi * (bi + 1) / 2 > blk) --bi;
+            const int bj = blk - bi * (bi + 1) / 2;
+            const int ra = 4 * bi + u, cb = 4 * bj + v;
+            if (ra < p && cb < p && ra >= cb) {
+                s.H[ra * ld + cb] = hp[e];
+                s.H[cb * ld + ra] = hp[e];
+            }
+        }
+        // 2. Jacobi (redundant per CTA, bitwise identical)
+        __syncthreads();
+        JacobiWork js{s.cs, s.sn, s.pa, s.pb, &s.flag, s.red};
+        const int sweeps = jacobi_sym(s.H, s.Q, p, js, 60);
+        sort_desc_diag(s.H, p, s.order);
+        for (int k = t; k < p; k += NT) s.theta[k] = s.H[s.order[k] * ld + s.order[k]];
+        __syncthreads();
+        // Qs[a][k] = Q[a][order[k]] into H (P-wide rows)
+        for (int e = t; e < P * P; e += NT) {
+            const int aa = e / P, k = e % P;
+            s.H[e] = (aa < p && k < p) ? s.Q[aa * ld + s.order[k]] : 0.0;
+        }
+        __syncthreads();
+        // 3. Vr = V Qs, Y = W Qs (warp per row, in place)
+        for (int i = warp; i < nrows; i += NT / 32) {
+            double v0 = 0.0, v1 = 0.0, y0 = 0.0, y1 = 0.0;
+            for (int aa = 0; aa < p; ++aa) {
+                const double va = s.V[sw(i, aa)], wa = s.Y[sw(i, aa)];
+                const double q0 = s.H[aa * P + lane], q1 = s.H[aa * P + lane + 32];
+                v0 = fma(va, q0, v0);
+                v1 = fma(va, q1, v1);
+                y0 = fma(wa, q0, y0);
+                y1 = fma(wa, q1, y1);
+            }
+            __syncwarp();
+            s.V[sw(i, lane)] = v0;
+            s.V[sw(i, lane + 32)] = v1;
+            s.Y[sw(i, lane)] = y0;
+            s.Y[sw(i, lane + 32)] = y1;
+        }
+        __syncthreads();
+        // 4. residuals
+        col_partials(s, nrows, a.r, s.vec, [&](int i, int k) {
+            const double d = s.Y[sw(i, k)] - s.theta[k] * s.V[sw(i, k)];
+            return d * d;
+        });
+        cl_reduce<OP_SUM>(cl, s, round, s.vec, s.vec, a.r);
+        const double theta1 = s.theta[0];
+        double rmax = 0.0;
+        for (int k = 0; k < a.r; ++k) rmax = fmax(rmax, sqrt(s.vec[k]));
+        const double rel = theta1 > 0.0 ? rmax / theta1 : 0.0;
+        const bool conv = (a.it + 1 >= kMinIters) && (rel <= kTol);
+        if (conv || a.last) {
+            // 5. sign rule R6 per column: max |u| (cluster max), then the first global index with
+            //    |u_i| >= max/2 (cluster min of 2 i + [u_i < 0])
+            if (t < a.r) {
+                double mx = 0.0;
+                for (int i = 0; i < nrows; ++i) mx = fmax(mx, fabs(s.V[sw(i, t)]));
+                s.vec[t] = mx;
+            }
+            __syncthreads();
+            cl_reduce<OP_MAX>(cl, s, round, s.vec, s.vec, a.r);
+            if (t < a.r) {
+                const double half = 0.5 * s.vec[t];
+                double code = 1e300;
+                for (int i = 0; i < nrows; ++i) {
+                    const double v = s.V[sw(i, t)];
+                    if (fabs(v) >= half) {
+                        code = 2.0 * (double)(i0 + i) + (v < 0.0 ? 1.0 : 0.0);
+                        break;
+                    }
+                }
+                s.tmp[t] = code;
+            }
+            __syncthreads();
+            cl_reduce<OP_MIN>(cl, s, round, s.tmp, s.tmp, a.r);
+            for (int e = t; e < nrows * a.r; e += NT) {
+                const int i = e / a.r, k = e % a.r;
+                const double code = s.tmp[k];
+                const bool flip = code < 1e299 && fmod(code, 2.0) == 1.0;
+                const double v = s.V[sw(i, k)];
+                a.U[(size_t)(i0 + i) * a.r + k] = flip ? -v : v;
+            }
+            if (cl.block_rank() == 0) {
+                for (int k = t; k < a.r; k += NT) {
+                    const double th = s.theta[k];
+                    if (a.lambda) a.lambda[k] = th;
+                    if (a.sigma) a.sigma[k] = sqrt(fmax(th, 0.0));
+                }
+                if (t == 0) {
+                    a.st->done = 1;
+                    a.st->converged = conv ? 1 : 0;
+                    a.st->iters = a.it + 1;
+                    a.st->sweeps = sweeps;
+                    a.st->resid = rel;
+                    a.st->lambda1 = theta1;
+                }
+            }
+            cl.sync();  // keep every CTA's shared memory alive until remote reads are done
+            return;
+        }
+        if (cl.block_rank() == 0 && t == 0) {
+            a.st->iters = a.it + 1;
+            a.st->resid = rel;
+            a.st->sweeps = sweeps;
+        }
+    }
+    // 6. next basis V = CGS2(Y)
+    cgs2_cluster(cl, s, round, p, nrows, i0);
+    for (int e = t; e < p * RB; e += NT) {
+        const int j = e / RB, i = e % RB;
+        if (i < nrows) a.Vt[(size_t)j * n + i0 + i] = s.Y[sw(i, j)];
+    }
+    cl.sync();
+}
+
+}  // namespace eigc
+
+// Cluster size for n rows (power of two, <= 16), or 0 when n is out of range.
+int eig_cluster_size(int64_t n) {
+    const int64_t c = ceil_div(n, eigc::RB);
+    if (c > 16) return 0;
+    int cs = 1;
+    while (cs < c) cs <<= 1;
+    return cs;
+}
+
+size_t eig_cluster_smem() { return sizeof(eigc::Smem); }
+
+// Launch one Rayleigh–Ritz(+CGS2) step (orth_only = 1: CGS2 of Wt only).  Returns false if the
+// cluster cannot be scheduled (caller falls back to the single-CTA path).
+bool eig_cluster_supported(int64_t n) {
+    const int cs = eig_cluster_size(n);
+    if (cs == 0) return false;
+    static int ok16 = -1;
+    if (cudaFuncSetAttribute(eigc::k_rr_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)eig_cluster_smem()) != cudaSuccess)
+        return false;
+    if (cs > 8) {
+        if (ok16 < 0) {
+            ok16 = cudaFuncSetAttribute(eigc::k_rr_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                   cudaSuccess;
+            if (ok16) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(cs);
+                cfg.blockDim = dim3(eigc::NT);
+                cfg.dynamicSmemBytes = eig_cluster_smem();
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = cs;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int nc = 0;
+                ok16 = cudaOccupancyMaxActiveClusters(&nc, eigc::k_rr_cluster, &cfg) == cudaSuccess && nc > 0;
+            }
+            cudaGetLastError();
+        }
+        return ok16 == 1;
+    }
+    return true;
+}
+
+int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
+                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st) {
+    const int cs = eig_cluster_size(n);
+    eigc::Args a{n, p, r, it, last, orth_only, Vt, Wt, U, lambda, sigma, static_cast<eigc::State*>(state)};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(eigc::NT);
+    cfg.dynamicSmemBytes = eig_cluster_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TK_CUDA(cudaLaunchKernelEx(&cfg, eigc::k_rr_cluster, a));
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+}  // namespace tk

@@ -28,6 +28,11 @@ size_t eig_ws_bytes(int64_t n, int r);
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma,
                void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot);
 
+// Cluster Rayleigh–Ritz step (eig_cluster.cu); n <= 2048.
+bool eig_cluster_supported(int64_t n);
+int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
+                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st);
+
 // Core beta = F x1 U1^T x2 U2^T x3 U3^T.
 size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,
