@@ -72,6 +72,10 @@ __device__ __forceinline__ void lds128(double& x, double& y, const double* p) {
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(smem_u32(p)));
 }
 
+__device__ __forceinline__ void lds128_u32(double& x, double& y, uint32_t addr) {
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
 // 128-byte swizzle (CU_TENSOR_MAP_SWIZZLE_128B): inside every 1024-byte-aligned group of eight
 // 128-byte lines, the 16-byte chunk index of line L is XOR-ed with (L & 7).  Tiles are stored as
 // lines of 16 doubles; element (line, col) lives at double offset swz(line, col).

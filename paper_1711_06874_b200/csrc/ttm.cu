@@ -11,6 +11,8 @@
 //   Ft[(i,j),k] = sum_c W[(i,j),c] U3[k,c] on DMMA tiles, fused with the streaming read of F and
 //   the per-CTA sums of (F - Ft)^2 and F^2; a single-CTA pass adds the CTA partials in index order.
 //   No float atomics: the result is bitwise reproducible.
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,163 +73,310 @@ int launch_small_gemm(const SmallGemm& p, cudaStream_t st) {
     return TUCKER_OK;
 }
 
-// ------------------------------------------------------------------------------------ TTM1
-// C (M x R) = A (M x K) * B^T, B (R x K) row-major; R <= 64.  CTA: 8 warps x 32 rows = 256 rows,
-// warp tile 32 x RP (RP = R rounded up to 8).  Stage = 16 k: A tile [256 lines][16], B tile
-// [64 lines][16], swizzled.  K-major fragments with k = 4q + s (see gram.cu).
+// ------------------------------------------------------------------------------- TTM1 + TTM2
+// Fused first two mode products over one slab F[i,:,:] (n2 x n3) per CTA row-tile:
+//   T1 tile (256 rows j x R) = F[i, j0:j0+256, :] U3            DMMA, streams F once
+//   P[b][c] = sum_{j in tile} U2[j][b] T1[j][c]                  DMMA epilogue (T1 stays on chip)
+// grid = (JT = ceil(n2/256), n1).  With JT = 1 the CTA writes T2[i] directly, otherwise P goes to
+// part[i][jt] and k_t2_reduce adds the JT partials in index order (deterministic).
+// Mainloop: 8 MMA warps x 32 rows, warp tile 32 x RP (RP = R rounded up to 8); stage = 16 k.
+// A tile [256 lines][16] arrives by TMA (3-D map over F, rows past n2 zero-filled, SWIZZLE_128B);
+// the B tile [RP lines][16] is a contiguous block of U3 pre-packed once per call in the same
+// swizzled layout and arrives by one cp.async.bulk; a 5-stage mbarrier ring, thread 0 producing.
+// Odd n3 (no TMA-legal stride) uses a cp.async variant of the same mainloop.
 namespace ttm1 {
-constexpr int BMR = 256, BK = 16, STAGES = 4;
-constexpr int ATILE = BMR * BK, BTILE = 64 * BK;
+constexpr int BMR = 256, BK = 16, STAGES = 5, STAGES_C = 4;
+constexpr int ATILE = BMR * BK;
 
-template <int NI>
-__device__ __forceinline__ void load_stage(const double* __restrict__ A, const double* __restrict__ B,
-                                           int64_t M, int64_t K, int R, int64_t m0, int64_t k0,
-                                           double* dA, double* dB, bool vec) {
-    const int tid = threadIdx.x;
-    if (vec) {  // 16-byte copies (row stride and base 16-B aligned)
-#pragma unroll
-        for (int u = 0; u < ATILE / 2 / 256; ++u) {
-            const int e = tid + 256 * u, line = e >> 3, ch = e & 7;
-            const int64_t m = m0 + line, k = k0 + 2 * ch;
-            const bool ok = (m < M) && (k < K);
-            const double* src = ok ? A + m * K + k : A;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dA + swz_chunk(line, ch))),
-                         "l"(src), "r"(ok ? 16 : 0)
-                         : "memory");
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < ATILE / 256; ++u) {
-            const int e = tid + 256 * u, line = e >> 4, col = e & 15;
-            const int64_t m = m0 + line, k = k0 + col;
-            const bool ok = (m < M) && (k < K);
-            cp_async8(dA + swz(line, col), ok ? A + m * K + k : A, ok);
-        }
-    }
-    for (int e = tid; e < NI * 8 * BK; e += 256) {
-        const int line = e >> 4, col = e & 15;
-        const int64_t k = k0 + col;
-        const bool ok = (line < R) && (k < K);
-        cp_async8(dB + swz(line, col), ok ? B + (int64_t)line * K + k : B, ok);
+struct Args12 {
+    const double* F;   // n1 x n2 x n3
+    const double* Bp;  // packed U3: [nkb][RP][16] swizzled
+    const double* U2;  // n2 x r2
+    double* out;       // JT == 1: T2 (n1 x r2 x R); else part (n1 x JT x r2 x R)
+    int64_t n2, n3;
+    int R, r2, JT;
+};
+
+// Bp[kb][c][kk] (swizzled) = U3[16 kb + kk][c]   (0 outside c < R, k < n3)
+__global__ void k_pack_u3(const double* __restrict__ U3, int64_t n3, int R, int RP, double* __restrict__ Bp) {
+    const int64_t nkb = ceil_div(n3, BK), tot = nkb * RP * BK;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t kb = t / (RP * BK);
+        const int rem = (int)(t % (RP * BK)), line = rem >> 4, col = rem & 15;
+        const int64_t k = kb * BK + col;
+        Bp[kb * RP * BK + swz(line, col)] = (line < R && k < n3) ? U3[k * R + line] : 0.0;
     }
 }
 
 template <int NI>
-__global__ void __launch_bounds__(256) k_ttm1(const double* __restrict__ A, const double* __restrict__ B,
-                                              double* __restrict__ C, int64_t M, int64_t K, int R, bool vec) {
-    extern __shared__ uint8_t smem_raw[];
-    double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    double* sA = smem;
-    double* sB = smem + STAGES * ATILE;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r = lane >> 2, q = lane & 3;
-    const int64_t m0 = (int64_t)blockIdx.x * BMR;
+__device__ __forceinline__ void mma_stage(const double* tA, const double* tB, double (&acc)[4][NI][2], int warp,
+                                          int r, int q) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double a[4][2], b[NI][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) lds128(a[mi][0], a[mi][1], tA + swz_chunk(warp * 32 + mi * 8 + r, 2 * q + h));
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) lds128(b[ni][0], b[ni][1], tB + swz_chunk(ni * 8 + r, 2 * q + h));
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi][s], b[ni][s]);
+    }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int NI, bool TMA>
+__global__ void __launch_bounds__(256, 1) k_ttm12(const __grid_constant__ CUtensorMap mapA, const Args12 g) {
+    constexpr int RP = NI * 8, BTILE = RP * BK;
+    constexpr uint32_t ABYTES = ATILE * 8, BBYTES = BTILE * 8;
+    constexpr int NS = TMA ? STAGES : STAGES_C;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    double* sA = reinterpret_cast<double*>(smem_raw);
+    double* sB = sA + NS * ATILE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * BTILE);
+    uint64_t* empty = full + NS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, q = lane & 3;
+    const int64_t i = blockIdx.y;
+    const int jt = blockIdx.x;
+    const int64_t m0 = (int64_t)jt * BMR, M = g.n2, K = g.n3;
+    const int R = g.R;
     const int64_t nkb = ceil_div(K, BK);
     double acc[4][NI][2];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nkb) load_stage<NI>(A, B, M, K, R, m0, s * BK, sA + s * ATILE, sB + s * BTILE, vec);
-        cp_async_commit();
-    }
-    for (int64_t kb = 0; kb < nkb; ++kb) {
-        cp_async_wait<STAGES - 2>();
+
+    if (TMA) {
+        if (tid == 0) {
+            for (int s = 0; s < NS; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], 8);
+            }
+            mbar_fence_init();
+        }
         __syncthreads();
-        const int stg = (int)(kb % STAGES);
-        const double* tA = sA + stg * ATILE;
-        const double* tB = sB + stg * BTILE;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double a[4][2], b[NI][2];
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi) lds128(a[mi][0], a[mi][1], tA + swz_chunk(warp * 32 + mi * 8 + r, 2 * q + h));
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) lds128(b[ni][0], b[ni][1], tB + swz_chunk(ni * 8 + r, 2 * q + h));
-#pragma unroll
-            for (int s = 0; s < 2; ++s)
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-                    for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi][s], b[ni][s]);
+        auto issue = [&](int slot, int64_t kb) {
+            mbar_arrive_expect_tx(&full[slot], ABYTES + BBYTES);
+            tma_load_3d(sA + slot * ATILE, &mapA, &full[slot], (int)(kb * BK), (int)m0, (int)i);
+            bulk_g2s(sB + slot * BTILE, g.Bp + kb * BTILE, BBYTES, &full[slot]);
+        };
+        if (tid == 0) {
+            tma_prefetch_desc(&mapA);
+            for (int s = 0; s < NS && s < nkb; ++s) issue(s, s);
         }
-        const int64_t nxt = kb + STAGES - 1;
-        if (nxt < nkb) {
-            const int ns = (int)(nxt % STAGES);
-            load_stage<NI>(A, B, M, K, R, m0, nxt * BK, sA + ns * ATILE, sB + ns * BTILE, vec);
+        for (int64_t kb = 0; kb < nkb; ++kb) {
+            if (tid == 0 && kb > 0) {
+                const int64_t prev = kb - 1, nk = prev + NS;
+                if (nk < nkb) {
+                    const int ps = (int)(prev % NS);
+                    mbar_wait(&empty[ps], (uint32_t)((prev / NS) & 1));
+                    issue(ps, nk);
+                }
+            }
+            const int stg = (int)(kb % NS);
+            mbar_wait(&full[stg], (uint32_t)((kb / NS) & 1));
+            mma_stage<NI>(sA + stg * ATILE, sB + stg * BTILE, acc, warp, r, q);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+        __syncthreads();  // all MMA reads done before the epilogue reuses the ring
+    } else {
+        const double* A = g.F + i * g.n2 * g.n3;
+        auto load = [&](int slot, int64_t kb) {
+            double* dA = sA + slot * ATILE;
+#pragma unroll
+            for (int u = 0; u < ATILE / 256; ++u) {
+                const int e = tid + 256 * u, line = e >> 4, col = e & 15;
+                const int64_t m = m0 + line, k = kb * BK + col;
+                const bool ok = (m < M) && (k < K);
+                cp_async8(dA + swz(line, col), ok ? A + m * K + k : A, ok);
+            }
+            const double* src = g.Bp + kb * BTILE;
+            double* dB = sB + slot * BTILE;
+            for (int e = tid; e < BTILE / 2; e += 256)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dB + 2 * e)), "l"(src + 2 * e)
+                             : "memory");
+        };
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s) {
+            if (s < nkb) load(s, s);
+            cp_async_commit();
+        }
+        for (int64_t kb = 0; kb < nkb; ++kb) {
+            cp_async_wait<NS - 2>();
+            __syncthreads();
+            const int stg = (int)(kb % NS);
+            mma_stage<NI>(sA + stg * ATILE, sB + stg * BTILE, acc, warp, r, q);
+            const int64_t nxt = kb + NS - 1;
+            if (nxt < nkb) load((int)(nxt % NS), nxt);
+            cp_async_commit();
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+
+    // Epilogue on DMMA: P (r2 x R) = U2[m0:m0+256]^T T1_tile, rows in chunks of CH; leading
+    // dimensions = 4 (mod 16) doubles make the fragment loads conflict-free (per half-warp).
+    const int r2 = g.r2, r2p = (r2 + 7) & ~7;
+    const int ldt = RP + ((4 - RP % 16) + 16) % 16, ldu = r2p + ((4 - r2p % 16) + 16) % 16;
+    const int ring = NS * (ATILE + BTILE);
+    const int CH = (BMR * (ldt + ldu) <= ring) ? BMR : (BMR / 2 * (ldt + ldu) <= ring ? BMR / 2 : BMR / 4);
+    double* sT = sA;               // [CH][ldt]
+    double* sU = sA + CH * ldt;    // [CH][ldu], zero-padded to r2p columns
+    const int tb = r2p / 8, ntile = tb * NI;
+    double pacc[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pacc[u][0] = pacc[u][1] = 0.0;
+    for (int c0 = 0; c0 < BMR; c0 += CH) {
+        for (int e = tid; e < CH * r2p; e += 256) {
+            const int row = e / r2p, b = e - row * r2p;
+            const int64_t j = m0 + c0 + row;
+            const bool ok = (j < M && b < r2);
+            cp_async8(sU + row * ldu + b, ok ? g.U2 + j * r2 + b : g.U2, ok);
         }
         cp_async_commit();
-    }
-    cp_async_wait<0>();
+        if (warp * 32 >= c0 && warp * 32 < c0 + CH) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-            const int64_t row = m0 + warp * 32 + mi * 8 + r;
-            const int col = ni * 8 + 2 * q;
-            if (row < M) {
-                if (col < R) C[row * R + col] = acc[mi][ni][0];
-                if (col + 1 < R) C[row * R + col + 1] = acc[mi][ni][1];
+                for (int ni = 0; ni < NI; ++ni) {
+                    const int row = warp * 32 + mi * 8 + r - c0, col = ni * 8 + 2 * q;
+                    sT[row * ldt + col] = acc[mi][ni][0];
+                    sT[row * ldt + col + 1] = acc[mi][ni][1];
+                }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = warp + 8 * u;
+            if (t < ntile) {
+                const int b0 = (t / NI) * 8, cc0 = (t % NI) * 8;
+                const double* pa = sU + q * ldu + b0 + r;
+                const double* pb = sT + q * ldt + cc0 + r;
+#pragma unroll 4
+                for (int k = 0; k < CH; k += 4) dmma(pacc[u], pa[k * ldu], pb[k * ldt]);
             }
         }
+        __syncthreads();
+    }
+    double* dst = g.out + ((size_t)i * g.JT + jt) * (size_t)(r2 * R);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int t = warp + 8 * u;
+        if (t < ntile) {
+            const int b = (t / NI) * 8 + r, c = (t % NI) * 8 + 2 * q;
+            if (b < r2) {
+                if (c < R) dst[b * R + c] = pacc[u][0];
+                if (c + 1 < R) dst[b * R + c + 1] = pacc[u][1];
+            }
+        }
+    }
 }
 
-static size_t smem_bytes() { return (size_t)STAGES * (ATILE + BTILE) * 8 + 1024; }
+template <int NI, bool TMA>
+size_t smem_bytes() {
+    constexpr int NS = TMA ? STAGES : STAGES_C;
+    return (size_t)NS * (ATILE + NI * 8 * BK) * 8 + 2 * NS * 8;
+}
 }  // namespace ttm1
 
+// T2[i][o] = sum_jt part[i][jt][o] in index order.
+__global__ void k_t2_reduce(const double* __restrict__ part, int JT, int64_t nout, int64_t total,
+                            double* __restrict__ T2) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / nout, o = t % nout;
+        const double* p = part + i * JT * nout + o;
+        double s = p[0];
+        for (int j = 1; j < JT; ++j) s += p[(int64_t)j * nout];
+        T2[t] = s;
+    }
+}
+
 template <int NI>
-static int run_ttm1(const double* A, const double* B, double* C, int64_t M, int64_t K, int R, cudaStream_t st) {
-    const size_t sm = ttm1::smem_bytes();
-    TK_CUDA(cudaFuncSetAttribute(ttm1::k_ttm1<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const bool vec = (K % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-    ttm1::k_ttm1<NI><<<(unsigned)ceil_div(M, ttm1::BMR), 256, sm, st>>>(A, B, C, M, K, R, vec);
+static int run_ttm12(const ttm1::Args12& a, int64_t n1, cudaStream_t st) {
+    const bool tma = (a.n3 % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.F) & 15) == 0) && a.n3 >= ttm1::BK;
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (tma) {
+        uint64_t dims[3] = {(uint64_t)a.n3, (uint64_t)a.n2, (uint64_t)n1};
+        uint64_t strides[2] = {(uint64_t)(a.n3 * 8), (uint64_t)(a.n2 * a.n3 * 8)};
+        uint32_t box[3] = {ttm1::BK, ttm1::BMR, 1};
+        if (!make_tmap_f64(&map, a.F, 3, dims, strides, box)) return TUCKER_ERR_CUDA;
+        const size_t sm = ttm1::smem_bytes<NI, true>();
+        TK_CUDA(cudaFuncSetAttribute(ttm1::k_ttm12<NI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        ttm1::k_ttm12<NI, true><<<dim3((unsigned)a.JT, (unsigned)n1), 256, sm, st>>>(map, a);
+    } else {
+        const size_t sm = ttm1::smem_bytes<NI, false>();
+        TK_CUDA(cudaFuncSetAttribute(ttm1::k_ttm12<NI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        ttm1::k_ttm12<NI, false><<<dim3((unsigned)a.JT, (unsigned)n1), 256, sm, st>>>(map, a);
+    }
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
 
-// C (M x R) = A (M x K) * B^T with B = R x K row-major.
-static int launch_ttm1(const double* A, const double* B, double* C, int64_t M, int64_t K, int R, cudaStream_t st) {
-    switch ((R + 7) / 8) {
-        case 1: return run_ttm1<1>(A, B, C, M, K, R, st);
-        case 2: return run_ttm1<2>(A, B, C, M, K, R, st);
-        case 3: return run_ttm1<3>(A, B, C, M, K, R, st);
-        case 4: return run_ttm1<4>(A, B, C, M, K, R, st);
-        case 5: return run_ttm1<5>(A, B, C, M, K, R, st);
-        case 6: return run_ttm1<6>(A, B, C, M, K, R, st);
-        case 7: return run_ttm1<7>(A, B, C, M, K, R, st);
-        case 8: return run_ttm1<8>(A, B, C, M, K, R, st);
+static int launch_ttm12(const ttm1::Args12& a, int64_t n1, cudaStream_t st) {
+    switch ((a.R + 7) / 8) {
+        case 1: return run_ttm12<1>(a, n1, st);
+        case 2: return run_ttm12<2>(a, n1, st);
+        case 3: return run_ttm12<3>(a, n1, st);
+        case 4: return run_ttm12<4>(a, n1, st);
+        case 5: return run_ttm12<5>(a, n1, st);
+        case 6: return run_ttm12<6>(a, n1, st);
+        case 7: return run_ttm12<7>(a, n1, st);
+        case 8: return run_ttm12<8>(a, n1, st);
         default: return TUCKER_ERR_UNSUPPORTED;
     }
 }
 
-__global__ void k_transpose(const double* __restrict__ U, double* __restrict__ UT, int64_t n, int r) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * r; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / r;
-        const int c = (int)(t % r);
-        UT[(int64_t)c * n + i] = U[t];
-    }
+
+static int64_t ttm_jt(const int64_t n[3]) { return ceil_div(n[1], ttm1::BMR); }
+
+static size_t packed_u3_bytes(const int64_t n[3], int R) {
+    return (size_t)ceil_div(n[2], ttm1::BK) * (size_t)(((R + 7) / 8) * 8) * ttm1::BK * 8;
 }
 
 size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]) {
-    return align_up((size_t)n[0] * n[1] * r[2] * 8, 256) + align_up((size_t)n[0] * r[1] * r[2] * 8, 256) +
-           align_up((size_t)n[2] * r[2] * 8, 256);
+    const int64_t JT = ttm_jt(n);
+    const size_t t2 = (size_t)n[0] * r[1] * r[2] * 8;
+    return align_up(JT > 1 ? JT * t2 : 0, 256) + align_up(t2, 256) + align_up(packed_u3_bytes(n, r[2]), 256);
 }
 
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                     const double* U3, double* core, void* ws, size_t ws_bytes, cudaStream_t st) {
     if (ws_bytes < ttm_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
+    if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    const int64_t JT = ttm_jt(n);
+    const size_t t2b = (size_t)n[0] * r[1] * r[2] * 8;
     char* w = static_cast<char*>(ws);
-    double* T1 = reinterpret_cast<double*>(w);
-    w += align_up((size_t)n[0] * n[1] * r[2] * 8, 256);
+    double* part = reinterpret_cast<double*>(w);
+    w += align_up(JT > 1 ? JT * t2b : 0, 256);
     double* T2 = reinterpret_cast<double*>(w);
-    w += align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
-    double* UT3 = reinterpret_cast<double*>(w);
-    k_transpose<<<64, 256, 0, st>>>(U3, UT3, n[2], r[2]);
+    w += align_up(t2b, 256);
+    double* Bp = reinterpret_cast<double*>(w);
+    const int RP = ((r[2] + 7) / 8) * 8;
+    ttm1::k_pack_u3<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(n[2], ttm1::BK) * RP * ttm1::BK, 256), 1024), 256, 0,
+                      st>>>(U3, n[2], r[2], RP, Bp);
     TK_CHECK_LAUNCH();
-    TK_RC(launch_ttm1(F, UT3, T1, n[0] * n[1], n[2], r[2], st));
-    SmallGemm g2{r[1], r[2], n[1], n[0], U2, 1, r[1], 0, T1, r[2], 1, n[1] * r[2], T2, r[2], 1, (int64_t)r[1] * r[2]};
-    TK_RC(launch_small_gemm(g2, st));
+    ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT};
+    TK_RC(launch_ttm12(a, n[0], st));
+    if (JT > 1) {
+        const int64_t nout = (int64_t)r[1] * r[2], total = n[0] * nout;
+        k_t2_reduce<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(part, (int)JT, nout, total,
+                                                                                              T2);
+        TK_CHECK_LAUNCH();
+    }
+    // TTM3: core (r1 x r2r3) = U1^T (r1 x n1) * T2 (n1 x r2r3)
     SmallGemm g3{r[0], (int64_t)r[1] * r[2], n[0], 1, U1, 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
                  (int64_t)r[1] * r[2], 1, 0};
     TK_RC(launch_small_gemm(g3, st));
@@ -236,87 +385,234 @@ int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, con
 
 // ---------------------------------------------------------------------------------- error
 namespace errk {
-constexpr int BM = 128, BN = 128;
+constexpr int BM = 64, BN = 64, NT = 128;
 
-// A = W (M x R), B = U3 (N x R); tiles [kb][128 lines][16] with R padded to KB*16.
-__global__ void __launch_bounds__(256) k_err(const double* __restrict__ W, const double* __restrict__ U3,
-                                             const double* __restrict__ F, int64_t M, int64_t N, int R, int KB,
-                                             double* __restrict__ partial) {
-    extern __shared__ uint8_t smem_raw[];
-    double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    double* sA = smem;                // KB * 2048
-    double* sB = smem + KB * BM * 16;  // KB * 2048
+// k -> (block, lane position) map shared by both operands.  Full 16-wide blocks are stored as is;
+// a trailing partial block of <= 8 values is placed on the positions {0,1,4,5,8,9,12,13} that the
+// first half-step (h = 0) of the K-major fragment loads reads, so the second half-step is skipped
+// and no padded k is multiplied (R = 40 -> exactly 2.5 blocks).
+__device__ __forceinline__ int kmap_inverse(int kb, int local, int full, int rem) {  // -> k or -1
+    if (kb < full) return 16 * kb + local;
+    if (rem > 8) return 16 * full + local;
+    if (local & 2) return -1;
+    return 16 * full + (local >> 2) * 2 + (local & 1);
+}
+
+__device__ __forceinline__ void kmap_forward(int k, int full, int rem, int& kb, int& local) {
+    if (k < 16 * full) {
+        kb = k >> 4;
+        local = k & 15;
+    } else {
+        const int j = k - 16 * full;
+        kb = full;
+        local = rem > 8 ? j : (j >> 1) * 4 + (j & 1);
+    }
+}
+
+struct ErrArgs {
+    const double* F;   // n1 x n2 x n3
+    const double* U2;  // n2 x r2
+    const double* X;   // n1 x r2 x R   (X[i] = sum_a U1[i,a] core[a,:,:])
+    const double* Up;  // packed U3: [ceil(n3/64)][KB][64][16], kmap + swizzle
+    double* partial;   // 2 per CTA
+    int64_t n2, n3;
+    int r2, R, KB;
+};
+
+// Up[t][kb][line][local] (swizzled) = U3[64 t + line][kmap_inverse(kb, local)]  (0 if none)
+__global__ void k_pack_u3_err(const double* __restrict__ U3, int64_t n3, int R, int KB, double* __restrict__ Up) {
+    const int full = R / 16, rem = R % 16;
+    const int64_t per = (int64_t)KB * BN * 16, tot = ceil_div(n3, BN) * per;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tile = t / per;
+        const int e = (int)(t % per), kb = e / (BN * 16), rr = e % (BN * 16), line = rr >> 4, col = rr & 15;
+        const int k = kmap_inverse(kb, col, full, rem);
+        const int64_t nn = tile * BN + line;
+        Up[tile * per + kb * BN * 16 + swz(line, col)] = (nn < n3 && k >= 0 && k < R) ? U3[nn * R + k] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void bulk_g2s_e(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__host__ __device__ inline int ld_mod(int w, int target) {  // smallest ld >= w with ld % 16 == target
+    return w + ((target - w % 16) + 16) % 16;
+}
+
+// W tiles for the error pass: for slab i and rows j0..j0+63,
+//   W (64 x R) = U2[j0:j0+64] X[i]   (DMMA), stored in the k_err A-operand layout
+//   Wp[(i * JE + jt)][kb][64][16] (kmap + swizzle, zeros elsewhere)
+// so that k_err fetches a whole tile with one cp.async.bulk.  Fragment-load leading dimensions
+// are 4 mod 16 doubles: a half-warp's 16 fragment addresses (4 rows x 4 k) hit 16 distinct
+// 8-byte bank slots.
+__global__ void __launch_bounds__(NT) k_err_w(const ErrArgs g, double* __restrict__ Wp) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const int KB = g.KB, R = g.R, r2 = g.r2;
+    const int r2p = (r2 + 7) & ~7, Rp = (R + 7) & ~7, ldu = ld_mod(r2p, 4), ldx = ld_mod(Rp, 4);
+    double* sW = reinterpret_cast<double*>(smem_raw);  // [KB][BM][16]
+    double* sU2 = sW + KB * BM * 16;                    // [BM][ldu]
+    double* sX = sU2 + BM * ldu;                        // [r2p][ldx]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, q = lane & 3;
+    const int full16 = R / 16, rem = R % 16;
+    const int64_t i = blockIdx.y, j0 = (int64_t)blockIdx.x * BM, M = g.n2;
+    for (int e = tid; e < KB * BM * 16; e += NT) sW[e] = 0.0;
+    for (int e = tid; e < BM * r2p; e += NT) {
+        const int row = e / r2p, b = e - row * r2p;
+        sU2[row * ldu + b] = (j0 + row < M && b < r2) ? g.U2[(j0 + row) * r2 + b] : 0.0;
+    }
+    const double* Xi = g.X + i * (int64_t)r2 * R;
+    for (int e = tid; e < r2p * Rp; e += NT) {
+        const int b = e / Rp, c = e - b * Rp;
+        sX[b * ldx + c] = (b < r2 && c < R) ? Xi[b * R + c] : 0.0;
+    }
+    __syncthreads();
+    const int tnn = Rp / 8;
+    for (int t = warp; t < (BM / 8) * tnn; t += NT / 32) {
+        const int mt = (t / tnn) * 8, nt = (t % tnn) * 8;
+        double d[2] = {0.0, 0.0};
+        const double* pa = sU2 + (mt + r) * ldu + q;
+        const double* pb = sX + q * ldx + nt + r;
+        for (int k = 0; k < r2p; k += 4) dmma(d, pa[k], pb[k * ldx]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int c = nt + 2 * q + u;
+            if (c < R) {
+                int kb, local;
+                kmap_forward(c, full16, rem, kb, local);
+                sW[kb * BM * 16 + swz(mt + r, local)] = d[u];
+            }
+        }
+    }
+    __syncthreads();
+    double2* dst = reinterpret_cast<double2*>(Wp + ((size_t)i * gridDim.x + blockIdx.x) * (size_t)(KB * BM * 16));
+    const double2* src = reinterpret_cast<const double2*>(sW);
+    for (int e = tid; e < KB * BM * 8; e += NT) dst[e] = src[e];
+}
+
+// One CTA = slab i, rows j0..j0+63 (grid = (ceil(n2/64), n1)), 4 warps as 2 (M) x 2 (N) of
+// 32 x 32; two CTAs per SM.
+//   W tile (k_err_w) and U3 tiles (pre-packed) arrive by cp.async.bulk (mbarriers; U3 in a
+//   2-slot ring);
+//   loop over column tiles of 64: the F values of the tile are loaded into registers (fragment
+//   layout, 16-byte evict-first loads) before its MMAs so HBM latency hides under them;
+//   Ft tile = W U3^T on DMMA; sum (F - Ft)^2 and F^2 per thread; fixed-order block reduction.
+__global__ void __launch_bounds__(NT, 2) k_err(const ErrArgs g, const double* __restrict__ Wp) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const int KB = g.KB, R = g.R;
+    double* sA = reinterpret_cast<double*>(smem_raw);  // [KB][BM][16]
+    double* sB = sA + KB * BM * 16;                    // [2][KB][BN][16]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 2 * KB * BN * 16);  // [0..1] U3 slots, [2] W
     __shared__ double red[40];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
-    const int64_t m0 = (int64_t)blockIdx.x * BM;
-    for (int e = tid; e < KB * BM * 16; e += 256) {
-        const int kb = e / (BM * 16), rem = e % (BM * 16), line = rem >> 4, col = rem & 15;
-        const int k = kb * 16 + col;
-        const int64_t m = m0 + line;
-        const bool ok = (m < M) && (k < R);
-        cp_async8(sA + kb * BM * 16 + swz(line, col), ok ? W + m * R + k : W, ok);
+    const int wm = warp >> 1, wn = warp & 1, r = lane >> 2, q = lane & 3;
+    const int full16 = R / 16, rem = R % 16;
+    const int64_t i = blockIdx.y, j0 = (int64_t)blockIdx.x * BM, M = g.n2, N = g.n3;
+    const int ntiles = (int)ceil_div(N, BN);
+    const uint32_t tbytes = (uint32_t)(KB * BN * 16 * 8), wbytes = (uint32_t)(KB * BM * 16 * 8);
+
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init(&bar[b], 1);
+        mbar_fence_init();
     }
-    cp_async_commit();
-    double sd = 0.0, sf = 0.0;
-    for (int64_t n0 = 0; n0 < N; n0 += BN) {
-        __syncthreads();  // previous tile's readers of sB are done
-        for (int e = tid; e < KB * BN * 16; e += 256) {
-            const int kb = e / (BN * 16), rem = e % (BN * 16), line = rem >> 4, col = rem & 15;
-            const int k = kb * 16 + col;
-            const int64_t nn = n0 + line;
-            const bool ok = (nn < N) && (k < R);
-            cp_async8(sB + kb * BN * 16 + swz(line, col), ok ? U3 + nn * R + k : U3, ok);
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[2], wbytes);
+        bulk_g2s_e(sA, Wp + ((size_t)i * gridDim.x + blockIdx.x) * (size_t)(KB * BM * 16), wbytes, &bar[2]);
+        for (int t = 0; t < 2 && t < ntiles; ++t) {
+            mbar_arrive_expect_tx(&bar[t], tbytes);
+            bulk_g2s_e(sB + t * KB * BN * 16, g.Up + (int64_t)t * KB * BN * 16, tbytes, &bar[t]);
         }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        double acc[8][4][2];
+    }
+    const uint32_t sA32 = smem_u32(sA), sB32 = smem_u32(sB);
+    // per-thread F row pointers (fragment rows), full-tile fast path when in range and aligned
+    const bool rows_ok = (j0 + BM <= M);
+    const bool vec2 = ((N & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.F) & 15) == 0);
+    const double* Fr = g.F + (i * M + j0 + wm * 32 + r) * N + wn * 32 + 2 * q;
+    double sd = 0.0, sf = 0.0;
+    mbar_wait(&bar[2], 0);
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int64_t n0 = (int64_t)tile * BN;
+        // 1. F of this tile -> registers
+        double f[4][4][2];
+        if (rows_ok && vec2 && n0 + BN <= N) {
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
+                    const double2 v = __ldcs(reinterpret_cast<const double2*>(Fr + (int64_t)mi * 8 * N + n0 + ni * 8));
+                    f[mi][ni][0] = v.x;
+                    f[mi][ni][1] = v.y;
+                }
+        } else {
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const int64_t row = j0 + wm * 32 + mi * 8 + r;
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
+                    const int64_t col = n0 + wn * 32 + ni * 8 + 2 * q;
+                    const double* src = Fr + (int64_t)mi * 8 * N + n0 + ni * 8;
+                    f[mi][ni][0] = (row < M && col < N) ? __ldcs(src) : 0.0;
+                    f[mi][ni][1] = (row < M && col + 1 < N) ? __ldcs(src + 1) : 0.0;
+                }
+            }
+        }
+        // 2. U3 tile ready
+        const int slot = tile & 1;
+        mbar_wait(&bar[slot], (uint32_t)((tile >> 1) & 1));
+        // 3. Ft tile on DMMA
+        const uint32_t tB0 = sB32 + (uint32_t)(slot * KB * BN * 16 * 8);
+        double acc[4][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
         for (int kb = 0; kb < KB; ++kb) {
-            const double* tA = sA + kb * BM * 16;
-            const double* tB = sB + kb * BN * 16;
+            const uint32_t tA = sA32 + (uint32_t)(kb * BM * 16 * 8);
+            const uint32_t tB = tB0 + (uint32_t)(kb * BN * 16 * 8);
+            const int halves = (kb < full16 || rem > 8) ? 2 : 1;
+            for (int h = 0; h < halves; ++h) {
+                double a[4][2], b[4][2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                double a[8][2], b[4][2];
+                for (int mi = 0; mi < 4; ++mi)
+                    lds128_u32(a[mi][0], a[mi][1], tA + 8u * (uint32_t)swz_chunk(wm * 32 + mi * 8 + r, 2 * q + h));
 #pragma unroll
-                for (int mi = 0; mi < 8; ++mi) lds128(a[mi][0], a[mi][1], tA + swz_chunk(wm * 64 + mi * 8 + r, 2 * q + h));
+                for (int ni = 0; ni < 4; ++ni)
+                    lds128_u32(b[ni][0], b[ni][1], tB + 8u * (uint32_t)swz_chunk(wn * 32 + ni * 8 + r, 2 * q + h));
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) lds128(b[ni][0], b[ni][1], tB + swz_chunk(wn * 32 + ni * 8 + r, 2 * q + h));
+                for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
-                for (int s = 0; s < 2; ++s)
+                    for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-                    for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-                        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi][s], b[ni][s]);
+                        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi][s2], b[ni][s2]);
             }
         }
+        __syncthreads();  // every warp is done with this slot
+        if (tid == 0 && tile + 2 < ntiles) {
+            mbar_arrive_expect_tx(&bar[slot], tbytes);
+            bulk_g2s_e(sB + slot * KB * BN * 16, g.Up + (int64_t)(tile + 2) * KB * BN * 16, tbytes, &bar[slot]);
+        }
+        // 4. residual and norm (out-of-range positions hold f = 0 and acc = 0)
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int64_t row = m0 + wm * 64 + mi * 8 + r;
-                const int64_t col = n0 + wn * 32 + ni * 8 + 2 * q;
-                if (row < M) {
+            for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-                    for (int u = 0; u < 2; ++u)
-                        if (col + u < N) {
-                            const double f = __ldcs(F + row * N + col + u);
-                            const double d = f - acc[mi][ni][u];
-                            sd = fma(d, d, sd);
-                            sf = fma(f, f, sf);
-                        }
+                for (int u = 0; u < 2; ++u) {
+                    const double d = f[mi][ni][u] - acc[mi][ni][u];
+                    sd = fma(d, d, sd);
+                    sf = fma(f[mi][ni][u], f[mi][ni][u], sf);
                 }
-            }
     }
     sd = block_sum(sd, red);
     sf = block_sum(sf, red);
     if (tid == 0) {
-        partial[2 * blockIdx.x] = sd;
-        partial[2 * blockIdx.x + 1] = sf;
+        const int64_t b = i * gridDim.x + blockIdx.x;
+        g.partial[2 * b] = sd;
+        g.partial[2 * b + 1] = sf;
     }
 }
 
@@ -340,35 +636,60 @@ __global__ void __launch_bounds__(1024) k_err_final(const double* __restrict__ p
 }
 }  // namespace errk
 
+static size_t err_w_smem(const int32_t r[3]) {
+    const int KB = (int)ceil_div(r[2], 16);
+    const int r2p = (r[1] + 7) & ~7, Rp = (r[2] + 7) & ~7;
+    return (size_t)KB * errk::BM * 16 * 8 +
+           ((size_t)errk::BM * errk::ld_mod(r2p, 4) + (size_t)r2p * errk::ld_mod(Rp, 4)) * 8;
+}
+static size_t err_smem(const int32_t r[3]) {
+    const int KB = (int)ceil_div(r[2], 16);
+    return (size_t)KB * (errk::BM + 2 * errk::BN) * 16 * 8 + 3 * 8;
+}
+
+static size_t packed_err_bytes(const int64_t n[3], const int32_t r[3]) {
+    return (size_t)ceil_div(n[2], errk::BN) * ceil_div(r[2], 16) * errk::BN * 16 * 8;
+}
+static size_t packed_w_bytes(const int64_t n[3], const int32_t r[3]) {
+    return (size_t)n[0] * ceil_div(n[1], errk::BM) * ceil_div(r[2], 16) * errk::BM * 16 * 8;
+}
+
 size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]) {
-    const int64_t M = n[0] * n[1];
-    return align_up((size_t)n[0] * r[1] * r[2] * 8, 256) + align_up((size_t)M * r[2] * 8, 256) +
-           align_up((size_t)2 * ceil_div(M, errk::BM) * 8, 256);
+    const int64_t nb = n[0] * ceil_div(n[1], errk::BM);
+    return align_up((size_t)n[0] * r[1] * r[2] * 8, 256) + align_up((size_t)2 * nb * 8, 256) +
+           align_up(packed_err_bytes(n, r), 256) + align_up(packed_w_bytes(n, r), 256);
 }
 
 int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                  const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, cudaStream_t st) {
     if (ws_bytes < err_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
-    if (r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
-    const int64_t M = n[0] * n[1];
+    if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    const int64_t JE = ceil_div(n[1], errk::BM), nb = n[0] * JE;
     char* w = static_cast<char*>(ws);
     double* X = reinterpret_cast<double*>(w);
     w += align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
-    double* W = reinterpret_cast<double*>(w);
-    w += align_up((size_t)M * r[2] * 8, 256);
     double* partial = reinterpret_cast<double*>(w);
+    w += align_up((size_t)2 * nb * 8, 256);
+    double* Up = reinterpret_cast<double*>(w);
+    w += align_up(packed_err_bytes(n, r), 256);
+    double* Wp = reinterpret_cast<double*>(w);
     const int64_t r23 = (int64_t)r[1] * r[2];
+    const int KB = (int)ceil_div(r[2], 16);
     // X (n1 x r2r3) = U1 (n1 x r1) * core (r1 x r2r3)
     SmallGemm gx{n[0], r23, r[0], 1, U1, r[0], 1, 0, core, r23, 1, 0, X, r23, 1, 0};
     TK_RC(launch_small_gemm(gx, st));
-    // W[i] (n2 x r3) = U2 (n2 x r2) * X[i] (r2 x r3)
-    SmallGemm gw{n[1], r[2], r[1], n[0], U2, r[1], 1, 0, X, r[2], 1, r23, W, r[2], 1, n[1] * r[2]};
-    TK_RC(launch_small_gemm(gw, st));
-    const int KB = (int)ceil_div(r[2], 16);
-    const size_t sm = (size_t)2 * KB * errk::BM * 16 * 8 + 1024;
+    const int64_t ptot = (int64_t)(packed_err_bytes(n, r) / 8);
+    errk::k_pack_u3_err<<<(unsigned)std::min<int64_t>(ceil_div(ptot, 256), 1024), 256, 0, st>>>(U3, n[2], r[2], KB, Up);
+    TK_CHECK_LAUNCH();
+    errk::ErrArgs a{F, U2, X, Up, partial, n[1], n[2], r[1], r[2], KB};
+    const dim3 grid((unsigned)JE, (unsigned)n[0]);
+    const size_t smw = err_w_smem(r);
+    TK_CUDA(cudaFuncSetAttribute(errk::k_err_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw));
+    errk::k_err_w<<<grid, errk::NT, smw, st>>>(a, Wp);
+    TK_CHECK_LAUNCH();
+    const size_t sm = err_smem(r);
     TK_CUDA(cudaFuncSetAttribute(errk::k_err, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int64_t nb = ceil_div(M, errk::BM);
-    errk::k_err<<<(unsigned)nb, 256, sm, st>>>(W, U3, F, M, n[2], r[2], KB, partial);
+    errk::k_err<<<grid, errk::NT, sm, st>>>(a, Wp);
     TK_CHECK_LAUNCH();
     errk::k_err_final<<<1, 1024, 0, st>>>(partial, nb, out3);
     TK_CHECK_LAUNCH();
