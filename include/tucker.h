@@ -137,6 +137,35 @@ TUCKER_API int tucker_approximate(const tucker_grid* grid, const tucker_kernel* 
                        double* F, double* const U_h[3], double* core_h, double* const sigma_h[3],
                        double* err_h, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
+/* ------------------------------------------------------------------------------------------
+ * a-7 fused generate-and-contract (BASELINE config 5's 2048^3 path): F is never materialised.
+ * The function tensor is regenerated from `grid` + `kernel` (bitwise the values tucker_fill
+ * would store) in plane chunks: for the Gram, chunks of ~32 MB are generated by a persistent
+ * cooperative grid into an L2-resident two-slot ring and consumed by the same TMA + DMMA tiles as
+ * tucker_gram (one grid barrier per chunk); for the core and the error, chunks of i-slabs
+ * (~1 GiB) are generated ahead of the fused TTM / error kernels.  Results equal the
+ * materialised path's up to the summation order of the Gram (split points differ).
+ * Workspace (dev, caller-owned) >= tucker_workspace_size_fused(grid, r); no F argument.
+ * Requirements: n3 even and >= 16 (TMA strides), ranks r_m <= 56.  Errors as above, plus
+ * TUCKER_ERR_UNSUPPORTED when the cooperative grid cannot be made resident.
+ */
+TUCKER_API size_t tucker_workspace_size_fused(const tucker_grid* grid, const int32_t r[3]);
+
+/* a-3 fused: G (dev, n_m x n_m, both triangles) <- F_(m) F_(m)^T with F generated on the fly. */
+TUCKER_API int tucker_gram_fused(const tucker_grid* grid, const tucker_kernel* kernel, int32_t mode, double* G,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* a-3..a-5 fused: truncated HOSVD of the function tensor of (grid, kernel); outputs as
+ * tucker_hosvd (dev U_m n_m x r_m, core r1*r2*r3, sigma_m r_m); `info` (host) may be NULL. */
+TUCKER_API int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
+                       double* U1, double* U2, double* U3, double* core, double* sigma1, double* sigma2,
+                       double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
+/* a-6 fused: out3 (dev) <- {E, ||F||, ||F - Ft||} with F regenerated chunk by chunk. */
+TUCKER_API int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
+                       const double* U1, const double* U2, const double* U3, const double* core, double* out3,
+                       void* ws, size_t ws_bytes, void* stream);
+
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
 TUCKER_API int64_t tucker_last_launch_count(void);
 

@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "fill_eval.cuh"
 #include "kernels.h"
 
 namespace tk {
@@ -139,6 +140,90 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
     return worst;
 }
 
+// ---------------------------------------------------------------- a-7 fused (F never stored)
+// Slab chunk (i-planes) for the fused core / error passes: about 1 GiB, and at least two waves
+// of k_ttm12 CTAs when the grid allows it.
+int64_t fused_slab_chunk(const int64_t n[3]) {
+    const int64_t plane = n[1] * n[2] * 8;
+    const int64_t target = fused_chunk_target((int64_t)1 << 30);
+    int64_t pc = std::max<int64_t>(1, target / plane);
+    const int64_t jt = ceil_div(n[1], 256);
+    if (target == ((int64_t)1 << 30)) pc = std::max<int64_t>(pc, ceil_div(2 * kNumSMs, jt));
+    return std::min<int64_t>(pc, n[0]);
+}
+
+// Fused workspace: [nodes x^2][K_nu table][G][scratch]; scratch = max(fused Gram ring + partials
+// + barrier, eigensolver, chunk + core, chunk + error).
+struct FusedLayout {
+    size_t nodes, cheb, G, scratch, total, scratch_bytes;
+    int64_t pc_slab;
+};
+
+FusedLayout plan_fused(const tucker_grid* g, const int32_t* rin) {
+    int32_t r[3];
+    for (int a = 0; a < 3; ++a) r[a] = rin ? rin[a] : (int32_t)std::min<int64_t>(g->n[a], 56);
+    const int64_t* n = g->n;
+    FusedLayout L{};
+    size_t off = 0;
+    L.nodes = off;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
+    L.cheb = off;
+    off += align_up((size_t)kChebIntervals * kChebN * 8, 256);
+    L.G = off;
+    const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
+    off += align_up((size_t)nmax * nmax * 8, 1024);
+    L.scratch = off;
+    size_t s = 0;
+    for (int m = 0; m < 3; ++m) {
+        const FusedGramPlan fp = fused_gram_plan(n, m);
+        s = std::max(s, 2 * align_up(fp.slot_elems * 8, 1024) + align_up(fp.part_bytes, 256) + 256);
+        s = std::max(s, eig_ws_bytes(n[m], r[m]));
+    }
+    L.pc_slab = fused_slab_chunk(n);
+    const size_t chunk = align_up((size_t)L.pc_slab * n[1] * n[2] * 8, 256);
+    s = std::max(s, chunk + ttm_ws_bytes(n, r));
+    s = std::max(s, chunk + err_ws_bytes_slabs(n, r, L.pc_slab));
+    L.scratch_bytes = align_up(s, 256);
+    off += L.scratch_bytes;
+    L.total = off;
+    return L;
+}
+
+KParams fused_kparams(const tucker_grid* g, const tucker_kernel* k) {
+    KParams kp = make_kparams(*k);
+    kp.centred = grid_centred(*g) ? 1 : 0;
+    return kp;
+}
+
+int fused_gram_into(const tucker_grid* g, int m, const KParams& kp, const FusedLayout& L, void* ws, double* G,
+                    cudaStream_t st) {
+    const FusedGramPlan fp = fused_gram_plan(g->n, m);
+    char* scr = at(ws, L.scratch);
+    double* ring = reinterpret_cast<double*>(scr);
+    double* part = reinterpret_cast<double*>(scr + 2 * align_up(fp.slot_elems * 8, 1024));
+    unsigned int* bar = reinterpret_cast<unsigned int*>(scr + 2 * align_up(fp.slot_elems * 8, 1024) +
+                                                        align_up(fp.part_bytes, 256));
+    return launch_gram_fused(g->n, m, kp, reinterpret_cast<const double*>(at(ws, L.cheb)),
+                             reinterpret_cast<const double*>(at(ws, L.nodes)), ring, part, bar, G, st);
+}
+
+FusedGen fused_gen(const tucker_grid* g, const KParams& kp, const FusedLayout& L, void* ws) {
+    FusedGen f{};
+    f.geo.pa = 0;
+    f.geo.mirror = (kp.centred && g->n[2] % 8 == 0) ? 1 : 0;
+    f.geo.n1 = g->n[0];
+    f.geo.n2 = g->n[1];
+    f.geo.n3 = g->n[2];
+    f.geo.np = g->n[0];
+    f.geo.g0 = 0;
+    f.geo.Pc = L.pc_slab;
+    f.kp = kp;
+    f.cheb = reinterpret_cast<const double*>(at(ws, L.cheb));
+    f.x2 = reinterpret_cast<const double*>(at(ws, L.nodes));
+    f.Pc = L.pc_slab;
+    return f;
+}
+
 }  // namespace
 }  // namespace tk
 
@@ -255,6 +340,77 @@ int tucker_approximate(const tucker_grid* grid, const tucker_kernel* kernel, con
     TK_CUDA(cudaMemcpyAsync(err_h, errd, 3 * 8, cudaMemcpyDeviceToHost, st));
     TK_CUDA(cudaStreamSynchronize(st));
     return rc;
+}
+
+size_t tucker_workspace_size_fused(const tucker_grid* grid, const int32_t r[3]) {
+    if (check_grid(grid) != TUCKER_OK) return 0;
+    return plan_fused(grid, r).total;
+}
+
+int tucker_gram_fused(const tucker_grid* grid, const tucker_kernel* kernel, int32_t mode, double* G, void* ws,
+                      size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    if (mode < 0 || mode > 2 || !G || !ws) return TUCKER_ERR_INVALID_ARG;
+    const int32_t r1[3] = {1, 1, 1};  // the Gram alone: no rank-dependent scratch
+    const FusedLayout L = plan_fused(grid, r1);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const KParams kp = fused_kparams(grid, kernel);
+    TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
+                           reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    return fused_gram_into(grid, mode, kp, L, ws, G, st);
+}
+
+int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* U1,
+                       double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, void* ws,
+                       size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    const FusedLayout L = plan_fused(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    if (info) std::memset(info, 0, sizeof(*info));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const KParams kp = fused_kparams(grid, kernel);
+    TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
+                           reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    double* G = reinterpret_cast<double*>(at(ws, L.G));
+    void* scr = at(ws, L.scratch);
+    int worst = TUCKER_OK;
+    for (int m = 0; m < 3; ++m) {
+        TK_RC(fused_gram_into(grid, m, kp, L, ws, G, st));
+        const int rc = launch_eig(grid->n[m], G, r[m], U[m], nullptr, S[m], scr, L.scratch_bytes, st, info, m);
+        if (rc == TUCKER_ERR_NOCONV) worst = rc;
+        else if (rc != TUCKER_OK) return rc;
+    }
+    const FusedGen gen = fused_gen(grid, kp, L, ws);
+    TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st));
+    return worst;
+}
+
+int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], const double* U1,
+                       const double* U2, const double* U3, const double* core, double* out3, void* ws,
+                       size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!U1 || !U2 || !U3 || !core || !out3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    const FusedLayout L = plan_fused(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const KParams kp = fused_kparams(grid, kernel);
+    TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
+                           reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    const FusedGen gen = fused_gen(grid, kp, L, ws);
+    return launch_error_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, out3, at(ws, L.scratch), L.scratch_bytes,
+                             st);
 }
 
 int64_t tucker_last_launch_count(void) { return launch_counter(); }

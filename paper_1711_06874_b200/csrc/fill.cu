@@ -16,6 +16,7 @@
 // evaluates one octant and writes each value to its 8 mirror images with 256-bit stores
 // (st.global.v4.f64 -> STG.E.ENL2.256); reversed positions stay inside the same cache lines.
 #include "common.cuh"
+#include "fill_eval.cuh"
 #include "kernels.h"
 
 namespace tk {
@@ -36,22 +37,6 @@ __global__ void k_nodes(double c0, double s0, int64_t n0, double c1, double s1, 
     x2[t] = __dmul_rn(x, x);
 }
 
-// ------------------------------------------------------------------------- K_nu Chebyshev table
-// e^z K_nu(z) = int_0^inf exp(-2 z sinh^2(t/2)) cosh(nu t) dt, trapezoid h = 1/32.
-__device__ double scaled_besselk_trapz(double nu, double z) {
-    const double h = 1.0 / 32.0;
-    double sum = 0.5, prev = 1.0;
-    for (int k = 1; k < 200000; ++k) {
-        double t = k * h;
-        double sh = sinh(0.5 * t);
-        double f = exp(-2.0 * z * sh * sh) * cosh(nu * t);
-        sum += f;
-        if (f < prev && f < 1e-18 * sum) break;
-        prev = f;
-    }
-    return h * sum;
-}
-
 // One block per dyadic interval j = kChebJmin + blockIdx.x; thread k < 21 computes the node
 // value at x_k = cos(pi (k+1/2)/21), then thread m the coefficient
 // c_m = 2/21 sum_k g_k cos(pi m (k+1/2)/21).
@@ -70,55 +55,6 @@ __global__ void k_cheb_table(double nu, double pref, double* table) {
         for (int t = 0; t < kChebN; ++t) c += g[t] * cospi(k * (t + 0.5) / kChebN);
         table[blockIdx.x * kChebN + k] = c * (2.0 / kChebN);
     }
-}
-
-// ----------------------------------------------------------------------------- point kernels
-struct KParams {
-    int family;
-    int closed;  // 0 general, 1: nu=1/2, 2: nu=3/2, 3: nu=5/2
-    double sigma2, ell, sqrt2nu, lambda, p, nu, pref;
-};
-
-__device__ __forceinline__ double cheb_eval(const double* c, double x) {
-    // y = c0/2 + sum_{m>=1} c_m T_m(x)  (Clenshaw)
-    double b1 = 0.0, b2 = 0.0, x2 = 2.0 * x;
-#pragma unroll
-    for (int m = kChebN - 1; m >= 1; --m) {
-        double b0 = fma(x2, b1, c[m] - b2);
-        b2 = b1;
-        b1 = b0;
-    }
-    return fma(x, b1, 0.5 * c[0] - b2);
-}
-
-__device__ __forceinline__ double eval_point(const KParams& kp, const double* cheb, double r2) {
-    const double r = __dsqrt_rn(r2);
-    if (kp.family == TUCKER_SLATER) {
-        double rp = (kp.p == 1.0) ? r : (kp.p == 2.0) ? r2 : pow(r, kp.p);
-        return __dmul_rn(kp.sigma2, exp(__dmul_rn(-kp.lambda, rp)));
-    }
-    if (r == 0.0) return kp.sigma2;  // R4: C(0) = sigma^2
-    const double z = __ddiv_rn(__dmul_rn(kp.sqrt2nu, r), kp.ell);
-    const double e = exp(-z);
-    switch (kp.closed) {
-        case 1: return __dmul_rn(kp.sigma2, e);
-        case 2: return __dmul_rn(kp.sigma2, __dmul_rn(__dadd_rn(1.0, z), e));
-        case 3: {
-            double poly = __dadd_rn(__dadd_rn(1.0, z), __ddiv_rn(__dmul_rn(z, z), 3.0));
-            return __dmul_rn(kp.sigma2, __dmul_rn(poly, e));
-        }
-        default: break;
-    }
-    int ex;
-    double m = frexp(z, &ex);  // z = m 2^ex, m in [1/2,1): interval j = ex - 1
-    int j = ex - 1 - kChebJmin;
-    if (j >= 0 && j < kChebIntervals) return e * cheb_eval(cheb + j * kChebN, 4.0 * m - 3.0);
-    return e * (kp.pref * pow(z, kp.nu) * scaled_besselk_trapz(kp.nu, z));
-}
-
-__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
-                 : "memory");
 }
 
 // Octant fill with 8-fold mirrored 256-bit stores.  Requires lo = -hi on all axes and
@@ -177,20 +113,25 @@ __global__ void __launch_bounds__(256) k_fill_general(KParams kp, const double* 
     }
 }
 
-// --------------------------------------------------------------------------------- launcher
-int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2,
-                double* cheb, cudaStream_t st) {
-    const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
-    double c[3], s[3];
-    for (int a = 0; a < 3; ++a) {  // host: exactly the oracle's expressions (R2)
-        c[a] = (g.lo[a] + g.hi[a]) * 0.5;
-        s[a] = (g.hi[a] - g.lo[a]) / (2.0 * (double)(g.n[a] - 1));
-    }
-    const int64_t tot = n1 + n2 + n3;
-    k_nodes<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(c[0], s[0], n1, c[1], s[1], n2, c[2],
-                                                          s[2], n3, nodes_x2);
-    TK_CHECK_LAUNCH();
+// Standalone plane-chunk generation (fused TTM / error passes, a-7).
+__global__ void __launch_bounds__(256) k_gen_chunk(ChunkGeo geo, KParams kp, const double* __restrict__ cheb,
+                                                   const double* __restrict__ x2, double* __restrict__ out) {
+    const int64_t items = chunk_items(geo);
+    gen_chunk(geo, kp, cheb, x2, out, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, items,
+              (int64_t)gridDim.x * blockDim.x);
+}
 
+int launch_gen_chunk(const ChunkGeo& geo, const KParams& kp, const double* cheb, const double* x2, double* out,
+                     cudaStream_t st) {
+    const int64_t items = chunk_items(geo);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16));
+    k_gen_chunk<<<(unsigned)blocks, 256, 0, st>>>(geo, kp, cheb, x2, out);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+// --------------------------------------------------------------------------------- launcher
+KParams make_kparams(const tucker_kernel& kn) {
     KParams kp{};
     kp.family = kn.family;
     kp.sigma2 = kn.sigma2;
@@ -205,13 +146,34 @@ int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double
         else if (kn.nu == 1.5) kp.closed = 2;
         else if (kn.nu == 2.5) kp.closed = 3;
     }
+    if (kn.family == TUCKER_MATERN && kp.closed == 0) kp.pref = kn.sigma2 * (pow(2.0, 1.0 - kn.nu) / tgamma(kn.nu));
+    return kp;
+}
+
+int launch_fill_prep(const tucker_grid& g, const tucker_kernel& kn, const KParams& kp, double* nodes_x2,
+                     double* cheb, cudaStream_t st) {
+    const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    double c[3], s[3];
+    for (int a = 0; a < 3; ++a) {  // host: exactly the oracle's expressions (R2)
+        c[a] = (g.lo[a] + g.hi[a]) * 0.5;
+        s[a] = (g.hi[a] - g.lo[a]) / (2.0 * (double)(g.n[a] - 1));
+    }
+    const int64_t tot = n1 + n2 + n3;
+    k_nodes<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(c[0], s[0], n1, c[1], s[1], n2, c[2], s[2], n3, nodes_x2);
+    TK_CHECK_LAUNCH();
     if (kn.family == TUCKER_MATERN && kp.closed == 0) {
-        kp.pref = kn.sigma2 * (pow(2.0, 1.0 - kn.nu) / tgamma(kn.nu));
         k_cheb_table<<<kChebIntervals, 32, 0, st>>>(kn.nu, kp.pref, cheb);
         TK_CHECK_LAUNCH();
     }
-    const bool centred = (g.lo[0] == -g.hi[0]) && (g.lo[1] == -g.hi[1]) && (g.lo[2] == -g.hi[2]);
-    if (centred && n3 % 8 == 0) {
+    return TUCKER_OK;
+}
+
+int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
+                cudaStream_t st) {
+    const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    const KParams kp = make_kparams(kn);
+    TK_RC(launch_fill_prep(g, kn, kp, nodes_x2, cheb, st));
+    if (grid_centred(g) && n3 % 8 == 0) {
         const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 8);
         const int64_t blocks = std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16);
         k_fill_octant<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F);

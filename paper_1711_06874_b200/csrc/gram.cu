@@ -22,7 +22,10 @@
 // (q = lane & 3), which is a permutation of the 16 k of a stage shared by both operands; M-major
 // tiles permute rows (m = 8r + mi for A, m = base(r) + ni for B) so that each lane reads
 // consecutive doubles.  The epilogue undoes the permutation.
+#include <cstdlib>
+
 #include "common.cuh"
+#include "fill_eval.cuh"
 #include "kernels.h"
 
 namespace tk {
@@ -144,6 +147,42 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* map, const Args& 
     }
 }
 
+// Mainloop over k-blocks [kb0, kb1) for output tile (ti, tj); `it0` is the ring iteration
+// counter at entry (stages/parities continue across calls; the ring must be drained, i.e. every
+// earlier iteration consumed, on entry).  Thread 0 produces, the 8 warps consume.
+template <int MODE>
+__device__ __forceinline__ void gram_consume(const CUtensorMap* map, const Args& a, int ti, int tj, bool diag,
+                                             int64_t kb0, int64_t kb1, int64_t it0, double* sA, double* sB,
+                                             uint64_t* full, uint64_t* empty, double (&acc)[8][4][2]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
+    const int64_t L = kb1 - kb0;
+    if (threadIdx.x == 0)
+        for (int64_t j = 0; j < STAGES && j < L; ++j) {
+            const int slot = (int)((it0 + j) % STAGES);
+            issue_stage<MODE>(map, a, &full[slot], sA + slot * TILE, sB + slot * TILE, ti, tj, diag, kb0 + j);
+        }
+    for (int64_t l = 0; l < L; ++l) {
+        const int64_t it = it0 + l;
+        if (threadIdx.x == 0 && l > 0) {
+            const int64_t prev = it - 1, nl = l - 1 + STAGES;
+            if (nl < L) {
+                const int ps = (int)(prev % STAGES);
+                mbar_wait(&empty[ps], (uint32_t)((prev / STAGES) & 1));
+                issue_stage<MODE>(map, a, &full[ps], sA + ps * TILE, sB + ps * TILE, ti, tj, diag, kb0 + nl);
+            }
+        }
+        const int stage = (int)(it % STAGES);
+        mbar_wait(&full[stage], (uint32_t)((it / STAGES) & 1));
+        const double* A = sA + stage * TILE;
+        const double* B = diag ? A : sB + stage * TILE;
+        if (MODE == 2) mma_mmajor(A, B, acc, wm, wn, r, q);
+        else mma_kmajor(A, B, acc, wm, wn, r, q);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(NCW * 32, 1)
     k_gram_tma(const __grid_constant__ CUtensorMap map, const Args a) {
@@ -169,11 +208,7 @@ __global__ void __launch_bounds__(NCW * 32, 1)
         mbar_fence_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        tma_prefetch_desc(&map);
-        for (int j = 0; j < STAGES && kb0 + j < kb1; ++j)
-            issue_stage<MODE>(&map, a, &full[j], sA + j * TILE, sB + j * TILE, ti, tj, diag, kb0 + j);
-    }
+    if (threadIdx.x == 0) tma_prefetch_desc(&map);
 
     const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
     double acc[8][4][2];
@@ -181,25 +216,105 @@ __global__ void __launch_bounds__(NCW * 32, 1)
     for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    gram_consume<MODE>(&map, a, ti, tj, diag, kb0, kb1, 0, sA, sB, full, empty, acc);
+    double* P = a.part + ((size_t)blockIdx.x * a.S + s) * (BM * BM);
+    store_partial<MODE == 2>(P, acc, wm, wn, r, q);
+}
 
-    for (int64_t kb = kb0; kb < kb1; ++kb) {
-        const int64_t it = kb - kb0;
-        if (threadIdx.x == 0 && it > 0) {
-            const int64_t prev = it - 1, nk = kb0 + prev + STAGES;
-            if (nk < kb1) {
-                const int ps = (int)(prev % STAGES);
-                mbar_wait(&empty[ps], (uint32_t)((prev / STAGES) & 1));
-                issue_stage<MODE>(&map, a, &full[ps], sA + ps * TILE, sB + ps * TILE, ti, tj, diag, nk);
-            }
+// --------------------------------------------------------------- a-7 fused generate-and-Gram
+// F is never materialised: plane chunks of F (mode 0 and 2: j-planes, layout [n1][Pc][n3];
+// mode 1: i-planes, [Pc][n2][n3]; see fill_eval.cuh) are generated by all CTAs into a 2-slot ring
+// sized to stay L2-resident (~2 x 32 MB), then consumed by the same TMA + DMMA mainloop as the
+// materialised Gram (the chunk is the sub-tensor whose mode-m Gram is the chunk's contribution).
+// One persistent cooperative grid of T x S CTAs (one per SM); per chunk c:
+//     generate chunk c+1 -> slot (c+1)&1  |  consume chunk c from slot c&1  |  grid barrier
+// Accumulators stay in registers across all chunks; the split-K partials and the fixed-order
+// k_gram_reduce are those of the materialised path.  Generic-proxy stores are ordered before the
+// async-proxy (TMA) reads of other CTAs by fence.proxy.async + the release/acquire grid barrier.
+struct FusedArgs {
+    Args a;             // virtual chunk shape (see launch_gram_fused), nkb of one chunk, S, part
+    ChunkGeo geo;       // g0 is set per chunk
+    KParams kp;
+    const double* cheb;
+    const double* x2;
+    double* slot[2];
+    int64_t nchunks;
+    unsigned int* bar;  // grid-barrier counter (zeroed before the launch)
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");  // my generic stores -> async proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned int v;
+        long long spins = 0;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+            if (++spins > (1ll << 27)) __trap();  // ~10 s: never hang the GPU
         }
-        const int stage = (int)(it % STAGES);
-        mbar_wait(&full[stage], (uint32_t)((it / STAGES) & 1));
-        const double* A = sA + stage * TILE;
-        const double* B = diag ? A : sB + stage * TILE;
-        if (MODE == 2) mma_mmajor(A, B, acc, wm, wn, r, q);
-        else mma_kmajor(A, B, acc, wm, wn, r, q);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+    __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NCW * 32, 1)
+    k_gram_fused(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+                 const FusedArgs f) {
+    extern __shared__ uint8_t smem_raw[];
+    double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    double* sA = smem;
+    double* sB = smem + STAGES * TILE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * TILE);
+    uint64_t* empty = full + STAGES;
+    const Args& a = f.a;
+    int ti, tj;
+    tile_decode(blockIdx.x, ti, tj);
+    const bool diag = (ti == tj);
+    const int s = blockIdx.y;
+    const int64_t kb0 = (int64_t)s * a.nkb / a.S, kb1 = (int64_t)(s + 1) * a.nkb / a.S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
+    const unsigned int ncta = gridDim.x * gridDim.y;
+    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&map0);
+        tma_prefetch_desc(&map1);
+    }
+    __syncthreads();
+
+    ChunkGeo geo = f.geo;
+    const int64_t items = chunk_items(geo);
+    const int64_t step = (int64_t)ncta * blockDim.x, lo = cta * blockDim.x + threadIdx.x;
+    geo.g0 = 0;
+    gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[0], lo, items, step);
+    unsigned int nbar = 1;
+    grid_barrier(f.bar, nbar * ncta);
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    int64_t it = 0;
+    for (int64_t c = 0; c < f.nchunks; ++c) {
+        if (c + 1 < f.nchunks) {
+            geo.g0 = (c + 1) * geo.Pc;
+            gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[(c + 1) & 1], lo, items, step);
+        }
+        gram_consume<MODE>((c & 1) ? &map1 : &map0, a, ti, tj, diag, kb0, kb1, it, sA, sB, full, empty, acc);
+        it += kb1 - kb0;
+        ++nbar;
+        grid_barrier(f.bar, nbar * ncta);
     }
     double* P = a.part + ((size_t)blockIdx.x * a.S + s) * (BM * BM);
     store_partial<MODE == 2>(P, acc, wm, wn, r, q);
@@ -404,6 +519,110 @@ int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* 
     }
     TK_CHECK_LAUNCH();
     k_gram_reduce<<<dim3(16, (unsigned)p.T), 256, 0, st>>>(a.part, p.S, p.n, G);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+// ------------------------------------------------------------------------- a-7 fused launcher
+// Chunk-size target in bytes; TUCKER_FUSED_CHUNK_KB (host environment) overrides it — a test
+// knob that forces many chunks on small grids.
+int64_t fused_chunk_target(int64_t dflt) {
+    const char* e = std::getenv("TUCKER_FUSED_CHUNK_KB");
+    if (e && *e) {
+        const long long v = std::atoll(e);
+        if (v > 0) return (int64_t)v << 10;
+    }
+    return dflt;
+}
+
+FusedGramPlan fused_gram_plan(const int64_t n[3], int mode) {
+    FusedGramPlan f{};
+    f.pa = (mode == 1) ? 0 : 1;
+    const int64_t nr = f.pa == 0 ? n[1] : n[0];
+    f.np = f.pa == 0 ? n[0] : n[1];
+    const int64_t plane = nr * n[2];
+    const int nt = (int)ceil_div(n[mode], gram::BM);
+    f.T = nt * (nt + 1) / 2;
+    f.S = std::max(1, kNumSMs / f.T);
+    f.Pc = std::max<int64_t>(1, std::min<int64_t>(f.np, fused_chunk_target(32 << 20) / (plane * 8)));
+    // at least ~16 k-blocks per CTA per chunk (pipeline restart amortisation)
+    auto nkb = [&](int64_t pc) {
+        return mode == 0 ? ceil_div(pc * n[2], gram::BK)
+                         : mode == 1 ? pc * ceil_div(n[2], gram::BK) : ceil_div(n[0] * pc, gram::BK);
+    };
+    while (f.Pc < f.np && nkb(f.Pc) < 16 * (int64_t)f.S) f.Pc *= 2;
+    f.Pc = std::min(f.Pc, f.np);
+    f.nchunks = ceil_div(f.np, f.Pc);
+    f.slot_elems = align_up((size_t)(f.Pc * plane), 128);
+    f.part_bytes = (size_t)f.T * f.S * gram::BM * gram::BM * sizeof(double);
+    return f;
+}
+
+int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const double* cheb, const double* x2,
+                      double* ring, double* part, unsigned int* bar, double* G, cudaStream_t st) {
+    using namespace gram;
+    if (n[2] % 2 != 0 || n[2] < BK) return TUCKER_ERR_UNSUPPORTED;
+    const FusedGramPlan fp = fused_gram_plan(n, mode);
+    if (fp.T * fp.S > kNumSMs) return TUCKER_ERR_UNSUPPORTED;
+    int64_t vn[3] = {n[0], n[1], n[2]};
+    if (fp.pa == 0) vn[0] = fp.Pc;
+    else vn[1] = fp.Pc;
+    FusedArgs f{};
+    Args& a = f.a;
+    a.mode = mode;
+    a.n1 = vn[0]; a.n2 = vn[1]; a.n3 = vn[2];
+    a.n = n[mode];
+    a.S = fp.S;
+    a.nkb3 = ceil_div(vn[2], BK);
+    if (mode == 0) a.nkb = ceil_div(vn[1] * vn[2], BK);
+    else if (mode == 1) a.nkb = vn[0] * a.nkb3;
+    else a.nkb = ceil_div(vn[0] * vn[1], BK);
+    a.F = ring;
+    a.part = part;
+    f.geo.pa = fp.pa;
+    f.geo.n1 = n[0]; f.geo.n2 = n[1]; f.geo.n3 = n[2];
+    f.geo.g0 = 0;
+    f.geo.Pc = fp.Pc;
+    f.geo.np = fp.np;
+    f.geo.mirror = (kp.centred && n[2] % 8 == 0) ? 1 : 0;
+    f.kp = kp;
+    f.cheb = cheb;
+    f.x2 = x2;
+    f.slot[0] = ring;
+    f.slot[1] = ring + fp.slot_elems;
+    f.nchunks = fp.nchunks;
+    f.bar = bar;
+    CUtensorMap maps[2];
+    for (int sl = 0; sl < 2; ++sl) {
+        bool ok;
+        if (mode == 0) {
+            uint64_t dims[2] = {(uint64_t)(vn[1] * vn[2]), (uint64_t)vn[0]};
+            uint64_t strides[1] = {(uint64_t)(vn[1] * vn[2] * 8)};
+            uint32_t box[2] = {BK, BM};
+            ok = make_tmap_f64(&maps[sl], f.slot[sl], 2, dims, strides, box);
+        } else if (mode == 1) {
+            uint64_t dims[3] = {(uint64_t)vn[2], (uint64_t)vn[1], (uint64_t)vn[0]};
+            uint64_t strides[2] = {(uint64_t)(vn[2] * 8), (uint64_t)(vn[1] * vn[2] * 8)};
+            uint32_t box[3] = {BK, BM, 1};
+            ok = make_tmap_f64(&maps[sl], f.slot[sl], 3, dims, strides, box);
+        } else {
+            uint64_t dims[2] = {(uint64_t)vn[2], (uint64_t)(vn[0] * vn[1])};
+            uint64_t strides[1] = {(uint64_t)(vn[2] * 8)};
+            uint32_t box[2] = {16, BK};
+            ok = make_tmap_f64(&maps[sl], f.slot[sl], 2, dims, strides, box);
+        }
+        if (!ok) return TUCKER_ERR_CUDA;
+    }
+    TK_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned int), st));
+    const size_t sm = smem_tma();
+    void* args[3] = {&maps[0], &maps[1], &f};
+    const dim3 grid((unsigned)fp.T, (unsigned)fp.S);
+    const void* fn = mode == 0 ? (const void*)k_gram_fused<0> : mode == 1 ? (const void*)k_gram_fused<1>
+                                                                          : (const void*)k_gram_fused<2>;
+    TK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    TK_CUDA(cudaLaunchCooperativeKernel(fn, grid, dim3(NCW * 32), args, sm, st));
+    TK_CHECK_LAUNCH();
+    k_gram_reduce<<<dim3(16, (unsigned)fp.T), 256, 0, st>>>(part, fp.S, n[mode], G);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }

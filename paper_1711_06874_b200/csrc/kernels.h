@@ -14,6 +14,22 @@ constexpr int kChebN = 21;  // degree 20
 constexpr int kChebJmin = -16;
 constexpr int kChebIntervals = 25;  // z in [2^-16, 2^9)
 
+// Point-kernel parameters (a-2; fill_eval.cuh evaluates them).
+struct KParams {
+    int family;
+    int closed;  // 0 general, 1: nu=1/2, 2: nu=3/2, 3: nu=5/2
+    int centred; // lo = -hi on every axis (set by the caller from the grid)
+    double sigma2, ell, sqrt2nu, lambda, p, nu, pref;
+};
+
+// Plane chunk of F for the fused paths (a-7; layout and generation in fill_eval.cuh).
+struct ChunkGeo {
+    int pa;
+    int mirror;
+    int64_t n1, n2, n3;
+    int64_t g0, Pc, np;
+};
+
 int launch_fill(const tucker_grid& g, const tucker_kernel& k, double* F, double* nodes_x2,
                 double* cheb, cudaStream_t st);
 
@@ -21,6 +37,20 @@ int launch_fill(const tucker_grid& g, const tucker_kernel& k, double* F, double*
 size_t gram_ws_bytes(const int64_t n[3]);
 int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
                 cudaStream_t st);
+
+// a-7 fused generate-and-Gram (F never materialised).  KParams / ChunkGeo: fill_eval.cuh.
+struct FusedGramPlan {
+    int pa;              // plane axis of the chunks (0: i-planes, 1: j-planes)
+    int T, S;            // output tiles, split-K factor (T*S <= SMs: one cooperative wave)
+    int64_t np, Pc;      // planes on that axis, planes per chunk
+    int64_t nchunks;
+    size_t slot_elems;   // doubles per ring slot (two slots)
+    size_t part_bytes;   // split-K partials
+};
+FusedGramPlan fused_gram_plan(const int64_t n[3], int mode);
+int64_t fused_chunk_target(int64_t dflt);  // TUCKER_FUSED_CHUNK_KB test override
+int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const double* cheb, const double* x2,
+                      double* ring, double* part, unsigned int* bar, double* G, cudaStream_t st);
 
 // Top-r eigenpairs of a symmetric PSD n x n matrix (dev).  iters/resid/... reported in `info`
 // slot `slot`.
@@ -38,6 +68,23 @@ size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,
                     const double* U2, const double* U3, double* core, void* ws, size_t ws_bytes,
                     cudaStream_t st);
+
+// Fused (F never materialised) variants of the core and the error: F is generated as chunks of
+// Pc i-slabs ([Pc][n2][n3], fill_eval.cuh) into the head of the workspace.
+struct FusedGen {
+    ChunkGeo geo;  // pa = 0; g0/Pc set per chunk
+    KParams kp;
+    const double* cheb;
+    const double* x2;
+    int64_t Pc;
+};
+int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
+                         const double* U1, const double* U2, const double* U3, double* core, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen, const double* U1,
+                      const double* U2, const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes,
+                      cudaStream_t st);
+size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs);
 
 // Relative Frobenius error {E, ||F||, ||F-Ft||}.
 size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]);

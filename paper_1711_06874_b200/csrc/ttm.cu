@@ -14,6 +14,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "fill_eval.cuh"
 #include "kernels.h"
 
 namespace tk {
@@ -95,6 +96,7 @@ struct Args12 {
     double* out;       // JT == 1: T2 (n1 x r2 x R); else part (n1 x JT x r2 x R)
     int64_t n2, n3;
     int R, r2, JT;
+    int64_t i_off;     // global index of slab 0 of F (fused path: F is a chunk of slabs)
 };
 
 // Bp[kb][c][kk] (swizzled) = U3[16 kb + kk][c]   (0 outside c < R, k < n3)
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(256, 1) k_ttm12(const __grid_constant__ CUtens
         }
         __syncthreads();
     }
-    double* dst = g.out + ((size_t)i * g.JT + jt) * (size_t)(r2 * R);
+    double* dst = g.out + ((size_t)(g.i_off + i) * g.JT + jt) * (size_t)(r2 * R);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const int t = warp + 8 * u;
@@ -304,7 +306,7 @@ __global__ void k_t2_reduce(const double* __restrict__ part, int JT, int64_t nou
 }
 
 template <int NI>
-static int run_ttm12(const ttm1::Args12& a, int64_t n1, cudaStream_t st) {
+static int run_ttm12(const ttm1::Args12& a, int64_t n1, cudaStream_t st) {  // n1 = slabs in a.F
     const bool tma = (a.n3 % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.F) & 15) == 0) && a.n3 >= ttm1::BK;
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
@@ -354,11 +356,21 @@ size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]) {
 
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                     const double* U3, double* core, void* ws, size_t ws_bytes, cudaStream_t st) {
-    if (ws_bytes < ttm_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
+    return launch_ttm_core_impl(n, r, F, nullptr, U1, U2, U3, core, ws, ws_bytes, st);
+}
+
+// Core with F either materialised (F != nullptr) or generated slab-chunk by slab-chunk (gen).
+int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
+                         const double* U1, const double* U2, const double* U3, double* core, void* ws,
+                         size_t ws_bytes, cudaStream_t st) {
+    const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
+    if (ws_bytes < ttm_ws_bytes(n, r) + chunk_b) return TUCKER_ERR_SIZE;
     if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
     const int64_t JT = ttm_jt(n);
     const size_t t2b = (size_t)n[0] * r[1] * r[2] * 8;
     char* w = static_cast<char*>(ws);
+    double* chunk = reinterpret_cast<double*>(w);
+    w += chunk_b;
     double* part = reinterpret_cast<double*>(w);
     w += align_up(JT > 1 ? JT * t2b : 0, 256);
     double* T2 = reinterpret_cast<double*>(w);
@@ -368,8 +380,21 @@ int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, con
     ttm1::k_pack_u3<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(n[2], ttm1::BK) * RP * ttm1::BK, 256), 1024), 256, 0,
                       st>>>(U3, n[2], r[2], RP, Bp);
     TK_CHECK_LAUNCH();
-    ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT};
-    TK_RC(launch_ttm12(a, n[0], st));
+    ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT, 0};
+    if (!gen) {
+        TK_RC(launch_ttm12(a, n[0], st));
+    } else {
+        for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
+            const int64_t pc = std::min<int64_t>(gen->Pc, n[0] - g0);
+            ChunkGeo geo = gen->geo;
+            geo.g0 = g0;
+            geo.Pc = pc;
+            TK_RC(launch_gen_chunk(geo, gen->kp, gen->cheb, gen->x2, chunk, st));
+            a.F = chunk;
+            a.i_off = g0;
+            TK_RC(launch_ttm12(a, pc, st));
+        }
+    }
     if (JT > 1) {
         const int64_t nout = (int64_t)r[1] * r[2], total = n[0] * nout;
         k_t2_reduce<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(part, (int)JT, nout, total,
@@ -417,6 +442,7 @@ struct ErrArgs {
     double* partial;   // 2 per CTA
     int64_t n2, n3;
     int r2, R, KB;
+    int64_t i_off;     // global index of slab 0 of F (fused path: F is a chunk of slabs)
 };
 
 // Up[t][kb][line][local] (swizzled) = U3[64 t + line][kmap_inverse(kb, local)]  (0 if none)
@@ -464,7 +490,7 @@ __global__ void __launch_bounds__(NT) k_err_w(const ErrArgs g, double* __restric
         const int row = e / r2p, b = e - row * r2p;
         sU2[row * ldu + b] = (j0 + row < M && b < r2) ? g.U2[(j0 + row) * r2 + b] : 0.0;
     }
-    const double* Xi = g.X + i * (int64_t)r2 * R;
+    const double* Xi = g.X + (g.i_off + i) * (int64_t)r2 * R;
     for (int e = tid; e < r2p * Rp; e += NT) {
         const int b = e / Rp, c = e - b * Rp;
         sX[b * ldx + c] = (b < r2 && c < R) ? Xi[b * R + c] : 0.0;
@@ -610,7 +636,7 @@ __global__ void __launch_bounds__(NT, 2) k_err(const ErrArgs g, const double* __
     sd = block_sum(sd, red);
     sf = block_sum(sf, red);
     if (tid == 0) {
-        const int64_t b = i * gridDim.x + blockIdx.x;
+        const int64_t b = (g.i_off + i) * gridDim.x + blockIdx.x;
         g.partial[2 * b] = sd;
         g.partial[2 * b + 1] = sf;
     }
@@ -650,22 +676,34 @@ static size_t err_smem(const int32_t r[3]) {
 static size_t packed_err_bytes(const int64_t n[3], const int32_t r[3]) {
     return (size_t)ceil_div(n[2], errk::BN) * ceil_div(r[2], 16) * errk::BN * 16 * 8;
 }
-static size_t packed_w_bytes(const int64_t n[3], const int32_t r[3]) {
-    return (size_t)n[0] * ceil_div(n[1], errk::BM) * ceil_div(r[2], 16) * errk::BM * 16 * 8;
+static size_t packed_w_bytes(const int64_t n[3], const int32_t r[3], int64_t slabs) {
+    return (size_t)slabs * ceil_div(n[1], errk::BM) * ceil_div(r[2], 16) * errk::BM * 16 * 8;
 }
 
-size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]) {
+size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]) { return err_ws_bytes_slabs(n, r, n[0]); }
+
+size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs) {
     const int64_t nb = n[0] * ceil_div(n[1], errk::BM);
     return align_up((size_t)n[0] * r[1] * r[2] * 8, 256) + align_up((size_t)2 * nb * 8, 256) +
-           align_up(packed_err_bytes(n, r), 256) + align_up(packed_w_bytes(n, r), 256);
+           align_up(packed_err_bytes(n, r), 256) + align_up(packed_w_bytes(n, r, slabs), 256);
 }
 
 int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                  const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, cudaStream_t st) {
-    if (ws_bytes < err_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
+    return launch_error_impl(n, r, F, nullptr, U1, U2, U3, core, out3, ws, ws_bytes, st);
+}
+
+int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen, const double* U1,
+                      const double* U2, const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    const int64_t slabs = gen ? gen->Pc : n[0];
+    const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
+    if (ws_bytes < err_ws_bytes_slabs(n, r, slabs) + chunk_b) return TUCKER_ERR_SIZE;
     if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
     const int64_t JE = ceil_div(n[1], errk::BM), nb = n[0] * JE;
     char* w = static_cast<char*>(ws);
+    double* chunk = reinterpret_cast<double*>(w);
+    w += chunk_b;
     double* X = reinterpret_cast<double*>(w);
     w += align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
     double* partial = reinterpret_cast<double*>(w);
@@ -681,16 +719,30 @@ int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const 
     const int64_t ptot = (int64_t)(packed_err_bytes(n, r) / 8);
     errk::k_pack_u3_err<<<(unsigned)std::min<int64_t>(ceil_div(ptot, 256), 1024), 256, 0, st>>>(U3, n[2], r[2], KB, Up);
     TK_CHECK_LAUNCH();
-    errk::ErrArgs a{F, U2, X, Up, partial, n[1], n[2], r[1], r[2], KB};
-    const dim3 grid((unsigned)JE, (unsigned)n[0]);
-    const size_t smw = err_w_smem(r);
+    const size_t smw = err_w_smem(r), sm = err_smem(r);
     TK_CUDA(cudaFuncSetAttribute(errk::k_err_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw));
-    errk::k_err_w<<<grid, errk::NT, smw, st>>>(a, Wp);
-    TK_CHECK_LAUNCH();
-    const size_t sm = err_smem(r);
     TK_CUDA(cudaFuncSetAttribute(errk::k_err, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    errk::k_err<<<grid, errk::NT, sm, st>>>(a, Wp);
-    TK_CHECK_LAUNCH();
+    auto block = [&](const double* Fb, int64_t ns, int64_t i_off) -> int {
+        errk::ErrArgs a{Fb, U2, X, Up, partial, n[1], n[2], r[1], r[2], KB, i_off};
+        const dim3 grid((unsigned)JE, (unsigned)ns);
+        errk::k_err_w<<<grid, errk::NT, smw, st>>>(a, Wp);
+        TK_CHECK_LAUNCH();
+        errk::k_err<<<grid, errk::NT, sm, st>>>(a, Wp);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    };
+    if (!gen) {
+        TK_RC(block(F, n[0], 0));
+    } else {
+        for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
+            const int64_t pc = std::min<int64_t>(gen->Pc, n[0] - g0);
+            ChunkGeo geo = gen->geo;
+            geo.g0 = g0;
+            geo.Pc = pc;
+            TK_RC(launch_gen_chunk(geo, gen->kp, gen->cheb, gen->x2, chunk, st));
+            TK_RC(block(chunk, pc, g0));
+        }
+    }
     errk::k_err_final<<<1, 1024, 0, st>>>(partial, nb, out3);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;

@@ -21,7 +21,8 @@ FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED"}
 EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
-           "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_last_launch_count",
+           "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
+           "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_last_launch_count",
            "tucker_strerror")
 
 
@@ -72,6 +73,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_hosvd": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_error": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_approximate": (ctypes.c_int, [pg, pk, pr, vp, P(vp), vp, P(vp), vp, vp, sz, vp, pi]),
+        "tucker_workspace_size_fused": (sz, [pg, pr]),
+        "tucker_gram_fused": (ctypes.c_int, [pg, pk, i32, vp, vp, sz, vp]),
+        "tucker_hosvd_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
+        "tucker_error_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_last_launch_count": (i64, []),
         "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
@@ -229,6 +234,56 @@ def error(grid, ranks, F, U, core, ws=None, stream=None) -> torch.Tensor:
     g = cgrid(grid)
     _check(lib.tucker_error(ctypes.byref(g), cranks(ranks), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
                             _ptr(core), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)), "tucker_error")
+    return out
+
+
+# ------------------------------------------------------------------ a-7 fused (F never stored)
+def workspace_bytes_fused(grid, ranks=None) -> int:
+    lib = load()
+    g = cgrid(grid)
+    return int(lib.tucker_workspace_size_fused(ctypes.byref(g), cranks(ranks) if ranks is not None else None))
+
+
+def workspace_fused(grid, ranks=None, device="cuda") -> torch.Tensor:
+    return torch.empty(workspace_bytes_fused(grid, ranks), dtype=torch.uint8, device=device)
+
+
+def gram_fused(grid, kernel, mode: int, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    lib = load()
+    n = int(grid.n[mode])
+    G = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ws = ws if ws is not None else workspace_fused(grid)
+    g, k = cgrid(grid), ckernel(kernel)
+    _check(lib.tucker_gram_fused(ctypes.byref(g), ctypes.byref(k), int(mode), _ptr(G), _ptr(ws), ws.numel(),
+                                 _stream(stream)), "tucker_gram_fused")
+    return G
+
+
+def hosvd_fused(grid, kernel, ranks, ws: torch.Tensor | None = None, stream=None) -> HosvdResult:
+    lib = load()
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device="cuda") for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device="cuda") for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device="cuda")
+    ws = ws if ws is not None else workspace_fused(grid, r)
+    info = CInfo()
+    g, k = cgrid(grid), ckernel(kernel)
+    rc = lib.tucker_hosvd_fused(ctypes.byref(g), ctypes.byref(k), cranks(r), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
+                                _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(),
+                                _stream(stream), ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd_fused")
+    return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+def error_fused(grid, kernel, ranks, U, core, ws=None, stream=None) -> torch.Tensor:
+    lib = load()
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    ws = ws if ws is not None else workspace_fused(grid, ranks)
+    g, k = cgrid(grid), ckernel(kernel)
+    _check(lib.tucker_error_fused(ctypes.byref(g), ctypes.byref(k), cranks(ranks), _ptr(U[0]), _ptr(U[1]),
+                                  _ptr(U[2]), _ptr(core), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)),
+           "tucker_error_fused")
     return out
 
 
