@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-host-tensor", action="store_true")
+    ap.add_argument("--no-fused", action="store_true", help="skip the 2048^3 fused (F never stored) line")
+    ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
 
@@ -285,11 +287,52 @@ def run_ours(args, rank, world, local):
             except RuntimeError as e:  # pinned allocation failure etc.
                 result["e2e_host_tensor"] = {"unavailable": str(e)[:200]}
     result["clocks"] = clk.summary()
+    if not args.no_fused and world == 1:
+        del F
+        torch.cuda.empty_cache()
+        result["fused"] = run_fused(T, args.fused_n, rr, stream)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
     if world > 1:
         dist.destroy_process_group()
     return result
+
+
+def run_fused(T, n: int, rr: int, stream) -> dict:
+    """BASELINE config 5f: HOSVD + error of the n^3 function tensor through the fused
+    generate-and-contract path (F never materialised; 68.7 GB at 2048^3 if it were)."""
+    import torch
+
+    from tucker_inputs import GridSpec, KernelSpec
+    grid = GridSpec.cube(n, 1.0)
+    kern = KernelSpec.matern(1.5, 0.2)
+    ranks = (rr, rr, rr)
+    N = grid.points
+    ws = T.workspace_fused(grid, ranks)
+    T.gram_fused(grid, kern, 0, ws, stream)  # warm-up (module load, first cooperative launch)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev[0].record(stream)
+    for m in range(3):
+        T.gram_fused(grid, kern, m, ws, stream)
+        ev[1 + m].record(stream)
+    torch.cuda.synchronize()
+    gram_ms = [ev[m].elapsed_time(ev[m + 1]) for m in range(3)]
+    ev[4].record(stream)
+    res = T.hosvd_fused(grid, kern, ranks, ws, stream)
+    err = T.error_fused(grid, kern, ranks, res.U, res.core, ws, stream)
+    ev[5].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[4].elapsed_time(ev[5])
+    flops = N * (n + 1)
+    ach = [flops / (g * 1e-3) / 1e12 for g in gram_ms]
+    e = err.cpu().tolist()
+    return {"workload": f"cfg5f_{n}cube_matern_nu1.5_ell0.2_fused", "grid": [n, n, n], "ranks": list(ranks),
+            "value": N / (ms * 1e-3), "unit": UNIT, "ms": ms, "F_bytes_never_stored": 8 * N,
+            "gram_ms": gram_ms, "gram_tflops": ach, "gram_frac": [a / FP64_PEAK_SPEC_TFLOPS for a in ach],
+            "E": e[0], "normF": e[1], "eig_info": res.info, "rc": res.rc,
+            "timed": "one hosvd_fused + error_fused call (CUDA events), after a warm-up Gram; gram_ms from "
+                     "three separate tucker_gram_fused calls"}
 
 
 # ------------------------------------------------------------------------------ oracle arm ----

@@ -226,8 +226,11 @@ __global__ void __launch_bounds__(NCW * 32, 1)
 // mode 1: i-planes, [Pc][n2][n3]; see fill_eval.cuh) are generated by all CTAs into a 2-slot ring
 // sized to stay L2-resident (~2 x 32 MB), then consumed by the same TMA + DMMA mainloop as the
 // materialised Gram (the chunk is the sub-tensor whose mode-m Gram is the chunk's contribution).
-// One persistent cooperative grid of T x S CTAs (one per SM); per chunk c:
-//     generate chunk c+1 -> slot (c+1)&1  |  consume chunk c from slot c&1  |  grid barrier
+// One persistent cooperative grid, one CTA per SM: T x S MMA CTAs (output tile x split-K slice) and
+// the remaining SMs as generator CTAs; per chunk c:
+//     generators: chunk c+1 -> slot (c+1)&1   ||   MMA CTAs: consume chunk c from slot c&1
+//     grid barrier
+// (with fewer than 2 spare SMs every CTA generates before consuming).
 // Accumulators stay in registers across all chunks; the split-K partials and the fixed-order
 // k_gram_reduce are those of the materialised path.  Generic-proxy stores are ordered before the
 // async-proxy (TMA) reads of other CTAs by fence.proxy.async + the release/acquire grid barrier.
@@ -240,6 +243,8 @@ struct FusedArgs {
     double* slot[2];
     int64_t nchunks;
     unsigned int* bar;  // grid-barrier counter (zeroed before the launch)
+    int nmma;           // CTAs 0..nmma-1: output tile x split-K slice (T x S)
+    int ngen;           // CTAs nmma..: dedicated generators (0: every CTA generates)
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
@@ -271,17 +276,18 @@ __global__ void __launch_bounds__(NCW * 32, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * TILE);
     uint64_t* empty = full + STAGES;
     const Args& a = f.a;
-    int ti, tj;
-    tile_decode(blockIdx.x, ti, tj);
+    const int cta = blockIdx.x, ncta = gridDim.x;
+    const bool mma = cta < f.nmma;
+    const int T = f.nmma / a.S;
+    const int tile = cta % T, s = cta / T;
+    int ti = 0, tj = 0;
+    if (mma) tile_decode(tile, ti, tj);
     const bool diag = (ti == tj);
-    const int s = blockIdx.y;
     const int64_t kb0 = (int64_t)s * a.nkb / a.S, kb1 = (int64_t)(s + 1) * a.nkb / a.S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
-    const unsigned int ncta = gridDim.x * gridDim.y;
-    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
 
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && mma) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NCW);
@@ -294,11 +300,15 @@ __global__ void __launch_bounds__(NCW * 32, 1)
 
     ChunkGeo geo = f.geo;
     const int64_t items = chunk_items(geo);
-    const int64_t step = (int64_t)ncta * blockDim.x, lo = cta * blockDim.x + threadIdx.x;
+    // chunk 0: every CTA generates; later chunks: the generator CTAs (if any) while the MMA CTAs
+    // consume the previous chunk, else everyone before consuming
     geo.g0 = 0;
-    gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[0], lo, items, step);
+    gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[0], (int64_t)cta * blockDim.x + threadIdx.x, items,
+              (int64_t)ncta * blockDim.x);
     unsigned int nbar = 1;
     grid_barrier(f.bar, nbar * ncta);
+    const bool gen_role = f.ngen > 0 ? !mma : true;
+    const int gidx = f.ngen > 0 ? cta - f.nmma : cta, gcount = f.ngen > 0 ? f.ngen : ncta;
 
     double acc[8][4][2];
 #pragma unroll
@@ -307,17 +317,22 @@ __global__ void __launch_bounds__(NCW * 32, 1)
         for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
     int64_t it = 0;
     for (int64_t c = 0; c < f.nchunks; ++c) {
-        if (c + 1 < f.nchunks) {
+        if (gen_role && c + 1 < f.nchunks) {
             geo.g0 = (c + 1) * geo.Pc;
-            gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[(c + 1) & 1], lo, items, step);
+            gen_chunk(geo, f.kp, f.cheb, f.x2, f.slot[(c + 1) & 1], (int64_t)gidx * blockDim.x + threadIdx.x, items,
+                      (int64_t)gcount * blockDim.x);
         }
-        gram_consume<MODE>((c & 1) ? &map1 : &map0, a, ti, tj, diag, kb0, kb1, it, sA, sB, full, empty, acc);
-        it += kb1 - kb0;
+        if (mma) {
+            gram_consume<MODE>((c & 1) ? &map1 : &map0, a, ti, tj, diag, kb0, kb1, it, sA, sB, full, empty, acc);
+            it += kb1 - kb0;
+        }
         ++nbar;
         grid_barrier(f.bar, nbar * ncta);
     }
-    double* P = a.part + ((size_t)blockIdx.x * a.S + s) * (BM * BM);
-    store_partial<MODE == 2>(P, acc, wm, wn, r, q);
+    if (mma) {
+        double* P = a.part + ((size_t)tile * a.S + s) * (BM * BM);
+        store_partial<MODE == 2>(P, acc, wm, wn, r, q);
+    }
 }
 
 // -------------------------------------------------------------------------- cp.async variant
@@ -614,9 +629,11 @@ int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const dou
         if (!ok) return TUCKER_ERR_CUDA;
     }
     TK_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned int), st));
+    f.nmma = fp.T * fp.S;
+    f.ngen = (kNumSMs - f.nmma >= 2) ? kNumSMs - f.nmma : 0;
     const size_t sm = smem_tma();
     void* args[3] = {&maps[0], &maps[1], &f};
-    const dim3 grid((unsigned)fp.T, (unsigned)fp.S);
+    const dim3 grid((unsigned)(f.nmma + f.ngen));
     const void* fn = mode == 0 ? (const void*)k_gram_fused<0> : mode == 1 ? (const void*)k_gram_fused<1>
                                                                           : (const void*)k_gram_fused<2>;
     TK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
