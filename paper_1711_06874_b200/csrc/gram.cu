@@ -47,6 +47,7 @@ struct Args {
     int64_t nkb3;  // ceil(n3/16) (mode 1)
     const double* F;
     double* part;  // [T][S][BM*BM]
+    int m3d;       // mode 2: 3-D tensor map (see make_mmajor_map)
 };
 
 __device__ __forceinline__ void tile_decode(int t, int& ti, int& tj) {
@@ -138,6 +139,9 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* map, const Args& 
         const int i = (int)(kb / a.nkb3), kk = (int)(kb % a.nkb3) * BK;
         tma_load_3d(dA, map, bar, kk, ti * BM, i);
         if (!diag) tma_load_3d(dB, map, bar, kk, tj * BM, i);
+    } else if (a.m3d) {  // one 3-D box {16 m, 16 k, 8 m-chunks} lands as [8][16][16] directly
+        tma_load_3d(dA, map, bar, 0, (int)(kb * BK), ti * (BM / 16));
+        if (!diag) tma_load_3d(dB, map, bar, 0, (int)(kb * BK), tj * (BM / 16));
     } else {
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
@@ -145,6 +149,22 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* map, const Args& 
             if (!diag) tma_load_2d(dB + b * BK * 16, map, bar, tj * BM + 16 * b, (int)(kb * BK));
         }
     }
+}
+
+// Mode-2 (M-major) tensor map over a row-major (rows x n3) matrix: preferably the 3-D view
+// {16, rows, n3/16} with strides {8 n3, 128} B and box {16, 16, 8} (one TMA per operand per
+// stage); else the 2-D view with 8 boxes of {16, 16}.  Returns 0/1 = 3-D used, -1 on failure.
+static int make_mmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t n3) {
+    if (n3 % 16 == 0) {
+        uint64_t dims[3] = {16, rows, n3 / 16};
+        uint64_t strides[2] = {n3 * 8, 128};
+        uint32_t box[3] = {16, BK, BM / 16};
+        if (make_tmap_f64(map, base, 3, dims, strides, box)) return 1;
+    }
+    uint64_t dims[2] = {n3, rows};
+    uint64_t strides[1] = {n3 * 8};
+    uint32_t box[2] = {16, BK};
+    return make_tmap_f64(map, base, 2, dims, strides, box) ? 0 : -1;
 }
 
 // Mainloop over k-blocks [kb0, kb1) for output tile (ti, tj); `it0` is the ring iteration
@@ -502,10 +522,9 @@ int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* 
             uint32_t box[3] = {BK, BM, 1};
             ok = make_tmap_f64(&map, F, 3, dims, strides, box);
         } else {
-            uint64_t dims[2] = {(uint64_t)a.n3, (uint64_t)(a.n1 * a.n2)};
-            uint64_t strides[1] = {(uint64_t)(a.n3 * 8)};
-            uint32_t box[2] = {16, BK};
-            ok = make_tmap_f64(&map, F, 2, dims, strides, box);
+            const int m3 = make_mmajor_map(&map, F, (uint64_t)(a.n1 * a.n2), (uint64_t)a.n3);
+            ok = m3 >= 0;
+            a.m3d = m3 == 1;
         }
         if (!ok) return TUCKER_ERR_CUDA;
         const size_t sm = smem_tma();
@@ -621,10 +640,9 @@ int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const dou
             uint32_t box[3] = {BK, BM, 1};
             ok = make_tmap_f64(&maps[sl], f.slot[sl], 3, dims, strides, box);
         } else {
-            uint64_t dims[2] = {(uint64_t)vn[2], (uint64_t)(vn[0] * vn[1])};
-            uint64_t strides[1] = {(uint64_t)(vn[2] * 8)};
-            uint32_t box[2] = {16, BK};
-            ok = make_tmap_f64(&maps[sl], f.slot[sl], 2, dims, strides, box);
+            const int m3 = make_mmajor_map(&maps[sl], f.slot[sl], (uint64_t)(vn[0] * vn[1]), (uint64_t)vn[2]);
+            ok = m3 >= 0;
+            a.m3d = m3 == 1;
         }
         if (!ok) return TUCKER_ERR_CUDA;
     }
