@@ -38,8 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1024)
-    ap.add_argument("--r", type=int, default=40)
+    ap.add_argument("--grid-n", "--n", dest="n", type=int, default=1024)
+    ap.add_argument("--tucker-rank", "--r", dest="r", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-host-tensor", action="store_true")
@@ -110,6 +110,23 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- rank helpers ----
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a per-rank scalar over the process group (device time = max over ranks)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(points_per_rank: int, world: int, ms_step_max: float) -> float:
+    """Weak scaling, replicas: every rank solves its own problem; value = all ranks' points / time."""
+    return world * points_per_rank / (ms_step_max * 1e-3)
 
 
 # ------------------------------------------------------------------------------ our GPU arm ----
@@ -195,11 +212,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms_total = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_total = float(tt.item())
+    ms_total = max_over_ranks(t0.elapsed_time(t1), world, dev)
     ms_step = ms_total / K
 
     # per-stage times (ms) averaged over the timed steps
@@ -224,7 +237,7 @@ def run_ours(args, rank, world, local):
             traffic = None
     total_flops = sum(gram_flops) + 2.0 * N * rr * 2  # Gram + TTM1 + error reconstruction (algorithmic)
     result = {
-        "metric": METRIC, "value": world * N / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "metric": METRIC, "value": whole_job_rate(N, world, ms_step), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2", "grid": [n, n, n], "box": [-1.0, 1.0],
@@ -256,13 +269,9 @@ def run_ours(args, rank, world, local):
             T.approximate(grid, kern, ranks, F, ws, host, stream)
         a1.record(stream)
         torch.cuda.synchronize()
-        ms_e2e = a0.elapsed_time(a1) / ke
-        if world > 1:
-            tt = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms_e2e = float(tt.item())
+        ms_e2e = max_over_ranks(a0.elapsed_time(a1) / ke, world, dev)
         param_bytes = ctypes.sizeof(g_c) + ctypes.sizeof(k_c) + ctypes.sizeof(r_c)
-        result["e2e"] = {"value": world * N / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": param_bytes,
+        result["e2e"] = {"value": whole_job_rate(N, world, ms_e2e), "unit": UNIT, "h2d_bytes_per_step": param_bytes,
                          "d2h_bytes_per_step": host.d2h_bytes, "ms_per_step": ms_e2e,
                          "call": "tucker_approximate (grid + kernel spec in, U/core/sigma/E to pinned host)"}
         # variant: the tensor F already sampled on the host (pinned) -> H2D copy inside the timed region
