@@ -166,6 +166,21 @@ TUCKER_API int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* 
                        const double* U1, const double* U2, const double* U3, const double* core, double* out3,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT f1: Tucker-ALS (HOOI) sweeps, the paper's second stage after HOSVD: for each
+ * mode m in turn U_m <- leading r_m left singular vectors of the single-hole unfolding
+ * (F x_{q != m} U_q^T)_(m) (top eigenvectors of its Gram), modes 1, 2, 3 in order; `sweeps`
+ * (>= 1) sweeps; then core = F x1 U1^T x2 U2^T x3 U3^T with the final factors.
+ *   F (dev, n1 x n2 x n3), U_m (dev, n_m x r_m, in: initial factors, e.g. tucker_hosvd's; out:
+ *   refined, sign rule R6), core (dev out), sigma_m (dev out: singular values of the last
+ *   single-hole unfoldings).  Workspace (dev) >= tucker_workspace_size_als(grid, r).
+ *   Errors: INVALID_ARG (null, sweeps < 1), RANK, SIZE, UNSUPPORTED (r_2 or r_3 > 64, r_m > 56),
+ *   NOCONV (best iterate returned), CUDA.  Synchronises `stream` once per mode and sweep. */
+TUCKER_API size_t tucker_workspace_size_als(const tucker_grid* grid, const int32_t r[3]);
+TUCKER_API int tucker_als(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1, double* U2,
+               double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, int32_t sweeps,
+               void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
 TUCKER_API int64_t tucker_last_launch_count(void);
 

@@ -413,6 +413,26 @@ int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, con
                              st);
 }
 
+size_t tucker_workspace_size_als(const tucker_grid* grid, const int32_t r[3]) {
+    if (check_grid(grid) != TUCKER_OK || !r || check_ranks(grid, r) != TUCKER_OK) return 0;
+    return als_ws_bytes(grid->n, r);
+}
+
+int tucker_als(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1, double* U2, double* U3,
+               double* core, double* sigma1, double* sigma2, double* sigma3, int32_t sweeps, void* ws,
+               size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws || sweeps < 1)
+        return TUCKER_ERR_INVALID_ARG;
+    if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    if (info) std::memset(info, 0, sizeof(*info));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    return launch_als(grid->n, r, F, U, core, S, sweeps, ws, ws_bytes, static_cast<cudaStream_t>(stream), info);
+}
+
 int64_t tucker_last_launch_count(void) { return launch_counter(); }
 
 const char* tucker_strerror(int code) {

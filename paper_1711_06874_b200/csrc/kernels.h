@@ -80,11 +80,19 @@ struct FusedGen {
 };
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
-                         size_t ws_bytes, cudaStream_t st);
+                         size_t ws_bytes, cudaStream_t st, double* t1_out = nullptr, double* t2_out = nullptr);
+// Tucker-ALS (f1): T1 = F x3 U3^T ((n1 n2) x r3) and Y1 = T1 x2 U2^T (n1 x r2 x r3), both stored.
+int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
+                     double* T1, double* Y1, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen, const double* U1,
                       const double* U2, const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes,
                       cudaStream_t st);
 size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs);
+
+// NEXT f1: Tucker-ALS sweeps from initial factors U (in/out); core and sigma of the last sweep.
+size_t als_ws_bytes(const int64_t n[3], const int32_t r[3]);
+int launch_als(const int64_t n[3], const int32_t r[3], const double* F, double* const U[3], double* core,
+               double* const sigma[3], int sweeps, void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info);
 
 // Relative Frobenius error {E, ||F||, ||F-Ft||}.
 size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]);

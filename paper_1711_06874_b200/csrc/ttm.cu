@@ -97,6 +97,7 @@ struct Args12 {
     int64_t n2, n3;
     int R, r2, JT;
     int64_t i_off;     // global index of slab 0 of F (fused path: F is a chunk of slabs)
+    double* t1_out;    // optional: T1 = F x3 U3^T stored as (n1 n2) x R (Tucker-ALS needs it)
 };
 
 // Bp[kb][c][kk] (swizzled) = U3[16 kb + kk][c]   (0 outside c < R, k < n3)
@@ -225,6 +226,22 @@ __global__ void __launch_bounds__(256, 1) k_ttm12(const __grid_constant__ CUtens
         }
         cp_async_wait<0>();
         __syncthreads();
+    }
+
+    if (g.t1_out) {  // optional T1 rows for the Tucker-ALS single-hole products
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int64_t j = m0 + warp * 32 + mi * 8 + r;
+            if (j < M) {
+                double* row = g.t1_out + ((g.i_off + i) * M + j) * R;
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) {
+                    const int c = ni * 8 + 2 * q;
+                    if (c < R) row[c] = acc[mi][ni][0];
+                    if (c + 1 < R) row[c + 1] = acc[mi][ni][1];
+                }
+            }
+        }
     }
 
     // Epilogue on DMMA: P (r2 x R) = U2[m0:m0+256]^T T1_tile, rows in chunks of CH; leading
@@ -359,10 +376,16 @@ int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, con
     return launch_ttm_core_impl(n, r, F, nullptr, U1, U2, U3, core, ws, ws_bytes, st);
 }
 
+// Tucker-ALS first pass: T1 = F x3 U3^T ((n1 n2) x r3, stored) and Y1 = T1 x2 U2^T (n1 x r2 x r3).
+int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
+                     double* T1, double* Y1, void* ws, size_t ws_bytes, cudaStream_t st) {
+    return launch_ttm_core_impl(n, r, F, nullptr, nullptr, U2, U3, nullptr, ws, ws_bytes, st, T1, Y1);
+}
+
 // Core with F either materialised (F != nullptr) or generated slab-chunk by slab-chunk (gen).
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
-                         size_t ws_bytes, cudaStream_t st) {
+                         size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out) {
     const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
     if (ws_bytes < ttm_ws_bytes(n, r) + chunk_b) return TUCKER_ERR_SIZE;
     if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
@@ -373,14 +396,14 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
     w += chunk_b;
     double* part = reinterpret_cast<double*>(w);
     w += align_up(JT > 1 ? JT * t2b : 0, 256);
-    double* T2 = reinterpret_cast<double*>(w);
+    double* T2 = t2_out ? t2_out : reinterpret_cast<double*>(w);
     w += align_up(t2b, 256);
     double* Bp = reinterpret_cast<double*>(w);
     const int RP = ((r[2] + 7) / 8) * 8;
     ttm1::k_pack_u3<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(n[2], ttm1::BK) * RP * ttm1::BK, 256), 1024), 256, 0,
                       st>>>(U3, n[2], r[2], RP, Bp);
     TK_CHECK_LAUNCH();
-    ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT, 0};
+    ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT, 0, t1_out};
     if (!gen) {
         TK_RC(launch_ttm12(a, n[0], st));
     } else {
@@ -401,6 +424,7 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
                                                                                               T2);
         TK_CHECK_LAUNCH();
     }
+    if (!core) return TUCKER_OK;  // (Tucker-ALS: T1 / Y1 only)
     // TTM3: core (r1 x r2r3) = U1^T (r1 x n1) * T2 (n1 x r2r3)
     SmallGemm g3{r[0], (int64_t)r[1] * r[2], n[0], 1, U1, 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
                  (int64_t)r[1] * r[2], 1, 0};

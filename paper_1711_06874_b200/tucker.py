@@ -22,8 +22,8 @@ ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED"}
 EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
-           "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_last_launch_count",
-           "tucker_strerror")
+           "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
+           "tucker_als", "tucker_last_launch_count", "tucker_strerror")
 
 
 class TuckerError(RuntimeError):
@@ -77,6 +77,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_gram_fused": (ctypes.c_int, [pg, pk, i32, vp, vp, sz, vp]),
         "tucker_hosvd_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_error_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "tucker_workspace_size_als": (sz, [pg, pr]),
+        "tucker_als": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
         "tucker_last_launch_count": (i64, []),
         "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
@@ -235,6 +237,30 @@ def error(grid, ranks, F, U, core, ws=None, stream=None) -> torch.Tensor:
     _check(lib.tucker_error(ctypes.byref(g), cranks(ranks), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
                             _ptr(core), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)), "tucker_error")
     return out
+
+
+# ------------------------------------------------------------------ NEXT f1: Tucker-ALS
+def als(grid, ranks, F: torch.Tensor, U_init, sweeps: int, ws: torch.Tensor | None = None, stream=None) -> HosvdResult:
+    """Tucker-ALS sweeps from initial factors U_init (copied); returns refined U, core,
+    sigma of the last single-hole unfoldings."""
+    lib = load()
+    _dev(F, "F")
+    r = tuple(int(v) for v in ranks)
+    U = [u[:, : r[m]].contiguous().clone() for m, u in enumerate(U_init)]
+    S = [torch.empty(r[m], dtype=torch.float64, device=F.device) for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device=F.device)
+    if ws is None:
+        g0 = cgrid(grid)
+        ws = torch.empty(int(lib.tucker_workspace_size_als(ctypes.byref(g0), cranks(r))), dtype=torch.uint8,
+                         device=F.device)
+    info = CInfo()
+    g = cgrid(grid)
+    rc = lib.tucker_als(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core),
+                        _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), int(sweeps), _ptr(ws), ws.numel(), _stream(stream),
+                        ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_als")
+    return HosvdResult(U, core, S, info.as_dict(), rc)
 
 
 # ------------------------------------------------------------------ a-7 fused (F never stored)
