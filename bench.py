@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-host-tensor", action="store_true")
     ap.add_argument("--no-fused", action="store_true", help="skip the 2048^3 fused (F never stored) line")
+    ap.add_argument("--no-als", action="store_true", help="skip the Tucker-ALS (NEXT f1) line")
     ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
@@ -296,6 +297,21 @@ def run_ours(args, rank, world, local):
             except RuntimeError as e:  # pinned allocation failure etc.
                 result["e2e_host_tensor"] = {"unavailable": str(e)[:200]}
     result["clocks"] = clk.summary()
+    if not args.no_als and world == 1:
+        res = T.hosvd(grid, ranks, F, ws, stream)
+        T.als(grid, ranks, F, res.U, 1, stream=stream)  # warm-up (workspace allocation, first launches)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        al = T.als(grid, ranks, F, res.U, 2, stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ea = T.error(grid, ranks, F, al.U, al.core, ws, stream).cpu().tolist()
+        eh = T.error(grid, ranks, F, res.U, res.core, ws, stream).cpu().tolist()
+        ms_als = a0.elapsed_time(a1) / 2
+        result["als"] = {"what": "Tucker-ALS / HOOI sweep (NEXT f1, P:571-579) on the same 1024^3 tensor, ranks 40",
+                         "ms_per_sweep": ms_als, "points_per_s_per_sweep": N / (ms_als * 1e-3),
+                         "E_hosvd": eh[0], "E_after_2_sweeps": ea[0], "rc": al.rc}
     if not args.no_fused and world == 1:
         del F
         torch.cuda.empty_cache()
