@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-host-tensor", action="store_true")
     ap.add_argument("--no-fused", action="store_true", help="skip the 2048^3 fused (F never stored) line")
     ap.add_argument("--no-als", action="store_true", help="skip the Tucker-ALS (NEXT f1) line")
+    ap.add_argument("--no-sym", action="store_true", help="skip the symmetry-exploiting (NEXT f3) line")
     ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
@@ -312,9 +313,12 @@ def run_ours(args, rank, world, local):
         result["als"] = {"what": "Tucker-ALS / HOOI sweep (NEXT f1, P:571-579) on the same 1024^3 tensor, ranks 40",
                          "ms_per_sweep": ms_als, "points_per_s_per_sweep": N / (ms_als * 1e-3),
                          "E_hosvd": eh[0], "E_after_2_sweeps": ea[0], "rc": al.rc}
-    if not args.no_fused and world == 1:
+    if not args.no_fused and world == 1 or not args.no_sym and world == 1:
         del F
         torch.cuda.empty_cache()
+    if not args.no_sym and world == 1:
+        result["symmetric"] = [run_sym(T, nn, rr, stream) for nn in (n, 2 * n)]
+    if not args.no_fused and world == 1:
         result["fused"] = run_fused(T, args.fused_n, rr, stream)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
@@ -358,6 +362,42 @@ def run_fused(T, n: int, rr: int, stream) -> dict:
             "E": e[0], "normF": e[1], "eig_info": res.info, "rc": res.rc,
             "timed": "one hosvd_fused + error_fused call (CUDA events), after a warm-up Gram; gram_ms from "
                      "three separate tucker_gram_fused calls"}
+
+
+def run_sym(T, n: int, rr: int, stream, reps: int = 3) -> dict:
+    """NEXT f3: the whole path (octant fill, 3 Grams, 3 eigensolves, core, error) on the weighted
+    octant tensor of a centred grid; algorithmic work is that of the octant (reported apart)."""
+    import torch
+
+    from tucker_inputs import GridSpec, KernelSpec
+    grid = GridSpec.cube(n, 1.0)
+    kern = KernelSpec.matern(1.5, 0.2)
+    ranks = (rr, rr, rr)
+    N = grid.points
+    h = (n + 1) // 2
+    lib = T.load()
+    import ctypes
+    g = T.cgrid(grid)
+    ws = torch.empty(int(lib.tucker_workspace_size_sym(ctypes.byref(g), T.cranks(ranks))), dtype=torch.uint8,
+                     device="cuda")
+    res, err = T.hosvd_sym(grid, kern, ranks, ws, stream)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        res, err = T.hosvd_sym(grid, kern, ranks, ws, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    Nh = h ** 3
+    flops = 3 * Nh * (h + 1) + 2.0 * Nh * rr * 2
+    e = err.cpu().tolist()
+    return {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2_symmetric", "grid": [n, n, n], "ranks": list(ranks),
+            "value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "algorithmic_flops_per_step": flops, "fp64_tflops_algorithmic": flops / (ms * 1e-3) / 1e12,
+            "E": e[0], "normF": e[1], "rc": res.rc,
+            "note": "weighted-octant reduction (exact on centred grids, DESIGN f3): N/8 points carry the "
+                    "work; Gram flops 3 (N/8)(n/2+1), TTM + error 4 (N/8) r"}
 
 
 # ------------------------------------------------------------------------------ oracle arm ----

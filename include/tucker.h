@@ -181,6 +181,22 @@ TUCKER_API int tucker_als(const tucker_grid* grid, const int32_t r[3], const dou
                double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, int32_t sweeps,
                void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT f3: symmetry-exploiting HOSVD for centred grids (lo = -hi on every axis; not in the paper).
+ * F is even in each index, so the path runs on the weighted octant tensor
+ * F_w[i,j,k] = sqrt(w_i w_j w_k) F[i,j,k] (i < ceil(n1/2) ..., w = 2, or 1 for the middle index of
+ * an odd axis): its mode-m Grams have the nonzero spectrum of G_m, their eigenvectors y give the
+ * (even) factors u = y / sqrt(w) mirrored to full length, and core and error equal those of F
+ * (f3).  Outputs as tucker_hosvd (full-length U_m, sign rule R6 on the full vector,
+ * core consistent with them) plus err3 (dev, nullable) = {E, ||F||, ||F - Ft||}.
+ * Requires r_m <= ceil(n_m/2) (the odd eigenvectors have eigenvalue 0): else TUCKER_ERR_RANK.
+ * Non-centred grid: TUCKER_ERR_UNSUPPORTED.  Workspace >= tucker_workspace_size_sym(grid, r);
+ * no F argument (the octant is generated into the workspace, N/8 doubles). */
+TUCKER_API size_t tucker_workspace_size_sym(const tucker_grid* grid, const int32_t r[3]);
+TUCKER_API int tucker_hosvd_sym(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
+                     double* U1, double* U2, double* U3, double* core, double* sigma1, double* sigma2,
+                     double* sigma3, double* err3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
 TUCKER_API int64_t tucker_last_launch_count(void);
 

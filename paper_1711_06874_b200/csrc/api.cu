@@ -433,6 +433,29 @@ int tucker_als(const tucker_grid* grid, const int32_t r[3], const double* F, dou
     return launch_als(grid->n, r, F, U, core, S, sweeps, ws, ws_bytes, static_cast<cudaStream_t>(stream), info);
 }
 
+size_t tucker_workspace_size_sym(const tucker_grid* grid, const int32_t r[3]) {
+    if (check_grid(grid) != TUCKER_OK || !r) return 0;
+    return sym_ws_bytes(*grid, r);
+}
+
+int tucker_hosvd_sym(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* U1,
+                     double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
+                     double* err3, void* ws, size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (!grid_centred(*grid)) return TUCKER_ERR_UNSUPPORTED;
+    for (int a = 0; a < 3; ++a)
+        if (r[a] > (grid->n[a] + 1) / 2) return TUCKER_ERR_RANK;
+    if (info) std::memset(info, 0, sizeof(*info));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    return launch_hosvd_sym(*grid, *kernel, r, U, core, S, err3, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                            info);
+}
+
 int64_t tucker_last_launch_count(void) { return launch_counter(); }
 
 const char* tucker_strerror(int code) {

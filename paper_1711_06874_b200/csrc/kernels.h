@@ -94,6 +94,13 @@ size_t als_ws_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_als(const int64_t n[3], const int32_t r[3], const double* F, double* const U[3], double* core,
                double* const sigma[3], int sweeps, void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info);
 
+// NEXT f3: symmetry-exploiting path on centred grids (sym.cu): the hot path on the weighted
+// octant tensor, factors expanded to full length.  err3 (dev, nullable) <- {E, ||F||, ||F-Ft||}.
+size_t sym_ws_bytes(const tucker_grid& g, const int32_t r[3]);
+int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_t r[3], double* const U[3],
+                     double* core, double* const sigma[3], double* err3, void* ws, size_t ws_bytes, cudaStream_t st,
+                     tucker_info* info);
+
 // Relative Frobenius error {E, ||F||, ||F-Ft||}.
 size_t err_ws_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,

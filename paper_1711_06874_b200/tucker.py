@@ -23,7 +23,8 @@ ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3
 EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
-           "tucker_als", "tucker_last_launch_count", "tucker_strerror")
+           "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_last_launch_count",
+           "tucker_strerror")
 
 
 class TuckerError(RuntimeError):
@@ -79,6 +80,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_error_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_workspace_size_als": (sz, [pg, pr]),
         "tucker_als": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
+        "tucker_workspace_size_sym": (sz, [pg, pr]),
+        "tucker_hosvd_sym": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_last_launch_count": (i64, []),
         "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
@@ -261,6 +264,29 @@ def als(grid, ranks, F: torch.Tensor, U_init, sweeps: int, ws: torch.Tensor | No
     if rc not in (0, 5):
         _check(rc, "tucker_als")
     return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+# ------------------------------------------------------------------ NEXT f3: symmetric variant
+def hosvd_sym(grid, kernel, ranks, ws: torch.Tensor | None = None, stream=None):
+    """Symmetry-exploiting HOSVD + error on a centred grid (weighted octant); returns
+    (HosvdResult, err3 tensor {E, ||F||, ||F-Ft||})."""
+    lib = load()
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device="cuda") for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device="cuda") for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device="cuda")
+    err = torch.empty(3, dtype=torch.float64, device="cuda")
+    g, k = cgrid(grid), ckernel(kernel)
+    if ws is None:
+        ws = torch.empty(int(lib.tucker_workspace_size_sym(ctypes.byref(g), cranks(r))), dtype=torch.uint8,
+                         device="cuda")
+    info = CInfo()
+    rc = lib.tucker_hosvd_sym(ctypes.byref(g), ctypes.byref(k), cranks(r), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
+                              _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(err), _ptr(ws), ws.numel(),
+                              _stream(stream), ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd_sym")
+    return HosvdResult(U, core, S, info.as_dict(), rc), err
 
 
 # ------------------------------------------------------------------ a-7 fused (F never stored)

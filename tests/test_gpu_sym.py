@@ -1,0 +1,122 @@
+"""NEXT f3 on the GPU: the symmetry-exploiting path (tucker_hosvd_sym) on centred grids.
+
+The weighted-octant reduction is exact (DESIGN.md f3), so its outputs meet the same bars as the
+generic path: T1 eigenvalues, T2 gap-separated columns, T2' orthonormality, T3 core block, T4
+error — against the oracle's HOSVD of the full tensor (small grids) and against the generic GPU
+path (1024^3).  Also: factors are even, odd sizes (middle index weight 1) work, and the
+documented error codes (r > ceil(n/2), off-centre grid).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tucker_inputs import GridSpec, KernelSpec  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_1711_06874_b200 import tucker
+    tucker.load()
+    return tucker
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+def _check(lam_ref, U_ref, core_ref, E_ref, res, err, r):
+    resolved = True
+    blocks = []
+    for m in range(3):
+        lam = to_np(res.sigma[m]) ** 2
+        lr = lam_ref[m]
+        pos = lr[: r[m]] > 0
+        assert np.all(np.abs(lam[pos] - lr[: r[m]][pos]) <= 1e-11 * lr[: r[m]][pos] + 1e-14 * lr[0]), m
+        U = to_np(res.U[m])
+        assert np.max(np.abs(U.T @ U - np.eye(r[m]))) <= 1e-12
+        assert np.array_equal(U, U[::-1]), "factors must be even"
+        for c in range(r[m]):
+            others = np.delete(lr, c)
+            if lr[c] >= 1e-10 * lr[0] and np.min(np.abs(others - lr[c])) >= 1e-6 * lr[0]:
+                assert np.max(np.abs(U[:, c] - U_ref[m][:, c])) <= 1e-9, (m, c)
+        resolved &= r[m] <= int(np.sum(lr[: r[m]] >= 1e-12 * lr[0]))
+        blocks.append(int(np.sum(lr[: r[m]] >= 1e-10 * lr[0])))
+    a, b, c = blocks
+    cg, co = to_np(res.core)[:a, :b, :c], core_ref[:a, :b, :c]
+    assert np.linalg.norm(cg - co) <= 1e-10 * np.linalg.norm(co)
+    assert abs(np.linalg.norm(to_np(res.core)) - np.linalg.norm(core_ref)) <= 1e-12 * np.linalg.norm(core_ref)
+    tol = 1e-12 if resolved else max(1e-12, 1e-15 / E_ref)
+    assert abs(err[0] - E_ref) <= tol, (err[0], E_ref)
+
+
+CASES = [
+    (GridSpec.cube(32, 1.0), KernelSpec.matern(0.5, 0.5), (8, 8, 8)),                              # config 1
+    (GridSpec((36, 40, 44), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)), KernelSpec.matern(0.7, 0.5), (10, 9, 8)),
+    (GridSpec((33, 31, 35), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)), KernelSpec.slater(1.0, 1.0), (7, 8, 6)),  # odd
+    (GridSpec.cube(129, 5.0), KernelSpec.slater(1.0, 1.0), (10, 10, 10)),                          # Table 2 grid
+]
+
+
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_sym_vs_oracle(T, orc, ci):
+    g, k, r = CASES[ci]
+    res, err = T.hosvd_sym(g, k, r)
+    assert res.rc == 0, res.info
+    F = orc.fill(orc.Grid(g.n, g.lo, g.hi), orc.Kernel(k.family, k.sigma2, k.ell, k.nu, k.lam, k.p, k.flags))
+    h = orc.hosvd(F, r)
+    E_o, nF, _ = orc.tucker_error(F, *h.U, h.core)
+    e = to_np(err)
+    assert abs(e[1] - nF) <= 1e-14 * nF
+    _check(h.lam, h.U, h.core, E_o, res, e, r)
+
+
+@pytest.mark.parametrize("r", [10, 40])
+def test_sym_vs_generic_1024(T, r):
+    g, k, rr = GridSpec.cube(1024, 1.0), KernelSpec.matern(1.5, 0.2), (r, r, r)
+    F = T.fill(g, k)
+    ref = T.hosvd(g, rr, F)
+    e_ref = to_np(T.error(g, rr, F, ref.U, ref.core))
+    del F
+    torch.cuda.empty_cache()
+    res, err = T.hosvd_sym(g, k, rr)
+    assert res.rc == 0
+    lam_ref = [to_np(s) ** 2 for s in ref.sigma]
+    # the generic GPU path is the reference here; its trailing noise eigenvalues are not pinned
+    e = to_np(err)
+    for m in range(3):
+        lam = to_np(res.sigma[m]) ** 2
+        assert np.all(np.abs(lam - lam_ref[m]) <= 1e-11 * lam_ref[m] + 1e-14 * lam_ref[m][0]), m
+        U, Ur = to_np(res.U[m]), to_np(ref.U[m])
+        for c in range(rr[m]):
+            lr = lam_ref[m]
+            others = np.delete(lr, c)
+            if lr[c] >= 1e-6 * lr[0] and np.min(np.abs(others - lr[c])) >= 1e-6 * lr[0]:
+                assert np.max(np.abs(U[:, c] - Ur[:, c])) <= 1e-9, (m, c)
+    assert abs(e[1] - e_ref[1]) <= 1e-13 * e_ref[1]
+    # T4 with the resolution threshold raised to 1e-11 (DESIGN R14: the generic Gram at K = n^2 =
+    # 1M terms carries ~1e-13 relative noise, SURVEY §8c allows tau = 1e-11 then)
+    resolved = all(rr[m] <= int(np.sum(lam_ref[m][: rr[m]] >= 1e-11 * lam_ref[m][0])) for m in range(3))
+    if resolved:
+        assert abs(e[0] - e_ref[0]) <= 1e-12, (e, e_ref)
+    else:
+        # noise regime: the generic Gram route mixes odd null vectors (exact eigenvalue 0) into the
+        # trailing columns; the symmetric path excludes them analytically, so its error is never
+        # higher (1024^3: r = 10 5.96844e-7 vs 5.96867e-7; r = 40 1.29e-8 vs 6.07e-8)
+        assert e[0] <= e_ref[0] * (1 + 1e-12), (e, e_ref)
+
+
+def test_sym_error_codes(T):
+    import ctypes
+    lib = T.load()
+    d = ctypes.c_void_p(1)
+    k = T.ckernel(KernelSpec.matern(1.5, 0.2))
+    g = T.cgrid(GridSpec.cube(16, 1.0))
+    assert lib.tucker_hosvd_sym(ctypes.byref(g), ctypes.byref(k), T.cranks((9, 8, 8)), d, d, d, d, d, d, d, None, d,
+                                1 << 40, None, None) == 3
+    off = T.cgrid(GridSpec((16, 16, 16), (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0)))
+    assert lib.tucker_hosvd_sym(ctypes.byref(off), ctypes.byref(k), T.cranks((4, 4, 4)), d, d, d, d, d, d, d, None,
+                                d, 1 << 40, None, None) == 7
