@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "tucker_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-MATERN, SLATER = 0, 1
+MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
 FORCE_GENERAL_BESSEL = 2
 
 
@@ -132,6 +132,11 @@ class Kernel:
     @staticmethod
     def slater(lam=1.0, p=1.0, sigma2=1.0):
         return Kernel(SLATER, sigma2, 1.0, 0.5, lam, p, 0)
+
+    @staticmethod
+    def spectral(alpha, nu, sigma2=1.0):
+        """Matérn spectral density C (alpha^2 + rho^2)^{-(nu + 3/2)}, alpha in `lam`."""
+        return Kernel(MATERN_SPECTRAL, sigma2, 1.0, nu, alpha, 1.0, 0)
 
     def c(self) -> OrcKernel:
         return OrcKernel(self.family, self.flags, self.sigma2, self.ell, self.nu, self.lam, self.p)

@@ -19,7 +19,8 @@
  *   orc_nodes           pinned (paper formula P:993, mirror exactness)
  *   orc_besselk_*       pinned (scipy.special.kv / mpmath, half-integer closed forms, recurrence,
  *                       Wronskian, small-z limit, overlap of regimes)
- *   orc_kernel_eval     pinned (closed forms vs general path, SPEC examples, C(0)=sigma^2)
+ *   orc_kernel_eval     pinned (closed forms vs general path, SPEC examples, C(0)=sigma^2;
+ *                       spectral density: exact values where alpha^2+rho^2 is a power of two)
  *   orc_fill            pinned (reflection symmetry, Gaussian separability, direct evaluation)
  *   orc_unfold/orc_gram pinned (numpy BLAS Gram, trace = ||F||^2, mode invariance on cubic grids)
  *   orc_jacobi_eig      pinned (numpy.linalg.eigh on random SPD, residuals, orthonormality)
@@ -43,7 +44,7 @@ typedef struct {
     double lo[3], hi[3];
 } orc_grid;
 
-enum { ORC_MATERN = 0, ORC_SLATER = 1 };
+enum { ORC_MATERN = 0, ORC_SLATER = 1, ORC_MATERN_SPECTRAL = 2 };
 enum { ORC_FORCE_GENERAL_BESSEL = 2 };
 
 typedef struct {
@@ -197,8 +198,15 @@ double orc_besselk(double nu, double z) { return orc_besselk_scaled(nu, z) * exp
  *   nu = 1/2 gives the exponential model; nu = 3/2, 5/2 are the half-integer closed
  *   forms of the same formula ((1+z)e^{-z}, (1+z+z^2/3)e^{-z}).
  * p-Slater, eq. (exp_p): C = sigma^2 exp(-lambda r^p); p = 2 is the
- *   Gaussian. */
+ *   Gaussian.
+ * Matérn spectral density, eq. (SD_matern) P:1046-1050 (NEXT f4): f(rho) = C (alpha^2 + rho^2)^{-(nu+d/2)}
+ *   with d = 3, rho = ||x|| (the grid is read as a frequency grid), C = sigma^2 (reading R17) and
+ *   alpha carried in the `lambda` field. */
 double orc_kernel_eval(const orc_kernel *k, double r, double r2) {
+    if (k->family == ORC_MATERN_SPECTRAL) {
+        double a2 = k->lambda * k->lambda;
+        return k->sigma2 * pow(a2 + r2, -(k->nu + 1.5));
+    }
     if (k->family == ORC_SLATER) {
         double rp = (k->p == 1.0) ? r : (k->p == 2.0) ? r2 : pow(r, k->p);
         return k->sigma2 * exp(-k->lambda * rp);
@@ -224,6 +232,10 @@ int orc_kernel_check(const orc_kernel *k) {
     }
     if (k->family == ORC_SLATER) {
         if (!(k->lambda > 0.0) || !(k->p > 0.0) || !(k->p <= 2.0)) return ORC_ERR_DOMAIN;
+        return ORC_OK;
+    }
+    if (k->family == ORC_MATERN_SPECTRAL) {
+        if (!(k->lambda > 0.0) || !(k->nu > 0.0)) return ORC_ERR_DOMAIN;
         return ORC_OK;
     }
     return ORC_ERR_ARG;

@@ -84,3 +84,60 @@ def test_fill_domain_errors(orc):
               orc.Kernel.matern(1.0, 1.0, sigma2=0.0)):
         with pytest.raises(ValueError):
             orc.fill(g, k)
+
+
+# ------------------------------------------------------------- NEXT f4: Matérn spectral density
+def test_spectral_density_exact_values(orc):
+    """f(rho) = C (alpha^2 + rho^2)^{-(nu + d/2)}, d = 3, C = sigma^2 (R17).  On the
+    n = 3 grid of [-1,1]^3 rho^2 is an integer 0..3; with alpha = 1 the base is 1..4, so the values
+    are the rationals 1/(1+rho^2)^s (exact for powers of two, correctly rounded otherwise)."""
+    from fractions import Fraction
+    g = orc.Grid.cube(3, 1.0)
+    for nu, s in ((0.5, 2), (1.5, 3), (2.5, 4)):
+        F = orc.fill(g, orc.Kernel.spectral(1.0, nu))
+        for i in range(3):
+            for j in range(3):
+                for k in range(3):
+                    rho2 = (i - 1) ** 2 + (j - 1) ** 2 + (k - 1) ** 2
+                    ref = Fraction(1, (1 + rho2) ** s)
+                    v = F[i, j, k]
+                    if (1 + rho2) in (1, 2, 4):
+                        assert v == float(ref), (nu, rho2)
+                    else:
+                        assert abs(Fraction(v) - ref) <= Fraction(np.spacing(float(ref))), (nu, rho2)
+    F2 = orc.fill(g, orc.Kernel.spectral(1.0, 0.5, sigma2=2.0))
+    assert np.array_equal(F2, 2.0 * orc.fill(g, orc.Kernel.spectral(1.0, 0.5)))
+
+
+def test_spectral_density_against_mpmath(orc):
+    g = orc.Grid((7, 6, 5), (-3.0, -2.0, -1.0), (3.0, 2.5, 1.0))
+    x = [orc.nodes(g.n[a], g.lo[a], g.hi[a]) for a in range(3)]
+    for alpha, nu in ((0.1, 0.4), (1.7, 1.1), (100.0, 0.4)):
+        F = orc.fill(g, orc.Kernel.spectral(alpha, nu))
+        for (i, j, k) in ((0, 0, 0), (3, 2, 1), (6, 5, 4), (2, 4, 0)):
+            with mp.workdps(40):
+                rho2 = mp.mpf(x[0][i]) ** 2 + mp.mpf(x[1][j]) ** 2 + mp.mpf(x[2][k]) ** 2
+                # exponent s = fl(nu + 3/2): the method's own double exponent (ln(base) amplifies a
+                # 1-ulp exponent difference to ~10 ulp of the result)
+                ref = float((mp.mpf(alpha) ** 2 + rho2) ** (-mp.mpf(nu + 1.5)))
+            assert abs(F[i, j, k] - ref) <= 4 * np.spacing(ref), (alpha, nu, i, j, k)
+
+
+def test_spectral_density_rank_depends_on_alpha(orc):
+    """the Tucker rank depends strongly on alpha — large alpha makes f nearly constant
+    (f ~ alpha^{-2s}(1 - s rho^2/alpha^2), separable to O(alpha^-4)), small alpha a sharp peak."""
+    g = orc.Grid.cube(24, 1.0)
+    err = {}
+    for alpha in (0.1, 100.0):
+        F = orc.fill(g, orc.Kernel.spectral(alpha, 0.4))
+        h = orc.hosvd(F, (8, 8, 8))
+        E = []
+        for r in range(1, 9):
+            U = [u[:, :r] for u in h.U]
+            core = orc.ttm_core(F, *U)
+            E.append(orc.tucker_error(F, *U, core)[0])
+        assert all(b <= a * (1 + 1e-12) + 1e-15 for a, b in zip(E, E[1:]))
+        err[alpha] = E
+    assert err[100.0][0] < 1e-8            # alpha = 100: rank 1 already at the Gram route's floor
+    assert err[0.1][1] > 1e-2              # alpha = 0.1: many more terms (measured 2.5e-2 at r = 2)
+    assert err[0.1][5] > 1e3 * err[100.0][5] and err[0.1][7] > 1e2 * err[100.0][7]

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-MATERN, SLATER = 0, 1
+MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
 SEED_CONFIG4 = 171106874
 
 
@@ -46,7 +46,14 @@ class KernelSpec:
     def slater(lam: float = 1.0, p: float = 1.0, sigma2: float = 1.0) -> "KernelSpec":
         return KernelSpec(SLATER, sigma2, 1.0, 0.5, lam, p, 0)
 
+    @staticmethod
+    def spectral(alpha: float, nu: float, sigma2: float = 1.0) -> "KernelSpec":
+        """Matérn spectral density sigma2 (alpha^2 + rho^2)^{-(nu + 3/2)} (NEXT f4)."""
+        return KernelSpec(MATERN_SPECTRAL, sigma2, 1.0, nu, alpha, 1.0, 0)
+
     def label(self) -> str:
+        if self.family == MATERN_SPECTRAL:
+            return f"spectral(alpha={self.lam:g},nu={self.nu:g})"
         if self.family == SLATER:
             return f"slater(lam={self.lam:g},p={self.p:g})"
         return f"matern(nu={self.nu:.6g},ell={self.ell:.6g})"
