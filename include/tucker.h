@@ -50,7 +50,7 @@ typedef struct {
     double lo[3], hi[3];
 } tucker_grid;
 
-enum { TUCKER_MATERN = 0, TUCKER_SLATER = 1 };
+enum { TUCKER_MATERN = 0, TUCKER_SLATER = 1, TUCKER_MATERN_SPECTRAL = 2 };
 
 /* Kernel parameters.
  *   TUCKER_MATERN: C(r) = sigma2 * 2^{1-nu}/Gamma(nu) * z^nu K_nu(z), z = sqrt(2 nu) r / ell
@@ -59,6 +59,9 @@ enum { TUCKER_MATERN = 0, TUCKER_SLATER = 1 };
  *                  unless TUCKER_FORCE_GENERAL_BESSEL is set.
  *   TUCKER_SLATER: C(r) = sigma2 * exp(-lambda r^p), 0 < p <= 2 (eq. exp_p; p = 2 is
  *                  the Gaussian).
+ *   TUCKER_MATERN_SPECTRAL (NEXT f4): the Matérn spectral density f(rho) = sigma2 (alpha^2 +
+ *                  rho^2)^{-(nu + 3/2)} (eq. SD_matern, d = 3, C = sigma2 by R17) with
+ *                  alpha = `lambda` > 0, nu > 0; rho = ||x|| on the (frequency) grid.
  * `flags` may hold TUCKER_FORCE_GENERAL_BESSEL. */
 typedef struct {
     int32_t family;

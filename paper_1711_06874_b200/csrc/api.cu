@@ -74,6 +74,11 @@ int check_kernel(const tucker_kernel* k) {
             return TUCKER_ERR_DOMAIN;
         return TUCKER_OK;
     }
+    if (k->family == TUCKER_MATERN_SPECTRAL) {
+        if (!(k->lambda > 0.0) || !(k->nu > 0.0) || !std::isfinite(k->lambda) || !std::isfinite(k->nu))
+            return TUCKER_ERR_DOMAIN;
+        return TUCKER_OK;
+    }
     return TUCKER_ERR_INVALID_ARG;
 }
 

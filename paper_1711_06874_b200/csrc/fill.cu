@@ -147,6 +147,10 @@ KParams make_kparams(const tucker_kernel& kn) {
         else if (kn.nu == 2.5) kp.closed = 3;
     }
     if (kn.family == TUCKER_MATERN && kp.closed == 0) kp.pref = kn.sigma2 * (pow(2.0, 1.0 - kn.nu) / tgamma(kn.nu));
+    if (kn.family == TUCKER_MATERN_SPECTRAL) {
+        kp.alpha2 = kn.lambda * kn.lambda;
+        kp.mexp = -(kn.nu + 1.5);
+    }
     return kp;
 }
 

@@ -1,7 +1,8 @@
 // fill_eval.cuh — a-2 point evaluation C(r) shared by the materialised fill (fill.cu) and the
 // fused generate-and-contract paths (gram.cu, ttm.cu): Matérn closed forms nu = 1/2, 3/2, 5/2
 // (P:353-358), general nu through the K_nu Chebyshev table (see fill.cu), p-Slater
-// (P:1029-1031).  Every path evaluates F bitwise identically.
+// (P:1029-1031), the Matérn spectral density (NEXT f4).  Every path evaluates F
+// bitwise identically.
 #pragma once
 
 #include "common.cuh"
@@ -40,6 +41,8 @@ __device__ __forceinline__ double cheb_eval(const double* c, double x) {
 }
 
 __device__ __forceinline__ double eval_point(const KParams& kp, const double* cheb, double r2) {
+    if (kp.family == TUCKER_MATERN_SPECTRAL)  // C (alpha^2 + rho^2)^{-(nu + 3/2)}
+        return __dmul_rn(kp.sigma2, pow(__dadd_rn(kp.alpha2, r2), kp.mexp));
     const double r = __dsqrt_rn(r2);
     if (kp.family == TUCKER_SLATER) {
         double rp = (kp.p == 1.0) ? r : (kp.p == 2.0) ? r2 : pow(r, kp.p);

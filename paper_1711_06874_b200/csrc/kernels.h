@@ -20,6 +20,7 @@ struct KParams {
     int closed;  // 0 general, 1: nu=1/2, 2: nu=3/2, 3: nu=5/2
     int centred; // lo = -hi on every axis (set by the caller from the grid)
     double sigma2, ell, sqrt2nu, lambda, p, nu, pref;
+    double alpha2, mexp;  // spectral density: alpha^2 and -(nu + 3/2)
 };
 
 // Plane chunk of F for the fused paths (a-7; layout and generation in fill_eval.cuh).
