@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-fused", action="store_true", help="skip the 2048^3 fused (F never stored) line")
     ap.add_argument("--no-als", action="store_true", help="skip the Tucker-ALS (NEXT f1) line")
     ap.add_argument("--no-sym", action="store_true", help="skip the symmetry-exploiting (NEXT f3) line")
+    ap.add_argument("--no-accurate", action="store_true", help="skip the SVD-accurate (NEXT f2) line")
     ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
@@ -313,6 +314,20 @@ def run_ours(args, rank, world, local):
         result["als"] = {"what": "Tucker-ALS / HOOI sweep (NEXT f1, P:571-579) on the same 1024^3 tensor, ranks 40",
                          "ms_per_sweep": ms_als, "points_per_s_per_sweep": N / (ms_als * 1e-3),
                          "E_hosvd": eh[0], "E_after_2_sweeps": ea[0], "rc": al.rc}
+    if not args.no_accurate and world == 1:
+        acc = T.hosvd_accurate(grid, ranks, F, 1, stream=stream)  # warm-up
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        acc = T.hosvd_accurate(grid, ranks, F, 1, stream=stream)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        ec = T.error(grid, ranks, F, acc.U, acc.core, ws, stream).cpu().tolist()
+        result["accurate"] = {"what": "SVD-accurate HOSVD (NEXT f2): Gram route + one Rayleigh-Ritz step on each "
+                                      "F_(m) (two streaming passes, CGS2, one-sided Jacobi SVD)",
+                              "ms": c0.elapsed_time(c1), "E": ec[0], "E_gram_route": E[0], "rc": acc.rc,
+                              "sigma_min_resolved": [float(s[-1]) / float(s[0]) for s in
+                                                     (x.cpu() for x in acc.sigma)]}
     if not args.no_fused and world == 1 or not args.no_sym and world == 1:
         del F
         torch.cuda.empty_cache()

@@ -200,6 +200,18 @@ TUCKER_API int tucker_hosvd_sym(const tucker_grid* grid, const tucker_kernel* ke
                      double* U1, double* U2, double* U3, double* core, double* sigma1, double* sigma2,
                      double* sigma3, double* err3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT f2: SVD-accurate HOSVD (beats the Gram route's sqrt(eps) floor; P:557-561 takes the SVD
+ * of each unfolding).  Per mode: the Gram route's p = min(n_m, r_m + 8, 56) leading eigenvectors
+ * V, then `iters` (>= 1) Rayleigh–Ritz steps on F_(m) itself: Y = F_(m)^T V, Q = CGS2(Y),
+ * B = F_(m) Q, U~ Sigma = one-sided-Jacobi SVD of B, V = U~ (no Gram, so singular values are
+ * resolved down to ~eps sigma_1 instead of ~1e-8 sigma_1).  Outputs as tucker_hosvd (sigma_m from
+ * the SVD of B).  Requires n_m <= 2048, r_m <= 56.  Workspace >= tucker_workspace_size_accurate. */
+TUCKER_API size_t tucker_workspace_size_accurate(const tucker_grid* grid, const int32_t r[3]);
+TUCKER_API int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1,
+                          double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
+                          int32_t iters, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
 TUCKER_API int64_t tucker_last_launch_count(void);
 

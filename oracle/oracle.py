@@ -279,6 +279,21 @@ def hosvd(F: np.ndarray, r) -> Hosvd:
     return Hosvd(U, core, lam, rc)
 
 
+def hosvd_svd(F: np.ndarray, r) -> Hosvd:
+    """Truncated HOSVD by the SVD of each explicit unfolding, as the paper computes it
+    ("SVD of the matrix unfolding A_(l)").  The SVD is LAPACK's (numpy.linalg.svd, a
+    library primitive); no Gram is formed, so singular values are resolved down to ~eps sigma_1
+    (the reference for NEXT f2).  `lam` holds sigma^2 of the full spectra; U sign-fixed by R6."""
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    U, lam = [], []
+    for m in range(3):
+        W, sv, _ = np.linalg.svd(unfold(F, m), full_matrices=False)
+        U.append(sign_fix(W[:, : r[m]]))
+        lam.append(sv ** 2)
+    core = ttm_core(F, *U)
+    return Hosvd(U, core, lam, 0)
+
+
 def hooi(F: np.ndarray, U_init, sweeps: int):
     """Test-only Tucker-ALS sweeps starting from U_init; returns (U, core, rc)."""
     F = np.ascontiguousarray(F, dtype=np.float64)

@@ -461,6 +461,70 @@ int tucker_hosvd_sym(const tucker_grid* grid, const tucker_kernel* kernel, const
                             info);
 }
 
+// NEXT f2 layout: [G][V (n_max x p)][scratch]
+static int accurate_p(int64_t n, int r) { return (int)std::min<int64_t>(n, std::min(r + 8, 56)); }
+
+static size_t accurate_plan(const tucker_grid* g, const int32_t* r, size_t* offV, size_t* offS) {
+    const int64_t* n = g->n;
+    const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
+    size_t off = align_up((size_t)nmax * nmax * 8, 256);
+    *offV = off;
+    off += align_up((size_t)nmax * 64 * 8, 256) + 64 * 8;  // V, then its Gram eigenvalues
+    *offS = off;
+    size_t s = gram_ws_bytes(n);
+    int pmax = 1;
+    for (int a = 0; a < 3; ++a) {
+        const int p = accurate_p(n[a], r[a]);
+        pmax = std::max(pmax, p);
+        s = std::max(s, eig_ws_bytes(n[a], p));
+    }
+    s = std::max(s, refine_ws_bytes(n, pmax));
+    s = std::max(s, ttm_ws_bytes(n, r));
+    return off + align_up(s, 256);
+}
+
+size_t tucker_workspace_size_accurate(const tucker_grid* grid, const int32_t r[3]) {
+    if (check_grid(grid) != TUCKER_OK || !r || check_ranks(grid, r) != TUCKER_OK) return 0;
+    size_t a, b;
+    return accurate_plan(grid, r, &a, &b);
+}
+
+int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1, double* U2,
+                          double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, int32_t iters,
+                          void* ws, size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws || iters < 1)
+        return TUCKER_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; ++a)
+        if (r[a] > 56 || grid->n[a] > 2048) return TUCKER_ERR_UNSUPPORTED;
+    size_t offV, offS;
+    const size_t total = accurate_plan(grid, r, &offV, &offS);
+    if (ws_bytes < total) return TUCKER_ERR_SIZE;
+    if (info) std::memset(info, 0, sizeof(*info));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* G = static_cast<double*>(ws);
+    double* V = reinterpret_cast<double*>(at(ws, offV));
+    const int64_t nmx = std::max(grid->n[0], std::max(grid->n[1], grid->n[2]));
+    double* lam = V + align_up((size_t)nmx * 64 * 8, 256) / 8;
+    void* scr = at(ws, offS);
+    const size_t sb = total - offS;
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    int worst = TUCKER_OK;
+    for (int m = 0; m < 3; ++m) {
+        const int p = accurate_p(grid->n[m], r[m]);
+        TK_RC(launch_gram(grid->n, m, F, G, scr, sb, st));
+        const int rc = launch_eig(grid->n[m], G, p, V, lam, nullptr, scr, sb, st, info, m);
+        if (rc == TUCKER_ERR_NOCONV) worst = rc;
+        else if (rc != TUCKER_OK) return rc;
+        TK_RC(launch_refine_mode(grid->n, m, F, V, lam, p, r[m], iters, U[m], S[m], scr, sb, st, nullptr));
+    }
+    TK_RC(launch_ttm_core(grid->n, r, F, U1, U2, U3, core, scr, sb, st));
+    return worst;
+}
+
 int64_t tucker_last_launch_count(void) { return launch_counter(); }
 
 const char* tucker_strerror(int code) {

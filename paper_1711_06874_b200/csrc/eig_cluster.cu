@@ -386,6 +386,154 @@ __global__ void __launch_bounds__(NT, 1) k_rr_cluster(Args a) {
     cl.sync();
 }
 
+// ------------------------------------------------------------------ NEXT f2: one-sided Jacobi SVD
+// Left singular vectors and singular values of B (n x p, row-major, dev) by one-sided (Hestenes)
+// Jacobi on its columns, rows distributed over the cluster like k_rr_cluster: per round of the
+// round-robin ordering (jacobi.cuh) every CTA forms its partial (||b_a||^2, ||b_b||^2, b_a.b_b)
+// for all pairs, one cluster reduction (rank order, deterministic) gives the same rotations in
+// every CTA, and each CTA rotates its rows.  Unlike an eigensolver on B^T B this keeps small
+// singular values to high relative accuracy (no squaring).  Outputs: Vout (n x p, columns sorted by
+// descending sigma, normalised, sign rule R6), U (n x r = Vout's first r columns), sigma (r).
+struct SvdArgs {
+    int64_t n;
+    int p, r;
+    const double* B;
+    double* Vout;
+    double* U;
+    double* sigma;
+    int* sweeps_out;
+};
+
+__global__ void __launch_bounds__(NT, 1) k_svd_cluster(SvdArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = NT / 32;
+    const int p = a.p;
+    const int64_t n = a.n;
+    const int64_t i0 = (int64_t)cl.block_rank() * RB;
+    const int64_t rem = n - i0;
+    const int nrows = rem <= 0 ? 0 : (rem >= RB ? RB : (int)rem);
+    int round = 0;
+    for (int e = t; e < RB * P; e += NT) {
+        const int j = e / RB, i = e % RB;
+        s.Y[sw(i, j)] = (i < nrows && j < p) ? a.B[(size_t)(i0 + i) * p + j] : 0.0;
+    }
+    __syncthreads();
+    const int m = p + (p & 1), half = m / 2;
+    const double eps = 2.220446049250313e-16;
+    int sweep = 0;
+    for (; sweep < 40; ++sweep) {
+        int any = 0;
+        for (int rd = 0; rd < m - 1; ++rd) {
+            // partial (alpha, beta, gamma) of each pair over the local rows: warp per pair
+            for (int w = warp; w < half; w += nw) {
+                int pa, pb;
+                rr_pair(rd, w, m, pa, pb);
+                double al = 0.0, be = 0.0, ga = 0.0;
+                if (pb < p)
+                    for (int i = lane; i < nrows; i += 32) {
+                        const double x = s.Y[sw(i, pa)], y = s.Y[sw(i, pb)];
+                        al = fma(x, x, al);
+                        be = fma(y, y, be);
+                        ga = fma(x, y, ga);
+                    }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum(ga);
+                if (lane == 0) {
+                    s.tmp[3 * w] = al;
+                    s.tmp[3 * w + 1] = be;
+                    s.tmp[3 * w + 2] = ga;
+                }
+            }
+            __syncthreads();
+            cl_reduce<OP_SUM>(cl, s, round, s.tmp, s.tmp, 3 * half);
+            // identical rotations in every CTA; warp per pair applies it to the local rows
+            for (int w = warp; w < half; w += nw) {
+                int pa, pb;
+                rr_pair(rd, w, m, pa, pb);
+                if (pb >= p) continue;
+                const double al = s.tmp[3 * w], be = s.tmp[3 * w + 1], ga = s.tmp[3 * w + 2];
+                if (!(fabs(ga) > eps * sqrt(al * be)) || al == 0.0 || be == 0.0) continue;
+                any = 1;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                const double c = rsqrt(fma(tt, tt, 1.0)), sn = tt * c;
+                for (int i = lane; i < nrows; i += 32) {
+                    const double x = s.Y[sw(i, pa)], y = s.Y[sw(i, pb)];
+                    s.Y[sw(i, pa)] = c * x - sn * y;
+                    s.Y[sw(i, pb)] = sn * x + c * y;
+                }
+            }
+            // every thread sees the same `any` (same reduced data); block barrier before the
+            // next round reads the columns and overwrites tmp
+            __syncthreads();
+        }
+        if (!__syncthreads_or(any)) break;
+    }
+    // column norms -> sigma, order, normalise, sign rule on the leading r (and all p) columns
+    col_partials(s, nrows, p, s.vec, [&](int i, int k) {
+        const double y = s.Y[sw(i, k)];
+        return y * y;
+    });
+    cl_reduce<OP_SUM>(cl, s, round, s.vec, s.vec, p);
+    for (int k = t; k < p; k += NT) s.theta[k] = sqrt(s.vec[k]);
+    __syncthreads();
+    for (int k = t; k < p; k += NT) {  // stable descending rank of sigma
+        const double v = s.theta[k];
+        int rank = 0;
+        for (int j = 0; j < p; ++j) rank += (s.theta[j] > v) || (s.theta[j] == v && j < k);
+        s.order[rank] = k;
+    }
+    __syncthreads();
+    // normalise in place
+    for (int e = t; e < nrows * p; e += NT) {
+        const int i = e / p, k = e % p;
+        const double sg = s.theta[k];
+        if (sg > 0.0) s.Y[sw(i, k)] /= sg;
+    }
+    __syncthreads();
+    // sign rule R6 on every output column (sorted position q -> source column order[q])
+    if (t < p) {
+        const int k = s.order[t];
+        double mx = 0.0;
+        for (int i = 0; i < nrows; ++i) mx = fmax(mx, fabs(s.Y[sw(i, k)]));
+        s.vec[t] = mx;
+    }
+    __syncthreads();
+    cl_reduce<OP_MAX>(cl, s, round, s.vec, s.vec, p);
+    if (t < p) {
+        const int k = s.order[t];
+        const double halfm = 0.5 * s.vec[t];
+        double code = 1e300;
+        for (int i = 0; i < nrows; ++i) {
+            const double v = s.Y[sw(i, k)];
+            if (fabs(v) >= halfm) {
+                code = 2.0 * (double)(i0 + i) + (v < 0.0 ? 1.0 : 0.0);
+                break;
+            }
+        }
+        s.tmp[t] = code;
+    }
+    __syncthreads();
+    cl_reduce<OP_MIN>(cl, s, round, s.tmp, s.tmp, p);
+    for (int e = t; e < nrows * p; e += NT) {
+        const int i = e / p, q = e % p;
+        const double code = s.tmp[q];
+        const bool flip = code < 1e299 && fmod(code, 2.0) == 1.0;
+        const double v = s.Y[sw(i, s.order[q])];
+        const double o = flip ? -v : v;
+        a.Vout[(size_t)(i0 + i) * p + q] = o;
+        if (q < a.r) a.U[(size_t)(i0 + i) * a.r + q] = o;
+    }
+    if (cl.block_rank() == 0) {
+        for (int q = t; q < a.r; q += NT) a.sigma[q] = s.theta[s.order[q]];
+        if (t == 0 && a.sweeps_out) *a.sweeps_out = sweep + 1;
+    }
+    cl.sync();
+}
+
 }  // namespace eigc
 
 // Cluster size for n rows (power of two, <= 16), or 0 when n is out of range.
@@ -432,6 +580,31 @@ bool eig_cluster_supported(int64_t n) {
         return ok16 == 1;
     }
     return true;
+}
+
+int launch_svd_cluster(int64_t n, int p, int r, const double* B, double* Vout, double* U, double* sigma,
+                       int* sweeps_out, cudaStream_t st) {
+    if (!eig_cluster_supported(n) || p > eigc::P) return TUCKER_ERR_UNSUPPORTED;
+    const int cs = eig_cluster_size(n);
+    TK_CUDA(cudaFuncSetAttribute(eigc::k_svd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)eig_cluster_smem()));
+    if (cs > 8) TK_CUDA(cudaFuncSetAttribute(eigc::k_svd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    eigc::SvdArgs a{n, p, r, B, Vout, U, sigma, sweeps_out};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(eigc::NT);
+    cfg.dynamicSmemBytes = eig_cluster_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TK_CUDA(cudaLaunchKernelEx(&cfg, eigc::k_svd_cluster, a));
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
 }
 
 int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,

@@ -64,6 +64,16 @@ bool eig_cluster_supported(int64_t n);
 int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
                       double* U, double* lambda, double* sigma, void* state, cudaStream_t st);
 
+// NEXT f2: left singular vectors of B (n x p, n <= 2048, p <= 64) by one-sided Jacobi in a cluster.
+int launch_svd_cluster(int64_t n, int p, int r, const double* B, double* Vout, double* U, double* sigma,
+                       int* sweeps_out, cudaStream_t st);
+
+// NEXT f2: Rayleigh–Ritz steps on F_(m) from the Gram route's V (refine.cu).
+size_t refine_ws_bytes(const int64_t n[3], int p);
+int launch_refine_mode(const int64_t n[3], int m, const double* F, const double* V0, const double* lam0, int p,
+                       int r, int iters, double* U, double* sigma, void* ws, size_t ws_bytes, cudaStream_t st,
+                       int* sweeps_out);
+
 // Core beta = F x1 U1^T x2 U2^T x3 U3^T.
 size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1,

@@ -1,0 +1,261 @@
+// refine.cu — NEXT f2: beating the sqrt(eps) floor of the Gram route.
+//
+// The paper takes the SVD of each unfolding; the hot path forms G_m = F_(m) F_(m)^T,
+// whose eigenvalues below ~1e-16 lambda_1 are rounding noise, so singular values below ~1e-8
+// sigma_1 are lost (E plateaus near 1e-8).  This pass recovers SVD accuracy with a Rayleigh–Ritz
+// step on F_(m) itself, starting from the Gram route's p = r + q leading eigenvectors V:
+//   pass 1   Y = F_(m)^T V                 (N/n_m x p, stored column-major as Yt = Y^T)
+//   CGS2     Q = orth(Y)                    (classical Gram–Schmidt twice, column by column over
+//                                            all SMs, deterministic fixed-order reductions)
+//   pass 2   B = F_(m) Q                    (n_m x p, split-K partials + fixed-order reduce)
+//   SVD      B = U~ Sigma W^T               (one-sided Jacobi in a thread-block cluster: no
+//                                            squaring, small singular values keep their accuracy)
+// and U_m = U~[:, :r], sigma_m = Sigma[:r]; `iters` repeats the step from V = U~.  Every product
+// is a plain FP64 contraction of F (no Gram), so the singular values are resolved down to
+// ~eps sigma_1.  The streaming products use the small-GEMM kernel (k_small_gemm).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tk {
+
+namespace {
+constexpr int kBlk = 4 * kNumSMs;  // CTAs of the CGS2 kernels
+constexpr int kNT = 256;
+
+__device__ __forceinline__ double hash_u(uint64_t idx) {  // SplitMix64 finaliser -> [-1,1)
+    uint64_t z = idx * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+__device__ __forceinline__ void row_range(int64_t M, int64_t& b0, int64_t& b1) {
+    b0 = (int64_t)blockIdx.x * M / gridDim.x;
+    b1 = (int64_t)(blockIdx.x + 1) * M / gridDim.x;
+}
+
+// part[blk][j] = sum_{rows of blk} Q_j[row] y[row], j < k (columns of Yt are contiguous, length M).
+__global__ void __launch_bounds__(kNT) k_cgs_dots(const double* __restrict__ Yt, int64_t M, int k,
+                                                  double* __restrict__ part, const int* __restrict__ done) {
+    if (*done) return;
+    __shared__ double red[40];
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    const double* y = Yt + (size_t)k * M;
+    for (int j0 = 0; j0 < k; j0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
+            const double yi = y[i];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (j0 + u < k) acc[u] = fma(Yt[(size_t)(j0 + u) * M + i], yi, acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double s = block_sum(acc[u], red);
+            if (threadIdx.x == 0 && j0 + u < k) part[(size_t)blockIdx.x * 64 + j0 + u] = s;
+        }
+    }
+}
+
+// h = sum over blocks (fixed order, every CTA); y -= Q h on this CTA's rows; npart[blk] = ||y||^2.
+__global__ void __launch_bounds__(kNT) k_cgs_update(double* __restrict__ Yt, int64_t M, int k,
+                                                    const double* __restrict__ part, int nblk,
+                                                    double* __restrict__ npart, const int* __restrict__ done) {
+    if (*done) return;
+    __shared__ double h[64];
+    __shared__ double red[40];
+    for (int j = threadIdx.x; j < k; j += kNT) {
+        double s = 0.0;
+        for (int b = 0; b < nblk; ++b) s += part[(size_t)b * 64 + j];
+        h[j] = s;
+    }
+    __syncthreads();
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    double* y = Yt + (size_t)k * M;
+    double ss = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
+        double yi = y[i];
+        for (int j = 0; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
+        y[i] = yi;
+        ss = fma(yi, yi, ss);
+    }
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) npart[blockIdx.x] = ss;
+}
+
+// n1 = ||y'||^2 (after pass 1), n2 = ||y''||^2 (after pass 2), fixed-order sums.  Kahan–Parlett
+// "twice is enough": accept y'' (normalised) if n2 >= n1 / 2; otherwise y was numerically in the
+// span of the previous columns — replace it by a deterministic pseudo-random vector and run the
+// two passes again (the last attempt is accepted unconditionally).
+// `skip` is read only; `accepted` is written (by CTA 0) and read by the launches of the next
+// attempt only — a kernel never reads a flag it writes.
+__global__ void __launch_bounds__(kNT) k_cgs_finish(double* __restrict__ Yt, int64_t M, int k,
+                                                    const double* __restrict__ npart, int nblk,
+                                                    const int* __restrict__ skip, int* accepted, int last) {
+    if (*skip) return;
+    __shared__ double tot, tot1;
+    if (threadIdx.x == 0) {
+        double s = 0.0, s1 = 0.0;
+        for (int b = 0; b < nblk; ++b) {
+            s1 += npart[b];
+            s += npart[nblk + b];
+        }
+        tot = s;
+        tot1 = s1;
+    }
+    __syncthreads();
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    double* y = Yt + (size_t)k * M;
+    const bool ok = (tot > 1e-300 && tot >= 0.5 * tot1) || last;
+    const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) y[i] = ok ? y[i] * inv : hash_u(0x5eedull * (k + 1) + i);
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ok) *accepted = 1;
+}
+
+// Start basis for the Rayleigh–Ritz steps: keep the Gram route's eigenvectors whose eigenvalue is
+// resolved (lambda_k >= tau lambda_1, tau = 1e-12), replace the others by deterministic
+// pseudo-random columns.  Unresolved Gram eigenvectors are not random: on symmetric grids they
+// are exactly even or odd, and a basis made only of odd null vectors would miss the even tail
+// directions that the refinement must find.
+__global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const double* __restrict__ lam) {
+    const double l1 = lam[0];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * p; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / p;
+        const int k = (int)(t % p);
+        if (!(lam[k] >= 1e-12 * l1)) V[t] = hash_u(0xba515ull * (k + 1) + (uint64_t)i);
+    }
+}
+
+// out[o] = sum_s part[s][o] (fixed order)
+__global__ void k_sum_partials(const double* __restrict__ part, int S, int64_t len, double* __restrict__ out) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < len; o += (int64_t)gridDim.x * blockDim.x) {
+        double s = part[o];
+        for (int q = 1; q < S; ++q) s += part[(size_t)q * len + o];
+        out[o] = s;
+    }
+}
+
+struct RefLayout {
+    size_t Yt, B, Bpart, V, dots, npart, flags, total;
+    int64_t Mmax;
+    int S2;
+};
+
+constexpr int kSplit = 64;  // split-K factor of pass 2
+
+RefLayout ref_plan(const int64_t n[3], int p) {
+    RefLayout L{};
+    const int64_t N = n[0] * n[1] * n[2];
+    const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
+    L.Mmax = N / std::min(n[0], std::min(n[1], n[2]));
+    size_t off = 0;
+    L.Yt = off;
+    off += align_up((size_t)p * L.Mmax * 8, 256);
+    L.B = off;
+    off += align_up((size_t)nmax * p * 8, 256);
+    L.Bpart = off;
+    // mode 1 (batched over i) needs n1 partials of n2 x p; modes 0, 2 need kSplit partials
+    off += align_up((size_t)std::max<int64_t>(kSplit, n[0]) * nmax * p * 8, 256);
+    L.V = off;
+    off += align_up((size_t)nmax * p * 8, 256);
+    L.dots = off;
+    off += align_up((size_t)kBlk * 64 * 8, 256);
+    L.npart = off;
+    off += align_up((size_t)2 * kBlk * 8, 256);
+    L.flags = off;
+    off += 256;
+    L.total = off;
+    return L;
+}
+}  // namespace
+
+size_t refine_ws_bytes(const int64_t n[3], int p) { return ref_plan(n, p).total; }
+
+// One or more Rayleigh–Ritz steps on F_(m) from V0 (n_m x p, dev; need not be orthonormal);
+// lam0 (dev, p, nullable): V0's Gram eigenvalues, unresolved columns are replaced (k_seed_basis).
+// Outputs U (n_m x r), sigma (r); ws >= refine_ws_bytes(n, p).
+int launch_refine_mode(const int64_t n[3], int m, const double* F, const double* V0, const double* lam0, int p,
+                       int r, int iters, double* U, double* sigma, void* ws, size_t ws_bytes, cudaStream_t st,
+                       int* sweeps_out) {
+    const RefLayout L = ref_plan(n, p);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    if (p > 64 || r > p) return TUCKER_ERR_UNSUPPORTED;
+    char* w = static_cast<char*>(ws);
+    double* Yt = reinterpret_cast<double*>(w + L.Yt);
+    double* B = reinterpret_cast<double*>(w + L.B);
+    double* Bpart = reinterpret_cast<double*>(w + L.Bpart);
+    double* V = reinterpret_cast<double*>(w + L.V);
+    double* dots = reinterpret_cast<double*>(w + L.dots);
+    double* npart = reinterpret_cast<double*>(w + L.npart);
+    int* flags = reinterpret_cast<int*>(w + L.flags);
+    const int64_t n1 = n[0], n2 = n[1], n3 = n[2], nm = n[m];
+    const int64_t M = n1 * n2 * n3 / nm;
+    TK_CUDA(cudaMemcpyAsync(V, V0, (size_t)nm * p * 8, cudaMemcpyDeviceToDevice, st));
+    if (lam0) {
+        k_seed_basis<<<64, 256, 0, st>>>(V, nm, p, lam0);
+        TK_CHECK_LAUNCH();
+    }
+    for (int it = 0; it < iters; ++it) {
+        // ---- pass 1: Yt (p x M) = V^T F_(m)
+        if (m == 0) {  // Yt[a][(j,k)] = sum_i V[i][a] F[i][(j,k)]
+            SmallGemm g{p, M, n1, 1, V, 1, p, 0, F, M, 1, 0, Yt, M, 1, 0};
+            TK_RC(launch_small_gemm(g, st));
+        } else if (m == 1) {  // Yt[b][(i,k)] = sum_j V[j][b] F[i][j][k], batched over i
+            SmallGemm g{p, n3, n2, n1, V, 1, p, 0, F, n3, 1, n2 * n3, Yt, M, 1, n3};
+            TK_RC(launch_small_gemm(g, st));
+        } else {  // Yt[c][(i,j)] = sum_k V[k][c] F[(i,j)][k]
+            SmallGemm g{p, M, n3, 1, V, 1, p, 0, F, 1, n3, 0, Yt, M, 1, 0};
+            TK_RC(launch_small_gemm(g, st));
+        }
+        // ---- CGS2 of the p columns of Y (each column contiguous in Yt)
+        // flags[0] = 0 (attempt 0 always runs), flags[1] = attempt 0 accepted (attempt 1 skipped)
+        for (int k = 0; k < p; ++k) {
+            TK_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), st));
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                const int* skip = flags + attempt;
+                for (int pass = 0; pass < 2; ++pass) {
+                    if (k > 0) {
+                        k_cgs_dots<<<kBlk, kNT, 0, st>>>(Yt, M, k, dots, skip);
+                        TK_CHECK_LAUNCH();
+                    }
+                    k_cgs_update<<<kBlk, kNT, 0, st>>>(Yt, M, k, dots, kBlk, npart + pass * kBlk, skip);
+                    TK_CHECK_LAUNCH();
+                }
+                k_cgs_finish<<<kBlk, kNT, 0, st>>>(Yt, M, k, npart, kBlk, skip, flags + attempt + 1, attempt);
+                TK_CHECK_LAUNCH();
+            }
+        }
+        // ---- pass 2: B (n_m x p) = F_(m) Q, split over the contraction, fixed-order sum
+        int S = kSplit;  // split of the contraction: the largest divisor of M not above kSplit
+        while (M % S) --S;
+        const int64_t Kc = M / S;
+        if (m == 0) {  // B[i][a] = sum_col F[i][col] Qt[a][col]
+            SmallGemm g{n1, p, Kc, S, F, M, 1, Kc, Yt, 1, M, Kc, Bpart, p, 1, n1 * p};
+            TK_RC(launch_small_gemm(g, st));
+            k_sum_partials<<<256, 256, 0, st>>>(Bpart, S, n1 * p, B);
+            TK_CHECK_LAUNCH();
+        } else if (m == 1) {  // B_i[j][b] = sum_k F[i][j][k] Qt[b][(i,k)], batched over i
+            SmallGemm g{n2, p, n3, n1, F, n3, 1, n2 * n3, Yt, 1, M, n3, Bpart, p, 1, n2 * p};
+            TK_RC(launch_small_gemm(g, st));
+            k_sum_partials<<<256, 256, 0, st>>>(Bpart, (int)n1, n2 * p, B);
+            TK_CHECK_LAUNCH();
+        } else {  // B[k][c] = sum_row F[row][k] Qt[c][row]
+            SmallGemm g{n3, p, Kc, S, F, 1, n3, Kc * n3, Yt, 1, M, Kc, Bpart, p, 1, n3 * p};
+            TK_RC(launch_small_gemm(g, st));
+            k_sum_partials<<<256, 256, 0, st>>>(Bpart, S, n3 * p, B);
+            TK_CHECK_LAUNCH();
+        }
+        // ---- SVD of B -> V (all p columns, sorted) and U, sigma (leading r)
+        TK_RC(launch_svd_cluster(nm, p, r, B, V, U, sigma, sweeps_out, st));
+    }
+    return TUCKER_OK;
+}
+
+}  // namespace tk

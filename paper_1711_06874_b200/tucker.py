@@ -23,8 +23,8 @@ ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3
 EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
-           "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_last_launch_count",
-           "tucker_strerror")
+           "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
+           "tucker_hosvd_accurate", "tucker_last_launch_count", "tucker_strerror")
 
 
 class TuckerError(RuntimeError):
@@ -82,6 +82,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_als": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
         "tucker_workspace_size_sym": (sz, [pg, pr]),
         "tucker_hosvd_sym": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
+        "tucker_workspace_size_accurate": (sz, [pg, pr]),
+        "tucker_hosvd_accurate": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
         "tucker_last_launch_count": (i64, []),
         "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
@@ -263,6 +265,28 @@ def als(grid, ranks, F: torch.Tensor, U_init, sweeps: int, ws: torch.Tensor | No
                         ctypes.byref(info))
     if rc not in (0, 5):
         _check(rc, "tucker_als")
+    return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+# ------------------------------------------------------------------ NEXT f2: SVD-accurate HOSVD
+def hosvd_accurate(grid, ranks, F: torch.Tensor, iters: int = 1, ws: torch.Tensor | None = None,
+                   stream=None) -> HosvdResult:
+    lib = load()
+    _dev(F, "F")
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device=F.device) for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device=F.device) for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device=F.device)
+    g = cgrid(grid)
+    if ws is None:
+        ws = torch.empty(int(lib.tucker_workspace_size_accurate(ctypes.byref(g), cranks(r))), dtype=torch.uint8,
+                         device=F.device)
+    info = CInfo()
+    rc = lib.tucker_hosvd_accurate(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
+                                   _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), int(iters), _ptr(ws), ws.numel(),
+                                   _stream(stream), ctypes.byref(info))
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd_accurate")
     return HosvdResult(U, core, S, info.as_dict(), rc)
 
 

@@ -296,3 +296,37 @@ def test_table2(orc, n):
         else:
             val = abs(1.0 - orc.tucker_point(U, core, c, c, c))
         assert _within_last_digit(val, cell), (n, r, val, cell)
+
+
+# ------------------------------------------------- NEXT f2 reference: HOSVD by SVD of unfoldings
+def test_hosvd_svd_pins(orc):
+    """orc.hosvd_svd (LAPACK SVD of the explicit unfoldings) — pinned against the Gram
+    route where both are accurate, full-rank exactness, and beating the Gram route's floor."""
+    g = orc.Grid((24, 20, 28), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    F = orc.fill(g, orc.Kernel.matern(1.5, 0.3))
+    r = (12, 12, 12)
+    hs, hg = orc.hosvd_svd(F, r), orc.hosvd(F, r)
+    for m in range(3):
+        l_svd, l_gram = hs.lam[m][: r[m]], hg.lam[m][: r[m]]
+        big = l_svd >= 1e-12 * l_svd[0]
+        # the T1 bar between the two routes (the Gram's eigenvalues carry ~eps lambda_1 absolute)
+        assert np.all(np.abs(l_svd - l_gram) <= 1e-11 * l_svd + 1e-14 * l_svd[0])
+        U = hs.U[m]
+        assert np.max(np.abs(U.T @ U - np.eye(r[m]))) <= 1e-13
+        for c in np.nonzero(big)[0]:  # resolved and gap-separated columns agree
+            others = np.delete(hs.lam[m], c)
+            if np.min(np.abs(others - hs.lam[m][c])) >= 1e-6 * hs.lam[m][0]:
+                assert np.max(np.abs(U[:, c] - hg.U[m][:, c])) <= 1e-9
+    # full rank: exact reconstruction
+    full = orc.hosvd_svd(F, F.shape)
+    assert orc.tucker_error(F, *full.U, full.core)[0] <= 1e-14
+    # the SVD route keeps decaying where the Gram route plateaus at ~1e-8 (P:424-430)
+    E_svd = [orc.tucker_error(F, *[u[:, :k] for u in hs.U], orc.ttm_core(F, *[u[:, :k] for u in hs.U]))[0]
+             for k in range(1, 13)]
+    E_gram = orc.tucker_error(F, *hg.U, hg.core)[0]
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(E_svd, E_svd[1:]))
+    assert E_svd[-1] < 1e-10 and E_svd[-1] < 1e-2 * E_gram, (E_svd[-1], E_gram)
+    # Eckart-Young per mode: sum of the discarded sigma^2 of every mode bounds E^2 ||F||^2 from above
+    nF2 = np.sum(F * F)
+    tail = sum(np.sum(hs.lam[m][r[m]:]) for m in range(3))
+    assert E_svd[-1] ** 2 * nF2 <= tail * (1 + 1e-10) + 1e-28 * nF2
