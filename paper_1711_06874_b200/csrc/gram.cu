@@ -176,6 +176,10 @@ __device__ __forceinline__ void gram_consume(const CUtensorMap* map, const Args&
                                              uint64_t* full, uint64_t* empty, double (&acc)[8][4][2]) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wm = warp >> 2, wn = warp & 3, r = lane >> 2, q = lane & 3;
+    // on a diagonal tile the warps whose 64 x 32 sub-tile lies strictly above the diagonal
+    // (rows 0..63, columns 64..127) skip their MMA: only the lower triangle reaches G (saves
+    // issue slots and power; the split-K wave is set by the full tiles)
+    const bool upper = diag && wm == 0 && wn >= 2;
     const int64_t L = kb1 - kb0;
     if (threadIdx.x == 0)
         for (int64_t j = 0; j < STAGES && j < L; ++j) {
@@ -196,8 +200,10 @@ __device__ __forceinline__ void gram_consume(const CUtensorMap* map, const Args&
         mbar_wait(&full[stage], (uint32_t)((it / STAGES) & 1));
         const double* A = sA + stage * TILE;
         const double* B = diag ? A : sB + stage * TILE;
-        if (MODE == 2) mma_mmajor(A, B, acc, wm, wn, r, q);
-        else mma_kmajor(A, B, acc, wm, wn, r, q);
+        if (!upper) {
+            if (MODE == 2) mma_mmajor(A, B, acc, wm, wn, r, q);
+            else mma_kmajor(A, B, acc, wm, wn, r, q);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
     }
