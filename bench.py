@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-als", action="store_true", help="skip the Tucker-ALS (NEXT f1) line")
     ap.add_argument("--no-sym", action="store_true", help="skip the symmetry-exploiting (NEXT f3) line")
     ap.add_argument("--no-accurate", action="store_true", help="skip the SVD-accurate (NEXT f2) line")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
     ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
@@ -328,8 +329,13 @@ def run_ours(args, rank, world, local):
                               "ms": c0.elapsed_time(c1), "E": ec[0], "E_gram_route": E[0], "rc": acc.rc,
                               "sigma_min_resolved": [float(s[-1]) / float(s[0]) for s in
                                                      (x.cpu() for x in acc.sigma)]}
-    if not args.no_fused and world == 1 or not args.no_sym and world == 1:
+    if not args.no_cfg4 and world == 1:
         del F
+        torch.cuda.empty_cache()
+        result["config4"] = run_cfg4(T, stream)
+        F = None
+    if not args.no_fused and world == 1 or not args.no_sym and world == 1:
+        F = None
         torch.cuda.empty_cache()
     if not args.no_sym and world == 1:
         result["symmetric"] = [run_sym(T, nn, rr, stream) for nn in (n, 2 * n)]
@@ -377,6 +383,42 @@ def run_fused(T, n: int, rr: int, stream) -> dict:
             "E": e[0], "normF": e[1], "eig_info": res.info, "rc": res.rc,
             "timed": "one hosvd_fused + error_fused call (CUDA events), after a warm-up Gram; gram_ms from "
                      "three separate tucker_gram_fused calls"}
+
+
+def run_cfg4(T, stream) -> dict:
+    """BASELINE config 4: 512^3, 16 seeded Matérn settings (R10), ranks 30 — the whole path per
+    setting (fill, 3 Grams, 3 eigensolves, core, error), timed over the batch."""
+    import torch
+
+    from tucker_inputs import config4
+    w = config4()
+    g, r = w.grid, w.ranks
+    F = torch.empty(tuple(g.n), dtype=torch.float64, device="cuda")
+    ws = T.workspace(g, r)
+
+    def one(k):
+        T.fill(g, k, F, ws, stream)
+        res = T.hosvd(g, r, F, ws, stream)
+        return res, T.error(g, r, F, res.U, res.core, ws, stream)
+
+    one(w.kernels[0])  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    errs, rcs = [], []
+    for k in w.kernels:
+        res, err = one(k)
+        errs.append(err)
+        rcs.append(res.rc)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    pts = len(w.kernels) * g.points
+    del F, ws
+    torch.cuda.empty_cache()
+    return {"workload": w.name, "settings": len(w.kernels), "ranks": list(r), "value": pts / (ms * 1e-3),
+            "unit": UNIT, "ms_total": ms, "ms_per_setting": ms / len(w.kernels), "rc": rcs,
+            "E_range": [min(float(e[0]) for e in errs), max(float(e[0]) for e in errs)]}
 
 
 def run_sym(T, n: int, rr: int, stream, reps: int = 3) -> dict:

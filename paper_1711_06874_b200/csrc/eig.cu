@@ -10,7 +10,7 @@
 //           Jacobi in shared memory (round-robin pairs, warp-parallel rotations, skip rule R7);
 //           Vr = V Q, Y = W Q; residual rho_k = ||Y_k - theta_k Vr_k||;
 //           stop when rho_k <= 1e-14 theta_1 for k < r after >= 3 iterations, else V = CGS2(Y).
-// Small matrices (n <= 96) are diagonalised directly by the same shared-memory Jacobi.
+// Small matrices (n <= 112) are diagonalised directly by the same shared-memory Jacobi.
 // Outputs are sorted descending (stable) and sign-fixed by rule R6: the first entry with
 // |u_i| >= max|u|/2 is made positive.  Everything is deterministic (fixed reduction orders).
 #include "common.cuh"
@@ -21,7 +21,7 @@ namespace tk {
 namespace eig {
 
 constexpr int kMaxP = 64;
-constexpr int kDirectMax = 96;
+constexpr int kDirectMax = 112;  // whole-matrix Jacobi fits in shared memory up to here (207 KB)
 constexpr int kThreads = 1024;
 constexpr int kBatch = 8;
 constexpr int kMaxIters = 96;

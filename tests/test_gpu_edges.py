@@ -1,0 +1,117 @@
+"""Edge cases of the CUDA path (through the C-ABI): the smallest grid, the largest supported rank,
+nearly-constant functions, and the largest grid both materialised and fused (2048^3: 68.7 GB of F
+in HBM against the never-stored path)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import _compare_hosvd, ogrid, okern  # noqa: E402
+from tucker_inputs import GridSpec, KernelSpec  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_1711_06874_b200 import tucker
+    tucker.load()
+    return tucker
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("r", [(1, 1, 1), (2, 2, 2), (1, 2, 1)])
+def test_smallest_grid(T, orc, r):
+    _compare_hosvd(T, orc, GridSpec((2, 2, 2), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)), KernelSpec.matern(1.5, 0.7), r)
+
+
+def test_largest_rank_and_beyond(T, orc):
+    g = GridSpec((160, 100, 128), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    _compare_hosvd(T, orc, g, KernelSpec.matern(0.5, 0.05), (56, 56, 56))  # eigensolver block limit
+    F = T.fill(g, KernelSpec.matern(0.5, 0.05))
+    import ctypes
+    lib = T.load()
+    U = [torch.empty((g.n[m], 57), dtype=torch.float64, device="cuda") for m in range(3)]
+    S = [torch.empty(57, dtype=torch.float64, device="cuda") for _ in range(3)]
+    core = torch.empty((57, 57, 57), dtype=torch.float64, device="cuda")
+    ws = T.workspace(g, (57, 57, 57))
+    rc = lib.tucker_hosvd(ctypes.byref(T.cgrid(g)), T.cranks((57, 57, 57)), T._ptr(F), *[T._ptr(u) for u in U],
+                          T._ptr(core), *[T._ptr(s) for s in S], T._ptr(ws), ws.numel(), None, None)
+    assert rc == 7  # TUCKER_ERR_UNSUPPORTED, documented in include/tucker.h
+
+
+def test_nearly_constant_function(T, orc):
+    """ell >> box: F ~ sigma^2 (1 - small), numerically rank 1; nothing may break (no NaN, sign rule,
+    orthonormal factors) and E(1) is tiny."""
+    g, k = GridSpec((40, 36, 32), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)), KernelSpec.matern(1.5, 1e4)
+    res, err = _compare_hosvd(T, orc, g, k, (3, 3, 3))
+    assert np.all(np.isfinite(to_np(res.core))) and err[0] < 1e-6
+
+
+def test_2048_materialised_vs_fused(T, orc):
+    """The largest grid in both forms: F materialised (68.7 GB) against the fused path."""
+    g, k, r = GridSpec.cube(2048, 1.0), KernelSpec.matern(1.5, 0.2), (10, 10, 10)
+    F = T.fill(g, k)
+    og, ok = ogrid(orc, g), okern(orc, k)
+    # sampled entries of the materialised fill against the oracle, one by one
+    rng = np.random.default_rng(7)
+    for i, j, l in rng.integers(0, 2048, size=(8, 3)):
+        ref = orc.fill_entry(og, ok, int(i), int(j), int(l))
+        assert abs(float(F[i, j, l]) - ref) <= 4 * np.spacing(ref)
+    ws = T.workspace(g, r)
+    G = T.gram(g, 2, F, ws)
+    Gn = to_np(G)
+    bar = 2.0 * 2048 * np.finfo(np.float64).eps
+    for a, b in rng.integers(0, 2048, size=(4, 2)):
+        ref = orc.gram_entry_fn(og, ok, 2, int(a), int(b))
+        assert abs(Gn[a, b] - ref) <= bar * np.sqrt(Gn[a, a] * Gn[b, b])
+    del G
+    ref = T.hosvd(g, r, F, ws)
+    e_ref = to_np(T.error(g, r, F, ref.U, ref.core, ws))
+    del F, ws
+    torch.cuda.empty_cache()
+    res = T.hosvd_fused(g, k, r)
+    e = to_np(T.error_fused(g, k, r, res.U, res.core))
+    assert ref.rc == 0 and res.rc == 0
+    for m in range(3):
+        lr, lam = to_np(ref.sigma[m]) ** 2, to_np(res.sigma[m]) ** 2
+        assert np.all(np.abs(lam - lr) <= 1e-11 * lr + 1e-14 * lr[0])
+        U, Ur = to_np(res.U[m]), to_np(ref.U[m])
+        for c in range(r[m]):
+            if lr[c] >= 1e-6 * lr[0] and np.min(np.abs(np.delete(lr, c) - lr[c])) >= 1e-6 * lr[0]:
+                assert np.max(np.abs(U[:, c] - Ur[:, c])) <= 1e-9
+    assert abs(e[1] - e_ref[1]) <= 1e-13 * e_ref[1]
+    assert abs(e[0] - e_ref[0]) <= max(1e-12, 1e-15 / e_ref[0])
+
+
+def test_config4_batch_512(T, orc):
+    """BASELINE config 4: 512^3, the 16 seeded Matérn settings (R10), ranks 30.  Every setting's
+    eigensolves converge; sampled entries against the oracle; E(r) non-increasing over r = 10,
+    20, 30; the orthogonal-projection identity at r = 30."""
+    from tucker_inputs import config4
+    w = config4()
+    g, r = w.grid, w.ranks
+    F = torch.empty(tuple(g.n), dtype=torch.float64, device="cuda")
+    ws = T.workspace(g, r)
+    rng = np.random.default_rng(4)
+    for k in w.kernels:
+        T.fill(g, k, F, ws)
+        for i, j, l in rng.integers(0, 512, size=(2, 3)):
+            ref = orc.fill_entry(ogrid(orc, g), okern(orc, k), int(i), int(j), int(l))
+            bound = 4 * np.spacing(ref) if k.nu in (0.5, 1.5, 2.5) else 1e-14 * abs(ref)
+            assert abs(float(F[i, j, l]) - ref) <= bound
+        res = T.hosvd(g, r, F, ws)
+        assert res.rc == 0 and all(res.info["converged"]), (k.label(), res.info)
+        es = []
+        for rr in (10, 20, 30):
+            U = [u[:, :rr].contiguous() for u in res.U]
+            core = T.ttm_core(g, (rr,) * 3, F, *U, ws=ws)
+            es.append(to_np(T.error(g, (rr,) * 3, F, U, core, ws)))
+        assert es[0][0] >= es[1][0] * (1 - 1e-12) >= es[2][0] * (1 - 1e-12) * (1 - 1e-12)
+        nb = np.linalg.norm(to_np(core))
+        e = es[2]
+        assert abs(e[1] ** 2 - nb ** 2 - e[2] ** 2) <= 1e-12 * e[1] ** 2
