@@ -6,8 +6,8 @@
 // G = Y_(m) Y_(m)^T.  One sweep streams F twice:
 //   pass A (k_ttm12, fused, TMA + DMMA):  T1 = F x3 U3^T (stored, n1 n2 x r3) and Y1 = T1 x2 U2^T
 //   Y1 -> Gram (k_gram, mode 0 of the n1 x r2 x r3 tensor) -> eigensolver -> U1
-//   Y2[j] = U1^T T1[:, j, :]       (batched small GEMM over j)   -> Gram -> eig -> U2
-//   pass B: Z = U1^T F_(1)          (r1 x n2 n3, small-GEMM kernel streaming F)
+//   Y2[j] = U1^T T1[:, j, :]       (batched DMMA GEMM over j)    -> Gram -> eig -> U2
+//   pass B: Z = U1^T F_(1)          (r1 x n2 n3, DMMA GEMM streaming F, gemm.cu)
 //   Y3[:, a, :] = Z[a]^T U2          (batched over a)              -> Gram -> eig -> U3
 // and after the last sweep the core beta[a,b,c] = sum_k U3[k,c] Y3[k,a,b] (no extra pass).
 // sigma_m are the singular values of the last single-hole unfoldings.  Everything reuses the
@@ -81,18 +81,18 @@ int launch_als(const int64_t n[3], const int32_t r[3], const double* F, double* 
         TK_RC(solve(0, Y1, r2, r3));
         // mode 2: Y2[j] (r1 x r3) = U1^T (r1 x n1) * T1[:, j, :] (n1 x r3, row stride n2 r3)
         SmallGemm g2{r1, r3, n1, n2, U[0], 1, r1, 0, T1, n2 * r3, 1, r3, Y2, r3, 1, r1 * r3};
-        TK_RC(launch_small_gemm(g2, st));
+        TK_RC(launch_gemm(g2, st));
         TK_RC(solve(1, Y2, r1, r3));
         // mode 3: pass B, Z (r1 x n2 n3) = U1^T F_(1); Y3[:, a, :] (n3 x r2) = Z[a]^T (n3 x n2) U2
         SmallGemm gz{r1, n2 * n3, n1, 1, U[0], 1, r1, 0, F, n2 * n3, 1, 0, Z, n2 * n3, 1, 0};
-        TK_RC(launch_small_gemm(gz, st));
+        TK_RC(launch_gemm(gz, st));
         SmallGemm g3{n3, r2, n2, r1, Z, 1, n3, n2 * n3, U[1], r2, 1, 0, Y3, r1 * r2, 1, r2};
-        TK_RC(launch_small_gemm(g3, st));
+        TK_RC(launch_gemm(g3, st));
         TK_RC(solve(2, Y3, r1, r2));
     }
     // core (r1 r2 x r3) = Y3_(3)^T (r1 r2 x n3) * U3 (n3 x r3)
     SmallGemm gc{r1 * r2, r3, n3, 1, Y3, 1, r1 * r2, 0, U[2], r3, 1, 0, core, r3, 1, 0};
-    TK_RC(launch_small_gemm(gc, st));
+    TK_RC(launch_gemm(gc, st));
     return worst;
 }
 

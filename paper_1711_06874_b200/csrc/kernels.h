@@ -129,5 +129,8 @@ struct SmallGemm {
     int64_t scm, scn, scb;
 };
 int launch_small_gemm(const SmallGemm& p, cudaStream_t st);
+// Same contract on the FP64 tensor cores (gemm.cu) when the contraction is large; falls back to
+// launch_small_gemm for small ones.
+int launch_gemm(const SmallGemm& p, cudaStream_t st);
 
 }  // namespace tk

@@ -12,7 +12,7 @@
 //                                            squaring, small singular values keep their accuracy)
 // and U_m = U~[:, :r], sigma_m = Sigma[:r]; `iters` repeats the step from V = U~.  Every product
 // is a plain FP64 contraction of F (no Gram), so the singular values are resolved down to
-// ~eps sigma_1.  The streaming products use the small-GEMM kernel (k_small_gemm).
+// ~eps sigma_1.  The streaming products run on the DMMA GEMM (gemm.cu).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -206,13 +206,13 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
         // ---- pass 1: Yt (p x M) = V^T F_(m)
         if (m == 0) {  // Yt[a][(j,k)] = sum_i V[i][a] F[i][(j,k)]
             SmallGemm g{p, M, n1, 1, V, 1, p, 0, F, M, 1, 0, Yt, M, 1, 0};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
         } else if (m == 1) {  // Yt[b][(i,k)] = sum_j V[j][b] F[i][j][k], batched over i
             SmallGemm g{p, n3, n2, n1, V, 1, p, 0, F, n3, 1, n2 * n3, Yt, M, 1, n3};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
         } else {  // Yt[c][(i,j)] = sum_k V[k][c] F[(i,j)][k]
             SmallGemm g{p, M, n3, 1, V, 1, p, 0, F, 1, n3, 0, Yt, M, 1, 0};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
         }
         // ---- CGS2 of the p columns of Y (each column contiguous in Yt)
         // flags[0] = 0 (attempt 0 always runs), flags[1] = attempt 0 accepted (attempt 1 skipped)
@@ -238,17 +238,17 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
         const int64_t Kc = M / S;
         if (m == 0) {  // B[i][a] = sum_col F[i][col] Qt[a][col]
             SmallGemm g{n1, p, Kc, S, F, M, 1, Kc, Yt, 1, M, Kc, Bpart, p, 1, n1 * p};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
             k_sum_partials<<<256, 256, 0, st>>>(Bpart, S, n1 * p, B);
             TK_CHECK_LAUNCH();
         } else if (m == 1) {  // B_i[j][b] = sum_k F[i][j][k] Qt[b][(i,k)], batched over i
             SmallGemm g{n2, p, n3, n1, F, n3, 1, n2 * n3, Yt, 1, M, n3, Bpart, p, 1, n2 * p};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
             k_sum_partials<<<256, 256, 0, st>>>(Bpart, (int)n1, n2 * p, B);
             TK_CHECK_LAUNCH();
         } else {  // B[k][c] = sum_row F[row][k] Qt[c][row]
             SmallGemm g{n3, p, Kc, S, F, 1, n3, Kc * n3, Yt, 1, M, Kc, Bpart, p, 1, n3 * p};
-            TK_RC(launch_small_gemm(g, st));
+            TK_RC(launch_gemm(g, st));
             k_sum_partials<<<256, 256, 0, st>>>(Bpart, S, n3 * p, B);
             TK_CHECK_LAUNCH();
         }
