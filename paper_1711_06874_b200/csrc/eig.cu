@@ -5,11 +5,12 @@
 //
 // Method (B200 design; the paper names no eigensolver): block subspace iteration with
 // Rayleigh–Ritz on p = r + q columns (q = min(16, 64 - r)):
-//   V_0 = orth(G Omega), Omega a fixed counter-hash block (deterministic)
+//   V_0 = orth(G Omega), Omega a fixed counter-hash block (deterministic); V_1 = orth(G V_0)
+//   (cluster path: plain power steps until the last of the kMinIters iterations)
 //   repeat: W = G V (multi-CTA DFMA GEMM); H = V^T W (p x p); H = Q Theta Q^T by parallel cyclic
 //           Jacobi in shared memory (round-robin pairs, warp-parallel rotations, skip rule R7);
 //           Vr = V Q, Y = W Q; residual rho_k = ||Y_k - theta_k Vr_k||;
-//           stop when rho_k <= 1e-14 theta_1 for k < r after >= 3 iterations, else V = CGS2(Y).
+//           stop when rho_k <= tol theta_1 for k < r after >= 3 iterations, else V = CGS2(Y).
 // Small matrices (n <= 112) are diagonalised directly by the same shared-memory Jacobi.
 // Outputs are sorted descending (stable) and sign-fixed by rule R6: the first entry with
 // |u_i| >= max|u|/2 is made positive.  Everything is deterministic (fixed reduction orders).
@@ -406,9 +407,17 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
         k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
         TK_CHECK_LAUNCH();
         TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
-        int it = 0;
+        // iterations 1 .. kMinIters-2 are plain power steps (V <- CGS2(G V), no Rayleigh–Ritz):
+        // the Ritz rotation does not change the subspace, and a single Jacobi solve of the dense
+        // H at the end replaces the per-iteration ones
+        for (int w = 1; w < kMinIters - 1; ++w) {
+            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
+            TK_CHECK_LAUNCH();
+            TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
+        }
+        int it = kMinIters - 1;
         while (true) {
-            const int batch = it == 0 ? 4 : kBatch;
+            const int batch = it == kMinIters - 1 ? 4 : kBatch;
             for (int b = 0; b < batch && it < kMaxIters; ++b, ++it) {
                 k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
                 TK_CHECK_LAUNCH();
