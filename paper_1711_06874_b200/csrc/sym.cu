@@ -27,7 +27,9 @@ constexpr double kSqrt2 = 1.4142135623730951;
 __device__ __forceinline__ bool is_mid(int64_t i, int64_t n) { return (n & 1) && i == (n - 1) / 2; }
 
 // F_w (h1 x h2 x h3, C order).  Values = the materialised fill's (same nodes, same association
-// order) times the exact weight {1, sqrt2, 2, 2 sqrt2}[# non-middle indices].
+// order) times the exact weight {1, sqrt2, 2, 2 sqrt2}[# non-middle indices].  An item is 4
+// consecutive k of one (i, j) row (one index decomposition per 4 evaluations; 256-bit stores when
+// h3 % 4 == 0).
 __global__ void __launch_bounds__(256) k_fill_sym(KParams kp, const double* __restrict__ cheb_g,
                                                   const double* __restrict__ x2, int64_t n1, int64_t n2,
                                                   int64_t n3, double* __restrict__ Fw) {
@@ -38,14 +40,30 @@ __global__ void __launch_bounds__(256) k_fill_sym(KParams kp, const double* __re
     const double* xa = x2;
     const double* xb = x2 + n1;
     const double* xc = x2 + n1 + n2;
-    const int64_t h1 = (n1 + 1) / 2, h2 = (n2 + 1) / 2, h3 = (n3 + 1) / 2;
-    const int64_t total = h1 * h2 * h3;
+    const int64_t h1 = (n1 + 1) / 2, h2 = (n2 + 1) / 2, h3 = (n3 + 1) / 2, q3 = (h3 + 3) / 4;
+    const int64_t total = h1 * h2 * q3;
     const double wtab[4] = {1.0, kSqrt2, 2.0, 2.0 * kSqrt2};
+    const bool vec = (h3 % 4) == 0;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total; it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = it % h3, ij = it / h3, j = ij % h2, i = ij / h2;
-        const double v = eval_point(kp, cheb, __dadd_rn(__dadd_rn(xa[i], xb[j]), xc[k]));
-        const int c = (is_mid(i, n1) ? 0 : 1) + (is_mid(j, n2) ? 0 : 1) + (is_mid(k, n3) ? 0 : 1);
-        Fw[it] = v * wtab[c];
+        const int64_t t = it % q3, ij = it / q3, j = ij % h2, i = ij / h2;
+        const int cij = (is_mid(i, n1) ? 0 : 1) + (is_mid(j, n2) ? 0 : 1);
+        const double s = __dadd_rn(xa[i], xb[j]);
+        const int64_t k0 = 4 * t;
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t k = k0 + u;
+            v[u] = 0.0;
+            if (k < h3) v[u] = eval_point(kp, cheb, __dadd_rn(s, xc[k])) * wtab[cij + (is_mid(k, n3) ? 0 : 1)];
+        }
+        double* row = Fw + (i * h2 + j) * h3;
+        if (vec) {
+            st_v4(row + k0, v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k0 + u < h3) row[k0 + u] = v[u];
+        }
     }
 }
 
@@ -143,7 +161,7 @@ int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_
     void* scr = w + L.scratch;
     const KParams kp = make_kparams(kn);
     TK_RC(launch_fill_prep(g, kn, kp, x2, cheb, st));
-    const int64_t tot = L.h[0] * L.h[1] * L.h[2];
+    const int64_t tot = L.h[0] * L.h[1] * ((L.h[2] + 3) / 4);
     k_fill_sym<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 256), (int64_t)kNumSMs * 16)), 256, 0,
                  st>>>(kp, cheb, x2, g.n[0], g.n[1], g.n[2], Fw);
     TK_CHECK_LAUNCH();
