@@ -447,14 +447,16 @@ def run_sym(T, n: int, rr: int, stream, reps: int = 3) -> dict:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     Nh = h ** 3
-    flops = 3 * Nh * (h + 1) + 2.0 * Nh * rr * 2
+    grams = 1  # cubic isotropic grid: one Gram serves all three modes (G_1 = G_2 = G_3)
+    flops = grams * Nh * (h + 1) + 2.0 * Nh * rr * 2
     e = err.cpu().tolist()
     return {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2_symmetric", "grid": [n, n, n], "ranks": list(ranks),
             "value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
             "algorithmic_flops_per_step": flops, "fp64_tflops_algorithmic": flops / (ms * 1e-3) / 1e12,
             "E": e[0], "normF": e[1], "rc": res.rc,
             "note": "weighted-octant reduction (exact on centred grids, DESIGN f3): N/8 points carry the "
-                    "work; Gram flops 3 (N/8)(n/2+1), TTM + error 4 (N/8) r"}
+                    "work; cubic isotropic grid: one Gram (N/8)(n/2+1) flops serves all modes; TTM + error "
+                    "4 (N/8) r"}
 
 
 # ------------------------------------------------------------------------------ oracle arm ----

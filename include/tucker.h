@@ -192,6 +192,8 @@ TUCKER_API int tucker_als(const tucker_grid* grid, const int32_t r[3], const dou
  * (even) factors u = y / sqrt(w) mirrored to full length, and core and error equal those of F
  * (f3).  Outputs as tucker_hosvd (full-length U_m, sign rule R6 on the full vector,
  * core consistent with them) plus err3 (dev, nullable) = {E, ||F||, ||F - Ft||}.
+ * On a cubic isotropic grid (equal n_m, boxes and ranks) the three mode Grams are equal and one
+ * Gram + eigensolve serves all modes (U1 = U2 = U3).
  * Requires r_m <= ceil(n_m/2) (the odd eigenvectors have eigenvalue 0): else TUCKER_ERR_RANK.
  * Non-centred grid: TUCKER_ERR_UNSUPPORTED.  Workspace >= tucker_workspace_size_sym(grid, r);
  * no F argument (the octant is generated into the workspace, N/8 doubles). */

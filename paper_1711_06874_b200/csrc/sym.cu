@@ -12,7 +12,9 @@
 //     odd eigenvectors have eigenvalue 0 (rank F_(m) <= h_m), so r_m <= h_m is required;
 //   * beta = F x1 U1^T x2 U2^T x3 U3^T = F_w x1 Y1^T x2 Y2^T x3 Y3^T (Y_m = the y's);
 //   * ||F - F~||^2 = ||F_w - F_w~||^2 and ||F|| = ||F_w||.
-// So the hot path runs unchanged on F_w (N/8 points): Grams cost 1/16, TTM and error 1/8.  The
+// So the hot path runs unchanged on F_w (N/8 points): Grams cost 1/16, TTM and error 1/8; on a
+// cubic isotropic grid (equal n, boxes and ranks) one Gram and one eigensolve serve all three
+// modes (F is then symmetric under index permutations: G_1 = G_2 = G_3).  The
 // factors are expanded and sign-fixed by rule R6 on the full vector (k_expand_sym), and the core
 // is formed from the sign-fixed y's so that it matches the returned U.
 #include "common.cuh"
@@ -167,8 +169,27 @@ int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_
     TK_CHECK_LAUNCH();
     double* Y[3];
     int worst = TUCKER_OK;
+    // cubic isotropic grid and equal ranks: F is symmetric under index permutations, so the three
+    // mode Grams are equal (up to the rounding of r^2's summation order) — one Gram and one
+    // eigensolve serve all modes
+    const bool iso = g.n[0] == g.n[1] && g.n[1] == g.n[2] && g.lo[0] == g.lo[1] && g.lo[1] == g.lo[2] &&
+                     g.hi[0] == g.hi[1] && g.hi[1] == g.hi[2] && r[0] == r[1] && r[1] == r[2];
     for (int m = 0; m < 3; ++m) {
         Y[m] = reinterpret_cast<double*>(w + L.Y[m]);
+        if (iso && m > 0) {
+            TK_CUDA(cudaMemcpyAsync(Y[m], Y[0], (size_t)L.h[m] * r[m] * 8, cudaMemcpyDeviceToDevice, st));
+            TK_CUDA(cudaMemcpyAsync(U[m], U[0], (size_t)g.n[m] * r[m] * 8, cudaMemcpyDeviceToDevice, st));
+            TK_CUDA(cudaMemcpyAsync(sigma[m], sigma[0], (size_t)r[m] * 8, cudaMemcpyDeviceToDevice, st));
+            if (info) {
+                info->iters[m] = info->iters[0];
+                info->converged[m] = info->converged[0];
+                info->block[m] = info->block[0];
+                info->sweeps[m] = info->sweeps[0];
+                info->resid[m] = info->resid[0];
+                info->lambda1[m] = info->lambda1[0];
+            }
+            continue;
+        }
         TK_RC(launch_gram(L.h, m, Fw, G, scr, L.scratch_bytes, st));
         const int rc = launch_eig(L.h[m], G, r[m], Y[m], nullptr, sigma[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
