@@ -1,7 +1,8 @@
 // gemm.cu — strided batched FP64 GEMM on the tensor cores (DMMA), for the large dense contractions
 // of the NEXT rows: the single-hole products of Tucker-ALS (f1) and the two streaming passes of
 // the SVD-accurate HOSVD (f2).  C[b] (M x N) = A[b] (M x K) * B[b] (K x N) with arbitrary element
-// strides (the operands are views of F, of factor matrices and of their transposes).
+// strides (the operands are views of F, of factor matrices and of their transposes); `sub`
+// selects C = C - A B (block Gram–Schmidt updates).
 //
 // CTA tile (32 WM) x (32 WN), WM x WN = 8 warps of 32 x 32; K-steps of 16 in a 4-stage cp.async
 // ring.  Both operands are staged k-major per output line in the 128-byte-swizzled layout of the
@@ -98,7 +99,10 @@ __global__ void __launch_bounds__(NT) k_dgemm(const SmallGemm g) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int64_t m = m0 + wm * 32 + mi * 8 + r, n = n0 + wn * 32 + ni * 8 + 2 * q + u;
-                if (m < g.M && n < g.N) C[m * g.scm + n * g.scn] = acc[mi][ni][u];
+                if (m < g.M && n < g.N) {
+                    double* c = C + m * g.scm + n * g.scn;
+                    *c = g.sub ? *c - acc[mi][ni][u] : acc[mi][ni][u];
+                }
             }
 }
 

@@ -127,6 +127,7 @@ struct SmallGemm {
     int64_t sbk, sbn, sbb;
     double* C;
     int64_t scm, scn, scb;
+    int sub;  // 0: C = A B;  1: C = C - A B
 };
 int launch_small_gemm(const SmallGemm& p, cudaStream_t st);
 // Same contract on the FP64 tensor cores (gemm.cu) when the contraction is large; falls back to

@@ -5,8 +5,10 @@
 // sigma_1 are lost (E plateaus near 1e-8).  This pass recovers SVD accuracy with a Rayleigh–Ritz
 // step on F_(m) itself, starting from the Gram route's p = r + q leading eigenvectors V:
 //   pass 1   Y = F_(m)^T V                 (N/n_m x p, stored column-major as Yt = Y^T)
-//   CGS2     Q = orth(Y)                    (classical Gram–Schmidt twice, column by column over
-//                                            all SMs, deterministic fixed-order reductions)
+//   BCGS2    Q = orth(Y)                    (block classical Gram–Schmidt twice: blocks of 8
+//                                            columns, one pass over the earlier columns per
+//                                            block projection, CGS2 inside a block; fixed-order
+//                                            reductions)
 //   pass 2   B = F_(m) Q                    (n_m x p, split-K partials + fixed-order reduce)
 //   SVD      B = U~ Sigma W^T               (one-sided Jacobi in a thread-block cluster: no
 //                                            squaring, small singular values keep their accuracy)
@@ -37,13 +39,14 @@ __device__ __forceinline__ void row_range(int64_t M, int64_t& b0, int64_t& b1) {
 
 // part[blk][j] = sum_{rows of blk} Q_j[row] y[row], j < k (columns of Yt are contiguous, length M).
 __global__ void __launch_bounds__(kNT) k_cgs_dots(const double* __restrict__ Yt, int64_t M, int k,
-                                                  double* __restrict__ part, const int* __restrict__ done) {
+                                                  double* __restrict__ part, const int* __restrict__ done,
+                                                  const int* __restrict__ jstart) {
     if (*done) return;
     __shared__ double red[40];
     int64_t b0, b1;
     row_range(M, b0, b1);
     const double* y = Yt + (size_t)k * M;
-    for (int j0 = 0; j0 < k; j0 += 8) {
+    for (int j0 = *jstart; j0 < k; j0 += 8) {
         double acc[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = 0.0;
@@ -61,18 +64,30 @@ __global__ void __launch_bounds__(kNT) k_cgs_dots(const double* __restrict__ Yt,
     }
 }
 
-// h = sum over blocks (fixed order, every CTA); y -= Q h on this CTA's rows; npart[blk] = ||y||^2.
+// h[j] = sum over blocks of part[blk][j] (j in [jstart, k)): one warp per j, lanes strided over the
+// blocks, fixed shuffle tree (deterministic).
+__global__ void __launch_bounds__(1024) k_reduce_h(const double* __restrict__ part, int nblk, int k,
+                                                   const int* __restrict__ done, const int* __restrict__ jstart,
+                                                   double* __restrict__ h) {
+    if (*done) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = *jstart + warp; j < k; j += 32) {
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += part[(size_t)b * 64 + j];
+        s = warp_sum(s);
+        if (lane == 0) h[j] = s;
+    }
+}
+
+// y -= Q h on this CTA's rows (j in [jstart, k)); npart[blk] = ||y||^2 of its rows.
 __global__ void __launch_bounds__(kNT) k_cgs_update(double* __restrict__ Yt, int64_t M, int k,
-                                                    const double* __restrict__ part, int nblk,
-                                                    double* __restrict__ npart, const int* __restrict__ done) {
+                                                    const double* __restrict__ hg, double* __restrict__ npart,
+                                                    const int* __restrict__ done, const int* __restrict__ jstart) {
     if (*done) return;
     __shared__ double h[64];
     __shared__ double red[40];
-    for (int j = threadIdx.x; j < k; j += kNT) {
-        double s = 0.0;
-        for (int b = 0; b < nblk; ++b) s += part[(size_t)b * 64 + j];
-        h[j] = s;
-    }
+    const int js = *jstart;
+    for (int j = threadIdx.x; j < k; j += kNT) h[j] = j < js ? 0.0 : hg[j];
     __syncthreads();
     int64_t b0, b1;
     row_range(M, b0, b1);
@@ -80,7 +95,7 @@ __global__ void __launch_bounds__(kNT) k_cgs_update(double* __restrict__ Yt, int
     double ss = 0.0;
     for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
         double yi = y[i];
-        for (int j = 0; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
+        for (int j = js; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
         y[i] = yi;
         ss = fma(yi, yi, ss);
     }
@@ -99,14 +114,18 @@ __global__ void __launch_bounds__(kNT) k_cgs_finish(double* __restrict__ Yt, int
                                                     const int* __restrict__ skip, int* accepted, int last) {
     if (*skip) return;
     __shared__ double tot, tot1;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // lanes strided over the blocks, fixed shuffle tree
         double s = 0.0, s1 = 0.0;
-        for (int b = 0; b < nblk; ++b) {
+        for (int b = threadIdx.x; b < nblk; b += 32) {
             s1 += npart[b];
             s += npart[nblk + b];
         }
-        tot = s;
-        tot1 = s1;
+        s = warp_sum(s);
+        s1 = warp_sum(s1);
+        if (threadIdx.x == 0) {
+            tot = s;
+            tot1 = s1;
+        }
     }
     __syncthreads();
     int64_t b0, b1;
@@ -133,6 +152,110 @@ __global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const dou
     }
 }
 
+// Block projection coefficients, per-CTA partials: part[blk][j * bb + t] = sum over this CTA's rows
+// of Q_j[i] Y_{c0+t}[i], j < c0, t < bb.  Rows are staged 32 at a time in shared memory (all
+// column segments contiguous, coalesced); each thread owns (j, t) pairs.
+__global__ void __launch_bounds__(kNT) k_block_dots(const double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                    double* __restrict__ part) {
+    __shared__ double tile[32][64 + 8 + 1];
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    const int ncol = c0 + bb, npair = c0 * bb;
+    double acc[2] = {0.0, 0.0};  // pairs threadIdx.x and threadIdx.x + 256 (npair <= 56 * 8 = 448)
+    for (int64_t r0 = b0; r0 < b1; r0 += 32) {
+        const int rows = (b1 - r0) < 32 ? (int)(b1 - r0) : 32;
+        for (int e = threadIdx.x; e < 32 * ncol; e += kNT) {
+            const int c = e / 32, i = e % 32;
+            tile[i][c] = i < rows ? Yt[(size_t)c * M + r0 + i] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int pr = threadIdx.x + kNT * u;
+            if (pr < npair) {
+                const int j = pr / bb, t = pr % bb;
+                double a = acc[u];
+                for (int i = 0; i < 32; ++i) a = fma(tile[i][j], tile[i][c0 + t], a);
+                acc[u] = a;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int pr = threadIdx.x + kNT * u;
+        if (pr < npair) part[(size_t)blockIdx.x * npair + pr] = acc[u];
+    }
+}
+
+// Y_{c0+t}[i] -= sum_j Q_j[i] H[j][t] on this CTA's rows, then per-CTA partial squared norms of
+// the updated block columns (cnpart[blk][t]).
+__global__ void __launch_bounds__(kNT) k_block_update(double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                      const double* __restrict__ H, double* __restrict__ cnpart) {
+    __shared__ double h[64 * 8];
+    __shared__ double red[40];
+    for (int e = threadIdx.x; e < c0 * bb; e += kNT) h[e] = H[e];
+    __syncthreads();
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    double nrm[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) nrm[t] = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
+        double y[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) y[t] = t < bb ? Yt[(size_t)(c0 + t) * M + i] : 0.0;
+        for (int j = 0; j < c0; ++j) {
+            const double qj = Yt[(size_t)j * M + i];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (t < bb) y[t] = fma(-qj, h[j * bb + t], y[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (t < bb) {
+                Yt[(size_t)(c0 + t) * M + i] = y[t];
+                nrm[t] = fma(y[t], y[t], nrm[t]);
+            }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const double v = block_sum(nrm[t], red);
+        if (threadIdx.x == 0) cnpart[(size_t)blockIdx.x * 8 + t] = v;
+    }
+}
+
+// After the two inter-block passes: column t keeps its block-local projection start c0 when
+// ||y''||^2 >= ||y'||^2 / 2 (Kahan–Parlett), else it is treated as dependent on the earlier
+// blocks: start 0 (the intra-block step then projects it against every earlier column, and its
+// own acceptance test replaces it by a pseudo-random vector if needed).
+__global__ void k_block_check(const double* __restrict__ part1, const double* __restrict__ part2, int nblk, int bb,
+                              int c0, int* __restrict__ jstart) {
+    const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp per column, lanes over blocks
+    if (t >= bb) return;
+    double n1 = 0.0, n2 = 0.0;
+    for (int b = lane; b < nblk; b += 32) {
+        n1 += part1[(size_t)b * 8 + t];
+        n2 += part2[(size_t)b * 8 + t];
+    }
+    n1 = warp_sum(n1);
+    n2 = warp_sum(n2);
+    if (lane == 0) jstart[c0 + t] = (n2 > 1e-300 && n2 >= 0.5 * n1) ? c0 : 0;
+}
+
+// out[o] = sum_s part[s][o] for short outputs and many partials: warp per output, lanes strided
+// over s, fixed shuffle tree.
+__global__ void k_sum_partials_warp(const double* __restrict__ part, int S, int64_t len, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t o = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; o < len;
+         o += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double s = 0.0;
+        for (int q = lane; q < S; q += 32) s += part[(size_t)q * len + o];
+        s = warp_sum(s);
+        if (lane == 0) out[o] = s;
+    }
+}
+
 // out[o] = sum_s part[s][o] (fixed order)
 __global__ void k_sum_partials(const double* __restrict__ part, int S, int64_t len, double* __restrict__ out) {
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < len; o += (int64_t)gridDim.x * blockDim.x) {
@@ -143,12 +266,13 @@ __global__ void k_sum_partials(const double* __restrict__ part, int S, int64_t l
 }
 
 struct RefLayout {
-    size_t Yt, B, Bpart, V, dots, npart, flags, total;
+    size_t Yt, B, Bpart, V, dots, npart, flags, H, Hpart, cn, jst, total;
     int64_t Mmax;
     int S2;
 };
 
-constexpr int kSplit = 64;  // split-K factor of pass 2
+constexpr int kSplit = 64;  // split-K factor of pass 2 and of the block projections
+constexpr int kBS = 8;      // block width of the block Gram–Schmidt
 
 RefLayout ref_plan(const int64_t n[3], int p) {
     RefLayout L{};
@@ -171,6 +295,14 @@ RefLayout ref_plan(const int64_t n[3], int p) {
     off += align_up((size_t)2 * kBlk * 8, 256);
     L.flags = off;
     off += 256;
+    L.H = off;
+    off += align_up((size_t)64 * kBS * 8, 256);
+    L.Hpart = off;
+    off += align_up((size_t)std::max(kSplit, kBlk) * 64 * kBS * 8, 256);
+    L.cn = off;
+    off += align_up((size_t)2 * kBlk * 8 * 8, 256);
+    L.jst = off;
+    off += align_up((size_t)(64 + 1) * sizeof(int), 256);
     L.total = off;
     return L;
 }
@@ -195,6 +327,9 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
     double* dots = reinterpret_cast<double*>(w + L.dots);
     double* npart = reinterpret_cast<double*>(w + L.npart);
     int* flags = reinterpret_cast<int*>(w + L.flags);
+    double* H = reinterpret_cast<double*>(w + L.H);
+    double* Hpart = reinterpret_cast<double*>(w + L.Hpart);
+    double* cn = reinterpret_cast<double*>(w + L.cn);
     const int64_t n1 = n[0], n2 = n[1], n3 = n[2], nm = n[m];
     const int64_t M = n1 * n2 * n3 / nm;
     TK_CUDA(cudaMemcpyAsync(V, V0, (size_t)nm * p * 8, cudaMemcpyDeviceToDevice, st));
@@ -214,28 +349,52 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
             SmallGemm g{p, M, n3, 1, V, 1, p, 0, F, 1, n3, 0, Yt, M, 1, 0};
             TK_RC(launch_gemm(g, st));
         }
-        // ---- CGS2 of the p columns of Y (each column contiguous in Yt)
-        // flags[0] = 0 (attempt 0 always runs), flags[1] = attempt 0 accepted (attempt 1 skipped)
-        for (int k = 0; k < p; ++k) {
-            TK_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), st));
-            for (int attempt = 0; attempt < 2; ++attempt) {
-                const int* skip = flags + attempt;
+        // ---- block CGS2 of the p columns of Y (each column contiguous in Yt): blocks of kBS
+        // columns; two inter-block passes (H = Q_<c0^T Y_B from per-CTA partials summed in a fixed
+        // order, Y_B -= Q_<c0 H), then column-by-column CGS2 inside the block.
+        int S = kSplit;  // split of the M-long contractions: the largest divisor of M not above kSplit
+        while (M % S) --S;
+        const int64_t Kc = M / S;
+        int* jstart = reinterpret_cast<int*>(w + L.jst);
+        int* jzero = jstart + 64;
+        TK_CUDA(cudaMemsetAsync(jstart, 0, 65 * sizeof(int), st));
+        for (int c0 = 0; c0 < p; c0 += kBS) {
+            const int bb = std::min(kBS, p - c0);
+            double* YB = Yt + (size_t)c0 * M;
+            if (c0 > 0) {
                 for (int pass = 0; pass < 2; ++pass) {
-                    if (k > 0) {
-                        k_cgs_dots<<<kBlk, kNT, 0, st>>>(Yt, M, k, dots, skip);
-                        TK_CHECK_LAUNCH();
-                    }
-                    k_cgs_update<<<kBlk, kNT, 0, st>>>(Yt, M, k, dots, kBlk, npart + pass * kBlk, skip);
+                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart);
+                    TK_CHECK_LAUNCH();
+                    k_sum_partials_warp<<<48, 256, 0, st>>>(Hpart, kBlk, (int64_t)c0 * bb, H);
+                    TK_CHECK_LAUNCH();
+                    k_block_update<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, H, cn + (size_t)pass * kBlk * 8);
                     TK_CHECK_LAUNCH();
                 }
-                k_cgs_finish<<<kBlk, kNT, 0, st>>>(Yt, M, k, npart, kBlk, skip, flags + attempt + 1, attempt);
+                k_block_check<<<1, 256, 0, st>>>(cn, cn + (size_t)kBlk * 8, kBlk, bb, c0, jstart);
                 TK_CHECK_LAUNCH();
+            }
+            // flags[0] = 0 (attempt 0 always runs), flags[1] = attempt 0 accepted (attempt 1 skipped)
+            for (int k = c0; k < c0 + bb; ++k) {
+                TK_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), st));
+                for (int attempt = 0; attempt < 2; ++attempt) {
+                    const int* skip = flags + attempt;
+                    const int* js = attempt == 0 ? jstart + k : jzero;  // a replaced column: full projection
+                    for (int pass = 0; pass < 2; ++pass) {
+                        if (k > 0) {
+                            k_cgs_dots<<<kBlk, kNT, 0, st>>>(Yt, M, k, dots, skip, js);
+                            TK_CHECK_LAUNCH();
+                            k_reduce_h<<<1, 1024, 0, st>>>(dots, kBlk, k, skip, js, H);
+                            TK_CHECK_LAUNCH();
+                        }
+                        k_cgs_update<<<kBlk, kNT, 0, st>>>(Yt, M, k, H, npart + pass * kBlk, skip, js);
+                        TK_CHECK_LAUNCH();
+                    }
+                    k_cgs_finish<<<kBlk, kNT, 0, st>>>(Yt, M, k, npart, kBlk, skip, flags + attempt + 1, attempt);
+                    TK_CHECK_LAUNCH();
+                }
             }
         }
         // ---- pass 2: B (n_m x p) = F_(m) Q, split over the contraction, fixed-order sum
-        int S = kSplit;  // split of the contraction: the largest divisor of M not above kSplit
-        while (M % S) --S;
-        const int64_t Kc = M / S;
         if (m == 0) {  // B[i][a] = sum_col F[i][col] Qt[a][col]
             SmallGemm g{n1, p, Kc, S, F, M, 1, Kc, Yt, 1, M, Kc, Bpart, p, 1, n1 * p};
             TK_RC(launch_gemm(g, st));

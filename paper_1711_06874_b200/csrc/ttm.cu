@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(256) k_small_gemm(SmallGemm p) {
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int64_t m = m0 + ty * 4 + u, n = n0 + tx * 4 + v;
-            if (m < p.M && n < p.N) C[m * p.scm + n * p.scn] = acc[u][v];
+            if (m < p.M && n < p.N) {
+                double* c = C + m * p.scm + n * p.scn;
+                *c = p.sub ? *c - acc[u][v] : acc[u][v];
+            }
         }
 }
 
