@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-sym", action="store_true", help="skip the symmetry-exploiting (NEXT f3) line")
     ap.add_argument("--no-accurate", action="store_true", help="skip the SVD-accurate (NEXT f2) line")
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
+    ap.add_argument("--no-f4", action="store_true", help="skip the NEXT f4 workloads line")
     ap.add_argument("--fused-n", type=int, default=2048)
     return ap.parse_args()
 
@@ -329,6 +330,8 @@ def run_ours(args, rank, world, local):
                               "ms": c0.elapsed_time(c1), "E": ec[0], "E_gram_route": E[0], "rc": acc.rc,
                               "sigma_min_resolved": [float(s[-1]) / float(s[0]) for s in
                                                      (x.cpu() for x in acc.sigma)]}
+    if not args.no_f4 and world == 1:
+        result["f4"] = run_f4(T, grid, ranks, F, ws, stream)
     if not args.no_cfg4 and world == 1:
         del F
         torch.cuda.empty_cache()
@@ -383,6 +386,32 @@ def run_fused(T, n: int, rr: int, stream) -> dict:
             "E": e[0], "normF": e[1], "eig_info": res.info, "rc": res.rc,
             "timed": "one hosvd_fused + error_fused call (CUDA events), after a warm-up Gram; gram_ms from "
                      "three separate tucker_gram_fused calls"}
+
+
+def run_f4(T, grid, ranks, F, ws, stream) -> dict:
+    """NEXT f4: the paper's other workloads through the same step on the same 1024^3 grid —
+    Matérn spectral density (alpha = 0.1 and 100, nu = 0.4) and p-Slater
+    (p = 0.1, 1.9): fill + HOSVD + error per kernel."""
+    import torch
+
+    from tucker_inputs import KernelSpec
+    out = []
+    for k in (KernelSpec.spectral(0.1, 0.4), KernelSpec.spectral(100.0, 0.4), KernelSpec.slater(1.0, 0.1),
+              KernelSpec.slater(1.0, 1.9)):
+        T.fill(grid, k, F, ws, stream)  # warm-up of this fill
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        T.fill(grid, k, F, ws, stream)
+        e[1].record(stream)
+        res = T.hosvd(grid, ranks, F, ws, stream)
+        err = T.error(grid, ranks, F, res.U, res.core, ws, stream)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        ms = e[0].elapsed_time(e[2])
+        out.append({"kernel": k.label(), "ms_per_step": ms, "fill_ms": e[0].elapsed_time(e[1]),
+                    "value": grid.points / (ms * 1e-3), "E": float(err[0]), "rc": res.rc})
+    return {"grid": list(grid.n), "ranks": list(ranks), "unit": UNIT, "workloads": out}
 
 
 def run_cfg4(T, stream) -> dict:
