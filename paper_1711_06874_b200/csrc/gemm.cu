@@ -19,8 +19,24 @@ namespace dg {
 
 constexpr int BK = 16, STAGES = 4, NT = 256;
 
+// Element e of a [L lines][16 k] stage -> (line, col).  k-fast operands: 16 consecutive lanes read
+// one line's 16 consecutive k (128 B).  Line-fast operands: a half-warp covers 8 consecutive lines x
+// 2 adjacent k (two 64-B global segments) — in the swizzled layout those are 16 distinct 8-byte
+// bank slots, so the cp.async shared-memory writes are conflict-free.
+template <int L>
+__device__ __forceinline__ void map_elem(int e, bool kfast, int& line, int& col) {
+    if (kfast) {
+        line = e >> 4;
+        col = e & 15;
+    } else {
+        const int sub = e & 15, blk = e >> 4;
+        line = (blk % (L / 8)) * 8 + (sub & 7);
+        col = (blk / (L / 8)) * 2 + (sub >> 3);
+    }
+}
+
 template <int WM, int WN>
-__global__ void __launch_bounds__(NT) k_dgemm(const SmallGemm g) {
+__global__ void __launch_bounds__(NT, 2) k_dgemm(const SmallGemm g) {
     constexpr int BM = 32 * WM, BN = 32 * WN;
     constexpr int AT = BM * BK, BT = BN * BK;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -41,7 +57,8 @@ __global__ void __launch_bounds__(NT) k_dgemm(const SmallGemm g) {
 #pragma unroll
         for (int u = 0; u < AT / NT; ++u) {
             const int e = tid + NT * u;
-            const int line = a_kfast ? e >> 4 : e % BM, col = a_kfast ? e & 15 : e / BM;
+            int line, col;
+            map_elem<BM>(e, a_kfast, line, col);
             const int64_t m = m0 + line, k = k0 + col;
             const bool ok = (m < g.M) && (k < g.K);
             cp_async8(dA + swz(line, col), ok ? A + m * g.sam + k * g.sak : A, ok);
@@ -49,7 +66,8 @@ __global__ void __launch_bounds__(NT) k_dgemm(const SmallGemm g) {
 #pragma unroll
         for (int u = 0; u < BT / NT; ++u) {
             const int e = tid + NT * u;
-            const int line = b_kfast ? e >> 4 : e % BN, col = b_kfast ? e & 15 : e / BN;
+            int line, col;
+            map_elem<BN>(e, b_kfast, line, col);
             const int64_t n = n0 + line, k = k0 + col;
             const bool ok = (n < g.N) && (k < g.K);
             cp_async8(dB + swz(line, col), ok ? B + k * g.sbk + n * g.sbn : B, ok);
