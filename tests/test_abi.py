@@ -78,3 +78,43 @@ def test_workspace_size_monotone(lib):
     assert 0 < a < b <= c
     big = T.workspace_bytes(GridSpec.cube(1024, 1.0), (40, 40, 40))
     assert big < 4 * 2 ** 30  # scratch for 1024^3 at ranks 40 stays well inside 180 GB
+
+
+def test_validation_codes_next_rows(lib):
+    """The fused, symmetric, ALS and SVD-accurate entry points validate before any launch."""
+    from paper_1711_06874_b200 import tucker as T
+    from tucker_inputs import GridSpec, KernelSpec
+    d = ctypes.c_void_p(1)
+    g = T.cgrid(GridSpec.cube(16, 1.0))
+    k = T.ckernel(KernelSpec.matern(1.5, 0.2))
+    bad_k = T.ckernel(KernelSpec.matern(-1.0, 0.2))
+    r4, r_bad = T.cranks((4, 4, 4)), T.cranks((17, 4, 4))
+    big = 1 << 40
+    # fused
+    assert lib.tucker_workspace_size_fused(ctypes.byref(g), r4) > 0
+    assert lib.tucker_gram_fused(ctypes.byref(g), ctypes.byref(k), 3, d, d, big, None) == 1
+    assert lib.tucker_gram_fused(ctypes.byref(g), ctypes.byref(bad_k), 0, d, d, big, None) == 2
+    assert lib.tucker_gram_fused(ctypes.byref(g), ctypes.byref(k), 0, d, d, 16, None) == 4
+    assert lib.tucker_hosvd_fused(ctypes.byref(g), ctypes.byref(k), r_bad, d, d, d, d, d, d, d, d, big, None,
+                                  None) == 3
+    assert lib.tucker_error_fused(ctypes.byref(g), ctypes.byref(k), r4, None, d, d, d, d, d, big, None) == 1
+    # symmetric: rank above ceil(n/2), off-centre grid
+    assert lib.tucker_hosvd_sym(ctypes.byref(g), ctypes.byref(k), T.cranks((9, 4, 4)), d, d, d, d, d, d, d, None, d,
+                                big, None, None) == 3
+    off = T.cgrid(GridSpec((16, 16, 16), (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0)))
+    assert lib.tucker_hosvd_sym(ctypes.byref(off), ctypes.byref(k), r4, d, d, d, d, d, d, d, None, d, big, None,
+                                None) == 7
+    # ALS: sweeps < 1, rank out of range, workspace too small
+    assert lib.tucker_als(ctypes.byref(g), r4, d, d, d, d, d, d, d, d, 0, d, big, None, None) == 1
+    assert lib.tucker_als(ctypes.byref(g), r_bad, d, d, d, d, d, d, d, d, 1, d, big, None, None) == 3
+    assert lib.tucker_als(ctypes.byref(g), r4, d, d, d, d, d, d, d, d, 1, d, 16, None, None) == 4
+    assert lib.tucker_workspace_size_als(ctypes.byref(g), r_bad) == 0
+    # SVD-accurate: iters < 1, rank > 56, workspace too small
+    assert lib.tucker_hosvd_accurate(ctypes.byref(g), r4, d, d, d, d, d, d, d, d, 0, d, big, None, None) == 1
+    g2 = T.cgrid(GridSpec.cube(64, 1.0))
+    assert lib.tucker_hosvd_accurate(ctypes.byref(g2), T.cranks((57, 4, 4)), d, d, d, d, d, d, d, d, 1, d, big, None,
+                                     None) == 7
+    assert lib.tucker_hosvd_accurate(ctypes.byref(g), r4, d, d, d, d, d, d, d, d, 1, d, 16, None, None) == 4
+    # spectral density domain
+    sk = T.ckernel(KernelSpec.spectral(0.0, 0.4))
+    assert lib.tucker_fill(ctypes.byref(g), ctypes.byref(sk), d, d, big, None) == 2
