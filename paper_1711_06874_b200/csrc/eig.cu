@@ -354,9 +354,11 @@ __global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int
     }
 }
 
+// Guard vectors q: 16 for small ranks; 8 from r = 32 on (the Jacobi and CGS2 costs grow as p^2,
+// and at such ranks the spectra of the workloads are far down in the Gram's noise by then).
 static int block_width(int64_t n, int r) {
     if (n <= kDirectMax) return (int)n;
-    const int q = std::min(16, kMaxP - r);
+    const int q = r >= 32 ? 8 : std::min(16, kMaxP - r);
     return (int)std::min<int64_t>(n, r + q);
 }
 
