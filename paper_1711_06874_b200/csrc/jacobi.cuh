@@ -6,7 +6,7 @@
 // (s-w) mod (m-1), so every pair meets exactly once per sweep and the m/2 rotations of a round
 // commute.  The pairing is computed in closed form (no serial bookkeeping thread).  Skip rule R7:
 // rotate (a,b) only if |h_ab| > max(eps sqrt|h_aa h_bb|, eps max_i|h_ii| / p) — the absolute floor
-// lets the rounding-noise block converge.  The off-diagonal pair entry is set to
+// lets the rounding-noise block converge.  The test is evaluated on squares.  The off-diagonal pair entry is set to
 // exactly 0 after its rotation.  A warp owns pairs warp, warp+nw, ...: its lanes compute their
 // rotations in parallel and the warp rotates their rows; then all warps rotate columns — two
 // barriers per round (requires half <= 32 * nwarps); H and Q use an odd leading
@@ -81,10 +81,14 @@ __device__ inline int jacobi_sym(double* H, double* Q, int p, JacobiWork js, int
                     rr_pair(s, w, m, a, b);
                     if (b < p) {
                         const double apq = H[a * ld + b], app = H[a * ld + a], aqq = H[b * ld + b];
-                        const double thr = fmax(eps * sqrt(fabs(app * aqq)), floor_abs);
-                        if (fabs(apq) > thr) {
-                            const double tau = (aqq - app) / (2.0 * apq);
-                            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+                        // |apq| > max(eps sqrt|app aqq|, floor) tested on squares (no sqrt); the
+                        // rotation t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / h, d = aqq - app,
+                        // h = 2 apq, is formed as t = sign(d) h / (|d| + sqrt(d^2 + h^2)): one sqrt,
+                        // one division, one rsqrt on the dependent chain
+                        const double apq2 = apq * apq;
+                        if (apq2 > fmax(eps * eps * fabs(app * aqq), floor_abs * floor_abs)) {
+                            const double d = aqq - app, h = 2.0 * apq;
+                            const double t = copysign(1.0, d) * h / (fabs(d) + sqrt(fma(d, d, h * h)));
                             c = rsqrt(fma(t, t, 1.0));
                             sn = t * c;
                             rot = 1;
