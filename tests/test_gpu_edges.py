@@ -115,3 +115,24 @@ def test_config4_batch_512(T, orc):
         nb = np.linalg.norm(to_np(core))
         e = es[2]
         assert abs(e[1] ** 2 - nb ** 2 - e[2] ** 2) <= 1e-12 * e[1] ** 2
+
+
+def test_eig_single_cta_fallback_beyond_cluster(T, orc):
+    """n > 2048 exceeds the 16-CTA cluster: tucker_eig falls back to the single-CTA Rayleigh–Ritz
+    path.  Against numpy.linalg.eigh (LAPACK) on the oracle's Gram of a 2100 x 8 x 6 tensor."""
+    from tucker_inputs import GridSpec, KernelSpec
+    g = GridSpec((2100, 8, 6), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    F = orc.fill(ogrid(orc, g), okern(orc, KernelSpec.matern(0.7, 0.3)))
+    G = orc.gram_mode(F, 0)
+    lam_ref, V_ref = np.linalg.eigh(G)
+    lam_ref, V_ref = lam_ref[::-1], V_ref[:, ::-1]
+    r = 12
+    U, lam, info, rc = T.eig(torch.from_numpy(G).cuda(), r)
+    assert rc == 0, info
+    U, lam = to_np(U), to_np(lam)
+    assert np.all(np.abs(lam - lam_ref[:r]) <= 1e-11 * np.abs(lam_ref[:r]) + 1e-14 * lam_ref[0])
+    assert np.max(np.abs(U.T @ U - np.eye(r))) <= 1e-12
+    for c in range(r):
+        if np.min(np.abs(np.delete(lam_ref, c) - lam_ref[c])) >= 1e-6 * lam_ref[0]:
+            v = V_ref[:, c] * np.sign(V_ref[np.argmax(np.abs(V_ref[:, c]) >= 0.5 * np.max(np.abs(V_ref[:, c]))), c])
+            assert np.max(np.abs(U[:, c] - v)) <= 1e-9, c
