@@ -108,6 +108,18 @@ TUCKER_API int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel,
 TUCKER_API int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,
                 size_t ws_bytes, void* stream);
 
+/* a-3 on the INT8 tensor cores (tcgen05 kind::i8): the same G as tucker_gram, to FP64 accuracy by
+ * modular emulation (R18).  Every row a_i of F_(m) is scaled by 2^(b - E_i)
+ * (max_k |a_ik| < 2^E_i, b <= 51) and rounded to integers X; S = X X^T is formed exactly from its
+ * residues modulo 16 pairwise-coprime moduli (int8 Gram matrices on the tensor cores, exact int32
+ * accumulation) and reconstructed by the Chinese remainder theorem; G_ij = fl(2^(E_i+E_j-2b) S_ij),
+ * one rounding.  Deterministic and independent of the launch configuration.  Workspace:
+ * tucker_workspace_size_i8 (residues of up to 8 GiB of the unfolding at a time, partials).
+ * TUCKER_ERR_UNSUPPORTED if some n_m > 16384. */
+TUCKER_API size_t tucker_workspace_size_i8(const tucker_grid* grid);
+TUCKER_API int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,
+                size_t ws_bytes, void* stream);
+
 /* a-4: leading r eigenpairs of a symmetric PSD n x n matrix G (dev): U (dev, n x r row-major,
  * sorted by descending eigenvalue, sign rule R6), lambda (dev, r).  Synchronises `stream`.
  * `info_mode` (host, nullable) receives {iters, converged, block, sweeps, resid, lambda1} in

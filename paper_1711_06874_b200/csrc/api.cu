@@ -261,6 +261,19 @@ int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* 
     return launch_gram(grid->n, mode, F, G, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
+size_t tucker_workspace_size_i8(const tucker_grid* grid) {
+    if (check_grid(grid) != TUCKER_OK || !gram_i8_supported(grid->n)) return 0;
+    return gram_i8_ws_bytes(grid->n);
+}
+
+int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws, size_t ws_bytes,
+                   void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    if (mode < 0 || mode > 2 || !F || !G || !ws) return TUCKER_ERR_INVALID_ARG;
+    return launch_gram_i8(grid->n, mode, F, G, ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
+}
+
 int tucker_eig(int64_t n, const double* G, int32_t r, double* U, double* lambda, void* ws, size_t ws_bytes,
                void* stream, tucker_info* info_mode) {
     launch_counter() = 0;

@@ -1,0 +1,661 @@
+// gram_i8.cu — a-3 on the INT8 tensor cores (tcgen05 kind::i8, SASS UTCIMMA): the Gram matrix
+// G_m = F_(m) F_(m)^T of the mode-m unfolding (the HOSVD's Gram route) to FP64 accuracy
+// by modular (Ozaki-II / Chinese-remainder) emulation.  B200 has no FP64 tcgen05 kind; its INT8
+// tensor path is ~100x the DMMA rate, so the exact integer product is cheaper to form there.
+//
+//   1. row scaling (k_i8_rowmax, k_i8_residues): every row a_i of F_(m) is scaled by the power of
+//      two 2^(b - E_i), max_k |a_ik| < 2^E_i, and rounded to the integer x_ik = rint(a_ik 2^(b-E_i)),
+//      |x_ik| <= 2^b (b <= 50: the rounding error is 2^-(b+1) of the row maximum, R18).
+//   2. S = X X^T is an exact integer matrix with |S_ij| <= K 2^(2b) < P/2, P = prod p_l over 16
+//      pairwise-coprime odd moduli p_l <= 253 (P ~ 2^125).  Its residues S mod p_l are Gram
+//      matrices of the residue matrices R_l = X mod p_l (symmetric representatives, |r| <= 127,
+//      int8), formed on the tensor cores with exact int32 accumulation over K-chunks of 2^17
+//      (127^2 2^17 < 2^31) (k_i8_gemm), summed mod p_l across chunks (k_i8_reduce).
+//   3. S_ij is reconstructed exactly (Garner mixed radix, 128-bit integer) and G_ij = 2^(E_i+E_j-2b)
+//      S_ij is rounded once to FP64 (k_i8_crt).  Both triangles are written.
+// So G̃ = fl(D X X^T D) with D = diag(2^(E_i - b)): the only error is the input rounding of step 1
+// plus one final rounding — no accumulation-order error at all, and the result is bit-for-bit
+// independent of the launch configuration.
+//
+// k_i8_gemm: persistent, warp-specialised (warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
+// warps 2-5 epilogue); lower-triangle tiles of 128 rows x up to 256 columns (N trimmed at the
+// diagonal), 4-stage TMA ring of 128-byte K-blocks (SWIZZLE_128B, K-major A and B), accumulators
+// double-buffered in TMEM (2 x 256 columns).  A unit is (modulus, K-chunk, tile); its int32
+// accumulator is written to a partials buffer ([col][row], coalesced) that k_i8_reduce folds.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <cmath>
+#include <cstdlib>
+#include <utility>
+
+namespace tk {
+namespace i8 {
+
+constexpr int NMOD = 16;
+// 16 pairwise-coprime odd moduli <= 253 (253 = 11*23, 249 = 3*83, 247 = 13*19, 245 = 5*7^2, the rest prime)
+__host__ __device__ constexpr int kMod(int l) {
+    constexpr int m[NMOD] = {253, 251, 249, 247, 245, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191};
+    return m[l];
+}
+constexpr int BM = 128, BN = 256, BKB = 128, STAGES = 4;
+constexpr int64_t KCH = (int64_t)1 << 17;  // K per exact int32 accumulation
+constexpr int NT = 192;                      // 6 warps
+constexpr uint32_t STAGE_A = BM * BKB, STAGE_B = BN * BKB, STAGE_BYTES = STAGE_A + STAGE_B;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
+constexpr int RT_ROWS = 32, RT_K = 128;  // residue tile
+
+__host__ __device__ constexpr int pow2mod(int e, int p) {
+    int64_t r = 1;
+    for (int i = 0; i < e; ++i) r = (r * 2) % p;
+    return (int)r;
+}
+__host__ __device__ constexpr int invmod(int a, int p) {  // p prime-power-free small modulus, gcd(a, p) = 1
+    for (int x = 1; x < p; ++x)
+        if ((int64_t)a * x % p == 1) return x;
+    return 0;
+}
+
+// Largest b <= 50 with K 2^(2b) < P/2 (log2 P of the 16 moduli ~ 125.09).  b <= 50 keeps
+// |rint(t)| <= 2^50 inside the 1.5 2^52 rounding trick of k_i8_residues.
+inline int scale_bits(int64_t K) {
+    double lp = 0.0;
+    for (int l = 0; l < NMOD; ++l) lp += std::log2((double)kMod(l));
+    const double lk = std::log2((double)std::max<int64_t>(K, 1));
+    const int b = (int)std::floor((lp - 1.0 - lk - 1e-9) / 2.0);
+    return std::min(50, b);
+}
+
+// ------------------------------------------------------------------------------------------
+// 1a. per-mode row maxima of |F| in one pass (bit patterns of non-negative doubles order as u64).
+//     CTA = one i-plane, in k-blocks of 1024: thread t owns k = kb + t + 256 e (e < 4) and keeps
+//     their maxima over all lines j in registers (mode 2); every line's maximum (mode 1) is a warp
+//     reduction + a cross-warp pass over 32 lines at a time; the plane maximum gives mode 0.
+constexpr int RM_KB = 1024;
+__global__ void __launch_bounds__(256) k_i8_rowmax(const double* __restrict__ F, int64_t n1, int64_t n2, int64_t n3,
+                                                   unsigned long long* __restrict__ mx0,
+                                                   unsigned long long* __restrict__ mx1,
+                                                   unsigned long long* __restrict__ mx2) {
+    __shared__ double s_line[32][9];
+    const int64_t i = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double pmax = 0.0;
+    for (int64_t kb = 0; kb < n3; kb += RM_KB) {
+        double km[4] = {0.0, 0.0, 0.0, 0.0};
+        bool kin[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kin[e] = kb + tid + 256 * e < n3;
+        for (int64_t j0 = 0; j0 < n2; j0 += 32) {
+            const int nl = (int)min((int64_t)32, n2 - j0);
+#pragma unroll 4
+            for (int jj = 0; jj < nl; ++jj) {
+                const double* line = F + (i * n2 + j0 + jj) * n3 + kb + tid;
+                double lm = 0.0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (kin[e]) {
+                        const double v = fabs(__ldg(line + 256 * e));
+                        km[e] = fmax(km[e], v);
+                        lm = fmax(lm, v);
+                    }
+                lm = warp_max(lm);
+                if (lane == 0) s_line[jj][warp] = lm;
+            }
+            __syncthreads();
+            if (tid < nl) {
+                double m = s_line[tid][0];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) m = fmax(m, s_line[tid][w]);
+                atomicMax(&mx1[j0 + tid], (unsigned long long)__double_as_longlong(m));
+                pmax = fmax(pmax, m);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (kin[e]) atomicMax(&mx2[kb + tid + 256 * e], (unsigned long long)__double_as_longlong(km[e]));
+    }
+    if (warp == 0) {
+        pmax = warp_max(pmax);
+        if (lane == 0) atomicMax(&mx0[i], (unsigned long long)__double_as_longlong(pmax));
+    }
+}
+
+__device__ __forceinline__ double pow2d(int e) {  // 2^e, -1022 <= e <= 1023
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// ------------------------------------------------------------------------------------------
+// 1b. residues of the scaled, rounded rows: R[l][row][kk] = x mod p_l (kk in [0, Kc) of the
+//     super-chunk starting at unfolding column k0).  Unfolding column order: mode 0 (j, k),
+//     mode 1 (i, k), mode 2 (i, j) — any fixed order gives the same Gram.
+struct ResArgs {
+    const double* F;
+    int64_t n1, n2, n3;
+    int mode;
+    int64_t rows, Kfull, k0, Kc, ldr;  // ldr: bytes per residue row (>= Kc, multiple of 16)
+    const unsigned long long* mx;      // row maxima of this mode
+    int b;
+    int8_t* R;                         // [NMOD][rows][ldr]
+};
+
+// Residues of 16 elements modulo p_L (compile-time constants) -> one 16-byte store.
+template <int L>
+__device__ __forceinline__ void store_residues(const float (&u)[16][4], int8_t* out) {
+    constexpr int p = kMod(L);
+    constexpr float c1 = (float)pow2mod(13, p), c2 = (float)pow2mod(26, p), c3 = (float)pow2mod(39, p);
+    constexpr float fp = (float)p, inv = 1.0f / (float)p;
+    uint32_t w[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        // s = x (mod p) from the 13-bit limbs of x (top limb signed); exact in FP32 (|s| < 2^23)
+        const float s = fmaf(u[e][3], c3, fmaf(u[e][2], c2, fmaf(u[e][1], c1, u[e][0])));
+        const float qq = fmaf(s, inv, 12582912.f) - 12582912.f;  // round(s / p), +-1 near ties
+        const float r = fmaf(qq, -fp, s);                         // |r| <= (p+1)/2 <= 127
+        w[e] = (uint32_t)__float_as_int(r + 12582912.f);          // low byte = r (two's complement)
+    }
+    uint4 v;
+    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
+    v.z = __byte_perm(__byte_perm(w[8], w[9], 0x0040), __byte_perm(w[10], w[11], 0x0040), 0x5410);
+    v.w = __byte_perm(__byte_perm(w[12], w[13], 0x0040), __byte_perm(w[14], w[15], 0x0040), 0x5410);
+    *reinterpret_cast<uint4*>(out) = v;
+}
+template <int... L>
+__device__ __forceinline__ void store_all_residues(const float (&u)[16][4], int8_t* out, size_t lstride,
+                                                   std::integer_sequence<int, L...>) {
+    (store_residues<L>(u, out + L * lstride), ...);
+}
+
+__global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
+    __shared__ double tile[RT_ROWS][RT_K / 16][17];  // 16-column groups padded: conflict-free reads
+    __shared__ double s1[RT_ROWS], s2[RT_ROWS];
+    const int tid = threadIdx.x;
+    const int64_t row0 = (int64_t)blockIdx.y * RT_ROWS;
+    const int64_t kb = (int64_t)blockIdx.x * RT_K;  // within the super-chunk
+    if (tid < RT_ROWS) {
+        const int64_t row = row0 + tid;
+        double m = 0.0;
+        if (row < a.rows) m = __longlong_as_double((long long)a.mx[row]);
+        int E = 0;
+        if (m > 0.0) frexp(m, &E);
+        const int sh = a.b - E;  // |a_ik| 2^sh < 2^b
+        const int h = sh / 2;
+        s1[tid] = pow2d(h);
+        s2[tid] = pow2d(sh - h);
+    }
+    // gather the 32 x 128 tile, coalesced along the unit-stride axis of F; all 16 addresses of a
+    // thread are formed before the loads so they issue back to back
+    const int64_t n23 = a.n2 * a.n3;
+    double v[16];
+    if (a.mode != 2) {
+        const int kk = tid & 127;
+        const int64_t kg = a.k0 + kb + kk;
+        const bool kin = (kb + kk) < a.Kc;
+        int64_t base_k = 0, stride_row = 0;
+        if (a.mode == 0) {
+            base_k = kg;
+            stride_row = n23;
+        } else {  // mode 1: kg = i n3 + k, row = j
+            const int64_t i = kg / a.n3, k = kg - i * a.n3;
+            base_k = i * n23 + k;
+            stride_row = a.n3;
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            const int64_t row = row0 + (tid >> 7) + 2 * it;
+            v[it] = (kin && row < a.rows) ? __ldg(a.F + base_k + row * stride_row) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) tile[(tid >> 7) + 2 * it][kk >> 4][kk & 15] = v[it];
+    } else {  // mode 2: row = k, kg = i n2 + j; lanes run along k (unit stride)
+        const int rr = tid & 31;
+        const int64_t row = row0 + rr;
+        const int64_t kg0 = a.k0 + kb;
+        const int64_t i0 = kg0 / a.n2, j0 = kg0 - i0 * a.n2;
+        int64_t off[16];
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            int64_t jj = j0 + (tid >> 5) + 8 * it, ii = i0;
+            if (jj >= a.n2) {
+                const int64_t d = jj / a.n2;
+                ii += d;
+                jj -= d * a.n2;
+            }
+            off[it] = ii * n23 + jj * a.n3 + row;
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            const int kk = (tid >> 5) + 8 * it;
+            v[it] = ((kb + kk) < a.Kc && row < a.rows) ? __ldg(a.F + off[it]) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            const int kk = (tid >> 5) + 8 * it;
+            tile[rr][kk >> 4][kk & 15] = v[it];
+        }
+    }
+    __syncthreads();
+    // each thread: one row, 16 consecutive columns -> one 16-byte store per modulus
+    const int rr = tid >> 3, q = tid & 7;
+    const int64_t row = row0 + rr;
+    const int64_t kcol = kb + q * 16;
+    if (row >= a.rows || kcol >= a.Kc) return;
+    float u[16][4];
+    const double sa = s1[rr], sb = s2[rr];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const double t = (tile[rr][q][e] * sa) * sb;          // exact power-of-two scaling, |t| < 2^50
+        const double y = __dadd_rn(t, 6755399441055744.0);    // 1.5 2^52: v = rint(t) + 2^51 in the low 52 bits
+        const uint32_t lo = (uint32_t)__double2loint(y);
+        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+        const uint32_t l0 = lo & 0x1FFFu, l1 = (lo >> 13) & 0x1FFFu;
+        const uint32_t l2 = __funnelshift_r(lo, hi, 26) & 0x1FFFu, l3 = hi >> 7;
+        // x = rint(t) = (l3 - 2^12) 2^39 + l2 2^26 + l1 2^13 + l0  (signed top limb)
+        u[e][0] = __int_as_float(0x4B000000 | l0) - 8388608.f;
+        u[e][1] = __int_as_float(0x4B000000 | l1) - 8388608.f;
+        u[e][2] = __int_as_float(0x4B000000 | l2) - 8388608.f;
+        u[e][3] = __int_as_float(0x4B000000 | l3) - (8388608.f + 4096.f);
+    }
+    int8_t* out = a.R + row * a.ldr + kcol;
+    const size_t lstride = (size_t)a.rows * a.ldr;
+    store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+}
+
+// ------------------------------------------------------------------------------------------
+// 2. tcgen05 int8 Gram of the residue matrices.
+struct GemmArgs {
+    int n;         // rows per modulus
+    int nJ;        // column blocks of BN
+    int ntiles;    // lower-triangle tiles
+    int nchunks;   // K-chunks of KCH in this super-chunk
+    int nunits;    // NMOD * nchunks * ntiles
+    int64_t Kc;    // K of this super-chunk
+    int32_t* P;    // partials [unit][BN][BM]
+};
+
+__device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
+    for (int i = 0;; ++i) {
+        const int c = min(((i * BM + BM - 1) / BN) + 1, nJ);
+        if (t < c) {
+            I = i;
+            J = t;
+            return;
+        }
+        t -= c;
+    }
+}
+__device__ __forceinline__ int tile_cols(int I, int J, int n) {  // N of the MMA: multiple of 32, <= BN
+    int c = min(BN, I * BM + BM - J * BN);
+    c = min(c, n - J * BN);
+    return (c + 31) & ~31;
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ uint32_t idesc_i8(int N) {  // D s32, A/B signed 8-bit, K-major, M = 128
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+__global__ void __launch_bounds__(NT, 1) k_i8_gemm(const __grid_constant__ CUtensorMap map, const GemmArgs g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&map);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int u = blockIdx.x; u < g.nunits; u += gridDim.x) {
+                const int t = u % g.ntiles, grp = u / g.ntiles;
+                const int l = grp / g.nchunks, c = grp % g.nchunks;
+                int I, J;
+                tile_of(t, g.nJ, I, J);
+                const int N = tile_cols(I, J, g.n);
+                const int64_t kbeg = (int64_t)c * KCH;
+                const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
+                const int rowA = l * g.n + I * BM, rowB = l * g.n + J * BN;
+                const uint32_t bytes = STAGE_A + (N > 128 ? 2u : 1u) * (BKB * 128);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty[stage], ph ^ 1);
+                    uint8_t* sA = smem + stage * STAGE_BYTES;
+                    uint8_t* sB = sA + STAGE_A;
+                    const int kx = (int)(kbeg + (int64_t)kb * BKB);
+                    mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_2d(sA, &map, &full[stage], kx, rowA);
+                    tma_load_2d(sB, &map, &full[stage], kx, rowB);
+                    if (N > 128) tma_load_2d(sB + BKB * 128, &map, &full[stage], kx, rowB + 128);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            int stage = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int u = blockIdx.x; u < g.nunits; u += gridDim.x, ++it) {
+                const int t = u % g.ntiles, grp = u / g.ntiles;
+                const int c = grp % g.nchunks;
+                int I, J;
+                tile_of(t, g.nJ, I, J);
+                const int N = tile_cols(I, J, g.n);
+                const uint32_t idesc = idesc_i8(N);
+                const int64_t kbeg = (int64_t)c * KCH;
+                const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
+                const int ab = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                mbar_wait(&tempty[ab], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + ab * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES), b0 = a0 + STAGE_A;
+#pragma unroll
+                    for (int k = 0; k < BKB / 32; ++k)
+                        umma_i8(d, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                                (kb | k) ? 1u : 0u);
+                    umma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(&tfull[ab]);
+            }
+        }
+    } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
+        const int lg = warp & 3;
+        const int row = lg * 32 + lane;
+        int it = 0;
+        for (int u = blockIdx.x; u < g.nunits; u += gridDim.x, ++it) {
+            const int t = u % g.ntiles;
+            int I, J;
+            tile_of(t, g.nJ, I, J);
+            const int N = tile_cols(I, J, g.n);
+            const int ab = it & 1;
+            mbar_wait(&tfull[ab], (it >> 1) & 1);
+            tc_fence_after();
+            int32_t* P = g.P + (size_t)u * (BN * BM);
+            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + ab * BN;
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + c0));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * BM + row] = (int32_t)v[j];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+        }
+    }
+    __syncwarp();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// 2b. fold the chunk partials: Racc[l][t][col][row] = (Racc + sum_c P) mod p_l  (Racc in [0, p))
+__global__ void __launch_bounds__(256) k_i8_reduce(const int32_t* __restrict__ P, int32_t* __restrict__ Racc,
+                                                   int ntiles, int nchunks, int first) {
+    const int64_t per = (int64_t)ntiles * BN * BM;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= per * NMOD) return;
+    const int l = (int)(idx / per);
+    const int64_t e = idx - (int64_t)l * per;  // t * BN*BM + col*BM + row
+    int64_t s = first ? 0 : Racc[idx];
+    for (int c = 0; c < nchunks; ++c) s += P[((int64_t)l * nchunks + c) * per + e];
+    int p = 0;
+#pragma unroll
+    for (int q = 0; q < NMOD; ++q)
+        if (q == l) p = kMod(q);
+    int64_t r = s % p;
+    if (r < 0) r += p;
+    Racc[idx] = (int32_t)r;
+}
+
+template <int L, int Q>
+__device__ __forceinline__ int garner_step(int vl, int vq) {
+    constexpr int p = kMod(L);
+    constexpr int iv = invmod(kMod(Q) % p, p);
+    int d = vl - (vq >= p ? vq - p : vq);
+    d += (d < 0) ? p : 0;
+    return (d * iv) % p;
+}
+template <int L, int... Q>
+__device__ __forceinline__ void garner_row(int (&v)[NMOD], std::integer_sequence<int, Q...>) {
+    ((v[L] = garner_step<L, Q>(v[L], v[Q])), ...);
+}
+template <int... L>
+__device__ __forceinline__ void garner_all(int (&v)[NMOD], std::integer_sequence<int, L...>) {
+    (garner_row<L>(v, std::make_integer_sequence<int, L>{}), ...);
+}
+__device__ __forceinline__ unsigned __int128 prod_moduli() {
+    unsigned __int128 P = 1;
+#pragma unroll
+    for (int l = 0; l < NMOD; ++l) P *= (uint64_t)kMod(l);
+    return P;
+}
+
+// 3. Garner reconstruction of S_ij (exact, 128-bit) and G_ij = fl(2^(E_i + E_j - 2b) S_ij).
+__device__ __forceinline__ double u128_to_double_rn(unsigned __int128 m) {
+    const uint64_t hi = (uint64_t)(m >> 64);
+    if (hi == 0) return __ull2double_rn((uint64_t)m);
+    const int lz = __clzll((long long)hi);
+    const unsigned __int128 x = m << lz;
+    uint64_t top = (uint64_t)(x >> 64);
+    top |= ((uint64_t)x != 0) ? 1ull : 0ull;  // sticky below the 64 kept bits
+    return ldexp(__ull2double_rn(top), 64 - lz);
+}
+
+__global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const unsigned long long* __restrict__ mx,
+                                                int n, int nJ, int ntiles, int b, double* __restrict__ G) {
+    // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (blockIdx.y * 8 > blockIdx.x * 32 + 31) return;
+    if (i >= n || j >= n || j > i) return;
+    const int I = i / BM, J = j / BN;
+    int t = 0;
+    for (int q = 0; q < I; ++q) t += min(((q * BM + BM - 1) / BN) + 1, nJ);
+    t += J;
+    const int64_t per = (int64_t)ntiles * BN * BM;
+    const int64_t e = (int64_t)t * BN * BM + (int64_t)(j - J * BN) * BM + (i - I * BM);
+    int v[NMOD];
+#pragma unroll
+    for (int l = 0; l < NMOD; ++l) v[l] = Racc[l * per + e];
+    // Garner: v_l <- ((v_l - v_0) inv(p_0) - v_1) inv(p_1) ... mod p_l  (mixed-radix digits)
+    garner_all(v, std::make_integer_sequence<int, NMOD>{});
+    // S = v_0 + p_0 (v_1 + p_1 (v_2 + ...)), Horner from the top digit (exact in 128 bits)
+    unsigned __int128 S = (uint32_t)v[NMOD - 1];
+#pragma unroll
+    for (int l = NMOD - 2; l >= 0; --l) S = S * (uint64_t)kMod(l) + (uint32_t)v[l];
+    const unsigned __int128 Pp = prod_moduli();
+    const unsigned __int128 half = Pp >> 1;  // P odd: S in (P/2, P) represents S - P < 0
+    const bool neg = S > half;
+    const unsigned __int128 mag = neg ? (Pp - S) : S;
+    double d = u128_to_double_rn(mag);
+    int Ei = 0, Ej = 0;
+    const double mi = __longlong_as_double((long long)mx[i]), mj = __longlong_as_double((long long)mx[j]);
+    if (mi > 0.0) frexp(mi, &Ei);
+    if (mj > 0.0) frexp(mj, &Ej);
+    d = ldexp(d, Ei + Ej - 2 * b);
+    if (neg) d = -d;
+    G[(int64_t)i * n + j] = d;
+    G[(int64_t)j * n + i] = d;
+}
+
+struct Plan {
+    int64_t rows, Kfull, Ksc, ldr, nsuper;
+    int nJ, ntiles, nchunks, nunits, b;
+    size_t off_mx, off_R, off_P, off_Racc, total;
+};
+
+inline int count_tiles(int64_t n, int& nJ) {
+    nJ = (int)ceil_div(n, BN);
+    const int nI = (int)ceil_div(n, BM);
+    int t = 0;
+    for (int i = 0; i < nI; ++i) t += std::min((i * BM + BM - 1) / BN + 1, nJ);
+    return t;
+}
+
+// Residue buffer per super-chunk: 8 GiB (env TUCKER_I8_RESIDUE_MB overrides it; test knob).
+inline size_t residue_cap() {
+    const char* e = std::getenv("TUCKER_I8_RESIDUE_MB");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? (size_t)v << 20 : (size_t)8 << 30;
+}
+
+Plan make_plan(const int64_t n[3], int mode) {
+    Plan p{};
+    p.rows = n[mode];
+    p.Kfull = n[0] * n[1] * n[2] / n[mode];
+    int64_t ksc = (int64_t)(residue_cap() / ((size_t)NMOD * p.rows));
+    ksc = std::max<int64_t>(KCH, ksc / KCH * KCH);
+    p.Ksc = std::min(ksc, p.Kfull);
+    p.nsuper = ceil_div(p.Kfull, p.Ksc);
+    p.ldr = (int64_t)align_up((size_t)p.Ksc, 16);
+    p.ntiles = count_tiles(p.rows, p.nJ);
+    p.nchunks = (int)ceil_div(p.Ksc, KCH);
+    p.nunits = NMOD * p.nchunks * p.ntiles;
+    p.b = scale_bits(p.Kfull);
+    size_t off = 0;
+    p.off_mx = off;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
+    p.off_R = off;
+    off += align_up((size_t)NMOD * p.rows * p.ldr, 1024);
+    p.off_P = off;
+    off += align_up((size_t)p.nunits * BN * BM * 4, 256);
+    p.off_Racc = off;
+    off += align_up((size_t)NMOD * p.ntiles * BN * BM * 4, 256);
+    p.total = off;
+    return p;
+}
+
+}  // namespace i8
+
+size_t gram_i8_ws_bytes(const int64_t n[3]) {
+    size_t s = 0;
+    for (int m = 0; m < 3; ++m) s = std::max(s, i8::make_plan(n, m).total);
+    return s;
+}
+
+bool gram_i8_supported(const int64_t n[3]) {
+    // row counts up to 2^15 keep tile indices and the 2-D tensor map in range
+    for (int m = 0; m < 3; ++m)
+        if (n[m] > 32768) return false;
+    return true;
+}
+
+// Row maxima of all three unfoldings (one pass over F) into ws + off_mx.
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, void* ws, cudaStream_t st) {
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(ws);
+    TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 8, st));
+    i8::k_i8_rowmax<<<(unsigned)n[0], 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1]);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+// G (n_m x n_m, both triangles).  If have_max, the row maxima are already in the workspace head.
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
+                   cudaStream_t st, bool have_max) {
+    using namespace i8;
+    if (mode < 0 || mode > 2) return TUCKER_ERR_INVALID_ARG;
+    if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
+    const Plan p = make_plan(n, mode);
+    if (ws_bytes < p.total) return TUCKER_ERR_SIZE;
+    char* w = static_cast<char*>(ws);
+    if (!have_max) TK_RC(launch_gram_i8_rowmax(n, F, w + p.off_mx, st));
+    const unsigned long long* mx = reinterpret_cast<const unsigned long long*>(w + p.off_mx);
+    const unsigned long long* mxm = mx + (mode == 0 ? 0 : (mode == 1 ? n[0] : n[0] + n[1]));
+    int8_t* R = reinterpret_cast<int8_t*>(w + p.off_R);
+    int32_t* P = reinterpret_cast<int32_t*>(w + p.off_P);
+    int32_t* Racc = reinterpret_cast<int32_t*>(w + p.off_Racc);
+    TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    for (int64_t s = 0; s < p.nsuper; ++s) {
+        const int64_t k0 = s * p.Ksc;
+        const int64_t Kc = std::min(p.Ksc, p.Kfull - k0);
+        ResArgs ra{F, n[0], n[1], n[2], mode, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R};
+        const dim3 rg((unsigned)ceil_div(Kc, RT_K), (unsigned)ceil_div(p.rows, RT_ROWS));
+        k_i8_residues<<<rg, 256, 0, st>>>(ra);
+        TK_CHECK_LAUNCH();
+        CUtensorMap map;
+        {
+            PFN_tmapEncodeTiled enc = tmap_encoder();
+            if (!enc) return TUCKER_ERR_CUDA;
+            cuuint64_t dims[2] = {(cuuint64_t)Kc, (cuuint64_t)(NMOD * p.rows)};
+            cuuint64_t str[1] = {(cuuint64_t)p.ldr};
+            cuuint32_t box[2] = {BKB, 128}, es[2] = {1, 1};
+            if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return TUCKER_ERR_CUDA;
+        }
+        const int nchunks = (int)ceil_div(Kc, KCH);
+        GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nchunks, NMOD * nchunks * p.ntiles, Kc, P};
+        const int grid = std::min(ga.nunits, kNumSMs);
+        k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
+        TK_CHECK_LAUNCH();
+        const int64_t tot = (int64_t)NMOD * p.ntiles * BN * BM;
+        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
+        TK_CHECK_LAUNCH();
+    }
+    const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+}  // namespace tk

@@ -39,6 +39,13 @@ size_t gram_ws_bytes(const int64_t n[3]);
 int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
                 cudaStream_t st);
 
+// a-3 on the INT8 tensor cores (gram_i8.cu): modular emulation of the FP64 Gram.
+bool gram_i8_supported(const int64_t n[3]);
+size_t gram_i8_ws_bytes(const int64_t n[3]);
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, void* ws, cudaStream_t st);
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
+                   cudaStream_t st, bool have_max);
+
 // a-7 fused generate-and-Gram (F never materialised).  KParams / ChunkGeo: fill_eval.cuh.
 struct FusedGramPlan {
     int pa;              // plane axis of the chunks (0: i-planes, 1: j-planes)

@@ -24,7 +24,8 @@ EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", 
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
-           "tucker_hosvd_accurate", "tucker_last_launch_count", "tucker_strerror")
+           "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8",
+           "tucker_last_launch_count", "tucker_strerror")
 
 
 class TuckerError(RuntimeError):
@@ -69,6 +70,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_workspace_size": (sz, [pg, pr]),
         "tucker_fill": (ctypes.c_int, [pg, pk, vp, vp, sz, vp]),
         "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
+        "tucker_workspace_size_i8": (sz, [pg]),
+        "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_eig": (ctypes.c_int, [i64, vp, i32, vp, vp, vp, sz, vp, pi]),
         "tucker_ttm_core": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_hosvd": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
@@ -175,6 +178,28 @@ def gram(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, strea
     g = cgrid(grid)
     _check(lib.tucker_gram(ctypes.byref(g), int(mode), _ptr(F), _ptr(G), _ptr(ws), ws.numel(), _stream(stream)),
            "tucker_gram")
+    return G
+
+
+def workspace_i8(grid) -> torch.Tensor:
+    lib = load()
+    g = cgrid(grid)
+    n = lib.tucker_workspace_size_i8(ctypes.byref(g))
+    if n == 0:
+        raise TuckerError(7, "tucker_workspace_size_i8")
+    return torch.empty(n, dtype=torch.uint8, device="cuda")
+
+
+def gram_i8(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a-3 on the INT8 tensor cores (modular emulation of the FP64 Gram, R18)."""
+    lib = load()
+    _dev(F, "F")
+    n = int(grid.n[mode])
+    G = torch.empty((n, n), dtype=torch.float64, device=F.device)
+    ws = ws if ws is not None else workspace_i8(grid)
+    g = cgrid(grid)
+    _check(lib.tucker_gram_i8(ctypes.byref(g), int(mode), _ptr(F), _ptr(G), _ptr(ws), ws.numel(), _stream(stream)),
+           "tucker_gram_i8")
     return G
 
 

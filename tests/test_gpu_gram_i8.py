@@ -1,0 +1,115 @@
+"""a-3 on the INT8 tensor cores (tucker_gram_i8, R18) against exact arithmetic and the oracle.
+
+The emulated Gram is G~ = fl(D X X^T D), X = rint(D^-1 F_(m)), D = diag(2^(E_i - b)): X X^T is formed
+exactly (residues mod 16 coprime moduli on the int8 tensor cores + CRT), so
+  * integer-valued F (|F| < 2^bits, every Gram entry exact in FP64) must give the exact Gram bit for bit;
+  * for general F the error is the input rounding only: with m_i = max_k |a_ik| and u = 2^-(b+1)
+    (b = 50 at these sizes), |G~_ij - G_ij| <= 2^(E_i-b-1) ||a_j||_1 + 2^(E_j-b-1) ||a_i||_1
+    + 3 2^(E_i+E_j-2b-2) K + eps |G_ij|, checked element by element against the oracle's FP64 Gram
+    (whose own error, K eps |a_i||a_j|, is added to the bound).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tucker_inputs import GridSpec, KernelSpec  # noqa: E402
+from test_gpu_parity import ogrid, okern, to_np  # noqa: E402
+
+EPS = np.finfo(np.float64).eps
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_1711_06874_b200 import tucker
+    tucker.load()
+    return tucker
+
+
+def unfold(F, m):
+    return np.moveaxis(F, m, 0).reshape(F.shape[m], -1)
+
+
+GRIDS = [GridSpec((2, 2, 2), (-1.0,) * 3, (1.0,) * 3),
+         GridSpec.cube(32, 1.0),
+         GridSpec((40, 36, 33), (-1.0,) * 3, (1.0,) * 3),            # ragged K (not a multiple of 16)
+         GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)),
+         GridSpec((300, 40, 21), (-1.0,) * 3, (1.0,) * 3),           # 3 row blocks, 2 column blocks
+         GridSpec((520, 17, 9), (-1.0,) * 3, (1.0,) * 3)]            # 5 row blocks, 3 column blocks, trimmed N
+
+
+@pytest.mark.parametrize("gi", [0, 1, 2, 4, 5])
+def test_gram_i8_exact_on_integers(T, gi):
+    g = GRIDS[gi]
+    rng = np.random.default_rng(11 + gi)
+    Kmax = max(np.prod(g.n) // g.n[m] for m in range(3))
+    bits = min(20, (53 - int(np.ceil(np.log2(Kmax)))) // 2)   # every Gram entry < 2^53: exact in FP64
+    F = rng.integers(-(1 << bits), 1 << bits, size=tuple(g.n), dtype=np.int64)
+    F[min(1, g.n[0] - 1)] = 0                       # a zero slab: zero rows (mode 0), zero columns
+    F[0, 0, :] = rng.integers(-3, 4, size=g.n[2])   # tiny entries next to 2^20 ones
+    Fd = torch.from_numpy(F.astype(np.float64)).cuda()
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        A = unfold(F, m)
+        assert A.shape[1] * (1 << (2 * bits)) < (1 << 53)
+        exact = (A @ A.T).astype(np.float64)
+        G = to_np(T.gram_i8(g, m, Fd, ws))
+        assert np.array_equal(G, exact), (gi, m, np.max(np.abs(G - exact)))
+
+
+def _bound(A, b):
+    m = np.max(np.abs(A), axis=1)
+    E = np.where(m > 0, np.frexp(m)[1], 0).astype(np.float64)
+    l1 = np.sum(np.abs(A), axis=1)
+    s = np.exp2(E - b - 1)
+    K = A.shape[1]
+    absG = np.abs(A) @ np.abs(A).T
+    return np.outer(s, l1) + np.outer(l1, s) + 3 * np.outer(s, s) * K + 2 * K * EPS * absG
+
+
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+@pytest.mark.parametrize("kern", [KernelSpec.matern(1.3, 0.5), KernelSpec.matern(0.5, 0.1), KernelSpec.slater(1.0, 1.0)])
+def test_gram_i8_parity(T, orc, gi, kern):
+    g = GRIDS[gi]
+    Fg = T.fill(g, kern)
+    F = orc.fill(ogrid(orc, g), okern(orc, kern))
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        G = to_np(T.gram_i8(g, m, Fg, ws))
+        R = orc.gram_mode(F, m)
+        A = unfold(F, m)
+        assert np.array_equal(G, G.T)
+        assert np.all(np.abs(G - R) <= _bound(A, 50)), (gi, m)
+        d = np.sqrt(np.diag(R))
+        assert np.max(np.abs(G - R) / np.outer(d, d)) <= 1e-14, (gi, m)
+
+
+def test_gram_i8_chunks_and_superchunks(T, orc, monkeypatch):
+    """K = 2^18 > 2^17: two exact-int32 K-chunks per unit; with a 16 MiB residue cap also two
+    super-chunks (residues rebuilt per K range, residue sums carried mod p)."""
+    g = GridSpec((64, 512, 512), (-1.0,) * 3, (1.0,) * 3)
+    kern = KernelSpec.matern(1.5, 0.3)
+    Fg = T.fill(g, kern)
+    F = orc.fill(ogrid(orc, g), okern(orc, kern))
+    R = orc.gram_mode(F, 0)
+    A = unfold(F, 0)
+    G1 = to_np(T.gram_i8(g, 0, Fg))
+    assert np.all(np.abs(G1 - R) <= _bound(A, 50))
+    monkeypatch.setenv("TUCKER_I8_RESIDUE_MB", "16")
+    G2 = to_np(T.gram_i8(g, 0, Fg))
+    assert np.array_equal(G1, G2)  # the result does not depend on how K is split
+
+
+def test_gram_i8_deterministic_and_vs_dmma(T):
+    g = GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0))
+    F = T.fill(g, KernelSpec.matern(0.7, 0.5))
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        G = T.gram_i8(g, m, F, ws)
+        assert torch.equal(G, T.gram_i8(g, m, F, ws))
+        D = T.gram(g, m, F)
+        d = torch.sqrt(torch.diagonal(D))
+        assert float(torch.max(torch.abs(G - D) / torch.outer(d, d))) <= 1e-14

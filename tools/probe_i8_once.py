@@ -1,0 +1,12 @@
+import os, sys
+sys.path.insert(0, os.getcwd())
+import torch
+from paper_1711_06874_b200 import tucker as T
+from tucker_inputs import GridSpec, KernelSpec
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+m = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+g = GridSpec.cube(n, 1.0)
+F = T.fill(g, KernelSpec.matern(1.5, 0.2))
+ws8 = T.workspace_i8(g)
+G = T.gram_i8(g, m, F, ws8)
+torch.cuda.synchronize()
