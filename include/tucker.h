@@ -117,6 +117,12 @@ TUCKER_API int tucker_gram(const tucker_grid* grid, int32_t mode, const double* 
  * tucker_workspace_size_i8 (residues of up to 8 GiB of the unfolding at a time, partials).
  * TUCKER_ERR_UNSUPPORTED if some n_m > 16384. */
 TUCKER_API size_t tucker_workspace_size_i8(const tucker_grid* grid);
+/* Gram engine of tucker_gram, tucker_hosvd and tucker_approximate (process-wide, not thread-safe;
+ * set it before sizing workspaces: tucker_workspace_size depends on it).  TUCKER_GRAM_AUTO
+ * (default): the INT8 emulation where supported (every n_m <= 16384), DMMA otherwise. */
+enum { TUCKER_GRAM_AUTO = 0, TUCKER_GRAM_DMMA = 1, TUCKER_GRAM_INT8 = 2 };
+TUCKER_API int tucker_set_gram_engine(int32_t engine);
+TUCKER_API int32_t tucker_get_gram_engine(void);
 TUCKER_API int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,
                 size_t ws_bytes, void* stream);
 

@@ -90,10 +90,11 @@ int check_ranks(const tucker_grid* g, const int32_t* r) {
 }
 
 // Workspace layout (all 256-byte aligned):
-//   [nodes x^2 (n1+n2+n3)] [K_nu table] [G (max n_m^2)] [scratch = max(gram, eig, ttm, err)]
-//   [device outputs of tucker_approximate: U1 U2 U3 core sigma1..3 err3]
+//   [nodes x^2 (n1+n2+n3)] [K_nu table] [G (max n_m^2)] [row maxima (n1+n2+n3), INT8 Gram]
+//   [scratch = max(gram, eig, ttm, err)] [device outputs of tucker_approximate: U1 U2 U3 core
+//   sigma1..3 err3]
 struct Layout {
-    size_t nodes, cheb, G, scratch, outs, total;
+    size_t nodes, cheb, G, mx, scratch, outs, total;
     size_t scratch_bytes;
 };
 
@@ -110,8 +111,10 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     L.G = off;
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
     off += align_up((size_t)nmax * nmax * 8, 256);
+    L.mx = off;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
     L.scratch = off;
-    size_t s = gram_ws_bytes(n);
+    size_t s = gram_auto_ws_bytes(n);
     for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
     s = std::max(s, ttm_ws_bytes(n, r));
     s = std::max(s, err_ws_bytes(n, r));
@@ -135,8 +138,10 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
     double* G = reinterpret_cast<double*>(at(ws, L.G));
     void* scr = at(ws, L.scratch);
     int worst = TUCKER_OK;
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(at(ws, L.mx));
+    if (gram_use_i8(g->n)) TK_RC(launch_gram_i8_rowmax(g->n, F, mx, st));  // once for the three modes
     for (int m = 0; m < 3; ++m) {
-        TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));
+        TK_RC(launch_gram_auto(g->n, m, F, G, mx, scr, L.scratch_bytes, st));
         const int rc = launch_eig(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
@@ -258,8 +263,17 @@ int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* 
     launch_counter() = 0;
     TK_RC(check_grid(grid));
     if (mode < 0 || mode > 2 || !F || !G || !ws) return TUCKER_ERR_INVALID_ARG;
-    return launch_gram(grid->n, mode, F, G, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return launch_gram_auto(grid->n, mode, F, G, nullptr, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
+
+int tucker_set_gram_engine(int32_t engine) {
+    if (engine != TUCKER_GRAM_AUTO && engine != TUCKER_GRAM_DMMA && engine != TUCKER_GRAM_INT8)
+        return TUCKER_ERR_INVALID_ARG;
+    gram_engine() = engine;
+    return TUCKER_OK;
+}
+
+int32_t tucker_get_gram_engine(void) { return gram_engine(); }
 
 size_t tucker_workspace_size_i8(const tucker_grid* grid) {
     if (check_grid(grid) != TUCKER_OK || !gram_i8_supported(grid->n)) return 0;
@@ -271,7 +285,8 @@ int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, doubl
     launch_counter() = 0;
     TK_RC(check_grid(grid));
     if (mode < 0 || mode > 2 || !F || !G || !ws) return TUCKER_ERR_INVALID_ARG;
-    return launch_gram_i8(grid->n, mode, F, G, ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
+    if (!gram_i8_supported(grid->n)) return TUCKER_ERR_UNSUPPORTED;
+    return launch_gram_i8(grid->n, mode, F, G, nullptr, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int tucker_eig(int64_t n, const double* G, int32_t r, double* U, double* lambda, void* ws, size_t ws_bytes,

@@ -9,19 +9,20 @@
 //   2. S = X X^T is an exact integer matrix with |S_ij| <= K 2^(2b) < P/2, P = prod p_l over 16
 //      pairwise-coprime odd moduli p_l <= 253 (P ~ 2^125).  Its residues S mod p_l are Gram
 //      matrices of the residue matrices R_l = X mod p_l (symmetric representatives, |r| <= 127,
-//      int8), formed on the tensor cores with exact int32 accumulation over K-chunks of 2^17
-//      (127^2 2^17 < 2^31) (k_i8_gemm), summed mod p_l across chunks (k_i8_reduce).
+//      int8), formed on the tensor cores with exact int32 accumulation over K-chunks of 2^16
+//      (127^2 2^16 < 2^31) (k_i8_gemm), summed mod p_l across chunks (k_i8_reduce).
 //   3. S_ij is reconstructed exactly (Garner mixed radix, 128-bit integer) and G_ij = 2^(E_i+E_j-2b)
 //      S_ij is rounded once to FP64 (k_i8_crt).  Both triangles are written.
 // So G̃ = fl(D X X^T D) with D = diag(2^(E_i - b)): the only error is the input rounding of step 1
 // plus one final rounding — no accumulation-order error at all, and the result is bit-for-bit
 // independent of the launch configuration.
 //
-// k_i8_gemm: persistent, warp-specialised (warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
-// warps 2-5 epilogue); lower-triangle tiles of 128 rows x up to 256 columns (N trimmed at the
-// diagonal), 4-stage TMA ring of 128-byte K-blocks (SWIZZLE_128B, K-major A and B), accumulators
-// double-buffered in TMEM (2 x 256 columns).  A unit is (modulus, K-chunk, tile); its int32
-// accumulator is written to a partials buffer ([col][row], coalesced) that k_i8_reduce folds.
+// k_i8_gemm: persistent CTA pairs (cluster of 2, tcgen05 cta_group::2), warp-specialised (warp 0
+// TMA producer in both CTAs, warp 1 TMEM owner + MMA issuer in the leader, warps 2-5 epilogue);
+// lower-triangle pair tiles of 256 rows x up to 512 columns (N trimmed at the diagonal), 4-stage
+// TMA ring of 128-byte K-blocks (SWIZZLE_128B, K-major A and B).  A unit is (modulus, K-chunk,
+// tile); its int32 accumulator is written to a partials buffer ([col][row], coalesced) that
+// k_i8_reduce folds.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -38,10 +39,12 @@ __host__ __device__ constexpr int kMod(int l) {
     constexpr int m[NMOD] = {253, 251, 249, 247, 245, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191};
     return m[l];
 }
-constexpr int BM = 128, BN = 256, BKB = 128, STAGES = 4;
-constexpr int64_t KCH = (int64_t)1 << 17;  // K per exact int32 accumulation
+constexpr int PM = 256, PN = 512;          // CTA-pair tile (rows x columns of G)
+constexpr int BKB = 128, STAGES = 4;        // K-block bytes (one 128-byte swizzle row), ring depth
+constexpr int64_t KCH = (int64_t)1 << 16;  // K per exact int32 accumulation (127^2 2^16 < 2^31)
 constexpr int NT = 192;                      // 6 warps
-constexpr uint32_t STAGE_A = BM * BKB, STAGE_B = BN * BKB, STAGE_BYTES = STAGE_A + STAGE_B;
+constexpr uint32_t BOX = 128 * BKB;          // one TMA box: 128 rows x 128 bytes
+constexpr uint32_t STAGE_BYTES = 3 * BOX;    // A + two B halves
 constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
 constexpr int RT_ROWS = 32, RT_K = 128;  // residue tile
 
@@ -263,20 +266,26 @@ __global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// 2. tcgen05 int8 Gram of the residue matrices.
+// 2. tcgen05 int8 Gram of the residue matrices on CTA pairs (cta_group::2, M = 256).
+//    Pair tile: PM = 256 rows (128 per CTA: A is split by rows) x up to PN = 512 columns, issued as
+//    one or two N <= 256 MMAs whose B operand is split by N across the pair (each CTA stages N_q/2
+//    rows of B for instruction q).  Each CTA's TMEM holds its 128 rows x 512 columns.  Per K-byte a
+//    CTA streams 128 (A) + 256 (B) bytes for 128 x 512 MACs: half the L2 traffic per MAC of a
+//    128 x 256 single-CTA tile.
 struct GemmArgs {
     int n;         // rows per modulus
-    int nJ;        // column blocks of BN
-    int ntiles;    // lower-triangle tiles
+    int nJ;        // column blocks of PN
+    int ntiles;    // lower-triangle pair tiles
     int nchunks;   // K-chunks of KCH in this super-chunk
     int nunits;    // NMOD * nchunks * ntiles
     int64_t Kc;    // K of this super-chunk
-    int32_t* P;    // partials [unit][BN][BM]
+    int32_t* P;    // partials [unit][PN][PM]
 };
 
+__host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
 __device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
     for (int i = 0;; ++i) {
-        const int c = min(((i * BM + BM - 1) / BN) + 1, nJ);
+        const int c = tiles_in_row(i, nJ);
         if (t < c) {
             I = i;
             J = t;
@@ -285,9 +294,9 @@ __device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
         t -= c;
     }
 }
-__device__ __forceinline__ int tile_cols(int I, int J, int n) {  // N of the MMA: multiple of 32, <= BN
-    int c = min(BN, I * BM + BM - J * BN);
-    c = min(c, n - J * BN);
+__device__ __forceinline__ int tile_cols(int I, int J, int n) {  // columns of the pair tile: multiple of 32, <= PN
+    int c = min(PN, I * PM + PM - J * PN);
+    c = min(c, n - J * PN);
     return (c + 31) & ~31;
 }
 
@@ -295,72 +304,122 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ uint32_t idesc_i8(int N) {  // D s32, A/B signed 8-bit, K-major, M = 128
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+__device__ __forceinline__ uint32_t idesc_i8(int M, int N) {  // D s32, A/B signed 8-bit, both K-major
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-__device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same smem offset in cluster rank 0
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(smem_u32(p)));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAITC:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONEC;\n"
+        "bra LAB_WAITC;\n"
+        "DONEC:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 
-__global__ void __launch_bounds__(NT, 1) k_i8_gemm(const __grid_constant__ CUtensorMap map, const GemmArgs g) {
+struct UnitGeo {
+    int l, c, I, J, N, nB, N0, N1;
+};
+__device__ __forceinline__ UnitGeo unit_geo(int u, const GemmArgs& g) {
+    UnitGeo x;
+    const int t = u % g.ntiles, grp = u / g.ntiles;
+    x.l = grp / g.nchunks;
+    x.c = grp % g.nchunks;
+    tile_of(t, g.nJ, x.I, x.J);
+    x.N = tile_cols(x.I, x.J, g.n);
+    x.nB = x.N > 256 ? 2 : 1;
+    x.N0 = min(x.N, 256);
+    x.N1 = x.N - x.N0;
+    return x;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    k_i8_gemm(const __grid_constant__ CUtensorMap map, const GemmArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
-        }
+        mbar_init(&tfull, 1);
+        mbar_init(&tempty, 8);  // 4 epilogue warps x 2 CTAs
         mbar_fence_init();
         tma_prefetch_desc(&map);
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer
+        if (lane == 0) {  // TMA producer (both CTAs): own A half and own B halves, completion on the leader
             int stage = 0;
             uint32_t ph = 0;
-            for (int u = blockIdx.x; u < g.nunits; u += gridDim.x) {
-                const int t = u % g.ntiles, grp = u / g.ntiles;
-                const int l = grp / g.nchunks, c = grp % g.nchunks;
-                int I, J;
-                tile_of(t, g.nJ, I, J);
-                const int N = tile_cols(I, J, g.n);
-                const int64_t kbeg = (int64_t)c * KCH;
+            for (int u = pair; u < g.nunits; u += npairs) {
+                const UnitGeo x = unit_geo(u, g);
+                const int64_t kbeg = (int64_t)x.c * KCH;
                 const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const int rowA = l * g.n + I * BM, rowB = l * g.n + J * BN;
-                const uint32_t bytes = STAGE_A + (N > 128 ? 2u : 1u) * (BKB * 128);
+                const int rowA = x.l * g.n + x.I * PM + (int)rank * 128;
+                const int rowB0 = x.l * g.n + x.J * PN + (int)rank * (x.N0 / 2);
+                const int rowB1 = x.l * g.n + x.J * PN + 256 + (int)rank * (x.N1 / 2);
+                const uint32_t bytes = 2u * (1u + (uint32_t)x.nB) * BOX;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], ph ^ 1);
                     uint8_t* sA = smem + stage * STAGE_BYTES;
-                    uint8_t* sB = sA + STAGE_A;
+                    const uint32_t fl = leader_addr(&full[stage]);
                     const int kx = (int)(kbeg + (int64_t)kb * BKB);
-                    mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d(sA, &map, &full[stage], kx, rowA);
-                    tma_load_2d(sB, &map, &full[stage], kx, rowB);
-                    if (N > 128) tma_load_2d(sB + BKB * 128, &map, &full[stage], kx, rowB + 128);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_2d_pair(sA, &map, fl, kx, rowA);
+                    tma_load_2d_pair(sA + BOX, &map, fl, kx, rowB0);
+                    if (x.nB > 1) tma_load_2d_pair(sA + 2 * BOX, &map, fl, kx, rowB1);
                     if (++stage == STAGES) {
                         stage = 0;
                         ph ^= 1;
@@ -369,56 +428,51 @@ __global__ void __launch_bounds__(NT, 1) k_i8_gemm(const __grid_constant__ CUten
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
+        if (lane == 0 && rank == 0) {  // MMA issuer (leader CTA only)
             int stage = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int u = blockIdx.x; u < g.nunits; u += gridDim.x, ++it) {
-                const int t = u % g.ntiles, grp = u / g.ntiles;
-                const int c = grp % g.nchunks;
-                int I, J;
-                tile_of(t, g.nJ, I, J);
-                const int N = tile_cols(I, J, g.n);
-                const uint32_t idesc = idesc_i8(N);
-                const int64_t kbeg = (int64_t)c * KCH;
+            for (int u = pair; u < g.nunits; u += npairs, ++it) {
+                const UnitGeo x = unit_geo(u, g);
+                const int64_t kbeg = (int64_t)x.c * KCH;
                 const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const int ab = it & 1;
-                const uint32_t aph = (it >> 1) & 1;
-                mbar_wait(&tempty[ab], aph ^ 1);
+                const uint32_t id0 = idesc_i8(PM, x.N0), id1 = idesc_i8(PM, x.N1 > 0 ? x.N1 : 32);
+                mbar_wait_cluster(&tempty, (it & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + ab * BN;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], ph);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES), b0 = a0 + STAGE_A;
+                    const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BKB / 32; ++k)
-                        umma_i8(d, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                                (kb | k) ? 1u : 0u);
-                    umma_commit(&empty[stage]);
+                    for (int k = 0; k < BKB / 32; ++k) {
+                        const uint32_t acc = (kb | k) ? 1u : 0u;
+                        umma_i8_pair(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(a0 + BOX + 32 * k), id0, acc);
+                        if (x.nB > 1)
+                            umma_i8_pair(tmem + 256, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(a0 + 2 * BOX + 32 * k),
+                                         id1, acc);
+                    }
+                    umma_commit_pair(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         ph ^= 1;
                     }
                 }
-                umma_commit(&tfull[ab]);
+                umma_commit_pair(&tfull);
             }
         }
-    } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
+    } else {  // epilogue warps 2..5 (both CTAs): TMEM lanes 32*(warp%4) ..
         const int lg = warp & 3;
-        const int row = lg * 32 + lane;
+        const int row = (int)rank * 128 + lg * 32 + lane;
+        const uint32_t te = leader_addr(&tempty);
         int it = 0;
-        for (int u = blockIdx.x; u < g.nunits; u += gridDim.x, ++it) {
-            const int t = u % g.ntiles;
-            int I, J;
-            tile_of(t, g.nJ, I, J);
-            const int N = tile_cols(I, J, g.n);
-            const int ab = it & 1;
-            mbar_wait(&tfull[ab], (it >> 1) & 1);
+        for (int u = pair; u < g.nunits; u += npairs, ++it) {
+            const UnitGeo x = unit_geo(u, g);
+            mbar_wait(&tfull, it & 1);
             tc_fence_after();
-            int32_t* P = g.P + (size_t)u * (BN * BM);
-            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + ab * BN;
-            for (int c0 = 0; c0 < N; c0 += 32) {
+            int32_t* P = g.P + (size_t)u * (PN * PM);
+            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
+            for (int c0 = 0; c0 < x.N; c0 += 32) {
+                const int cc = c0 < x.N0 ? c0 : 256 + (c0 - x.N0);  // TMEM column of output column c0
                 uint32_t v[32];
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -428,21 +482,22 @@ __global__ void __launch_bounds__(NT, 1) k_i8_gemm(const __grid_constant__ CUten
                       "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
                       "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
                       "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + c0));
+                    : "r"(taddr + cc));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * BM + row] = (int32_t)v[j];
+                for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * PM + row] = (int32_t)v[j];
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
+            if (lane == 0) mbar_arrive_cluster(te);
         }
     }
     __syncwarp();
-    __syncthreads();
+    tc_fence_before();
+    cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
     }
 }
 
@@ -450,11 +505,11 @@ __global__ void __launch_bounds__(NT, 1) k_i8_gemm(const __grid_constant__ CUten
 // 2b. fold the chunk partials: Racc[l][t][col][row] = (Racc + sum_c P) mod p_l  (Racc in [0, p))
 __global__ void __launch_bounds__(256) k_i8_reduce(const int32_t* __restrict__ P, int32_t* __restrict__ Racc,
                                                    int ntiles, int nchunks, int first) {
-    const int64_t per = (int64_t)ntiles * BN * BM;
+    const int64_t per = (int64_t)ntiles * PN * PM;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= per * NMOD) return;
     const int l = (int)(idx / per);
-    const int64_t e = idx - (int64_t)l * per;  // t * BN*BM + col*BM + row
+    const int64_t e = idx - (int64_t)l * per;  // t * PN*PM + col*PM + row
     int64_t s = first ? 0 : Racc[idx];
     for (int c = 0; c < nchunks; ++c) s += P[((int64_t)l * nchunks + c) * per + e];
     int p = 0;
@@ -507,12 +562,12 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
     if (blockIdx.y * 8 > blockIdx.x * 32 + 31) return;
     if (i >= n || j >= n || j > i) return;
-    const int I = i / BM, J = j / BN;
+    const int I = i / PM, J = j / PN;
     int t = 0;
-    for (int q = 0; q < I; ++q) t += min(((q * BM + BM - 1) / BN) + 1, nJ);
+    for (int q = 0; q < I; ++q) t += tiles_in_row(q, nJ);
     t += J;
-    const int64_t per = (int64_t)ntiles * BN * BM;
-    const int64_t e = (int64_t)t * BN * BM + (int64_t)(j - J * BN) * BM + (i - I * BM);
+    const int64_t per = (int64_t)ntiles * PN * PM;
+    const int64_t e = (int64_t)t * PN * PM + (int64_t)(j - J * PN) * PM + (i - I * PM);
     int v[NMOD];
 #pragma unroll
     for (int l = 0; l < NMOD; ++l) v[l] = Racc[l * per + e];
@@ -544,18 +599,18 @@ struct Plan {
 };
 
 inline int count_tiles(int64_t n, int& nJ) {
-    nJ = (int)ceil_div(n, BN);
-    const int nI = (int)ceil_div(n, BM);
+    nJ = (int)ceil_div(n, PN);
+    const int nI = (int)ceil_div(n, PM);
     int t = 0;
-    for (int i = 0; i < nI; ++i) t += std::min((i * BM + BM - 1) / BN + 1, nJ);
+    for (int i = 0; i < nI; ++i) t += tiles_in_row(i, nJ);
     return t;
 }
 
-// Residue buffer per super-chunk: 8 GiB (env TUCKER_I8_RESIDUE_MB overrides it; test knob).
+// Residue buffer per super-chunk: 16 GiB (env TUCKER_I8_RESIDUE_MB overrides it; test knob).
 inline size_t residue_cap() {
     const char* e = std::getenv("TUCKER_I8_RESIDUE_MB");
     const long long v = e ? std::atoll(e) : 0;
-    return v > 0 ? (size_t)v << 20 : (size_t)8 << 30;
+    return v > 0 ? (size_t)v << 20 : (size_t)16 << 30;
 }
 
 Plan make_plan(const int64_t n[3], int mode) {
@@ -577,9 +632,9 @@ Plan make_plan(const int64_t n[3], int mode) {
     p.off_R = off;
     off += align_up((size_t)NMOD * p.rows * p.ldr, 1024);
     p.off_P = off;
-    off += align_up((size_t)p.nunits * BN * BM * 4, 256);
+    off += align_up((size_t)p.nunits * PN * PM * 4, 256);
     p.off_Racc = off;
-    off += align_up((size_t)NMOD * p.ntiles * BN * BM * 4, 256);
+    off += align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256);
     p.total = off;
     return p;
 }
@@ -593,15 +648,14 @@ size_t gram_i8_ws_bytes(const int64_t n[3]) {
 }
 
 bool gram_i8_supported(const int64_t n[3]) {
-    // row counts up to 2^15 keep tile indices and the 2-D tensor map in range
+    // row counts up to 2^14 keep tile indices and the 2-D tensor map comfortably in range
     for (int m = 0; m < 3; ++m)
-        if (n[m] > 32768) return false;
+        if (n[m] > 16384) return false;
     return true;
 }
 
 // Row maxima of all three unfoldings (one pass over F) into ws + off_mx.
-int launch_gram_i8_rowmax(const int64_t n[3], const double* F, void* ws, cudaStream_t st) {
-    unsigned long long* mx = reinterpret_cast<unsigned long long*>(ws);
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st) {
     TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 8, st));
     i8::k_i8_rowmax<<<(unsigned)n[0], 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1]);
     TK_CHECK_LAUNCH();
@@ -609,16 +663,20 @@ int launch_gram_i8_rowmax(const int64_t n[3], const double* F, void* ws, cudaStr
 }
 
 // G (n_m x n_m, both triangles).  If have_max, the row maxima are already in the workspace head.
-int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
-                   cudaStream_t st, bool have_max) {
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx_in,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
     using namespace i8;
     if (mode < 0 || mode > 2) return TUCKER_ERR_INVALID_ARG;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const Plan p = make_plan(n, mode);
     if (ws_bytes < p.total) return TUCKER_ERR_SIZE;
     char* w = static_cast<char*>(ws);
-    if (!have_max) TK_RC(launch_gram_i8_rowmax(n, F, w + p.off_mx, st));
-    const unsigned long long* mx = reinterpret_cast<const unsigned long long*>(w + p.off_mx);
+    const unsigned long long* mx = mx_in;
+    if (!mx) {
+        unsigned long long* own = reinterpret_cast<unsigned long long*>(w + p.off_mx);
+        TK_RC(launch_gram_i8_rowmax(n, F, own, st));
+        mx = own;
+    }
     const unsigned long long* mxm = mx + (mode == 0 ? 0 : (mode == 1 ? n[0] : n[0] + n[1]));
     int8_t* R = reinterpret_cast<int8_t*>(w + p.off_R);
     int32_t* P = reinterpret_cast<int32_t*>(w + p.off_P);
@@ -645,10 +703,10 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, voi
         }
         const int nchunks = (int)ceil_div(Kc, KCH);
         GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nchunks, NMOD * nchunks * p.ntiles, Kc, P};
-        const int grid = std::min(ga.nunits, kNumSMs);
+        const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
         k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
         TK_CHECK_LAUNCH();
-        const int64_t tot = (int64_t)NMOD * p.ntiles * BN * BM;
+        const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
         k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
         TK_CHECK_LAUNCH();
     }
@@ -656,6 +714,20 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, voi
     k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Engine selection for the materialised path: AUTO = INT8 emulation where supported, else DMMA.
+int& gram_engine() {
+    static int engine = TUCKER_GRAM_AUTO;
+    return engine;
+}
+bool gram_use_i8(const int64_t n[3]) { return gram_engine() != TUCKER_GRAM_DMMA && gram_i8_supported(n); }
+size_t gram_auto_ws_bytes(const int64_t n[3]) { return gram_use_i8(n) ? gram_i8_ws_bytes(n) : gram_ws_bytes(n); }
+int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (gram_use_i8(n)) return launch_gram_i8(n, mode, F, G, mx, ws, ws_bytes, st);
+    return launch_gram(n, mode, F, G, ws, ws_bytes, st);
 }
 
 }  // namespace tk

@@ -42,9 +42,17 @@ int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* 
 // a-3 on the INT8 tensor cores (gram_i8.cu): modular emulation of the FP64 Gram.
 bool gram_i8_supported(const int64_t n[3]);
 size_t gram_i8_ws_bytes(const int64_t n[3]);
-int launch_gram_i8_rowmax(const int64_t n[3], const double* F, void* ws, cudaStream_t st);
-int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
-                   cudaStream_t st, bool have_max);
+// Row maxima of the three unfoldings (n1 + n2 + n3 u64 bit patterns of non-negative doubles).
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st);
+// mx: row maxima from launch_gram_i8_rowmax, or nullptr (computed into the workspace).
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+                   void* ws, size_t ws_bytes, cudaStream_t st);
+// Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
+int& gram_engine();
+bool gram_use_i8(const int64_t n[3]);
+size_t gram_auto_ws_bytes(const int64_t n[3]);
+int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
 
 // a-7 fused generate-and-Gram (F never materialised).  KParams / ChunkGeo: fill_eval.cuh.
 struct FusedGramPlan {

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_expand_sym(double* __restrict__ Y, int6
 }
 
 struct SymLayout {
-    size_t nodes, cheb, Fw, Y[3], G, scratch, total, scratch_bytes;
+    size_t nodes, cheb, Fw, Y[3], G, mx, scratch, total, scratch_bytes;
     int64_t h[3];
 };
 
@@ -134,8 +134,10 @@ SymLayout sym_plan(const tucker_grid& g, const int32_t r[3]) {
     const int64_t hm = std::max(L.h[0], std::max(L.h[1], L.h[2]));
     L.G = off;
     off += align_up((size_t)hm * hm * 8, 256);
+    L.mx = off;
+    off += align_up((size_t)(L.h[0] + L.h[1] + L.h[2]) * 8, 256);
     L.scratch = off;
-    size_t s = gram_ws_bytes(L.h);
+    size_t s = gram_auto_ws_bytes(L.h);
     for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(L.h[a], r[a]));
     s = std::max(s, ttm_ws_bytes(L.h, r));
     s = std::max(s, err_ws_bytes(L.h, r));
@@ -167,6 +169,8 @@ int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_
     k_fill_sym<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 256), (int64_t)kNumSMs * 16)), 256, 0,
                  st>>>(kp, cheb, x2, g.n[0], g.n[1], g.n[2], Fw);
     TK_CHECK_LAUNCH();
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(w + L.mx);
+    if (gram_use_i8(L.h)) TK_RC(launch_gram_i8_rowmax(L.h, Fw, mx, st));
     double* Y[3];
     int worst = TUCKER_OK;
     // cubic isotropic grid and equal ranks: F is symmetric under index permutations, so the three
@@ -190,7 +194,7 @@ int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_
             }
             continue;
         }
-        TK_RC(launch_gram(L.h, m, Fw, G, scr, L.scratch_bytes, st));
+        TK_RC(launch_gram_auto(L.h, m, Fw, G, mx, scr, L.scratch_bytes, st));
         const int rc = launch_eig(L.h[m], G, r[m], Y[m], nullptr, sigma[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;

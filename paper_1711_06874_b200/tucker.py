@@ -17,6 +17,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libtucker_b200.so")
 
 MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
+GRAM_AUTO, GRAM_DMMA, GRAM_INT8 = 0, 1, 2
 FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED"}
@@ -25,6 +26,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", 
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
            "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8",
+           "tucker_set_gram_engine", "tucker_get_gram_engine",
            "tucker_last_launch_count", "tucker_strerror")
 
 
@@ -72,6 +74,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_workspace_size_i8": (sz, [pg]),
         "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
+        "tucker_set_gram_engine": (ctypes.c_int, [i32]),
+        "tucker_get_gram_engine": (i32, []),
         "tucker_eig": (ctypes.c_int, [i64, vp, i32, vp, vp, vp, sz, vp, pi]),
         "tucker_ttm_core": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_hosvd": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
@@ -179,6 +183,16 @@ def gram(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, strea
     _check(lib.tucker_gram(ctypes.byref(g), int(mode), _ptr(F), _ptr(G), _ptr(ws), ws.numel(), _stream(stream)),
            "tucker_gram")
     return G
+
+
+def set_gram_engine(engine: int) -> None:
+    """Gram engine of gram / hosvd / approximate: GRAM_AUTO (INT8 emulation where supported),
+    GRAM_DMMA or GRAM_INT8.  Process-wide; size workspaces after setting it."""
+    _check(load().tucker_set_gram_engine(int(engine)), "tucker_set_gram_engine")
+
+
+def get_gram_engine() -> int:
+    return int(load().tucker_get_gram_engine())
 
 
 def workspace_i8(grid) -> torch.Tensor:

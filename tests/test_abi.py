@@ -41,6 +41,7 @@ def test_sass_uses_dmma_and_tma():
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {tucker.LIB_PATH}").read()
     assert "DMMA.8x8x4" in sass            # FP64 tensor-core MMA (Gram, TTM1, error)
     assert "UTMALDG" in sass               # TMA tile loads (Gram)
+    assert "UTCIMMA" in sass               # tcgen05 kind::i8 MMA (INT8-emulated Gram)
     assert "STG.E.ENL2.256" in sass        # 256-bit stores (octant fill)
 
 
@@ -76,8 +77,18 @@ def test_workspace_size_monotone(lib):
     b = T.workspace_bytes(GridSpec.cube(128, 1.0), (8, 8, 8))
     c = T.workspace_bytes(GridSpec.cube(128, 1.0), (40, 40, 40))
     assert 0 < a < b <= c
-    big = T.workspace_bytes(GridSpec.cube(1024, 1.0), (40, 40, 40))
-    assert big < 4 * 2 ** 30  # scratch for 1024^3 at ranks 40 stays well inside 180 GB
+    T.set_gram_engine(T.GRAM_DMMA)
+    try:
+        dmma = T.workspace_bytes(GridSpec.cube(1024, 1.0), (40, 40, 40))
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
+    assert dmma < 4 * 2 ** 30  # scratch for 1024^3 at ranks 40 stays well inside 180 GB
+    # INT8 emulation: residues of up to 16 GiB of the unfolding + partials, still far below 180 GB
+    i8 = T.workspace_bytes(GridSpec.cube(1024, 1.0), (40, 40, 40))
+    assert dmma < i8 < 20 * 2 ** 30
+    assert T.get_gram_engine() == T.GRAM_AUTO
+    with pytest.raises(T.TuckerError):
+        T.set_gram_engine(7)
 
 
 def test_validation_codes_next_rows(lib):

@@ -105,7 +105,8 @@ def test_sym_vs_generic_1024(T, r):
     else:
         # noise regime: the generic Gram route mixes odd null vectors (exact eigenvalue 0) into the
         # trailing columns; the symmetric path excludes them analytically, so its error is never
-        # higher (1024^3: r = 10 5.96844e-7 vs 5.96867e-7; r = 40 1.29e-8 vs 6.07e-8)
+        # higher (1024^3, INT8-emulated Grams: r = 40 5.286e-9 vs 5.361e-9; with DMMA Grams
+        # 1.364e-8 vs 6.774e-8)
         assert e[0] <= e_ref[0] * (1 + 1e-12), (e, e_ref)
 
 
