@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
     ap.add_argument("--no-f4", action="store_true", help="skip the NEXT f4 workloads line")
     ap.add_argument("--fused-n", type=int, default=2048)
+    ap.add_argument("--gram-engine", default="auto", choices=["auto", "dmma", "int8"],
+                    help="Gram engine of the materialised path (auto: INT8 emulation)")
     return ap.parse_args()
 
 
@@ -117,6 +119,14 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_peaks() -> dict:
+    """Driver-written MEASURED_PEAKS.json (HBM GB/s, dense bf16 TF/s burst and sustained), or {}."""
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
 # --------------------------------------------------------------------------- rank helpers ----
 def max_over_ranks(value: float, world: int, device=None) -> float:
     """Max of a per-rank scalar over the process group (device time = max over ranks)."""
@@ -146,6 +156,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T.load()
+    T.set_gram_engine({"auto": T.GRAM_AUTO, "dmma": T.GRAM_DMMA, "int8": T.GRAM_INT8}[args.gram_engine])
     n, rr = args.n, args.r
     grid = GridSpec.cube(n, 1.0)
     kern = KernelSpec.matern(1.5, 0.2)
@@ -157,7 +168,6 @@ def run_ours(args, rank, world, local):
     dev = F.device
     U = [torch.empty((n, rr), dtype=torch.float64, device=dev) for _ in range(3)]
     S = [torch.empty(rr, dtype=torch.float64, device=dev) for _ in range(3)]
-    G = torch.empty((n, n), dtype=torch.float64, device=dev)
     core = torch.empty(ranks, dtype=torch.float64, device=dev)
     out3 = torch.empty(3, dtype=torch.float64, device=dev)
     lib = T.load()
@@ -167,35 +177,20 @@ def run_ours(args, rank, world, local):
     wsp, wsn = ctypes.c_void_p(ws.data_ptr()), ws.numel()
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
-    def step(ev=None):
-        """One pass of the path as separate ABI calls; returns kernel launches.  ev: list of events."""
+    def step():
+        """One pass of the path as three ABI calls (fill, hosvd = 3 x (Gram + eig) + core, error);
+        returns the number of kernel launches."""
         launches = 0
-
-        def rec(i):
-            if ev is not None:
-                ev[i].record(stream)
-
-        rec(0)
         T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, sp), "fill")
         launches += lib.tucker_last_launch_count()
-        rec(1)
-        for m in range(3):
-            T._check(lib.tucker_gram(ctypes.byref(g_c), m, P(F), P(G), wsp, wsn, sp), "gram")
-            launches += lib.tucker_last_launch_count()
-            rec(2 + 2 * m)
-            rc = lib.tucker_eig(n, P(G), rr, P(U[m]), P(S[m]), wsp, wsn, sp, None)  # S[m] <- lambda_m
-            if rc not in (0, 5):
-                T._check(rc, "eig")
-            launches += lib.tucker_last_launch_count()
-            rec(3 + 2 * m)
-        T._check(lib.tucker_ttm_core(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), wsp, wsn, sp),
-                 "ttm")
+        rc = lib.tucker_hosvd(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), P(S[0]), P(S[1]),
+                              P(S[2]), wsp, wsn, sp, None)
+        if rc not in (0, 5):
+            T._check(rc, "hosvd")
         launches += lib.tucker_last_launch_count()
-        rec(8)
         T._check(lib.tucker_error(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), P(out3), wsp,
                                   wsn, sp), "error")
         launches += lib.tucker_last_launch_count()
-        rec(9)
         return launches
 
     for _ in range(args.warmup):
@@ -203,60 +198,94 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
 
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    T.profile_read()  # drop anything recorded before
+    T.profile_enable(True)
     with ClockSampler(local) as clk:
         t0.record(stream)
         for k in range(K):
-            launches += step(evs[k])
+            launches += step()
         t1.record(stream)
         torch.cuda.synchronize()
+    T.profile_enable(False)
+    prof = T.profile_read()
     if world > 1:
         dist.barrier()
     ms_total = max_over_ranks(t0.elapsed_time(t1), world, dev)
     ms_step = ms_total / K
 
-    # per-stage times (ms) averaged over the timed steps
-    def stage(i, j):
-        return sum(evs[k][i].elapsed_time(evs[k][j]) for k in range(K)) / K
-
-    st = {"fill": stage(0, 1), "gram": [stage(1 + 2 * m, 2 + 2 * m) for m in range(3)],
-          "eig": [stage(2 + 2 * m, 3 + 2 * m) for m in range(3)], "ttm": stage(7, 8), "error": stage(8, 9)}
+    # per-stage device times (ms per step) from the library's event scopes on `stream`
+    st = {name: ms / K for name, (ms, cnt) in prof.items() if cnt}
+    calls = {name: cnt / K for name, (ms, cnt) in prof.items() if cnt}
     E = out3.cpu().tolist()
 
-    # ---- roofline: dominant kernel = the Gram stage (SYRK-count flops N (n_m + 1) per launch)
-    gram_flops = [N * (n + 1) for _ in range(3)]
-    gram_ms = sum(st["gram"]) / 3
-    achieved = (sum(gram_flops) / 3) / (gram_ms * 1e-3) / 1e12
-    peak = FP64_PEAK_SPEC_TFLOPS
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "gram_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    total_flops = sum(gram_flops) + 2.0 * N * rr * 2  # Gram + TTM1 + error reconstruction (algorithmic)
+    # ---- roofline of the dominant kernel
+    gram_flops_fp64 = N * (n + 1)  # SYRK count of one mode's FP64 Gram (n_m (n_m+1)/2 entries x 2K flops)
+    i8 = "i8_gemm" in st
+    if i8:
+        # k_i8_gemm: 16 residue Grams per mode, algorithmic int8 ops = 16 x n(n+1)/2 x K x 2 per mode
+        ops_mode = 16 * gram_flops_fp64
+        launch_ms = prof["i8_gemm"][0] / prof["i8_gemm"][1]
+        ops_launch = ops_mode * 3 * K / prof["i8_gemm"][1]
+        achieved = ops_launch / (launch_ms * 1e-3) / 1e12
+        peaks = measured_peaks()
+        if peaks.get("bf16_tflops_sustained"):
+            peak = 2.0 * peaks["bf16_tflops_sustained"]
+            peak_src = ("dense INT8 = 2 x measured sustained bf16 (MEASURED_PEAKS.json bf16_tflops_sustained "
+                        f"{peaks['bf16_tflops_sustained']}; nominal ratio 4.5/2.25 POPS): the kernel runs inside a "
+                        "long step at the power-capped clock")
+        else:
+            peak = 4500.0
+            peak_src = "nominal dense INT8 4.5 POPS (MEASURED_PEAKS.json absent)"
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "i8_gemm_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        gram_stage_ms = sum(st.get(s, 0.0) for s in ("i8_rowmax", "i8_residues", "i8_gemm", "i8_crt")) / 3
+        roof = {"bound": "tensor", "kernel": "k_i8_gemm (tcgen05 kind::i8, CTA pairs), per launch",
+                "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src, "ops_per_launch": ops_launch, "launch_ms": launch_ms,
+                "launches_per_step": calls["i8_gemm"],
+                "fp64_equivalent_gram_tflops": gram_flops_fp64 / (gram_stage_ms * 1e-3) / 1e12,
+                "fp64_equivalent_note": "FP64 SYRK flops of one mode / the whole emulated Gram stage (row maxima, "
+                                        "residues, int8 Grams, CRT) vs the 37.2 TF/s FP64 (DMMA) peak"}
+    else:
+        launch_ms = prof["dmma_gram"][0] / prof["dmma_gram"][1]
+        achieved = gram_flops_fp64 / (launch_ms * 1e-3) / 1e12
+        peak = FP64_PEAK_SPEC_TFLOPS
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "gram_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "tensor", "kernel": "k_gram_tma (+k_gram_reduce), per mode",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "FP64 tensor (DMMA) = FP64 FMA pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz "
+                               "(spec-derived; MEASURED_PEAKS.json has no FP64 entry)",
+                "flops_per_launch": gram_flops_fp64}
+    total_flops = 3 * gram_flops_fp64 + 2.0 * N * rr * 2  # FP64 Gram + TTM1 + error reconstruction (algorithmic)
     result = {
         "metric": METRIC, "value": whole_job_rate(N, world, ms_step), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64" + (" (Gram: int8-emulated, exact CRT)" if i8 else ""),
+        "data": "synthetic",
         "config": {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2", "grid": [n, n, n], "box": [-1.0, 1.0],
                    "kernel": {"family": "matern", "nu": 1.5, "ell": 0.2, "sigma2": 1.0}, "ranks": list(ranks),
+                   "gram_engine": "int8 emulation (tcgen05 kind::i8 + CRT)" if i8 else "dmma",
                    "l2": f"inputs larger than L2 (F = {8 * N / 1e9:.2f} GB per step, L2 = 126 MB)",
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
-        "stages_ms": st,
+        "stages_ms": st, "stage_calls_per_step": calls,
         "fp64_tflops_algorithmic": total_flops / (ms_step * 1e-3) / 1e12,
-        "roofline": {"bound": "tensor", "kernel": "k_gram_tma (+k_gram_reduce), per mode",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "peak_source": "FP64 tensor (DMMA) = FP64 FMA pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz "
-                                    "(spec-derived; MEASURED_PEAKS.json has no FP64 entry)",
-                     "flops_per_launch": gram_flops[0]},
+        "roofline": roof,
         "gpu_launches": launches,
         "error": {"E": E[0], "normF": E[1], "normDiff": E[2]},
     }

@@ -233,6 +233,25 @@ TUCKER_API int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3]
                           int32_t iters, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
+/* Opt-in per-stage device timing: while enabled, CUDA events are recorded on the launching stream
+ * around each stage's launches (off by default: no events, no overhead).  tucker_profile_read
+ * synchronises the recorded events, writes the total milliseconds and the number of timed calls of
+ * each stage into ms[TUCKER_PROF_NSTAGES] / count[TUCKER_PROF_NSTAGES] (host) and clears them. */
+enum {
+    TUCKER_PROF_FILL = 0,
+    TUCKER_PROF_I8_ROWMAX = 1,   /* INT8 Gram: row maxima of the three unfoldings            */
+    TUCKER_PROF_I8_RESIDUES = 2, /* INT8 Gram: scaled rounding + residues mod 16 moduli       */
+    TUCKER_PROF_I8_GEMM = 3,     /* INT8 Gram: tcgen05 kind::i8 residue Grams (k_i8_gemm)     */
+    TUCKER_PROF_I8_CRT = 4,      /* INT8 Gram: chunk fold + Chinese-remainder reconstruction  */
+    TUCKER_PROF_DMMA_GRAM = 5,   /* DMMA Gram (k_gram_tma / k_gram + reduction)                */
+    TUCKER_PROF_EIG = 6,
+    TUCKER_PROF_TTM = 7,
+    TUCKER_PROF_ERROR = 8,
+    TUCKER_PROF_NSTAGES = 9
+};
+TUCKER_API int tucker_profile_enable(int32_t on);
+TUCKER_API int tucker_profile_read(double* ms, int64_t* count);
+
 TUCKER_API int64_t tucker_last_launch_count(void);
 
 TUCKER_API const char* tucker_strerror(int code);

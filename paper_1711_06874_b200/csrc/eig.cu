@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "jacobi.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace tk {
 namespace eig {
@@ -381,6 +382,7 @@ size_t eig_ws_bytes(int64_t n, int r) {
 
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
                size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot) {
+    TK_PROF(TUCKER_PROF_EIG, st);
     using namespace eig;
     if (r < 1 || r > n) return TUCKER_ERR_RANK;
     if (n > kDirectMax && r > kMaxP - 8) return TUCKER_ERR_UNSUPPORTED;

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "fill_eval.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace tk {
 
@@ -174,6 +175,7 @@ int launch_fill_prep(const tucker_grid& g, const tucker_kernel& kn, const KParam
 
 int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
                 cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_FILL, st);
     const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
     const KParams kp = make_kparams(kn);
     TK_RC(launch_fill_prep(g, kn, kp, nodes_x2, cheb, st));

@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "fill_eval.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace tk {
 namespace gram {
@@ -501,6 +502,7 @@ size_t gram_ws_bytes(const int64_t n[3]) {
 
 int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* ws, size_t ws_bytes,
                 cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_DMMA_GRAM, st);
     using namespace gram;
     Plan p = make_plan(n, mode);
     if (ws_bytes < (size_t)p.T * p.S * BM * BM * sizeof(double)) return TUCKER_ERR_SIZE;

@@ -25,6 +25,7 @@
 // k_i8_reduce folds.
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 #include <cmath>
 #include <cstdlib>
@@ -656,6 +657,7 @@ bool gram_i8_supported(const int64_t n[3]) {
 
 // Row maxima of all three unfoldings (one pass over F) into ws + off_mx.
 int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
     TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 8, st));
     i8::k_i8_rowmax<<<(unsigned)n[0], 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1]);
     TK_CHECK_LAUNCH();
@@ -687,8 +689,11 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
         const int64_t Kc = std::min(p.Ksc, p.Kfull - k0);
         ResArgs ra{F, n[0], n[1], n[2], mode, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R};
         const dim3 rg((unsigned)ceil_div(Kc, RT_K), (unsigned)ceil_div(p.rows, RT_ROWS));
-        k_i8_residues<<<rg, 256, 0, st>>>(ra);
-        TK_CHECK_LAUNCH();
+        {
+            TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+            k_i8_residues<<<rg, 256, 0, st>>>(ra);
+            TK_CHECK_LAUNCH();
+        }
         CUtensorMap map;
         {
             PFN_tmapEncodeTiled enc = tmap_encoder();
@@ -704,13 +709,18 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
         const int nchunks = (int)ceil_div(Kc, KCH);
         GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nchunks, NMOD * nchunks * p.ntiles, Kc, P};
         const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
-        k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
-        TK_CHECK_LAUNCH();
+        {
+            TK_PROF(TUCKER_PROF_I8_GEMM, st);
+            k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
+            TK_CHECK_LAUNCH();
+        }
         const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
+        TK_PROF(TUCKER_PROF_I8_CRT, st);
         k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
         TK_CHECK_LAUNCH();
     }
     const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
+    TK_PROF(TUCKER_PROF_I8_CRT, st);
     k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "fill_eval.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace tk {
 
@@ -376,6 +377,7 @@ size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]) {
 
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                     const double* U3, double* core, void* ws, size_t ws_bytes, cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_TTM, st);
     return launch_ttm_core_impl(n, r, F, nullptr, U1, U2, U3, core, ws, ws_bytes, st);
 }
 
@@ -717,6 +719,7 @@ size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs)
 
 int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                  const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_ERROR, st);
     return launch_error_impl(n, r, F, nullptr, U1, U2, U3, core, out3, ws, ws_bytes, st);
 }
 

@@ -26,7 +26,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", 
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
            "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8",
-           "tucker_set_gram_engine", "tucker_get_gram_engine",
+           "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
            "tucker_last_launch_count", "tucker_strerror")
 
 
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_set_gram_engine": (ctypes.c_int, [i32]),
         "tucker_get_gram_engine": (i32, []),
+        "tucker_profile_enable": (ctypes.c_int, [i32]),
+        "tucker_profile_read": (ctypes.c_int, [P(ctypes.c_double), P(ctypes.c_int64)]),
         "tucker_eig": (ctypes.c_int, [i64, vp, i32, vp, vp, vp, sz, vp, pi]),
         "tucker_ttm_core": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
         "tucker_hosvd": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
@@ -193,6 +195,22 @@ def set_gram_engine(engine: int) -> None:
 
 def get_gram_engine() -> int:
     return int(load().tucker_get_gram_engine())
+
+
+PROF_STAGES = ("fill", "i8_rowmax", "i8_residues", "i8_gemm", "i8_crt", "dmma_gram", "eig", "ttm", "error")
+
+
+def profile_enable(on: bool = True) -> None:
+    """Record CUDA events around each stage's launches (on the launching stream) until disabled."""
+    _check(load().tucker_profile_enable(1 if on else 0), "tucker_profile_enable")
+
+
+def profile_read() -> dict:
+    """{stage: (total ms, timed calls)} since the last read; synchronises the recorded events."""
+    n = len(PROF_STAGES)
+    ms, cnt = (ctypes.c_double * n)(), (ctypes.c_int64 * n)()
+    _check(load().tucker_profile_read(ms, cnt), "tucker_profile_read")
+    return {PROF_STAGES[i]: (ms[i], cnt[i]) for i in range(n)}
 
 
 def workspace_i8(grid) -> torch.Tensor:
