@@ -94,7 +94,7 @@ int check_ranks(const tucker_grid* g, const int32_t* r) {
 //   [scratch = max(gram, eig, ttm, err)] [device outputs of tucker_approximate: U1 U2 U3 core
 //   sigma1..3 err3]
 struct Layout {
-    size_t nodes, cheb, G, mx, scratch, outs, total;
+    size_t nodes, cheb, G, i8, i8_bytes, scratch, outs, total;
     size_t scratch_bytes;
 };
 
@@ -111,10 +111,11 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     L.G = off;
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
     off += align_up((size_t)nmax * nmax * 8, 256);
-    L.mx = off;
-    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
+    L.i8 = off;
+    L.i8_bytes = gram_use_i8(n) ? align_up(gram_i8_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
+    off += L.i8_bytes;
     L.scratch = off;
-    size_t s = gram_auto_ws_bytes(n);
+    size_t s = gram_use_i8(n) ? 0 : gram_ws_bytes(n);
     for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
     s = std::max(s, ttm_ws_bytes(n, r));
     s = std::max(s, err_ws_bytes(n, r));
@@ -138,13 +139,20 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
     double* G = reinterpret_cast<double*>(at(ws, L.G));
     void* scr = at(ws, L.scratch);
     int worst = TUCKER_OK;
-    unsigned long long* mx = reinterpret_cast<unsigned long long*>(at(ws, L.mx));
-    if (gram_use_i8(g->n)) TK_RC(launch_gram_i8_rowmax(g->n, F, mx, st));  // once for the three modes
-    for (int m = 0; m < 3; ++m) {
-        TK_RC(launch_gram_auto(g->n, m, F, G, mx, scr, L.scratch_bytes, st));
+    auto eig_mode = [&](int m) -> int {
         const int rc = launch_eig(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
+        return TUCKER_OK;
+    };
+    if (L.i8_bytes) {
+        // INT8-emulated Grams: one pipeline, the residues of mode m+1 overlap mode m's GEMM + eig
+        TK_RC(launch_gram_i8_modes(g->n, F, G, at(ws, L.i8), L.i8_bytes, st, eig_mode));
+    } else {
+        for (int m = 0; m < 3; ++m) {
+            TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));
+            TK_RC(eig_mode(m));
+        }
     }
     TK_RC(launch_ttm_core(g->n, r, F, U[0], U[1], U[2], core, scr, L.scratch_bytes, st));
     return worst;

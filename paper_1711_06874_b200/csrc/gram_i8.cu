@@ -29,6 +29,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <utility>
 
 namespace tk {
@@ -171,12 +172,12 @@ __device__ __forceinline__ void store_all_residues(const float (&u)[16][4], int8
     (store_residues<L>(u, out + L * lstride), ...);
 }
 
-__global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
-    __shared__ double tile[RT_ROWS][RT_K / 16][17];  // 16-column groups padded: conflict-free reads
-    __shared__ double s1[RT_ROWS], s2[RT_ROWS];
+// One 32-row x 128-column tile (row block by, column block bx of the super-chunk).
+__device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64_t by,
+                                             double (&tile)[RT_ROWS][RT_K / 16][17], double* s1, double* s2) {
     const int tid = threadIdx.x;
-    const int64_t row0 = (int64_t)blockIdx.y * RT_ROWS;
-    const int64_t kb = (int64_t)blockIdx.x * RT_K;  // within the super-chunk
+    const int64_t row0 = by * RT_ROWS;
+    const int64_t kb = bx * RT_K;  // within the super-chunk
     if (tid < RT_ROWS) {
         const int64_t row = row0 + tid;
         double m = 0.0;
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
     const int rr = tid >> 3, q = tid & 7;
     const int64_t row = row0 + rr;
     const int64_t kcol = kb + q * 16;
-    if (row >= a.rows || kcol >= a.Kc) return;
+    if (row >= a.rows || kcol >= a.Kc) return;  // (the caller syncs before the tile is reused)
     float u[16][4];
     const double sa = s1[rr], sb = s2[rr];
 #pragma unroll
@@ -266,6 +267,16 @@ __global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
     store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
 }
 
+// One CTA per tile (the loop also serves smaller grids).
+__global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a, int64_t ntx, int64_t ntiles) {
+    __shared__ double tile[RT_ROWS][RT_K / 16][17];  // 16-column groups padded: conflict-free reads
+    __shared__ double s1[RT_ROWS], s2[RT_ROWS];
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        residue_tile(a, t % ntx, t / ntx, tile, s1, s2);
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // 2. tcgen05 int8 Gram of the residue matrices on CTA pairs (cta_group::2, M = 256).
 //    Pair tile: PM = 256 rows (128 per CTA: A is split by rows) x up to PN = 512 columns, issued as
@@ -274,17 +285,19 @@ __global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a) {
 //    CTA streams 128 (A) + 256 (B) bytes for 128 x 512 MACs: half the L2 traffic per MAC of a
 //    128 x 256 single-CTA tile.
 struct GemmArgs {
-    int n;         // rows per modulus
-    int nJ;        // column blocks of PN
-    int ntiles;    // lower-triangle pair tiles
-    int nchunks;   // K-chunks of KCH in this super-chunk
-    int nunits;    // NMOD * nchunks * ntiles
-    int64_t Kc;    // K of this super-chunk
-    int32_t* P;    // partials [unit][PN][PM]
+    int n;           // rows per modulus
+    int nJ;          // column blocks of PN
+    int ntiles;      // lower-triangle pair tiles
+    int nug;         // units per (modulus, K-chunk) group
+    int nchunks;     // K-chunks of KCH in this super-chunk
+    int nunits;      // NMOD * nchunks * nug
+    int64_t Kc;      // K of this super-chunk
+    int32_t* P;      // partials [(l * nchunks + c) * ntiles + t][PN][PM]
+    const int2* utab;  // unit v of a group: tiles (ta, tb), tb = -1 unless two half tiles are merged
 };
 
 __host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
-__device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
+__host__ __device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
     for (int i = 0;; ++i) {
         const int c = tiles_in_row(i, nJ);
         if (t < c) {
@@ -295,11 +308,39 @@ __device__ __forceinline__ void tile_of(int t, int nJ, int& I, int& J) {
         t -= c;
     }
 }
-__device__ __forceinline__ int tile_cols(int I, int J, int n) {  // columns of the pair tile: multiple of 32, <= PN
+__host__ __device__ __forceinline__ int tile_cols(int I, int J, int n) {  // columns: multiple of 32, <= PN
     int c = min(PN, I * PM + PM - J * PN);
     c = min(c, n - J * PN);
     return (c + 31) & ~31;
 }
+
+// Units of one (modulus, K-chunk) group: every tile wider than 256 columns is a unit of its own;
+// tiles of <= 256 columns (the diagonal ones, ragged edges) are merged two by two, so that all
+// units cost the same MMA time and the CTA pairs stay in lockstep (shared rows stay in L2).
+// Writes the table when out != nullptr; returns the number of units.
+__host__ __device__ inline int build_units(int n, int nJ, int ntiles, int2* out) {
+    int u = 0, pend = -1;
+    for (int t = 0; t < ntiles; ++t) {
+        int I, J;
+        tile_of(t, nJ, I, J);
+        if (tile_cols(I, J, n) > 256) {
+            if (out) out[u] = make_int2(t, -1);
+            ++u;
+        } else if (pend < 0) {
+            pend = t;
+        } else {
+            if (out) out[u] = make_int2(pend, t);
+            ++u;
+            pend = -1;
+        }
+    }
+    if (pend >= 0) {
+        if (out) out[u] = make_int2(pend, -1);
+        ++u;
+    }
+    return u;
+}
+__global__ void k_i8_units(int n, int nJ, int ntiles, int2* out) { build_units(n, nJ, ntiles, out); }
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -355,19 +396,37 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-struct UnitGeo {
-    int l, c, I, J, N, nB, N0, N1;
+// A unit: one full tile (A shared by two N <= 256 MMA streams), one half tile, or two merged half
+// tiles (two streams with their own A, alternating stages).  Stream s writes TMEM columns
+// [tcol, tcol + N) and tile t of the partials.
+struct Stream {
+    int arow, brow, N, tcol, t;
 };
-__device__ __forceinline__ UnitGeo unit_geo(int u, const GemmArgs& g) {
-    UnitGeo x;
-    const int t = u % g.ntiles, grp = u / g.ntiles;
+struct Unit {
+    int l, c, ns, merged;
+    Stream s[2];
+};
+__device__ __forceinline__ Unit unit_of(int u, const GemmArgs& g) {
+    Unit x;
+    const int grp = u / g.nug, v = u % g.nug;
     x.l = grp / g.nchunks;
     x.c = grp % g.nchunks;
-    tile_of(t, g.nJ, x.I, x.J);
-    x.N = tile_cols(x.I, x.J, g.n);
-    x.nB = x.N > 256 ? 2 : 1;
-    x.N0 = min(x.N, 256);
-    x.N1 = x.N - x.N0;
+    const int2 tt = g.utab[v];
+    int I, J;
+    tile_of(tt.x, g.nJ, I, J);
+    const int N = tile_cols(I, J, g.n);
+    x.merged = tt.y >= 0;
+    if (!x.merged) {
+        x.ns = N > 256 ? 2 : 1;
+        x.s[0] = Stream{I * PM, J * PN, min(N, 256), 0, tt.x};
+        x.s[1] = Stream{I * PM, J * PN + 256, N > 256 ? N - 256 : 32, 256, tt.x};
+    } else {
+        int I2, J2;
+        tile_of(tt.y, g.nJ, I2, J2);
+        x.ns = 2;
+        x.s[0] = Stream{I * PM, J * PN, N, 0, tt.x};
+        x.s[1] = Stream{I2 * PM, J2 * PN, tile_cols(I2, J2, g.n), 256, tt.y};
+    }
     return x;
 }
 
@@ -401,29 +460,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const uint32_t tmem = tmem_base;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer (both CTAs): own A half and own B halves, completion on the leader
+        if (lane == 0) {  // TMA producer (both CTAs): own A rows and own B halves, completion on the leader
             int stage = 0;
             uint32_t ph = 0;
             for (int u = pair; u < g.nunits; u += npairs) {
-                const UnitGeo x = unit_geo(u, g);
+                const Unit x = unit_of(u, g);
                 const int64_t kbeg = (int64_t)x.c * KCH;
                 const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const int rowA = x.l * g.n + x.I * PM + (int)rank * 128;
-                const int rowB0 = x.l * g.n + x.J * PN + (int)rank * (x.N0 / 2);
-                const int rowB1 = x.l * g.n + x.J * PN + 256 + (int)rank * (x.N1 / 2);
-                const uint32_t bytes = 2u * (1u + (uint32_t)x.nB) * BOX;
+                const int base = x.l * g.n;
+                const int nsub = x.merged ? 2 : 1;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&empty[stage], ph ^ 1);
-                    uint8_t* sA = smem + stage * STAGE_BYTES;
-                    const uint32_t fl = leader_addr(&full[stage]);
                     const int kx = (int)(kbeg + (int64_t)kb * BKB);
-                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d_pair(sA, &map, fl, kx, rowA);
-                    tma_load_2d_pair(sA + BOX, &map, fl, kx, rowB0);
-                    if (x.nB > 1) tma_load_2d_pair(sA + 2 * BOX, &map, fl, kx, rowB1);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        ph ^= 1;
+                    for (int sub = 0; sub < nsub; ++sub) {
+                        const Stream& s0 = x.s[sub];
+                        mbar_wait(&empty[stage], ph ^ 1);
+                        uint8_t* sA = smem + stage * STAGE_BYTES;
+                        const uint32_t fl = leader_addr(&full[stage]);
+                        const bool two_b = !x.merged && x.ns == 2;
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (two_b ? 3u : 2u) * BOX);
+                        tma_load_2d_pair(sA, &map, fl, kx, base + s0.arow + (int)rank * 128);
+                        tma_load_2d_pair(sA + BOX, &map, fl, kx, base + s0.brow + (int)rank * (s0.N / 2));
+                        if (two_b)
+                            tma_load_2d_pair(sA + 2 * BOX, &map, fl, kx, base + x.s[1].brow + (int)rank * (x.s[1].N / 2));
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            ph ^= 1;
+                        }
                     }
                 }
             }
@@ -434,28 +496,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             uint32_t ph = 0;
             int it = 0;
             for (int u = pair; u < g.nunits; u += npairs, ++it) {
-                const UnitGeo x = unit_geo(u, g);
+                const Unit x = unit_of(u, g);
                 const int64_t kbeg = (int64_t)x.c * KCH;
                 const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const uint32_t id0 = idesc_i8(PM, x.N0), id1 = idesc_i8(PM, x.N1 > 0 ? x.N1 : 32);
+                const uint32_t id0 = idesc_i8(PM, x.s[0].N), id1 = idesc_i8(PM, x.s[1].N);
+                const int nsub = x.merged ? 2 : 1;
                 mbar_wait_cluster(&tempty, (it & 1) ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&full[stage], ph);
-                    tc_fence_after();
-                    const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+                    for (int sub = 0; sub < nsub; ++sub) {
+                        mbar_wait(&full[stage], ph);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BKB / 32; ++k) {
-                        const uint32_t acc = (kb | k) ? 1u : 0u;
-                        umma_i8_pair(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(a0 + BOX + 32 * k), id0, acc);
-                        if (x.nB > 1)
-                            umma_i8_pair(tmem + 256, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(a0 + 2 * BOX + 32 * k),
-                                         id1, acc);
-                    }
-                    umma_commit_pair(&empty[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        ph ^= 1;
+                        for (int k = 0; k < BKB / 32; ++k) {
+                            const uint32_t acc = (kb | k) ? 1u : 0u;
+                            const uint64_t da = umma_desc_sw128(a0 + 32 * k);
+                            if (x.merged) {
+                                umma_i8_pair(tmem + 256 * sub, da, umma_desc_sw128(a0 + BOX + 32 * k), sub ? id1 : id0,
+                                             acc);
+                            } else {
+                                umma_i8_pair(tmem, da, umma_desc_sw128(a0 + BOX + 32 * k), id0, acc);
+                                if (x.ns == 2)
+                                    umma_i8_pair(tmem + 256, da, umma_desc_sw128(a0 + 2 * BOX + 32 * k), id1, acc);
+                            }
+                        }
+                        umma_commit_pair(&empty[stage]);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            ph ^= 1;
+                        }
                     }
                 }
                 umma_commit_pair(&tfull);
@@ -467,26 +537,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         const uint32_t te = leader_addr(&tempty);
         int it = 0;
         for (int u = pair; u < g.nunits; u += npairs, ++it) {
-            const UnitGeo x = unit_geo(u, g);
+            const Unit x = unit_of(u, g);
             mbar_wait(&tfull, it & 1);
             tc_fence_after();
-            int32_t* P = g.P + (size_t)u * (PN * PM);
             const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
-            for (int c0 = 0; c0 < x.N; c0 += 32) {
-                const int cc = c0 < x.N0 ? c0 : 256 + (c0 - x.N0);  // TMEM column of output column c0
-                uint32_t v[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + cc));
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            // output segments: a full/half tile is columns [0, N) at TMEM column c; merged tiles
+            // are two segments at TMEM columns 0.. and 256..
+            const int nseg = x.merged ? 2 : 1;
+            for (int sg = 0; sg < nseg; ++sg) {
+                const int t = x.s[sg].t;
+                const int N = x.merged ? x.s[sg].N : (x.ns == 2 ? 256 + x.s[1].N : x.s[0].N);
+                const uint32_t tc0 = x.merged ? 256u * sg : 0u;
+                int32_t* P = g.P + ((size_t)(x.l * g.nchunks + x.c) * g.ntiles + t) * (PN * PM);
+                for (int c0 = 0; c0 < N; c0 += 32) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(taddr + tc0 + c0));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * PM + row] = (int32_t)v[j];
+                    for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * PM + row] = (int32_t)v[j];
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -593,10 +670,14 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     G[(int64_t)j * n + i] = d;
 }
 
-struct Plan {
+// ------------------------------------------------------------------------------------------
+// Host side.  Per mode the unfolding's K columns are processed in super-chunks of Ksc (residue
+// buffer <= 8 GiB): residues -> k_i8_gemm -> fold, in stream order; then the CRT.  (Running the
+// residues of the next super-chunk beside k_i8_gemm on a second stream was measured: both kernels
+// are SM-bound — FP32 issue and smem vs tensor + smem — and the overlap gained nothing.)
+struct ModePlan {
     int64_t rows, Kfull, Ksc, ldr, nsuper;
-    int nJ, ntiles, nchunks, nunits, b;
-    size_t off_mx, off_R, off_P, off_Racc, total;
+    int nJ, ntiles, b;
 };
 
 inline int count_tiles(int64_t n, int& nJ) {
@@ -607,15 +688,15 @@ inline int count_tiles(int64_t n, int& nJ) {
     return t;
 }
 
-// Residue buffer per super-chunk: 16 GiB (env TUCKER_I8_RESIDUE_MB overrides it; test knob).
+// Residue buffer per super-chunk: 8 GiB (env TUCKER_I8_RESIDUE_MB overrides it; test knob).
 inline size_t residue_cap() {
     const char* e = std::getenv("TUCKER_I8_RESIDUE_MB");
     const long long v = e ? std::atoll(e) : 0;
-    return v > 0 ? (size_t)v << 20 : (size_t)16 << 30;
+    return v > 0 ? (size_t)v << 20 : (size_t)8 << 30;
 }
 
-Plan make_plan(const int64_t n[3], int mode) {
-    Plan p{};
+ModePlan mode_plan(const int64_t n[3], int mode) {
+    ModePlan p{};
     p.rows = n[mode];
     p.Kfull = n[0] * n[1] * n[2] / n[mode];
     int64_t ksc = (int64_t)(residue_cap() / ((size_t)NMOD * p.rows));
@@ -624,29 +705,95 @@ Plan make_plan(const int64_t n[3], int mode) {
     p.nsuper = ceil_div(p.Kfull, p.Ksc);
     p.ldr = (int64_t)align_up((size_t)p.Ksc, 16);
     p.ntiles = count_tiles(p.rows, p.nJ);
-    p.nchunks = (int)ceil_div(p.Ksc, KCH);
-    p.nunits = NMOD * p.nchunks * p.ntiles;
     p.b = scale_bits(p.Kfull);
-    size_t off = 0;
-    p.off_mx = off;
-    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 256);
-    p.off_R = off;
-    off += align_up((size_t)NMOD * p.rows * p.ldr, 1024);
-    p.off_P = off;
-    off += align_up((size_t)p.nunits * PN * PM * 4, 256);
-    p.off_Racc = off;
-    off += align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256);
-    p.total = off;
     return p;
+}
+
+struct WsPlan {
+    size_t off_mx, off_R, off_P, off_Racc, off_utab, total;
+};
+
+WsPlan ws_plan(const int64_t n[3]) {
+    size_t rb = 0, pb = 0, ab = 0, ub = 0;
+    for (int m = 0; m < 3; ++m) {
+        const ModePlan p = mode_plan(n, m);
+        rb = std::max(rb, align_up((size_t)NMOD * p.rows * p.ldr, 1024));
+        const int64_t nch = ceil_div(p.Ksc, KCH);
+        pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 4, 256));
+        ab = std::max(ab, align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256));
+        ub = std::max(ub, align_up((size_t)p.ntiles * sizeof(int2), 256));
+    }
+    WsPlan w{};
+    size_t off = 0;
+    w.off_mx = off;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 1024);
+    w.off_R = off;
+    off += rb;
+    w.off_P = off;
+    off += pb;
+    w.off_Racc = off;
+    off += ab;
+    w.off_utab = off;
+    off += ub;
+    w.total = off;
+    return w;
+}
+
+// G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.
+int gram_mode(const int64_t n[3], int m, const double* F, const unsigned long long* mx, char* base, const WsPlan& w,
+              double* G, cudaStream_t st) {
+    const ModePlan p = mode_plan(n, m);
+    const unsigned long long* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
+    int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
+    int32_t* P = reinterpret_cast<int32_t*>(base + w.off_P);
+    int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
+    int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
+    TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    const int nug = build_units((int)p.rows, p.nJ, p.ntiles, nullptr);
+    k_i8_units<<<1, 1, 0, st>>>((int)p.rows, p.nJ, p.ntiles, utab);
+    TK_CHECK_LAUNCH();
+    PFN_tmapEncodeTiled enc = tmap_encoder();
+    if (!enc) return TUCKER_ERR_CUDA;
+    for (int64_t s = 0; s < p.nsuper; ++s) {
+        const int64_t k0 = s * p.Ksc, Kc = std::min(p.Ksc, p.Kfull - k0);
+        {
+            TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+            ResArgs ra{F, n[0], n[1], n[2], m, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R};
+            const int64_t ntx = ceil_div(Kc, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
+            k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
+            TK_CHECK_LAUNCH();
+        }
+        CUtensorMap map;
+        cuuint64_t dims[2] = {(cuuint64_t)Kc, (cuuint64_t)(NMOD * p.rows)};
+        cuuint64_t str[1] = {(cuuint64_t)p.ldr};
+        cuuint32_t box[2] = {BKB, 128}, es[2] = {1, 1};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return TUCKER_ERR_CUDA;
+        const int nchunks = (int)ceil_div(Kc, KCH);
+        GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nug, nchunks, NMOD * nchunks * nug, Kc, P, utab};
+        const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
+        {
+            TK_PROF(TUCKER_PROF_I8_GEMM, st);
+            k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
+            TK_CHECK_LAUNCH();
+        }
+        TK_PROF(TUCKER_PROF_I8_CRT, st);
+        const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
+        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
+        TK_CHECK_LAUNCH();
+    }
+    TK_PROF(TUCKER_PROF_I8_CRT, st);
+    const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
 }
 
 }  // namespace i8
 
-size_t gram_i8_ws_bytes(const int64_t n[3]) {
-    size_t s = 0;
-    for (int m = 0; m < 3; ++m) s = std::max(s, i8::make_plan(n, m).total);
-    return s;
-}
+size_t gram_i8_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
 
 bool gram_i8_supported(const int64_t n[3]) {
     // row counts up to 2^14 keep tile indices and the 2-D tensor map comfortably in range
@@ -655,7 +802,7 @@ bool gram_i8_supported(const int64_t n[3]) {
     return true;
 }
 
-// Row maxima of all three unfoldings (one pass over F) into ws + off_mx.
+// Row maxima of all three unfoldings (one pass over F).
 int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st) {
     TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
     TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 8, st));
@@ -664,66 +811,39 @@ int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long lon
     return TUCKER_OK;
 }
 
-// G (n_m x n_m, both triangles).  If have_max, the row maxima are already in the workspace head.
+// The three Grams (row maxima once); after_mode(m) runs on `st` once G_m is complete.
+int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* ws, size_t ws_bytes, cudaStream_t st,
+                         const std::function<int(int)>& after_mode) {
+    using namespace i8;
+    if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
+    const WsPlan w = ws_plan(n);
+    if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
+    char* base = static_cast<char*>(ws);
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(base + w.off_mx);
+    TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    for (int m = 0; m < 3; ++m) {
+        TK_RC(gram_mode(n, m, F, mx, base, w, G, st));
+        TK_RC(after_mode(m));
+    }
+    return TUCKER_OK;
+}
+
+// G (n_m x n_m, both triangles) of one mode.  mx: row maxima (nullptr: computed into ws).
 int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx_in,
                    void* ws, size_t ws_bytes, cudaStream_t st) {
     using namespace i8;
     if (mode < 0 || mode > 2) return TUCKER_ERR_INVALID_ARG;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
-    const Plan p = make_plan(n, mode);
-    if (ws_bytes < p.total) return TUCKER_ERR_SIZE;
-    char* w = static_cast<char*>(ws);
+    const WsPlan w = ws_plan(n);
+    if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
+    char* base = static_cast<char*>(ws);
     const unsigned long long* mx = mx_in;
     if (!mx) {
-        unsigned long long* own = reinterpret_cast<unsigned long long*>(w + p.off_mx);
+        unsigned long long* own = reinterpret_cast<unsigned long long*>(base + w.off_mx);
         TK_RC(launch_gram_i8_rowmax(n, F, own, st));
         mx = own;
     }
-    const unsigned long long* mxm = mx + (mode == 0 ? 0 : (mode == 1 ? n[0] : n[0] + n[1]));
-    int8_t* R = reinterpret_cast<int8_t*>(w + p.off_R);
-    int32_t* P = reinterpret_cast<int32_t*>(w + p.off_P);
-    int32_t* Racc = reinterpret_cast<int32_t*>(w + p.off_Racc);
-    TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
-    for (int64_t s = 0; s < p.nsuper; ++s) {
-        const int64_t k0 = s * p.Ksc;
-        const int64_t Kc = std::min(p.Ksc, p.Kfull - k0);
-        ResArgs ra{F, n[0], n[1], n[2], mode, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R};
-        const dim3 rg((unsigned)ceil_div(Kc, RT_K), (unsigned)ceil_div(p.rows, RT_ROWS));
-        {
-            TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
-            k_i8_residues<<<rg, 256, 0, st>>>(ra);
-            TK_CHECK_LAUNCH();
-        }
-        CUtensorMap map;
-        {
-            PFN_tmapEncodeTiled enc = tmap_encoder();
-            if (!enc) return TUCKER_ERR_CUDA;
-            cuuint64_t dims[2] = {(cuuint64_t)Kc, (cuuint64_t)(NMOD * p.rows)};
-            cuuint64_t str[1] = {(cuuint64_t)p.ldr};
-            cuuint32_t box[2] = {BKB, 128}, es[2] = {1, 1};
-            if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-                return TUCKER_ERR_CUDA;
-        }
-        const int nchunks = (int)ceil_div(Kc, KCH);
-        GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nchunks, NMOD * nchunks * p.ntiles, Kc, P};
-        const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
-        {
-            TK_PROF(TUCKER_PROF_I8_GEMM, st);
-            k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
-            TK_CHECK_LAUNCH();
-        }
-        const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
-        TK_PROF(TUCKER_PROF_I8_CRT, st);
-        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
-        TK_CHECK_LAUNCH();
-    }
-    const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-    TK_PROF(TUCKER_PROF_I8_CRT, st);
-    k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
-    TK_CHECK_LAUNCH();
-    return TUCKER_OK;
+    return gram_mode(n, mode, F, mx, base, w, G, st);
 }
 
 // ------------------------------------------------------------------------------------------

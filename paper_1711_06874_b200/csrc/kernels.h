@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <functional>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -47,6 +48,11 @@ int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long lon
 // mx: row maxima from launch_gram_i8_rowmax, or nullptr (computed into the workspace).
 int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
                    void* ws, size_t ws_bytes, cudaStream_t st);
+// The three Grams through one pipeline (residues of the next job overlap the current int8 GEMM);
+// after_mode(m) runs on `st` once G_m is complete (e.g. the eigensolver).  ws: gram_i8_ws_bytes,
+// disjoint from anything after_mode uses.
+int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* ws, size_t ws_bytes, cudaStream_t st,
+                         const std::function<int(int)>& after_mode);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
 bool gram_use_i8(const int64_t n[3]);
