@@ -72,58 +72,89 @@ inline int scale_bits(int64_t K) {
 }
 
 // ------------------------------------------------------------------------------------------
-// 1a. per-mode row maxima of |F| in one pass (bit patterns of non-negative doubles order as u64).
+// 1a. per-mode row maxima of |F| in one pass.  Only the exponent of a row maximum is used
+//     (E with max |a| < 2^E), so the maxima are taken over the high 32-bit words of |F| (sign
+//     cleared): the exponent field of the largest high word is that of the largest |value|.
 //     CTA = one i-plane, in k-blocks of 1024: thread t owns k = kb + t + 256 e (e < 4) and keeps
-//     their maxima over all lines j in registers (mode 2); every line's maximum (mode 1) is a warp
-//     reduction + a cross-warp pass over 32 lines at a time; the plane maximum gives mode 0.
+//     their maxima over all lines in registers (mode 2); 32 lines at a time, every thread keeps one
+//     partial per line and a butterfly reduce-scatter leaves lane L with line L's warp maximum
+//     (31 shuffles for 32 lines), combined across the 8 warps in shared memory (mode 1); the plane
+//     maximum gives mode 0.
 constexpr int RM_KB = 1024;
 __global__ void __launch_bounds__(256) k_i8_rowmax(const double* __restrict__ F, int64_t n1, int64_t n2, int64_t n3,
-                                                   unsigned long long* __restrict__ mx0,
-                                                   unsigned long long* __restrict__ mx1,
-                                                   unsigned long long* __restrict__ mx2) {
-    __shared__ double s_line[32][9];
+                                                   uint32_t* __restrict__ mx0, uint32_t* __restrict__ mx1,
+                                                   uint32_t* __restrict__ mx2) {
+    __shared__ uint32_t s_line[8][33];
     const int64_t i = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double pmax = 0.0;
+    uint32_t pmax = 0;
     for (int64_t kb = 0; kb < n3; kb += RM_KB) {
-        double km[4] = {0.0, 0.0, 0.0, 0.0};
+        uint32_t km[4] = {0u, 0u, 0u, 0u};
         bool kin[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) kin[e] = kb + tid + 256 * e < n3;
         for (int64_t j0 = 0; j0 < n2; j0 += 32) {
             const int nl = (int)min((int64_t)32, n2 - j0);
-#pragma unroll 4
-            for (int jj = 0; jj < nl; ++jj) {
-                const double* line = F + (i * n2 + j0 + jj) * n3 + kb + tid;
-                double lm = 0.0;
+            const uint32_t* hw = reinterpret_cast<const uint32_t*>(F + (i * n2 + j0) * n3 + kb + tid) + 1;
+#pragma unroll 1
+            for (int g8 = 0; g8 < 4; ++g8) {  // 8 lines at a time
+                uint32_t a[8];
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (kin[e]) {
-                        const double v = fabs(__ldg(line + 256 * e));
-                        km[e] = fmax(km[e], v);
-                        lm = fmax(lm, v);
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t lm = 0u;
+                    if (8 * g8 + jj < nl) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (kin[e]) {
+                                const uint32_t h = __ldg(hw + 2 * ((8 * g8 + jj) * n3 + 256 * e)) & 0x7FFFFFFFu;
+                                km[e] = max(km[e], h);
+                                lm = max(lm, h);
+                            }
                     }
-                lm = warp_max(lm);
-                if (lane == 0) s_line[jj][warp] = lm;
+                    a[jj] = lm;
+                }
+                // reduce-scatter over lane bits 4..2, then a full reduction over bits 1..0: lane L
+                // (L & 3 == 0) holds the warp maximum of line 8 g8 + (L >> 2)
+#pragma unroll
+                for (int sft = 16, h = 4; sft >= 4; sft >>= 1, h >>= 1) {
+                    const bool up = (lane & sft) != 0;
+#pragma unroll
+                    for (int q = 0; q < h; ++q) {
+                        const uint32_t send = up ? a[q] : a[q + h];
+                        const uint32_t keep = up ? a[q + h] : a[q];
+                        a[q] = max(keep, __shfl_xor_sync(0xffffffffu, send, sft));
+                    }
+                }
+                a[0] = max(a[0], __shfl_xor_sync(0xffffffffu, a[0], 2));
+                a[0] = max(a[0], __shfl_xor_sync(0xffffffffu, a[0], 1));
+                if ((lane & 3) == 0) s_line[warp][8 * g8 + (lane >> 2)] = a[0];
             }
             __syncthreads();
             if (tid < nl) {
-                double m = s_line[tid][0];
+                uint32_t m = s_line[0][tid];
 #pragma unroll
-                for (int w = 1; w < 8; ++w) m = fmax(m, s_line[tid][w]);
-                atomicMax(&mx1[j0 + tid], (unsigned long long)__double_as_longlong(m));
-                pmax = fmax(pmax, m);
+                for (int w = 1; w < 8; ++w) m = max(m, s_line[w][tid]);
+                atomicMax(&mx1[j0 + tid], m);
+                pmax = max(pmax, m);
             }
             __syncthreads();
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (kin[e]) atomicMax(&mx2[kb + tid + 256 * e], (unsigned long long)__double_as_longlong(km[e]));
+            if (kin[e]) atomicMax(&mx2[kb + tid + 256 * e], km[e]);
     }
     if (warp == 0) {
-        pmax = warp_max(pmax);
-        if (lane == 0) atomicMax(&mx0[i], (unsigned long long)__double_as_longlong(pmax));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pmax = max(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+        if (lane == 0) atomicMax(&mx0[i], pmax);
     }
+}
+
+// E with |a| < 2^E for every |a| <= the row maximum whose high word is hw (frexp exponent of a
+// normal maximum; subnormal maxima use the bound 2^-1022; a zero row any E).
+__host__ __device__ __forceinline__ int row_exponent(uint32_t hw) {
+    const int ef = (int)(hw >> 20);
+    return hw == 0u ? 0 : (ef == 0 ? -1022 : ef - 1022);
 }
 
 __device__ __forceinline__ double pow2d(int e) {  // 2^e, -1022 <= e <= 1023
@@ -138,26 +169,29 @@ struct ResArgs {
     const double* F;
     int64_t n1, n2, n3;
     int mode;
-    int64_t rows, Kfull, k0, Kc, ldr;  // ldr: bytes per residue row (>= Kc, multiple of 16)
-    const unsigned long long* mx;      // row maxima of this mode
+    int64_t rows, Kfull, k0, Kc, ldr;  // ldr: bytes per residue row (multiple of 128 >= Kc)
+    const uint32_t* mx;                // row maxima (high words of |F|) of this mode
     int b;
     int8_t* R;                         // [NMOD][rows][ldr]
 };
 
-// Residues of 16 elements modulo p_L (compile-time constants) -> one 16-byte store.
+__host__ __device__ constexpr int balanced(int r, int p) { return r > p / 2 ? r - p : r; }
+
+// Residues of 16 elements modulo p_L (compile-time constants) -> one 16-byte store.  u[e][0..2]:
+// balanced 17-bit limbs of x (|u| <= 2^16 + 1), x = u0 + u1 2^17 + u2 2^34; with the balanced
+// constants |c| <= 126 every partial sum of s = u0 + c1 u1 + c2 u2 stays below 2^24: exact in FP32.
 template <int L>
-__device__ __forceinline__ void store_residues(const float (&u)[16][4], int8_t* out) {
+__device__ __forceinline__ void store_residues(const float (&u)[16][3], int8_t* out) {
     constexpr int p = kMod(L);
-    constexpr float c1 = (float)pow2mod(13, p), c2 = (float)pow2mod(26, p), c3 = (float)pow2mod(39, p);
+    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
     constexpr float fp = (float)p, inv = 1.0f / (float)p;
     uint32_t w[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-        // s = x (mod p) from the 13-bit limbs of x (top limb signed); exact in FP32 (|s| < 2^23)
-        const float s = fmaf(u[e][3], c3, fmaf(u[e][2], c2, fmaf(u[e][1], c1, u[e][0])));
-        const float qq = fmaf(s, inv, 12582912.f) - 12582912.f;  // round(s / p), +-1 near ties
-        const float r = fmaf(qq, -fp, s);                         // |r| <= (p+1)/2 <= 127
-        w[e] = (uint32_t)__float_as_int(r + 12582912.f);          // low byte = r (two's complement)
+        const float s = fmaf(u[e][2], c2, fmaf(u[e][1], c1, u[e][0]));  // = x (mod p), |s| < 2^24
+        const float qq = fmaf(s, inv, 12582912.f) - 12582912.f;          // round(s / p), +-1 near ties
+        const float r = fmaf(qq, -fp, s);                                 // |r| <= (p+1)/2 <= 127
+        w[e] = (uint32_t)__float_as_int(r + 12582912.f);                  // low byte = r (two's complement)
     }
     uint4 v;
     v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
@@ -167,7 +201,7 @@ __device__ __forceinline__ void store_residues(const float (&u)[16][4], int8_t* 
     *reinterpret_cast<uint4*>(out) = v;
 }
 template <int... L>
-__device__ __forceinline__ void store_all_residues(const float (&u)[16][4], int8_t* out, size_t lstride,
+__device__ __forceinline__ void store_all_residues(const float (&u)[16][3], int8_t* out, size_t lstride,
                                                    std::integer_sequence<int, L...>) {
     (store_residues<L>(u, out + L * lstride), ...);
 }
@@ -180,14 +214,15 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     const int64_t kb = bx * RT_K;  // within the super-chunk
     if (tid < RT_ROWS) {
         const int64_t row = row0 + tid;
-        double m = 0.0;
-        if (row < a.rows) m = __longlong_as_double((long long)a.mx[row]);
-        int E = 0;
-        if (m > 0.0) frexp(m, &E);
+        const int E = row < a.rows ? row_exponent(a.mx[row]) : 0;
         const int sh = a.b - E;  // |a_ik| 2^sh < 2^b
-        const int h = sh / 2;
-        s1[tid] = pow2d(h);
-        s2[tid] = pow2d(sh - h);
+        if (sh >= -1022 && sh <= 1023) {
+            s1[tid] = pow2d(sh);
+            s2[tid] = 1.0;
+        } else {  // beyond the double exponent range: two exact steps
+            s1[tid] = pow2d(sh / 2);
+            s2[tid] = pow2d(sh - sh / 2);
+        }
     }
     // gather the 32 x 128 tile, coalesced along the unit-stride axis of F; all 16 addresses of a
     // thread are formed before the loads so they issue back to back
@@ -244,27 +279,25 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     // each thread: one row, 16 consecutive columns -> one 16-byte store per modulus
     const int rr = tid >> 3, q = tid & 7;
     const int64_t row = row0 + rr;
-    const int64_t kcol = kb + q * 16;
-    if (row >= a.rows || kcol >= a.Kc) return;  // (the caller syncs before the tile is reused)
-    float u[16][4];
+    if (row >= a.rows) return;  // (the caller syncs before the tile is reused); columns >= Kc: residue 0
+    float u[16][3];
     const double sa = s1[rr], sb = s2[rr];
+    constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-        const double t = (tile[rr][q][e] * sa) * sb;          // exact power-of-two scaling, |t| < 2^50
-        const double y = __dadd_rn(t, 6755399441055744.0);    // 1.5 2^52: v = rint(t) + 2^51 in the low 52 bits
+        // y = 2^52 + w, w = rint(a 2^sh) + B in [0, 2^52): one rounding (the scaling is exact)
+        const double v = tile[rr][q][e];
+        const double y = (sb == 1.0) ? fma(v, sa, M2) : fma(v * sa, sb, M2);
         const uint32_t lo = (uint32_t)__double2loint(y);
         const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
-        const uint32_t l0 = lo & 0x1FFFu, l1 = (lo >> 13) & 0x1FFFu;
-        const uint32_t l2 = __funnelshift_r(lo, hi, 26) & 0x1FFFu, l3 = hi >> 7;
-        // x = rint(t) = (l3 - 2^12) 2^39 + l2 2^26 + l1 2^13 + l0  (signed top limb)
-        u[e][0] = __int_as_float(0x4B000000 | l0) - 8388608.f;
-        u[e][1] = __int_as_float(0x4B000000 | l1) - 8388608.f;
-        u[e][2] = __int_as_float(0x4B000000 | l2) - 8388608.f;
-        u[e][3] = __int_as_float(0x4B000000 | l3) - (8388608.f + 4096.f);
+        // balanced 17-bit digits: x = rint(a 2^sh) = (d0 - 2^16) + (d1 - 2^16) 2^17 + (d2 - 2^16) 2^34
+        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
+        u[e][0] = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        u[e][1] = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        u[e][2] = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
     }
-    int8_t* out = a.R + row * a.ldr + kcol;
-    const size_t lstride = (size_t)a.rows * a.ldr;
-    store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    int8_t* out = a.R + row * a.ldr + kb + q * 16;
+    store_all_residues(u, out, (size_t)a.rows * a.ldr, std::make_integer_sequence<int, NMOD>{});
 }
 
 // One CTA per tile (the loop also serves smaller grids).
@@ -369,11 +402,13 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same smem o
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(smem_u32(p)));
     return r;
 }
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1) {
+// Box (128 rows x 128 bytes) of modulus l, K-block kb, starting at `row` of the residue tensor.
+__device__ __forceinline__ void tma_load_res_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int l, int kb,
+                                                  int row) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(kb * BKB), "r"(row), "r"(l)
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -467,10 +502,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                 const Unit x = unit_of(u, g);
                 const int64_t kbeg = (int64_t)x.c * KCH;
                 const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const int base = x.l * g.n;
                 const int nsub = x.merged ? 2 : 1;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    const int kx = (int)(kbeg + (int64_t)kb * BKB);
+                    const int kx = (int)(kbeg / BKB) + kb;  // K-block index
                     for (int sub = 0; sub < nsub; ++sub) {
                         const Stream& s0 = x.s[sub];
                         mbar_wait(&empty[stage], ph ^ 1);
@@ -478,10 +512,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                         const uint32_t fl = leader_addr(&full[stage]);
                         const bool two_b = !x.merged && x.ns == 2;
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (two_b ? 3u : 2u) * BOX);
-                        tma_load_2d_pair(sA, &map, fl, kx, base + s0.arow + (int)rank * 128);
-                        tma_load_2d_pair(sA + BOX, &map, fl, kx, base + s0.brow + (int)rank * (s0.N / 2));
+                        tma_load_res_pair(sA, &map, fl, x.l, kx, s0.arow + (int)rank * 128);
+                        tma_load_res_pair(sA + BOX, &map, fl, x.l, kx, s0.brow + (int)rank * (s0.N / 2));
                         if (two_b)
-                            tma_load_2d_pair(sA + 2 * BOX, &map, fl, kx, base + x.s[1].brow + (int)rank * (x.s[1].N / 2));
+                            tma_load_res_pair(sA + 2 * BOX, &map, fl, x.l, kx, x.s[1].brow + (int)rank * (x.s[1].N / 2));
                         if (++stage == STAGES) {
                             stage = 0;
                             ph ^= 1;
@@ -633,7 +667,7 @@ __device__ __forceinline__ double u128_to_double_rn(unsigned __int128 m) {
     return ldexp(__ull2double_rn(top), 64 - lz);
 }
 
-__global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const unsigned long long* __restrict__ mx,
+__global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const uint32_t* __restrict__ mx,
                                                 int n, int nJ, int ntiles, int b, double* __restrict__ G) {
     // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -660,11 +694,7 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     const bool neg = S > half;
     const unsigned __int128 mag = neg ? (Pp - S) : S;
     double d = u128_to_double_rn(mag);
-    int Ei = 0, Ej = 0;
-    const double mi = __longlong_as_double((long long)mx[i]), mj = __longlong_as_double((long long)mx[j]);
-    if (mi > 0.0) frexp(mi, &Ei);
-    if (mj > 0.0) frexp(mj, &Ej);
-    d = ldexp(d, Ei + Ej - 2 * b);
+    d = ldexp(d, row_exponent(mx[i]) + row_exponent(mx[j]) - 2 * b);
     if (neg) d = -d;
     G[(int64_t)i * n + j] = d;
     G[(int64_t)j * n + i] = d;
@@ -676,7 +706,7 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
 // residues of the next super-chunk beside k_i8_gemm on a second stream was measured: both kernels
 // are SM-bound — FP32 issue and smem vs tensor + smem — and the overlap gained nothing.)
 struct ModePlan {
-    int64_t rows, Kfull, Ksc, ldr, nsuper;
+    int64_t rows, Kfull, Ksc, ldr, nsuper;  // ldr: residue row bytes (multiple of 128)
     int nJ, ntiles, b;
 };
 
@@ -703,7 +733,7 @@ ModePlan mode_plan(const int64_t n[3], int mode) {
     ksc = std::max<int64_t>(KCH, ksc / KCH * KCH);
     p.Ksc = std::min(ksc, p.Kfull);
     p.nsuper = ceil_div(p.Kfull, p.Ksc);
-    p.ldr = (int64_t)align_up((size_t)p.Ksc, 16);
+    p.ldr = ceil_div(p.Ksc, (int64_t)BKB) * BKB;
     p.ntiles = count_tiles(p.rows, p.nJ);
     p.b = scale_bits(p.Kfull);
     return p;
@@ -740,10 +770,10 @@ WsPlan ws_plan(const int64_t n[3]) {
 }
 
 // G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.
-int gram_mode(const int64_t n[3], int m, const double* F, const unsigned long long* mx, char* base, const WsPlan& w,
+int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, char* base, const WsPlan& w,
               double* G, cudaStream_t st) {
     const ModePlan p = mode_plan(n, m);
-    const unsigned long long* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
+    const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
     int32_t* P = reinterpret_cast<int32_t*>(base + w.off_P);
     int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
@@ -763,11 +793,13 @@ int gram_mode(const int64_t n[3], int m, const double* F, const unsigned long lo
             k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
             TK_CHECK_LAUNCH();
         }
+        // residues [NMOD][rows][ldr]: 3-D map (K bytes, rows, modulus), box = 128 rows x 128 bytes
         CUtensorMap map;
-        cuuint64_t dims[2] = {(cuuint64_t)Kc, (cuuint64_t)(NMOD * p.rows)};
-        cuuint64_t str[1] = {(cuuint64_t)p.ldr};
-        cuuint32_t box[2] = {BKB, 128}, es[2] = {1, 1};
-        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        const int64_t kpad = ceil_div(Kc, (int64_t)BKB) * BKB;  // the residue kernel writes whole K-blocks
+        cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)p.rows, (cuuint64_t)NMOD};
+        cuuint64_t str[2] = {(cuuint64_t)p.ldr, (cuuint64_t)(p.rows * p.ldr)};
+        cuuint32_t box[3] = {BKB, 128, 1}, es[3] = {1, 1, 1};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return TUCKER_ERR_CUDA;
@@ -803,9 +835,9 @@ bool gram_i8_supported(const int64_t n[3]) {
 }
 
 // Row maxima of all three unfoldings (one pass over F).
-int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st) {
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, uint32_t* mx, cudaStream_t st) {
     TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
-    TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 8, st));
+    TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 4, st));
     i8::k_i8_rowmax<<<(unsigned)n[0], 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1]);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
@@ -819,7 +851,7 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
     const WsPlan w = ws_plan(n);
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
-    unsigned long long* mx = reinterpret_cast<unsigned long long*>(base + w.off_mx);
+    uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
     for (int m = 0; m < 3; ++m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G, st));
@@ -829,7 +861,7 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
 }
 
 // G (n_m x n_m, both triangles) of one mode.  mx: row maxima (nullptr: computed into ws).
-int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx_in,
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx_in,
                    void* ws, size_t ws_bytes, cudaStream_t st) {
     using namespace i8;
     if (mode < 0 || mode > 2) return TUCKER_ERR_INVALID_ARG;
@@ -837,9 +869,9 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
     const WsPlan w = ws_plan(n);
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
-    const unsigned long long* mx = mx_in;
+    const uint32_t* mx = mx_in;
     if (!mx) {
-        unsigned long long* own = reinterpret_cast<unsigned long long*>(base + w.off_mx);
+        uint32_t* own = reinterpret_cast<uint32_t*>(base + w.off_mx);
         TK_RC(launch_gram_i8_rowmax(n, F, own, st));
         mx = own;
     }
@@ -854,7 +886,7 @@ int& gram_engine() {
 }
 bool gram_use_i8(const int64_t n[3]) { return gram_engine() != TUCKER_GRAM_DMMA && gram_i8_supported(n); }
 size_t gram_auto_ws_bytes(const int64_t n[3]) { return gram_use_i8(n) ? gram_i8_ws_bytes(n) : gram_ws_bytes(n); }
-int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,
                      void* ws, size_t ws_bytes, cudaStream_t st) {
     if (gram_use_i8(n)) return launch_gram_i8(n, mode, F, G, mx, ws, ws_bytes, st);
     return launch_gram(n, mode, F, G, ws, ws_bytes, st);

@@ -44,9 +44,9 @@ int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* 
 bool gram_i8_supported(const int64_t n[3]);
 size_t gram_i8_ws_bytes(const int64_t n[3]);
 // Row maxima of the three unfoldings (n1 + n2 + n3 u64 bit patterns of non-negative doubles).
-int launch_gram_i8_rowmax(const int64_t n[3], const double* F, unsigned long long* mx, cudaStream_t st);
+int launch_gram_i8_rowmax(const int64_t n[3], const double* F, uint32_t* mx, cudaStream_t st);
 // mx: row maxima from launch_gram_i8_rowmax, or nullptr (computed into the workspace).
-int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,
                    void* ws, size_t ws_bytes, cudaStream_t st);
 // The three Grams through one pipeline (residues of the next job overlap the current int8 GEMM);
 // after_mode(m) runs on `st` once G_m is complete (e.g. the eigensolver).  ws: gram_i8_ws_bytes,
@@ -57,7 +57,7 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
 int& gram_engine();
 bool gram_use_i8(const int64_t n[3]);
 size_t gram_auto_ws_bytes(const int64_t n[3]);
-int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const unsigned long long* mx,
+int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,
                      void* ws, size_t ws_bytes, cudaStream_t st);
 
 // a-7 fused generate-and-Gram (F never materialised).  KParams / ChunkGeo: fill_eval.cuh.

@@ -169,7 +169,7 @@ int launch_hosvd_sym(const tucker_grid& g, const tucker_kernel& kn, const int32_
     k_fill_sym<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 256), (int64_t)kNumSMs * 16)), 256, 0,
                  st>>>(kp, cheb, x2, g.n[0], g.n[1], g.n[2], Fw);
     TK_CHECK_LAUNCH();
-    unsigned long long* mx = reinterpret_cast<unsigned long long*>(w + L.mx);
+    uint32_t* mx = reinterpret_cast<uint32_t*>(w + L.mx);
     if (gram_use_i8(L.h)) TK_RC(launch_gram_i8_rowmax(L.h, Fw, mx, st));
     double* Y[3];
     int worst = TUCKER_OK;
