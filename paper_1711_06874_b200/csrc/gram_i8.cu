@@ -181,17 +181,22 @@ __host__ __device__ constexpr int balanced(int r, int p) { return r > p / 2 ? r 
 // balanced 17-bit limbs of x (|u| <= 2^16 + 1), x = u0 + u1 2^17 + u2 2^34; with the balanced
 // constants |c| <= 126 every partial sum of s = u0 + c1 u1 + c2 u2 stays below 2^24: exact in FP32.
 template <int L>
-__device__ __forceinline__ void store_residues(const float (&u)[16][3], int8_t* out) {
+__device__ __forceinline__ void store_residues(const float2 (&u)[8][3], int8_t* out) {
+    // two elements per instruction (FFMA2 / FADD2, sm_100): u[e2][.] = limbs of elements 2 e2, 2 e2 + 1
     constexpr int p = kMod(L);
     constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
     constexpr float fp = (float)p, inv = 1.0f / (float)p;
+    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
+    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
+    const float2 NP = make_float2(-fp, -fp);
     uint32_t w[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const float s = fmaf(u[e][2], c2, fmaf(u[e][1], c1, u[e][0]));  // = x (mod p), |s| < 2^24
-        const float qq = fmaf(s, inv, 12582912.f) - 12582912.f;          // round(s / p), +-1 near ties
-        const float r = fmaf(qq, -fp, s);                                 // |r| <= (p+1)/2 <= 127
-        w[e] = (uint32_t)__float_as_int(r + 12582912.f);                  // low byte = r (two's complement)
+    for (int e = 0; e < 8; ++e) {
+        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));  // = x (mod p), |s| < 2^24
+        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);                   // round(s / p), +-1 near ties
+        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);                     // r + 1.5 2^23, |r| <= 127
+        w[2 * e] = (uint32_t)__float_as_int(r2.x);                                     // low byte = r
+        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
     }
     uint4 v;
     v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
@@ -201,7 +206,7 @@ __device__ __forceinline__ void store_residues(const float (&u)[16][3], int8_t* 
     *reinterpret_cast<uint4*>(out) = v;
 }
 template <int... L>
-__device__ __forceinline__ void store_all_residues(const float (&u)[16][3], int8_t* out, size_t lstride,
+__device__ __forceinline__ void store_all_residues(const float2 (&u)[8][3], int8_t* out, size_t lstride,
                                                    std::integer_sequence<int, L...>) {
     (store_residues<L>(u, out + L * lstride), ...);
 }
@@ -280,7 +285,7 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     const int rr = tid >> 3, q = tid & 7;
     const int64_t row = row0 + rr;
     if (row >= a.rows) return;  // (the caller syncs before the tile is reused); columns >= Kc: residue 0
-    float u[16][3];
+    float2 u[8][3];
     const double sa = s1[rr], sb = s2[rr];
     constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
 #pragma unroll
@@ -292,9 +297,18 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
         const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
         // balanced 17-bit digits: x = rint(a 2^sh) = (d0 - 2^16) + (d1 - 2^16) 2^17 + (d2 - 2^16) 2^34
         const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
-        u[e][0] = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
-        u[e][1] = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
-        u[e][2] = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        if (e & 1) {
+            u[e >> 1][0].y = f0;
+            u[e >> 1][1].y = f1;
+            u[e >> 1][2].y = f2;
+        } else {
+            u[e >> 1][0].x = f0;
+            u[e >> 1][1].x = f1;
+            u[e >> 1][2].x = f2;
+        }
     }
     int8_t* out = a.R + row * a.ldr + kb + q * 16;
     store_all_residues(u, out, (size_t)a.rows * a.ldr, std::make_integer_sequence<int, NMOD>{});
