@@ -315,7 +315,7 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
 }
 
 // One CTA per tile (the loop also serves smaller grids).
-__global__ void __launch_bounds__(256, 3) k_i8_residues(const ResArgs a, int64_t ntx, int64_t ntiles) {
+__global__ void __launch_bounds__(256, 4) k_i8_residues(const ResArgs a, int64_t ntx, int64_t ntiles) {
     __shared__ double tile[RT_ROWS][RT_K / 16][17];  // 16-column groups padded: conflict-free reads
     __shared__ double s1[RT_ROWS], s2[RT_ROWS];
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
