@@ -19,7 +19,13 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__average_warp_latency_issue_stalled_barrier", "sm__cycles_elapsed.avg"]
+        "smsp__average_warp_latency_issue_stalled_barrier", "sm__cycles_elapsed.avg",
+        "sm__cycles_elapsed.avg.per_second", "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "l1tex__m_xbar2l1tex_read_bytes.sum"]
 
 
 def to_us(v, unit):
@@ -59,8 +65,10 @@ def report(path):
         print(f"## `{name.split('(')[0]}` (ID {r[h.index('ID')]})\n")
         print("| metric | value | unit |\n|---|---:|---|")
         for k in KEYS:
-            if k in h:
-                i = h.index(k)
+            # raw-page columns may carry a section prefix ("TPC.TriageCompute.<metric>")
+            idx = [i for i, c in enumerate(h) if c == k or c.endswith("." + k)]
+            if idx:
+                i = idx[0]
                 print(f"| {k} | {r[i]} | {units[i]} |")
         print()
 
