@@ -170,9 +170,11 @@ struct ResArgs {
     int64_t n1, n2, n3;
     int mode;
     int64_t rows, Kfull, k0, Kc, ldr;  // ldr: bytes per residue row (multiple of 128 >= Kc)
+                                       // layout [NMOD][ldr / 128][rows][128]: K-block-major, so a
+                                       // TMA box (128 rows x 128 B) and a tile's stores are contiguous
     const uint32_t* mx;                // row maxima (high words of |F|) of this mode
     int b;
-    int8_t* R;                         // [NMOD][rows][ldr]
+    int8_t* R;                         // [NMOD][K-block][rows][128]
 };
 
 __host__ __device__ constexpr int balanced(int r, int p) { return r > p / 2 ? r - p : r; }
@@ -310,7 +312,7 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
             u[e >> 1][2].x = f2;
         }
     }
-    int8_t* out = a.R + row * a.ldr + kb + q * 16;
+    int8_t* out = a.R + ((kb / RT_K) * a.rows + row) * RT_K + q * 16;
     store_all_residues(u, out, (size_t)a.rows * a.ldr, std::make_integer_sequence<int, NMOD>{});
 }
 
@@ -420,9 +422,9 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same smem o
 __device__ __forceinline__ void tma_load_res_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int l, int kb,
                                                   int row) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(kb * BKB), "r"(row), "r"(l)
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(0), "r"(row), "r"(kb), "r"(l)
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -807,13 +809,14 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
             k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
             TK_CHECK_LAUNCH();
         }
-        // residues [NMOD][rows][ldr]: 3-D map (K bytes, rows, modulus), box = 128 rows x 128 bytes
+        // residues [NMOD][K-block][rows][128 B]: 4-D map (byte, row, K-block, modulus); a box of
+        // 128 rows x 128 bytes is one contiguous 16 KB block
         CUtensorMap map;
-        const int64_t kpad = ceil_div(Kc, (int64_t)BKB) * BKB;  // the residue kernel writes whole K-blocks
-        cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)p.rows, (cuuint64_t)NMOD};
-        cuuint64_t str[2] = {(cuuint64_t)p.ldr, (cuuint64_t)(p.rows * p.ldr)};
-        cuuint32_t box[3] = {BKB, 128, 1}, es[3] = {1, 1, 1};
-        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        const int64_t nkb = p.ldr / BKB;
+        cuuint64_t dims[4] = {(cuuint64_t)BKB, (cuuint64_t)p.rows, (cuuint64_t)nkb, (cuuint64_t)NMOD};
+        cuuint64_t str[3] = {(cuuint64_t)BKB, (cuuint64_t)(p.rows * BKB), (cuuint64_t)(p.rows * p.ldr)};
+        cuuint32_t box[4] = {BKB, 128, 1, 1}, es[4] = {1, 1, 1, 1};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return TUCKER_ERR_CUDA;
