@@ -400,21 +400,30 @@ def run_fused(T, n: int, rr: int, stream) -> dict:
         ev[1 + m].record(stream)
     torch.cuda.synchronize()
     gram_ms = [ev[m].elapsed_time(ev[m + 1]) for m in range(3)]
+    T.profile_read()
+    T.profile_enable(True)
     ev[4].record(stream)
     res = T.hosvd_fused(grid, kern, ranks, ws, stream)
     err = T.error_fused(grid, kern, ranks, res.U, res.core, ws, stream)
     ev[5].record(stream)
     torch.cuda.synchronize()
+    T.profile_enable(False)
+    prof = {k: v[0] for k, v in T.profile_read().items() if v[1]}
     ms = ev[4].elapsed_time(ev[5])
     flops = N * (n + 1)
     ach = [flops / (g * 1e-3) / 1e12 for g in gram_ms]
     e = err.cpu().tolist()
+    i8 = "i8_gemm" in prof
     return {"workload": f"cfg5f_{n}cube_matern_nu1.5_ell0.2_fused", "grid": [n, n, n], "ranks": list(ranks),
             "value": N / (ms * 1e-3), "unit": UNIT, "ms": ms, "F_bytes_never_stored": 8 * N,
-            "gram_ms": gram_ms, "gram_tflops": ach, "gram_frac": [a / FP64_PEAK_SPEC_TFLOPS for a in ach],
+            "gram_engine": "int8 emulation (F generated in ~1 GiB plane chunks, residues streamed)" if i8 else "dmma",
+            "stages_ms": prof,
+            "gram_ms_separate_calls": gram_ms, "fp64_equivalent_gram_tflops": ach,
+            "gram_frac_of_fp64_peak": [a / FP64_PEAK_SPEC_TFLOPS for a in ach],
             "E": e[0], "normF": e[1], "eig_info": res.info, "rc": res.rc,
-            "timed": "one hosvd_fused + error_fused call (CUDA events), after a warm-up Gram; gram_ms from "
-                     "three separate tucker_gram_fused calls"}
+            "timed": "one hosvd_fused + error_fused call (CUDA events; stages from the library's stage timer), "
+                     "after a warm-up Gram; gram_ms from three separate tucker_gram_fused calls (each INT8 call "
+                     "includes its own row-maxima generation pass)"}
 
 
 def run_f4(T, grid, ranks, F, ws, stream) -> dict:

@@ -146,7 +146,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         return TUCKER_OK;
     };
     if (L.i8_bytes) {
-        // INT8-emulated Grams: one pipeline, the residues of mode m+1 overlap mode m's GEMM + eig
+        // INT8-emulated Grams (row maxima once per F), each followed by its eigensolve
         TK_RC(launch_gram_i8_modes(g->n, F, G, at(ws, L.i8), L.i8_bytes, st, eig_mode));
     } else {
         for (int m = 0; m < 3; ++m) {
@@ -173,9 +173,11 @@ int64_t fused_slab_chunk(const int64_t n[3]) {
 // Fused workspace: [nodes x^2][K_nu table][G][scratch]; scratch = max(fused Gram ring + partials
 // + barrier, eigensolver, chunk + core, chunk + error).
 struct FusedLayout {
-    size_t nodes, cheb, G, scratch, total, scratch_bytes;
+    size_t nodes, cheb, G, i8, i8_bytes, scratch, total, scratch_bytes;
     int64_t pc_slab;
 };
+
+bool fused_use_i8(const int64_t n[3]) { return gram_use_i8(n) && gram_i8_fused_supported(n); }
 
 FusedLayout plan_fused(const tucker_grid* g, const int32_t* rin) {
     int32_t r[3];
@@ -190,11 +192,18 @@ FusedLayout plan_fused(const tucker_grid* g, const int32_t* rin) {
     L.G = off;
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
     off += align_up((size_t)nmax * nmax * 8, 1024);
+    // INT8 Gram (F never stored): residues, chunk buffer, row maxima; its own region (the row
+    // maxima live across the three modes and their eigensolves)
+    L.i8 = off;
+    L.i8_bytes = fused_use_i8(n) ? align_up(gram_i8_fused_ws_bytes(n), 1024) : 0;
+    off += L.i8_bytes;
     L.scratch = off;
     size_t s = 0;
     for (int m = 0; m < 3; ++m) {
-        const FusedGramPlan fp = fused_gram_plan(n, m);
-        s = std::max(s, 2 * align_up(fp.slot_elems * 8, 1024) + align_up(fp.part_bytes, 256) + 256);
+        if (!L.i8_bytes) {
+            const FusedGramPlan fp = fused_gram_plan(n, m);
+            s = std::max(s, 2 * align_up(fp.slot_elems * 8, 1024) + align_up(fp.part_bytes, 256) + 256);
+        }
         s = std::max(s, eig_ws_bytes(n[m], r[m]));
     }
     L.pc_slab = fused_slab_chunk(n);
@@ -401,6 +410,12 @@ int tucker_gram_fused(const tucker_grid* grid, const tucker_kernel* kernel, int3
     const KParams kp = fused_kparams(grid, kernel);
     TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
                            reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    if (L.i8_bytes) {
+        const I8Gen gen{kp, reinterpret_cast<const double*>(at(ws, L.cheb)),
+                        reinterpret_cast<const double*>(at(ws, L.nodes))};
+        return launch_gram_i8_fused_modes(grid->n, gen, G, at(ws, L.i8), L.i8_bytes, st, mode, mode,
+                                          [](int) { return (int)TUCKER_OK; });
+    }
     return fused_gram_into(grid, mode, kp, L, ws, G, st);
 }
 
@@ -424,11 +439,21 @@ int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* kernel, con
     double* G = reinterpret_cast<double*>(at(ws, L.G));
     void* scr = at(ws, L.scratch);
     int worst = TUCKER_OK;
-    for (int m = 0; m < 3; ++m) {
-        TK_RC(fused_gram_into(grid, m, kp, L, ws, G, st));
+    auto eig_mode = [&](int m) -> int {
         const int rc = launch_eig(grid->n[m], G, r[m], U[m], nullptr, S[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
+        return TUCKER_OK;
+    };
+    if (L.i8_bytes) {
+        const I8Gen gen{kp, reinterpret_cast<const double*>(at(ws, L.cheb)),
+                        reinterpret_cast<const double*>(at(ws, L.nodes))};
+        TK_RC(launch_gram_i8_fused_modes(grid->n, gen, G, at(ws, L.i8), L.i8_bytes, st, 0, 2, eig_mode));
+    } else {
+        for (int m = 0; m < 3; ++m) {
+            TK_RC(fused_gram_into(grid, m, kp, L, ws, G, st));
+            TK_RC(eig_mode(m));
+        }
     }
     const FusedGen gen = fused_gen(grid, kp, L, ws);
     TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st));

@@ -24,6 +24,7 @@
 // tile); its int32 accumulator is written to a partials buffer ([col][row], coalesced) that
 // k_i8_reduce folds.
 #include "common.cuh"
+#include "fill_eval.cuh"
 #include "kernels.h"
 #include "prof.h"
 
@@ -83,9 +84,10 @@ inline int scale_bits(int64_t K) {
 constexpr int RM_KB = 1024;
 __global__ void __launch_bounds__(256) k_i8_rowmax(const double* __restrict__ F, int64_t n1, int64_t n2, int64_t n3,
                                                    uint32_t* __restrict__ mx0, uint32_t* __restrict__ mx1,
-                                                   uint32_t* __restrict__ mx2) {
+                                                   uint32_t* __restrict__ mx2, int64_t jblk) {
     __shared__ uint32_t s_line[8][33];
     const int64_t i = blockIdx.x;
+    const int64_t jlo = (int64_t)blockIdx.y * jblk, jhi = min(n2, jlo + jblk);  // this CTA's lines of plane i
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint32_t pmax = 0;
     for (int64_t kb = 0; kb < n3; kb += RM_KB) {
@@ -93,8 +95,8 @@ __global__ void __launch_bounds__(256) k_i8_rowmax(const double* __restrict__ F,
         bool kin[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) kin[e] = kb + tid + 256 * e < n3;
-        for (int64_t j0 = 0; j0 < n2; j0 += 32) {
-            const int nl = (int)min((int64_t)32, n2 - j0);
+        for (int64_t j0 = jlo; j0 < jhi; j0 += 32) {
+            const int nl = (int)min((int64_t)32, jhi - j0);
             const uint32_t* hw = reinterpret_cast<const uint32_t*>(F + (i * n2 + j0) * n3 + kb + tid) + 1;
 #pragma unroll 1
             for (int g8 = 0; g8 < 4; ++g8) {  // 8 lines at a time
@@ -175,6 +177,7 @@ struct ResArgs {
     const uint32_t* mx;                // row maxima (high words of |F|) of this mode
     int b;
     int8_t* R;                         // [NMOD][K-block][rows][128]
+    int64_t kout;                      // first residue column written by this launch (multiple of 128)
 };
 
 __host__ __device__ constexpr int balanced(int r, int p) { return r > p / 2 ? r - p : r; }
@@ -312,7 +315,7 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
             u[e >> 1][2].x = f2;
         }
     }
-    int8_t* out = a.R + ((kb / RT_K) * a.rows + row) * RT_K + q * 16;
+    int8_t* out = a.R + (((kb + a.kout) / RT_K) * a.rows + row) * RT_K + q * 16;
     store_all_residues(u, out, (size_t)a.rows * a.ldr, std::make_integer_sequence<int, NMOD>{});
 }
 
@@ -741,12 +744,13 @@ inline size_t residue_cap() {
     return v > 0 ? (size_t)v << 20 : (size_t)8 << 30;
 }
 
-ModePlan mode_plan(const int64_t n[3], int mode) {
+// align: super-chunks hold a multiple of `align` columns (the fused path: whole planes of F).
+ModePlan mode_plan(const int64_t n[3], int mode, int64_t align = KCH) {
     ModePlan p{};
     p.rows = n[mode];
     p.Kfull = n[0] * n[1] * n[2] / n[mode];
     int64_t ksc = (int64_t)(residue_cap() / ((size_t)NMOD * p.rows));
-    ksc = std::max<int64_t>(KCH, ksc / KCH * KCH);
+    ksc = std::max<int64_t>(align, ksc / align * align);
     p.Ksc = std::min(ksc, p.Kfull);
     p.nsuper = ceil_div(p.Kfull, p.Ksc);
     p.ldr = ceil_div(p.Ksc, (int64_t)BKB) * BKB;
@@ -759,10 +763,10 @@ struct WsPlan {
     size_t off_mx, off_R, off_P, off_Racc, off_utab, total;
 };
 
-WsPlan ws_plan(const int64_t n[3]) {
+WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     size_t rb = 0, pb = 0, ab = 0, ub = 0;
     for (int m = 0; m < 3; ++m) {
-        const ModePlan p = mode_plan(n, m);
+        const ModePlan p = align ? mode_plan(n, m, align[m]) : mode_plan(n, m);
         rb = std::max(rb, align_up((size_t)NMOD * p.rows * p.ldr, 1024));
         const int64_t nch = ceil_div(p.Ksc, KCH);
         pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 4, 256));
@@ -785,10 +789,11 @@ WsPlan ws_plan(const int64_t n[3]) {
     return w;
 }
 
-// G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.
-int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, char* base, const WsPlan& w,
-              double* G, cudaStream_t st) {
-    const ModePlan p = mode_plan(n, m);
+// G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.  produce(k0, Kc, R)
+// enqueues the residues of unfolding columns [k0, k0 + Kc) into R (K-block-major, column 0 = k0).
+template <class Produce>
+int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
+                   double* G, cudaStream_t st, Produce&& produce) {
     const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
     int32_t* P = reinterpret_cast<int32_t*>(base + w.off_P);
@@ -802,15 +807,7 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
     if (!enc) return TUCKER_ERR_CUDA;
     for (int64_t s = 0; s < p.nsuper; ++s) {
         const int64_t k0 = s * p.Ksc, Kc = std::min(p.Ksc, p.Kfull - k0);
-        {
-            TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
-            ResArgs ra{F, n[0], n[1], n[2], m, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R};
-            const int64_t ntx = ceil_div(Kc, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
-            k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
-            TK_CHECK_LAUNCH();
-        }
-        // residues [NMOD][K-block][rows][128 B]: 4-D map (byte, row, K-block, modulus); a box of
-        // 128 rows x 128 bytes is one contiguous 16 KB block
+        TK_RC(produce(k0, Kc, R));
         CUtensorMap map;
         const int64_t nkb = p.ldr / BKB;
         cuuint64_t dims[4] = {(cuuint64_t)BKB, (cuuint64_t)p.rows, (cuuint64_t)nkb, (cuuint64_t)NMOD};
@@ -840,6 +837,21 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
     return TUCKER_OK;
 }
 
+// Materialised F: one residue launch per super-chunk.
+int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, char* base, const WsPlan& w, double* G,
+              cudaStream_t st) {
+    const ModePlan p = mode_plan(n, m);
+    const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
+    return gram_mode_impl(n, m, p, mx, base, w, G, st, [&](int64_t k0, int64_t Kc, int8_t* R) -> int {
+        TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+        ResArgs ra{F, n[0], n[1], n[2], m, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R, 0};
+        const int64_t ntx = ceil_div(Kc, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
+        k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    });
+}
+
 }  // namespace i8
 
 size_t gram_i8_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
@@ -855,7 +867,7 @@ bool gram_i8_supported(const int64_t n[3]) {
 int launch_gram_i8_rowmax(const int64_t n[3], const double* F, uint32_t* mx, cudaStream_t st) {
     TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
     TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 4, st));
-    i8::k_i8_rowmax<<<(unsigned)n[0], 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1]);
+    i8::k_i8_rowmax<<<dim3((unsigned)n[0], 1), 256, 0, st>>>(F, n[0], n[1], n[2], mx, mx + n[0], mx + n[0] + n[1], n[1]);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
@@ -893,6 +905,106 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
         mx = own;
     }
     return gram_mode(n, mode, F, mx, base, w, G, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// a-7 with the INT8 Gram: F is never stored.  Plane chunks of F (~1 GiB; j-planes for mode 0,
+// i-planes for modes 1 and 2, generated by the a-7 chunk generator, bitwise the materialised
+// fill) feed the residue kernel directly; a residue super-chunk holds whole chunks.  The row
+// maxima take one generation pass over i-plane chunks.  The Grams are bitwise those of the
+// materialised INT8 route (same values, exact integer products).
+namespace i8 {
+
+struct FusedI8Plan {
+    int64_t Pc[3], w[3], planes[3], align[3];  // per mode: planes per chunk, columns per plane
+    int pa[3];
+    size_t chunk_bytes;
+    WsPlan ws;
+    size_t off_chunk, total;
+    bool ok;
+};
+
+FusedI8Plan fused_i8_plan(const int64_t n[3]) {
+    FusedI8Plan f{};
+    f.ok = true;
+    const int64_t target = fused_chunk_target((int64_t)1 << 30) / 8;  // doubles per chunk (1 GiB; test knob)
+    for (int m = 0; m < 3; ++m) {
+        f.pa[m] = m == 0 ? 1 : 0;
+        f.w[m] = m == 2 ? n[1] : n[2];
+        f.planes[m] = m == 0 ? n[1] : n[0];
+        const int64_t plane_elems = m == 0 ? n[0] * n[2] : n[1] * n[2];
+        const int64_t q = 128 / std::__gcd<int64_t>(f.w[m], 128);  // planes per 128-column multiple
+        int64_t pc = std::max<int64_t>(1, target / plane_elems) / q * q;
+        if (pc == 0 || pc >= f.planes[m]) pc = f.planes[m];  // one chunk per mode
+        f.Pc[m] = pc;
+        f.align[m] = pc * f.w[m];
+        const ModePlan mp = mode_plan(n, m, f.align[m]);
+        // whole chunks per super-chunk; a single chunk per mode must then be the whole K
+        if (pc == f.planes[m] && mp.Ksc < mp.Kfull) f.ok = false;
+        f.chunk_bytes = std::max(f.chunk_bytes, (size_t)pc * plane_elems * 8);
+    }
+    // the row-maxima pass uses the modes' i-plane chunks
+    f.chunk_bytes = std::max(f.chunk_bytes, (size_t)f.Pc[1] * n[1] * n[2] * 8);
+    f.ws = ws_plan(n, f.align);
+    f.off_chunk = align_up(f.ws.total, 1024);
+    f.total = f.off_chunk + align_up(f.chunk_bytes, 1024);
+    return f;
+}
+
+}  // namespace i8
+
+bool gram_i8_fused_supported(const int64_t n[3]) { return gram_i8_supported(n) && i8::fused_i8_plan(n).ok; }
+size_t gram_i8_fused_ws_bytes(const int64_t n[3]) { return i8::fused_i8_plan(n).total; }
+
+int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
+                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode) {
+    using namespace i8;
+    if (!gram_i8_fused_supported(n)) return TUCKER_ERR_UNSUPPORTED;
+    const FusedI8Plan f = fused_i8_plan(n);
+    if (ws_bytes < f.total) return TUCKER_ERR_SIZE;
+    char* base = static_cast<char*>(ws);
+    double* chunk = reinterpret_cast<double*>(base + f.off_chunk);
+    uint32_t* mx = reinterpret_cast<uint32_t*>(base + f.ws.off_mx);
+    const int mirror = (gen.kp.centred && n[2] % 8 == 0) ? 1 : 0;
+    {  // row maxima: one generation pass over i-plane chunks
+        TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
+        TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 4, st));
+        const int64_t pc = f.Pc[1];
+        for (int64_t g0 = 0; g0 < n[0]; g0 += pc) {
+            ChunkGeo geo{0, mirror, n[0], n[1], n[2], g0, pc, n[0]};
+            TK_RC(launch_gen_chunk(geo, gen.kp, gen.cheb, gen.x2, chunk, st));
+            const int64_t valid = std::min(pc, n[0] - g0);
+            // few planes per chunk at large n: split each plane's lines over enough CTAs
+            const int64_t nb = std::min<int64_t>(ceil_div(n[1], 32), std::max<int64_t>(1, ceil_div(4 * kNumSMs, valid)));
+            const int64_t jblk = ceil_div(ceil_div(n[1], nb), 32) * 32;
+            k_i8_rowmax<<<dim3((unsigned)valid, (unsigned)ceil_div(n[1], jblk)), 256, 0, st>>>(
+                chunk, valid, n[1], n[2], mx + g0, mx + n[0], mx + n[0] + n[1], jblk);
+            TK_CHECK_LAUNCH();
+        }
+    }
+    for (int m = m_first; m <= m_last; ++m) {
+        const ModePlan p = mode_plan(n, m, f.align[m]);
+        const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
+        const int64_t w = f.w[m], pc = f.Pc[m];
+        TK_RC(gram_mode_impl(n, m, p, mx, base, f.ws, G, st, [&](int64_t k0, int64_t Kc, int8_t* R) -> int {
+            const int64_t plo = k0 / w, phi = (k0 + Kc) / w;  // whole planes
+            for (int64_t g0 = plo; g0 < phi; g0 += pc) {
+                ChunkGeo geo{f.pa[m], mirror, n[0], n[1], n[2], g0, pc, f.planes[m]};
+                TK_RC(launch_gen_chunk(geo, gen.kp, gen.cheb, gen.x2, chunk, st));
+                const int64_t valid = std::min(pc, phi - g0);
+                TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+                // the chunk as a small tensor: mode 0 [n1][pc][n3]; modes 1, 2 [pc][n2][n3]
+                const int64_t c1 = m == 0 ? n[0] : pc, c2 = m == 0 ? pc : n[1];
+                ResArgs ra{chunk, c1, c2, n[2], m, p.rows, p.Kfull, 0, valid * w, p.ldr, mxm, p.b, R, (g0 - plo) * w};
+                const int64_t ntx = ceil_div(valid * w, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
+                k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
+                TK_CHECK_LAUNCH();
+            }
+            return TUCKER_OK;
+        }));
+        TK_RC(after_mode(m));
+    }
+    return TUCKER_OK;
 }
 
 // ------------------------------------------------------------------------------------------

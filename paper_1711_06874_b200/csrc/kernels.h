@@ -53,6 +53,16 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
 // disjoint from anything after_mode uses.
 int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* ws, size_t ws_bytes, cudaStream_t st,
                          const std::function<int(int)>& after_mode);
+// a-7 with the INT8 Gram (F never stored): generator of the plane chunks.
+struct I8Gen {
+    KParams kp;
+    const double* cheb;
+    const double* x2;
+};
+bool gram_i8_fused_supported(const int64_t n[3]);
+size_t gram_i8_fused_ws_bytes(const int64_t n[3]);
+int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
+                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
 bool gram_use_i8(const int64_t n[3]);

@@ -130,3 +130,23 @@ def test_int8_route_lowers_the_noise_floor(T):
         finally:
             T.set_gram_engine(T.GRAM_AUTO)
     assert 2 * E[T.GRAM_INT8] < E[T.GRAM_DMMA], E
+
+
+@pytest.mark.parametrize("g,k,kb,mb", [
+    (GridSpec.cube(128, 1.0), KernelSpec.matern(1.5, 0.2), None, None),
+    (GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)), KernelSpec.matern(0.7, 0.5), 256, None),
+    (GridSpec((144, 136, 130), (-0.5, -2.0, 0.1), (1.5, 1.0, 0.9)), KernelSpec.matern(1.5, 0.2), 300, 1),
+    (GridSpec((130, 129, 136), (-1.0,) * 3, (1.0,) * 3), KernelSpec.slater(1.0, 1.0), 200, 2)])
+def test_gram_i8_fused_bitwise_equals_materialised(T, monkeypatch, g, k, kb, mb):
+    """a-7 through the INT8 Gram: F generated in plane chunks (test knob: chunk KB, residue MB) never
+    stored; the residues are of bitwise the same values and the integer products are exact, so the
+    fused Gram equals the materialised INT8 Gram bit for bit."""
+    if kb:
+        monkeypatch.setenv("TUCKER_FUSED_CHUNK_KB", str(kb))
+    if mb:
+        monkeypatch.setenv("TUCKER_I8_RESIDUE_MB", str(mb))
+    F = T.fill(g, k)
+    ws = T.workspace_i8(g)
+    wsf = T.workspace_fused(g)
+    for m in range(3):
+        assert torch.equal(T.gram_fused(g, k, m, wsf), T.gram_i8(g, m, F, ws)), m
