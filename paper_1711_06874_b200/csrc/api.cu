@@ -525,14 +525,21 @@ int tucker_hosvd_sym(const tucker_grid* grid, const tucker_kernel* kernel, const
 // NEXT f2 layout: [G][V (n_max x p)][scratch]
 static int accurate_p(int64_t n, int r) { return (int)std::min<int64_t>(n, std::min(r + 8, 56)); }
 
-static size_t accurate_plan(const tucker_grid* g, const int32_t* r, size_t* offV, size_t* offS) {
+// [G][V, its Gram eigenvalues][INT8 Gram region (if that engine is in effect)][scratch]
+static size_t accurate_plan(const tucker_grid* g, const int32_t* r, size_t* offV, size_t* offS, size_t* offI8 = nullptr,
+                            size_t* i8_bytes = nullptr) {
     const int64_t* n = g->n;
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
     size_t off = align_up((size_t)nmax * nmax * 8, 256);
     *offV = off;
-    off += align_up((size_t)nmax * 64 * 8, 256) + 64 * 8;  // V, then its Gram eigenvalues
+    off += align_up((size_t)nmax * 64 * 8, 256) + 64 * 8;
+    off = align_up(off, 1024);
+    const size_t ib = gram_use_i8(n) ? align_up(gram_i8_ws_bytes(n), 1024) : 0;
+    if (offI8) *offI8 = off;
+    if (i8_bytes) *i8_bytes = ib;
+    off += ib;
     *offS = off;
-    size_t s = gram_ws_bytes(n);
+    size_t s = ib ? 0 : gram_ws_bytes(n);
     int pmax = 1;
     for (int a = 0; a < 3; ++a) {
         const int p = accurate_p(n[a], r[a]);
@@ -560,8 +567,8 @@ int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3], const dou
         return TUCKER_ERR_INVALID_ARG;
     for (int a = 0; a < 3; ++a)
         if (r[a] > 56 || grid->n[a] > 2048) return TUCKER_ERR_UNSUPPORTED;
-    size_t offV, offS;
-    const size_t total = accurate_plan(grid, r, &offV, &offS);
+    size_t offV, offS, offI8, i8_bytes;
+    const size_t total = accurate_plan(grid, r, &offV, &offS, &offI8, &i8_bytes);
     if (ws_bytes < total) return TUCKER_ERR_SIZE;
     if (info) std::memset(info, 0, sizeof(*info));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -574,13 +581,20 @@ int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3], const dou
     double* const U[3] = {U1, U2, U3};
     double* const S[3] = {sigma1, sigma2, sigma3};
     int worst = TUCKER_OK;
-    for (int m = 0; m < 3; ++m) {
+    auto after = [&](int m) -> int {  // Gram route's subspace, then the Rayleigh-Ritz steps on F_(m)
         const int p = accurate_p(grid->n[m], r[m]);
-        TK_RC(launch_gram(grid->n, m, F, G, scr, sb, st));
         const int rc = launch_eig(grid->n[m], G, p, V, lam, nullptr, scr, sb, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
-        TK_RC(launch_refine_mode(grid->n, m, F, V, lam, p, r[m], iters, U[m], S[m], scr, sb, st, nullptr));
+        return launch_refine_mode(grid->n, m, F, V, lam, p, r[m], iters, U[m], S[m], scr, sb, st, nullptr);
+    };
+    if (i8_bytes) {
+        TK_RC(launch_gram_i8_modes(grid->n, F, G, at(ws, offI8), i8_bytes, st, after));
+    } else {
+        for (int m = 0; m < 3; ++m) {
+            TK_RC(launch_gram(grid->n, m, F, G, scr, sb, st));
+            TK_RC(after(m));
+        }
     }
     TK_RC(launch_ttm_core(grid->n, r, F, U1, U2, U3, core, scr, sb, st));
     return worst;
