@@ -95,7 +95,7 @@ int check_ranks(const tucker_grid* g, const int32_t* r) {
 //   sigma1..3 err3]
 struct Layout {
     size_t nodes, cheb, G, i8, i8_bytes, scratch, outs, total;
-    size_t scratch_bytes;
+    size_t scratch_bytes, g_bytes;
 };
 
 Layout plan(const tucker_grid* g, const int32_t* rin) {
@@ -110,7 +110,8 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     off += align_up((size_t)kChebIntervals * kChebN * 8, 256);
     L.G = off;
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
-    off += align_up((size_t)nmax * nmax * 8, 256);
+    L.g_bytes = align_up((size_t)nmax * nmax * 8, 256);
+    off += (gram_use_i8(n) ? 3 : 1) * L.g_bytes;  // INT8 route: one G per mode (eigensolves overlap)
     L.i8 = off;
     L.i8_bytes = gram_use_i8(n) ? align_up(gram_i8_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
     off += L.i8_bytes;
@@ -146,8 +147,40 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         return TUCKER_OK;
     };
     if (L.i8_bytes) {
-        // INT8-emulated Grams (row maxima once per F), each followed by its eigensolve
-        TK_RC(launch_gram_i8_modes(g->n, F, G, at(ws, L.i8), L.i8_bytes, st, eig_mode));
+        // INT8-emulated Grams (row maxima once per F).  The eigensolve of mode m runs on a side stream
+        // while the Gram of mode m+1 runs on `st` (its own G buffer; the eigensolver is latency-bound
+        // on one cluster, the Gram kernels are throughput-bound) — joined before the core.
+        cudaStream_t side = side_stream();
+        if (!side) return TUCKER_ERR_CUDA;
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        auto cleanup = [&]() {
+            for (cudaEvent_t e : ev)
+                if (e) cudaEventDestroy(e);
+        };
+        for (int i = 0; i < 4; ++i)
+            if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
+                cleanup();
+                return TUCKER_ERR_CUDA;
+            }
+        double* Gm[3] = {G, reinterpret_cast<double*>(at(ws, L.G + L.g_bytes)),
+                         reinterpret_cast<double*>(at(ws, L.G + 2 * L.g_bytes))};
+        auto eig_side = [&](int m) -> int {
+            if (cudaStreamWaitEvent(side, ev[m], 0) != cudaSuccess) return TUCKER_ERR_CUDA;
+            const int rc = launch_eig(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, side, info, m);
+            if (rc == TUCKER_ERR_NOCONV) worst = rc;
+            else if (rc != TUCKER_OK) return rc;
+            return TUCKER_OK;
+        };
+        int rc = launch_gram_i8_modes_into(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, [&](int m) -> int {
+            if (cudaEventRecord(ev[m], st) != cudaSuccess) return TUCKER_ERR_CUDA;
+            return m > 0 ? eig_side(m - 1) : TUCKER_OK;  // host waits in eig(m-1) while Gram(m) runs
+        });
+        if (rc == TUCKER_OK) rc = eig_side(2);
+        if (rc == TUCKER_OK && (cudaEventRecord(ev[3], side) != cudaSuccess ||
+                                cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess))
+            rc = TUCKER_ERR_CUDA;
+        cleanup();
+        TK_RC(rc);
     } else {
         for (int m = 0; m < 3; ++m) {
             TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));

@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <functional>
+#include <mutex>
 #include <utility>
 
 namespace tk {
@@ -887,6 +888,33 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
         TK_RC(after_mode(m));
     }
     return TUCKER_OK;
+}
+
+// Same, mode m into G[m] (three buffers); after_mode(m) is called once G_m is enqueued.
+int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
+                              cudaStream_t st, const std::function<int(int)>& after_mode) {
+    using namespace i8;
+    if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
+    const WsPlan w = ws_plan(n);
+    if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
+    char* base = static_cast<char*>(ws);
+    uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
+    TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    for (int m = 0; m < 3; ++m) {
+        TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
+        TK_RC(after_mode(m));
+    }
+    return TUCKER_OK;
+}
+
+cudaStream_t side_stream() {
+    static cudaStream_t s[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) s[dev] = nullptr;
+    return s[dev];
 }
 
 // G (n_m x n_m, both triangles) of one mode.  mx: row maxima (nullptr: computed into ws).
