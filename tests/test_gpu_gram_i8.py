@@ -150,3 +150,38 @@ def test_gram_i8_fused_bitwise_equals_materialised(T, monkeypatch, g, k, kb, mb)
     wsf = T.workspace_fused(g)
     for m in range(3):
         assert torch.equal(T.gram_fused(g, k, m, wsf), T.gram_i8(g, m, F, ws)), m
+
+
+def test_stage_profiler_and_engine_switch(T):
+    """tucker_profile_*: per-stage event times on the launching stream; the engine switch routes
+    tucker_hosvd through the INT8 Gram (AUTO) or the DMMA Gram, with matching results."""
+    g, k, rr = GridSpec.cube(256, 1.0), KernelSpec.matern(1.5, 0.2), (16, 16, 16)
+    F = T.fill(g, k)
+    T.profile_read()
+    T.profile_enable(True)
+    try:
+        a = T.hosvd(g, rr, F)
+        torch.cuda.synchronize()
+    finally:
+        T.profile_enable(False)
+    p = T.profile_read()
+    assert p["i8_gemm"][1] == 3 and p["i8_residues"][1] >= 3 and p["i8_rowmax"][1] == 1 and p["eig"][1] == 3
+    assert p["dmma_gram"][1] == 0 and all(v[0] >= 0.0 for v in p.values())
+    assert p["i8_gemm"][0] > 0.0
+    assert T.profile_read()["i8_gemm"] == (0.0, 0)  # cleared; disabled: nothing recorded
+    T.hosvd(g, rr, F)
+    assert T.profile_read()["i8_gemm"] == (0.0, 0)
+    T.set_gram_engine(T.GRAM_DMMA)
+    try:
+        T.profile_enable(True)
+        b = T.hosvd(g, rr, F)
+        torch.cuda.synchronize()
+        T.profile_enable(False)
+        q = T.profile_read()
+    finally:
+        T.profile_enable(False)
+        T.set_gram_engine(T.GRAM_AUTO)
+    assert q["dmma_gram"][1] == 3 and q["i8_gemm"][1] == 0
+    for m in range(3):
+        la, lb = a.sigma[m] ** 2, b.sigma[m] ** 2
+        assert float(torch.max(torch.abs(la - lb) / la[0])) <= 1e-12
