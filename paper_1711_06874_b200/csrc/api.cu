@@ -94,7 +94,7 @@ int check_ranks(const tucker_grid* g, const int32_t* r) {
 //   [scratch = max(gram, eig, ttm, err)] [device outputs of tucker_approximate: U1 U2 U3 core
 //   sigma1..3 err3]
 struct Layout {
-    size_t nodes, cheb, G, i8, i8_bytes, scratch, outs, total;
+    size_t nodes, cheb, G, i8, i8_bytes, eig, eig_bytes, t2, scratch, outs, total;
     size_t scratch_bytes, g_bytes;
 };
 
@@ -112,12 +112,23 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     const int64_t nmax = std::max(n[0], std::max(n[1], n[2]));
     L.g_bytes = align_up((size_t)nmax * nmax * 8, 256);
     off += (gram_use_i8(n) ? 3 : 1) * L.g_bytes;  // INT8 route: one G per mode (eigensolves overlap)
+    const bool i8 = gram_use_i8(n);
     L.i8 = off;
-    L.i8_bytes = gram_use_i8(n) ? align_up(gram_i8_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
+    L.i8_bytes = i8 ? align_up(gram_i8_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
     off += L.i8_bytes;
+    if (i8) {  // the eigensolves run beside the Grams and the core's first two products: own regions
+        size_t e = 0;
+        for (int a = 0; a < 3; ++a) e = std::max(e, eig_ws_bytes(n[a], r[a]));
+        L.eig = off;
+        L.eig_bytes = align_up(e, 256);
+        off += L.eig_bytes;
+        L.t2 = off;
+        off += align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
+    }
     L.scratch = off;
-    size_t s = gram_use_i8(n) ? 0 : gram_ws_bytes(n);
-    for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
+    size_t s = i8 ? 0 : gram_ws_bytes(n);
+    if (!i8)
+        for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
     s = std::max(s, ttm_ws_bytes(n, r));
     s = std::max(s, err_ws_bytes(n, r));
     L.scratch_bytes = align_up(s, 256);
@@ -147,40 +158,56 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         return TUCKER_OK;
     };
     if (L.i8_bytes) {
-        // INT8-emulated Grams (row maxima once per F).  The eigensolve of mode m runs on a side stream
-        // while the Gram of mode m+1 runs on `st` (its own G buffer; the eigensolver is latency-bound
-        // on one cluster, the Gram kernels are throughput-bound) — joined before the core.
+        // INT8-emulated Grams (row maxima once per F), modes in the order 2, 1, 0.  Each eigensolve
+        // runs on a side stream while the next Gram runs on `st` (one G per mode; the eigensolver is
+        // latency-bound on one cluster); the last one (mode 0: U1) runs beside the core's first two
+        // products (which need U2, U3 only); the third product waits for it.
         cudaStream_t side = side_stream();
         if (!side) return TUCKER_ERR_CUDA;
-        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
         auto cleanup = [&]() {
             for (cudaEvent_t e : ev)
                 if (e) cudaEventDestroy(e);
         };
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 5; ++i)
             if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
                 cleanup();
                 return TUCKER_ERR_CUDA;
             }
         double* Gm[3] = {G, reinterpret_cast<double*>(at(ws, L.G + L.g_bytes)),
                          reinterpret_cast<double*>(at(ws, L.G + 2 * L.g_bytes))};
-        auto eig_side = [&](int m) -> int {
+        void* escr = at(ws, L.eig);
+        double* T2 = reinterpret_cast<double*>(at(ws, L.t2));
+        auto eig_side = [&](int m) -> int {  // host waits here while `st` keeps running
             if (cudaStreamWaitEvent(side, ev[m], 0) != cudaSuccess) return TUCKER_ERR_CUDA;
-            const int rc = launch_eig(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, side, info, m);
+            const int rc = launch_eig(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr, L.eig_bytes, side, info, m);
             if (rc == TUCKER_ERR_NOCONV) worst = rc;
             else if (rc != TUCKER_OK) return rc;
             return TUCKER_OK;
         };
-        int rc = launch_gram_i8_modes_into(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, [&](int m) -> int {
-            if (cudaEventRecord(ev[m], st) != cudaSuccess) return TUCKER_ERR_CUDA;
-            return m > 0 ? eig_side(m - 1) : TUCKER_OK;  // host waits in eig(m-1) while Gram(m) runs
+        const int order[3] = {2, 1, 0};
+        int rc = launch_gram_i8_modes_into(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, order, [&](int idx) -> int {
+            if (cudaEventRecord(ev[order[idx]], st) != cudaSuccess) return TUCKER_ERR_CUDA;
+            return idx > 0 ? eig_side(order[idx - 1]) : TUCKER_OK;
         });
-        if (rc == TUCKER_OK) rc = eig_side(2);
+        // U2, U3 ready on `side` -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve
         if (rc == TUCKER_OK && (cudaEventRecord(ev[3], side) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
+        if (rc == TUCKER_OK)
+            rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
+                                      nullptr, T2);
+        if (rc == TUCKER_OK) rc = eig_side(0);
+        if (rc == TUCKER_OK && (cudaEventRecord(ev[4], side) != cudaSuccess ||
+                                cudaStreamWaitEvent(st, ev[4], 0) != cudaSuccess))
+            rc = TUCKER_ERR_CUDA;
         cleanup();
         TK_RC(rc);
+        // TTM3: core (r1 x r2 r3) = U1^T (r1 x n1) * T2 (n1 x r2 r3)
+        SmallGemm g3{r[0], (int64_t)r[1] * r[2], g->n[0], 1, U[0], 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
+                     (int64_t)r[1] * r[2], 1, 0};
+        TK_RC(launch_small_gemm(g3, st));
+        return worst;
     } else {
         for (int m = 0; m < 3; ++m) {
             TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));

@@ -890,9 +890,10 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
     return TUCKER_OK;
 }
 
-// Same, mode m into G[m] (three buffers); after_mode(m) is called once G_m is enqueued.
+// Same, modes in `order`, mode m into G[m] (three buffers); after_mode(idx) is called once the
+// Gram of mode order[idx] is enqueued.
 int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                              cudaStream_t st, const std::function<int(int)>& after_mode) {
+                              cudaStream_t st, const int order[3], const std::function<int(int)>& after_mode) {
     using namespace i8;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const WsPlan w = ws_plan(n);
@@ -900,9 +901,10 @@ int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
-    for (int m = 0; m < 3; ++m) {
+    for (int idx = 0; idx < 3; ++idx) {
+        const int m = order[idx];
         TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
-        TK_RC(after_mode(m));
+        TK_RC(after_mode(idx));
     }
     return TUCKER_OK;
 }

@@ -377,7 +377,6 @@ size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]) {
 
 int launch_ttm_core(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                     const double* U3, double* core, void* ws, size_t ws_bytes, cudaStream_t st) {
-    TK_PROF(TUCKER_PROF_TTM, st);
     return launch_ttm_core_impl(n, r, F, nullptr, U1, U2, U3, core, ws, ws_bytes, st);
 }
 
@@ -391,6 +390,7 @@ int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, co
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
                          size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out) {
+    TK_PROF(TUCKER_PROF_TTM, st);
     const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
     if (ws_bytes < ttm_ws_bytes(n, r) + chunk_b) return TUCKER_ERR_SIZE;
     if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
