@@ -114,7 +114,7 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     off += (gram_use_i8(n) ? 3 : 1) * L.g_bytes;  // INT8 route: one G per mode (eigensolves overlap)
     const bool i8 = gram_use_i8(n);
     L.i8 = off;
-    L.i8_bytes = i8 ? align_up(gram_i8_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
+    L.i8_bytes = i8 ? align_up(gram_i8_hosvd_ws_bytes(n), 1024) : 0;  // INT8 Gram pipeline (own region)
     off += L.i8_bytes;
     if (i8) {  // the eigensolves run beside the Grams and the core's first two products: own regions
         size_t e = 0;
@@ -185,10 +185,16 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
             else if (rc != TUCKER_OK) return rc;
             return TUCKER_OK;
         };
-        const int order[3] = {2, 1, 0};
-        int rc = launch_gram_i8_modes_into(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, order, [&](int idx) -> int {
-            if (cudaEventRecord(ev[order[idx]], st) != cudaSuccess) return TUCKER_ERR_CUDA;
-            return idx > 0 ? eig_side(order[idx - 1]) : TUCKER_OK;
+        int pend[3], npend = 0;  // Grams enqueued, eigensolves not yet issued
+        int rc = launch_gram_i8_hosvd(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, [&](const int* ms, int cnt) -> int {
+            for (int i = 0; i < cnt; ++i)
+                if (cudaEventRecord(ev[ms[i]], st) != cudaSuccess) return TUCKER_ERR_CUDA;
+            // the previous phase's modes: eigensolve now, beside this phase's Grams
+            for (int i = 0; i < npend; ++i)
+                if (pend[i] != 0) TK_RC(eig_side(pend[i]));
+            npend = 0;
+            for (int i = 0; i < cnt; ++i) pend[npend++] = ms[i];
+            return TUCKER_OK;
         });
         // U2, U3 ready on `side` -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve
         if (rc == TUCKER_OK && (cudaEventRecord(ev[3], side) != cudaSuccess ||

@@ -217,6 +217,49 @@ __device__ __forceinline__ void store_all_residues(const float2 (&u)[8][3], int8
     (store_residues<L>(u, out + L * lstride), ...);
 }
 
+// Scale (2^sh as one or two exact factors) of a row with high-word maximum hw.
+__device__ __forceinline__ void row_scale(uint32_t hw, int b, double& sa, double& sb) {
+    const int sh = b - row_exponent(hw);  // |a_ik| 2^sh < 2^b
+    if (sh >= -1022 && sh <= 1023) {
+        sa = pow2d(sh);
+        sb = 1.0;
+    } else {  // beyond the double exponent range: two exact steps
+        sa = pow2d(sh / 2);
+        sb = pow2d(sh - sh / 2);
+    }
+}
+
+// Residues of the 16 values v[e * stride] (one row, 16 consecutive unfolding columns) -> one
+// 16-byte store per modulus at out + l * lstride.
+template <int STRIDE>
+__device__ __forceinline__ void residues16(const double* v, double sa, double sb, int8_t* out, size_t lstride) {
+    float2 u[8][3];
+    constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        // y = 2^52 + w, w = rint(a 2^sh) + B in [0, 2^52): one rounding (the scaling is exact)
+        const double x = v[e * STRIDE];
+        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
+        const uint32_t lo = (uint32_t)__double2loint(y);
+        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+        // balanced 17-bit digits: x = rint(a 2^sh) = (d0 - 2^16) + (d1 - 2^16) 2^17 + (d2 - 2^16) 2^34
+        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
+        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        if (e & 1) {
+            u[e >> 1][0].y = f0;
+            u[e >> 1][1].y = f1;
+            u[e >> 1][2].y = f2;
+        } else {
+            u[e >> 1][0].x = f0;
+            u[e >> 1][1].x = f1;
+            u[e >> 1][2].x = f2;
+        }
+    }
+    store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+}
+
 // One 32-row x 128-column tile (row block by, column block bx of the super-chunk).
 __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64_t by,
                                              double (&tile)[RT_ROWS][RT_K / 16][17], double* s1, double* s2) {
@@ -225,15 +268,10 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     const int64_t kb = bx * RT_K;  // within the super-chunk
     if (tid < RT_ROWS) {
         const int64_t row = row0 + tid;
-        const int E = row < a.rows ? row_exponent(a.mx[row]) : 0;
-        const int sh = a.b - E;  // |a_ik| 2^sh < 2^b
-        if (sh >= -1022 && sh <= 1023) {
-            s1[tid] = pow2d(sh);
-            s2[tid] = 1.0;
-        } else {  // beyond the double exponent range: two exact steps
-            s1[tid] = pow2d(sh / 2);
-            s2[tid] = pow2d(sh - sh / 2);
-        }
+        double sa, sb;
+        row_scale(row < a.rows ? a.mx[row] : 0u, a.b, sa, sb);
+        s1[tid] = sa;
+        s2[tid] = sb;
     }
     // gather the 32 x 128 tile, coalesced along the unit-stride axis of F; all 16 addresses of a
     // thread are formed before the loads so they issue back to back
@@ -291,33 +329,8 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     const int rr = tid >> 3, q = tid & 7;
     const int64_t row = row0 + rr;
     if (row >= a.rows) return;  // (the caller syncs before the tile is reused); columns >= Kc: residue 0
-    float2 u[8][3];
-    const double sa = s1[rr], sb = s2[rr];
-    constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        // y = 2^52 + w, w = rint(a 2^sh) + B in [0, 2^52): one rounding (the scaling is exact)
-        const double v = tile[rr][q][e];
-        const double y = (sb == 1.0) ? fma(v, sa, M2) : fma(v * sa, sb, M2);
-        const uint32_t lo = (uint32_t)__double2loint(y);
-        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
-        // balanced 17-bit digits: x = rint(a 2^sh) = (d0 - 2^16) + (d1 - 2^16) 2^17 + (d2 - 2^16) 2^34
-        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
-        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
-        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
-        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
-        if (e & 1) {
-            u[e >> 1][0].y = f0;
-            u[e >> 1][1].y = f1;
-            u[e >> 1][2].y = f2;
-        } else {
-            u[e >> 1][0].x = f0;
-            u[e >> 1][1].x = f1;
-            u[e >> 1][2].x = f2;
-        }
-    }
     int8_t* out = a.R + (((kb + a.kout) / RT_K) * a.rows + row) * RT_K + q * 16;
-    store_all_residues(u, out, (size_t)a.rows * a.ldr, std::make_integer_sequence<int, NMOD>{});
+    residues16<1>(&tile[rr][q][0], s1[rr], s2[rr], out, (size_t)a.rows * a.ldr);
 }
 
 // One CTA per tile (the loop also serves smaller grids).
@@ -764,16 +777,17 @@ struct WsPlan {
     size_t off_mx, off_R, off_P, off_Racc, off_utab, total;
 };
 
+// align: per-mode super-chunk alignment (the fused path).
 WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     size_t rb = 0, pb = 0, ab = 0, ub = 0;
-    for (int m = 0; m < 3; ++m) {
-        const ModePlan p = align ? mode_plan(n, m, align[m]) : mode_plan(n, m);
+    auto add = [&](const ModePlan& p) {
         rb = std::max(rb, align_up((size_t)NMOD * p.rows * p.ldr, 1024));
         const int64_t nch = ceil_div(p.Ksc, KCH);
         pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 4, 256));
         ab = std::max(ab, align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256));
         ub = std::max(ub, align_up((size_t)p.ntiles * sizeof(int2), 256));
-    }
+    };
+    for (int m = 0; m < 3; ++m) add(align ? mode_plan(n, m, align[m]) : mode_plan(n, m));
     WsPlan w{};
     size_t off = 0;
     w.off_mx = off;
@@ -790,25 +804,34 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     return w;
 }
 
-// G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.  produce(k0, Kc, R)
-// enqueues the residues of unfolding columns [k0, k0 + Kc) into R (K-block-major, column 0 = k0).
-template <class Produce>
-int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
-                   double* G, cudaStream_t st, Produce&& produce) {
-    const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
-    int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
-    int32_t* P = reinterpret_cast<int32_t*>(base + w.off_P);
-    int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
-    int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
-    TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
-    const int nug = build_units((int)p.rows, p.nJ, p.ntiles, nullptr);
-    k_i8_units<<<1, 1, 0, st>>>((int)p.rows, p.nJ, p.ntiles, utab);
-    TK_CHECK_LAUNCH();
-    PFN_tmapEncodeTiled enc = tmap_encoder();
-    if (!enc) return TUCKER_ERR_CUDA;
-    for (int64_t s = 0; s < p.nsuper; ++s) {
-        const int64_t k0 = s * p.Ksc, Kc = std::min(p.Ksc, p.Kfull - k0);
-        TK_RC(produce(k0, Kc, R));
+
+
+// One mode's int8 Grams, driven super-chunk by super-chunk: init() builds the unit table, run()
+// takes the residues of one super-chunk (K-block-major in R) through k_i8_gemm and folds its
+// partials into Racc (mod p), crt() reconstructs G (both triangles).
+struct ModeGemm {
+    const int64_t* n;
+    int m;
+    ModePlan p;
+    const uint32_t* mxm;
+    int8_t* R;
+    int32_t *P, *Racc;
+    int2* utab;
+    int nug;
+    cudaStream_t st;
+
+    int init() {
+        TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+        nug = build_units((int)p.rows, p.nJ, p.ntiles, nullptr);
+        k_i8_units<<<1, 1, 0, st>>>((int)p.rows, p.nJ, p.ntiles, utab);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    }
+    int run(int64_t s, int64_t Kc) {
+        PFN_tmapEncodeTiled enc = tmap_encoder();
+        if (!enc) return TUCKER_ERR_CUDA;
+        // residues [NMOD][K-block][rows][128 B]: 4-D map (byte, row, K-block, modulus); a box of
+        // 128 rows x 128 bytes is one contiguous 16 KB block
         CUtensorMap map;
         const int64_t nkb = p.ldr / BKB;
         cuuint64_t dims[4] = {(cuuint64_t)BKB, (cuuint64_t)p.rows, (cuuint64_t)nkb, (cuuint64_t)NMOD};
@@ -830,12 +853,36 @@ int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t*
         const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
         k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
         TK_CHECK_LAUNCH();
+        return TUCKER_OK;
     }
-    TK_PROF(TUCKER_PROF_I8_CRT, st);
-    const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-    k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
-    TK_CHECK_LAUNCH();
-    return TUCKER_OK;
+    int crt(double* G) {
+        TK_PROF(TUCKER_PROF_I8_CRT, st);
+        const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
+        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    }
+};
+
+inline const uint32_t* mode_max(const uint32_t* mx, const int64_t n[3], int m) {
+    return mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
+}
+
+// G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.  produce(k0, Kc, R)
+// enqueues the residues of unfolding columns [k0, k0 + Kc) into R (K-block-major, column 0 = k0).
+template <class Produce>
+int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
+                   double* G, cudaStream_t st, Produce&& produce) {
+    ModeGemm g{n, m, p, mode_max(mx, n, m), reinterpret_cast<int8_t*>(base + w.off_R),
+               reinterpret_cast<int32_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
+               reinterpret_cast<int2*>(base + w.off_utab), 0, st};
+    TK_RC(g.init());
+    for (int64_t s = 0; s < p.nsuper; ++s) {
+        const int64_t k0 = s * p.Ksc, Kc = std::min(p.Ksc, p.Kfull - k0);
+        TK_RC(produce(k0, Kc, g.R));
+        TK_RC(g.run(s, Kc));
+    }
+    return g.crt(G);
 }
 
 // Materialised F: one residue launch per super-chunk.
@@ -890,10 +937,12 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
     return TUCKER_OK;
 }
 
-// Same, modes in `order`, mode m into G[m] (three buffers); after_mode(idx) is called once the
-// Gram of mode order[idx] is enqueued.
-int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                              cudaStream_t st, const int order[3], const std::function<int(int)>& after_mode) {
+// The three Grams of a HOSVD into G[0..2] (row maxima once), modes 2, 1, 0.  on_phase(modes, count)
+// is called after each phase's Grams are enqueued on `st` (the caller overlaps eigensolves with the
+// next phase).  ws: gram_i8_hosvd_ws_bytes.  (A joint modes-1/2 residue pass reading F once was
+// measured: 12.3 ms against 12.6 ms for the two passes, for 8 GiB more workspace — not kept.)
+int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase) {
     using namespace i8;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const WsPlan w = ws_plan(n);
@@ -901,13 +950,14 @@ int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
-    for (int idx = 0; idx < 3; ++idx) {
-        const int m = order[idx];
+    for (int m = 2; m >= 0; --m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
-        TK_RC(after_mode(idx));
+        TK_RC(on_phase(&m, 1));
     }
     return TUCKER_OK;
 }
+
+size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
 
 cudaStream_t side_stream() {
     static cudaStream_t s[64] = {};

@@ -63,8 +63,9 @@ bool gram_i8_fused_supported(const int64_t n[3]);
 size_t gram_i8_fused_ws_bytes(const int64_t n[3]);
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
                                cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode);
-int launch_gram_i8_modes_into(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                              cudaStream_t st, const int order[3], const std::function<int(int)>& after_mode);
+int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase);
+size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
 // Per-device non-blocking side stream of the library (created once).
 cudaStream_t side_stream();
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
