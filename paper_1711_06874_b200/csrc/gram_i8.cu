@@ -57,14 +57,15 @@ __host__ __device__ constexpr int pow2mod(int e, int p) {
     for (int i = 0; i < e; ++i) r = (r * 2) % p;
     return (int)r;
 }
-__host__ __device__ constexpr int invmod(int a, int p) {  // p prime-power-free small modulus, gcd(a, p) = 1
+__host__ __device__ constexpr int invmod(int a, int p) {  // a^-1 mod p for gcd(a, p) = 1 (compile time)
     for (int x = 1; x < p; ++x)
         if ((int64_t)a * x % p == 1) return x;
     return 0;
 }
 
-// Largest b <= 50 with K 2^(2b) < P/2 (log2 P of the 16 moduli ~ 125.09).  b <= 50 keeps
-// |rint(t)| <= 2^50 inside the 1.5 2^52 rounding trick of k_i8_residues.
+// Largest b <= 50 with K 2^(2b) < P/2 (log2 P of the 16 moduli ~ 125.09), so |S_ij| <= K 2^(2b)
+// is recovered uniquely from its residues.  b <= 50 keeps w = rint(t) + B in [0, 2^52) for the
+// one-DFMA rounding of k_i8_residues (B = 2^50 + 2^33 + 2^16).
 inline int scale_bits(int64_t K) {
     double lp = 0.0;
     for (int l = 0; l < NMOD; ++l) lp += std::log2((double)kMod(l));
@@ -165,9 +166,10 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e, -1022 <= e <= 1023
 }
 
 // ------------------------------------------------------------------------------------------
-// 1b. residues of the scaled, rounded rows: R[l][row][kk] = x mod p_l (kk in [0, Kc) of the
-//     super-chunk starting at unfolding column k0).  Unfolding column order: mode 0 (j, k),
-//     mode 1 (i, k), mode 2 (i, j) — any fixed order gives the same Gram.
+// 1b. residues of the scaled, rounded rows: x mod p_l for unfolding columns [k0, k0 + Kc) of a
+//     super-chunk, stored K-block-major R[l][kk / 128][row][kk % 128] (kk relative to the
+//     super-chunk, + kout).  Unfolding column order: mode 0 (j, k), mode 1 (i, k), mode 2 (i, j) —
+//     any fixed order gives the same Gram.
 struct ResArgs {
     const double* F;
     int64_t n1, n2, n3;
