@@ -15,8 +15,12 @@
 // and U_m = U~[:, :r], sigma_m = Sigma[:r]; `iters` repeats the step from V = U~.  Every product
 // is a plain FP64 contraction of F (no Gram), so the singular values are resolved down to
 // ~eps sigma_1.  The streaming products run on the DMMA GEMM (gemm.cu).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace tk {
 
@@ -136,6 +140,94 @@ __global__ void __launch_bounds__(kNT) k_cgs_finish(double* __restrict__ Yt, int
     for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) y[i] = ok ? y[i] * inv : hash_u(0x5eedull * (k + 1) + i);
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0 && ok) *accepted = 1;
+}
+
+// The column-by-column CGS2 of one block (columns k in [c0, c0 + bb)) in a single cooperative
+// launch: the same arithmetic as k_cgs_dots / k_reduce_h / k_cgs_update / k_cgs_finish (same row
+// ranges, same fixed-order block and shuffle reductions — bitwise the same result), with grid-wide
+// barriers instead of kernel boundaries.  Every CTA reduces the per-CTA partials itself (same
+// order), so the projection coefficients and the accept decision need no broadcast.
+__global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                      double* __restrict__ part, double* __restrict__ npart,
+                                                      const int* __restrict__ jstart_all) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[40];
+    __shared__ double h[64];
+    __shared__ double tot_s, tot1_s;
+    const int nblk = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    for (int k = c0; k < c0 + bb; ++k) {
+        double* y = Yt + (size_t)k * M;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            const int js = attempt == 0 ? jstart_all[k] : 0;  // a replaced column: full projection
+            for (int pass = 0; pass < 2; ++pass) {
+                if (k > 0) {
+                    // dots: part[blk][j] over this CTA's rows (as k_cgs_dots)
+                    for (int j0 = js; j0 < k; j0 += 8) {
+                        double acc[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+                        for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
+                            const double yi = y[i];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (j0 + u < k) acc[u] = fma(Yt[(size_t)(j0 + u) * M + i], yi, acc[u]);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const double sum = block_sum(acc[u], red);
+                            if (threadIdx.x == 0 && j0 + u < k) part[(size_t)blockIdx.x * 64 + j0 + u] = sum;
+                        }
+                    }
+                    grid.sync();
+                    // h[j] = sum over blocks (as k_reduce_h: warp per j, lanes strided, shuffle tree)
+                    for (int j = js + warp; j < k; j += kNT / 32) {
+                        double sum = 0.0;
+                        for (int b = lane; b < nblk; b += 32) sum += part[(size_t)b * 64 + j];
+                        sum = warp_sum(sum);
+                        if (lane == 0) h[j] = sum;
+                    }
+                    for (int j = threadIdx.x; j < js; j += kNT) h[j] = 0.0;
+                    __syncthreads();
+                }
+                // update (as k_cgs_update): y -= Q h, npart[pass][blk] = ||y||^2 of this CTA's rows
+                double ss = 0.0;
+                for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
+                    double yi = y[i];
+                    for (int j = js; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
+                    y[i] = yi;
+                    ss = fma(yi, yi, ss);
+                }
+                ss = block_sum(ss, red);
+                if (threadIdx.x == 0) npart[pass * nblk + blockIdx.x] = ss;
+                grid.sync();
+            }
+            // finish (as k_cgs_finish): Kahan-Parlett acceptance, normalise or replace
+            if (threadIdx.x < 32) {
+                double sum = 0.0, sum1 = 0.0;
+                for (int b = threadIdx.x; b < nblk; b += 32) {
+                    sum1 += npart[b];
+                    sum += npart[nblk + b];
+                }
+                sum = warp_sum(sum);
+                sum1 = warp_sum(sum1);
+                if (threadIdx.x == 0) {
+                    tot_s = sum;
+                    tot1_s = sum1;
+                }
+            }
+            __syncthreads();
+            const double tot = tot_s, tot1 = tot1_s;
+            const bool ok = (tot > 1e-300 && tot >= 0.5 * tot1) || attempt == 1;
+            const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+            for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT)
+                y[i] = ok ? y[i] * inv : hash_u(0x5eedull * (k + 1) + i);
+            grid.sync();
+            if (ok) break;
+        }
+    }
 }
 
 // Start basis for the Rayleigh–Ritz steps: keep the Gram route's eigenvectors whose eigenvalue is
@@ -337,6 +429,12 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
         k_seed_basis<<<64, 256, 0, st>>>(V, nm, p, lam0);
         TK_CHECK_LAUNCH();
     }
+    int nb_sm = 0, dev = 0;  // cooperative CGS2 needs all kBlk CTAs resident
+    TK_CUDA(cudaGetDevice(&dev));
+    int coop_attr = 0;
+    TK_CUDA(cudaDeviceGetAttribute(&coop_attr, cudaDevAttrCooperativeLaunch, dev));
+    TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_sm, k_cgs_block, kNT, 0));
+    const bool coop_ok = coop_attr && nb_sm * kNumSMs >= kBlk;
     for (int it = 0; it < iters; ++it) {
         // ---- pass 1: Yt (p x M) = V^T F_(m)
         if (m == 0) {  // Yt[a][(j,k)] = sum_i V[i][a] F[i][(j,k)]
@@ -372,6 +470,13 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
                 }
                 k_block_check<<<1, 256, 0, st>>>(cn, cn + (size_t)kBlk * 8, kBlk, bb, c0, jstart);
                 TK_CHECK_LAUNCH();
+            }
+            if (coop_ok) {  // one cooperative launch for the block's column-by-column CGS2
+                void* args[] = {(void*)&Yt, (void*)&M, (void*)&c0, (void*)&bb, (void*)&dots, (void*)&npart,
+                                (void*)&jstart};
+                TK_CUDA(cudaLaunchCooperativeKernel((void*)k_cgs_block, dim3(kBlk), dim3(kNT), args, 0, st));
+                TK_LAUNCHED();
+                continue;
             }
             // flags[0] = 0 (attempt 0 always runs), flags[1] = attempt 0 accepted (attempt 1 skipped)
             for (int k = c0; k < c0 + bb; ++k) {
