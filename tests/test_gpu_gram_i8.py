@@ -201,3 +201,23 @@ def test_gram_i8_2048_materialised_equals_fused(T):
     assert torch.equal(G, Gf)
     d = torch.sqrt(torch.diagonal(G))
     assert bool(torch.all(d > 0)) and torch.equal(G, G.T)
+
+
+def test_gram_i8_extreme_dynamic_range(T, orc):
+    """Row scales far apart: slabs multiplied by 2^e, e in {-1000, -600, 0, 300, 500} (mode-0 rows
+    2^-1000 take the two-step scaling, 2^(50+1000) being out of the double exponent range; modes 1
+    and 2 mix all scales in every row).  Entries whose exact value underflows are 0 on both sides; the
+    rest stay within the R18 bound and no Inf/NaN appears."""
+    g = GridSpec((40, 24, 20), (-1.0,) * 3, (1.0,) * 3)
+    k = KernelSpec.matern(1.5, 0.3)
+    Fo = orc.fill(ogrid(orc, g), okern(orc, k))
+    e = np.array([-1000, -600, 0, 300, 500])[np.arange(g.n[0]) % 5]
+    F = Fo * np.exp2(e.astype(np.float64))[:, None, None]
+    Fd = torch.from_numpy(F).cuda()
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        G = to_np(T.gram_i8(g, m, Fd, ws))
+        R = orc.gram_mode(F, m)
+        assert np.all(np.isfinite(G)), m
+        A = unfold(F, m)
+        assert np.all(np.abs(G - R) <= _bound(A, 50) + np.finfo(np.float64).tiny), m
