@@ -276,7 +276,10 @@ def run_ours(args, rank, world, local):
     result = {
         "metric": METRIC, "value": whole_job_rate(N, world, ms_step), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64" + (" (Gram: int8-emulated, exact CRT)" if i8 else ""),
+        "vs_baseline": None, "dtype": "f64",
+        "dtype_note": ("FP64 path; the Grams are formed exactly from int8 residues on the tensor cores (tcgen05 "
+                       "kind::i8, 16 moduli) and reconstructed to FP64 by the CRT (DESIGN.md R18)") if i8 else
+                      "FP64 path; Grams on the FP64 tensor cores (DMMA)",
         "data": "synthetic",
         "config": {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2", "grid": [n, n, n], "box": [-1.0, 1.0],
                    "kernel": {"family": "matern", "nu": 1.5, "ell": 0.2, "sigma2": 1.0}, "ranks": list(ranks),
