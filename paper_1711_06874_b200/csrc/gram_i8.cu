@@ -52,6 +52,12 @@ constexpr uint32_t STAGE_BYTES = 3 * BOX;    // A + two B halves
 constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
 constexpr int RT_ROWS = 32, RT_K = 128;  // residue tile
 
+// run-time modulus tables for the k_i8_gemm epilogue (index l is not a compile-time constant there)
+__constant__ int c_mod[NMOD] = {253, 251, 249, 247, 245, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191};
+__constant__ double c_invmod[NMOD] = {1.0 / 253, 1.0 / 251, 1.0 / 249, 1.0 / 247, 1.0 / 245, 1.0 / 241, 1.0 / 239,
+                                      1.0 / 233, 1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 211, 1.0 / 199, 1.0 / 197,
+                                      1.0 / 193, 1.0 / 191};
+
 __host__ __device__ constexpr int pow2mod(int e, int p) {
     int64_t r = 1;
     for (int i = 0; i < e; ++i) r = (r * 2) % p;
@@ -360,7 +366,7 @@ struct GemmArgs {
     int nchunks;     // K-chunks of KCH in this super-chunk
     int nunits;      // NMOD * nchunks * nug
     int64_t Kc;      // K of this super-chunk
-    int32_t* P;      // partials [(l * nchunks + c) * ntiles + t][PN][PM]
+    int16_t* P;      // partials mod p_l, [(l * nchunks + c) * ntiles + t][PN][PM]
     const int2* utab;  // unit v of a group: tiles (ta, tb), tb = -1 unless two half tiles are merged
 };
 
@@ -613,11 +619,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             // output segments: a full/half tile is columns [0, N) at TMEM column c; merged tiles
             // are two segments at TMEM columns 0.. and 256..
             const int nseg = x.merged ? 2 : 1;
+            const int pmod = c_mod[x.l];
+            const double invp = c_invmod[x.l];
             for (int sg = 0; sg < nseg; ++sg) {
                 const int t = x.s[sg].t;
                 const int N = x.merged ? x.s[sg].N : (x.ns == 2 ? 256 + x.s[1].N : x.s[0].N);
                 const uint32_t tc0 = x.merged ? 256u * sg : 0u;
-                int32_t* P = g.P + ((size_t)(x.l * g.nchunks + x.c) * g.ntiles + t) * (PN * PM);
+                int16_t* P = g.P + ((size_t)(x.l * g.nchunks + x.c) * g.ntiles + t) * (PN * PM);
                 for (int c0 = 0; c0 < N; c0 += 32) {
                     uint32_t v[32];
                     asm volatile(
@@ -630,8 +638,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                           "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(taddr + tc0 + c0));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    // exact int32 chunk sum -> a representative mod p in (-p, p) (int16: half the
+                    // partials traffic); v - p rint(v / p) with the quotient from FP64 (|v| < 2^31)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) P[(size_t)(c0 + j) * PM + row] = (int32_t)v[j];
+                    for (int j = 0; j < 32; ++j) {
+                        const int vi = (int)v[j];
+                        const int q = __double2int_rn((double)vi * invp);
+                        P[(size_t)(c0 + j) * PM + row] = (int16_t)(vi - q * pmod);
+                    }
                 }
             }
             tc_fence_before();
@@ -650,22 +664,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 
 // ------------------------------------------------------------------------------------------
 // 2b. fold the chunk partials: Racc[l][t][col][row] = (Racc + sum_c P) mod p_l  (Racc in [0, p))
-__global__ void __launch_bounds__(256) k_i8_reduce(const int32_t* __restrict__ P, int32_t* __restrict__ Racc,
+__global__ void __launch_bounds__(256) k_i8_reduce(const int16_t* __restrict__ P, int32_t* __restrict__ Racc,
                                                    int ntiles, int nchunks, int first) {
     const int64_t per = (int64_t)ntiles * PN * PM;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= per * NMOD) return;
     const int l = (int)(idx / per);
     const int64_t e = idx - (int64_t)l * per;  // t * PN*PM + col*PM + row
-    int64_t s = first ? 0 : Racc[idx];
+    int s = first ? 0 : Racc[idx];            // |s| <= p (nchunks + 1) << 2^31
     for (int c = 0; c < nchunks; ++c) s += P[((int64_t)l * nchunks + c) * per + e];
-    int p = 0;
-#pragma unroll
-    for (int q = 0; q < NMOD; ++q)
-        if (q == l) p = kMod(q);
-    int64_t r = s % p;
-    if (r < 0) r += p;
-    Racc[idx] = (int32_t)r;
+    const int p = c_mod[l];
+    int r = s - p * __double2int_rn((double)s * c_invmod[l]);  // in [-p/2 - 1, p/2 + 1]
+    r += r < 0 ? p : 0;
+    Racc[idx] = r >= p ? r - p : r;
 }
 
 template <int L, int Q>
@@ -785,7 +796,7 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     auto add = [&](const ModePlan& p) {
         rb = std::max(rb, align_up((size_t)NMOD * p.rows * p.ldr, 1024));
         const int64_t nch = ceil_div(p.Ksc, KCH);
-        pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 4, 256));
+        pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 2, 256));
         ab = std::max(ab, align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256));
         ub = std::max(ub, align_up((size_t)p.ntiles * sizeof(int2), 256));
     };
@@ -817,7 +828,8 @@ struct ModeGemm {
     ModePlan p;
     const uint32_t* mxm;
     int8_t* R;
-    int32_t *P, *Racc;
+    int16_t* P;
+    int32_t* Racc;
     int2* utab;
     int nug;
     cudaStream_t st;
@@ -876,7 +888,7 @@ template <class Produce>
 int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
                    double* G, cudaStream_t st, Produce&& produce) {
     ModeGemm g{n, m, p, mode_max(mx, n, m), reinterpret_cast<int8_t*>(base + w.off_R),
-               reinterpret_cast<int32_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
+               reinterpret_cast<int16_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
                reinterpret_cast<int2*>(base + w.off_utab), 0, st};
     TK_RC(g.init());
     for (int64_t s = 0; s < p.nsuper; ++s) {
