@@ -160,6 +160,100 @@ __global__ void __launch_bounds__(256) k_i8_rowmax(const double* __restrict__ F,
     }
 }
 
+// Row maxima of the function tensor without storing it (a-7): the same reduction as k_i8_rowmax
+// over values evaluated on the fly — bitwise the fill's values (same squared nodes, same
+// association (x_i^2 + y_j^2) + z_k^2, same eval_point) — so the maxima equal those of the
+// materialised tensor, at ALU cost instead of a 8N-byte write and read.
+__global__ void __launch_bounds__(256) k_i8_rowmax_gen(KParams kp, const double* __restrict__ cheb,
+                                                       const double* __restrict__ x2, int64_t n1, int64_t n2,
+                                                       int64_t n3, uint32_t* __restrict__ mx0,
+                                                       uint32_t* __restrict__ mx1, uint32_t* __restrict__ mx2,
+                                                       int64_t jblk) {
+    __shared__ uint32_t s_line[8][33];
+    const double* xa = x2;
+    const double* xb = x2 + n1;
+    const double* xc = x2 + n1 + n2;
+    const int64_t i = blockIdx.x;
+    const int64_t jlo = (int64_t)blockIdx.y * jblk, jhi = min(n2, jlo + jblk);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t pmax = 0;
+    for (int64_t kb = 0; kb < n3; kb += RM_KB) {
+        uint32_t km[4] = {0u, 0u, 0u, 0u};
+        bool kin[4];
+        double zc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            kin[e] = kb + tid + 256 * e < n3;
+            zc[e] = kin[e] ? xc[kb + tid + 256 * e] : 0.0;
+        }
+        for (int64_t j0 = jlo; j0 < jhi; j0 += 32) {
+            const int nl = (int)min((int64_t)32, jhi - j0);
+#pragma unroll 1
+            for (int g8 = 0; g8 < 4; ++g8) {
+                uint32_t a[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t lm = 0u;
+                    if (8 * g8 + jj < nl) {
+                        const double sij = __dadd_rn(xa[i], xb[j0 + 8 * g8 + jj]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (kin[e]) {
+                                const double v = eval_point(kp, cheb, __dadd_rn(sij, zc[e]));
+                                const uint32_t h = (uint32_t)__double2hiint(v) & 0x7FFFFFFFu;
+                                km[e] = max(km[e], h);
+                                lm = max(lm, h);
+                            }
+                    }
+                    a[jj] = lm;
+                }
+#pragma unroll
+                for (int sft = 16, h = 4; sft >= 4; sft >>= 1, h >>= 1) {
+                    const bool up = (lane & sft) != 0;
+#pragma unroll
+                    for (int q = 0; q < h; ++q) {
+                        const uint32_t send = up ? a[q] : a[q + h];
+                        const uint32_t keep = up ? a[q + h] : a[q];
+                        a[q] = max(keep, __shfl_xor_sync(0xffffffffu, send, sft));
+                    }
+                }
+                a[0] = max(a[0], __shfl_xor_sync(0xffffffffu, a[0], 2));
+                a[0] = max(a[0], __shfl_xor_sync(0xffffffffu, a[0], 1));
+                if ((lane & 3) == 0) s_line[warp][8 * g8 + (lane >> 2)] = a[0];
+            }
+            __syncthreads();
+            if (tid < nl) {
+                uint32_t m = s_line[0][tid];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) m = max(m, s_line[w][tid]);
+                atomicMax(&mx1[j0 + tid], m);
+                pmax = max(pmax, m);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (kin[e]) atomicMax(&mx2[kb + tid + 256 * e], km[e]);
+    }
+    if (warp == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pmax = max(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+        if (lane == 0) atomicMax(&mx0[i], pmax);
+    }
+}
+
+// mx_a[idx] = mx_a[n_a - 1 - idx] for the second half of every axis (centred grids).
+__global__ void k_i8_mirror_max(uint32_t* m0, uint32_t* m1, uint32_t* m2, int64_t n1, int64_t n2, int64_t n3) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t* m;
+    int64_t n, idx;
+    if (t < n1) { m = m0; n = n1; idx = t; }
+    else if (t < n1 + n2) { m = m1; n = n2; idx = t - n1; }
+    else if (t < n1 + n2 + n3) { m = m2; n = n3; idx = t - n1 - n2; }
+    else return;
+    if (idx >= (n + 1) / 2) m[idx] = m[n - 1 - idx];
+}
+
 // E with |a| < 2^E for every |a| <= the row maximum whose high word is hw (frexp exponent of a
 // normal maximum; subnormal maxima use the bound 2^-1022; a zero row any E).
 __host__ __device__ __forceinline__ int row_exponent(uint32_t hw) {
@@ -1060,20 +1154,45 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
     double* chunk = reinterpret_cast<double*>(base + f.off_chunk);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + f.ws.off_mx);
     const int mirror = (gen.kp.centred && n[2] % 8 == 0) ? 1 : 0;
-    {  // row maxima: one generation pass over i-plane chunks
+    {  // row maxima
         TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
         TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n[0] + n[1] + n[2]) * 4, st));
-        const int64_t pc = f.Pc[1];
-        for (int64_t g0 = 0; g0 < n[0]; g0 += pc) {
-            ChunkGeo geo{0, mirror, n[0], n[1], n[2], g0, pc, n[0]};
-            TK_RC(launch_gen_chunk(geo, gen.kp, gen.cheb, gen.x2, chunk, st));
-            const int64_t valid = std::min(pc, n[0] - g0);
-            // few planes per chunk at large n: split each plane's lines over enough CTAs
-            const int64_t nb = std::min<int64_t>(ceil_div(n[1], 32), std::max<int64_t>(1, ceil_div(4 * kNumSMs, valid)));
-            const int64_t jblk = ceil_div(ceil_div(n[1], nb), 32) * 32;
-            k_i8_rowmax<<<dim3((unsigned)valid, (unsigned)ceil_div(n[1], jblk)), 256, 0, st>>>(
-                chunk, valid, n[1], n[2], mx + g0, mx + n[0], mx + n[0] + n[1], jblk);
+        if (gen.kp.centred) {
+            // centred grid: F is even in every index (bitwise: mirrored squared nodes), so every row
+            // maximum is attained in the first octant — evaluate it there (N/8 values, nothing
+            // stored) and mirror the maxima
+            const int64_t h[3] = {(n[0] + 1) / 2, (n[1] + 1) / 2, (n[2] + 1) / 2};
+            uint32_t* m0 = mx;
+            uint32_t* m1 = mx + n[0];
+            uint32_t* m2 = mx + n[0] + n[1];
+            const int64_t nb = std::min<int64_t>(ceil_div(h[1], 32), std::max<int64_t>(1, ceil_div(4 * kNumSMs, h[0])));
+            const int64_t jblk = ceil_div(ceil_div(h[1], nb), 32) * 32;
+            const double* xa = gen.x2;  // squared nodes of the octant: the leading h_a entries
+            KParams kp = gen.kp;
+            // k_i8_rowmax_gen indexes x2 as [n1'][n2'][n3'] blocks: pass the three axes' arrays
+            // through a packed copy of their leading halves
+            double* xh = reinterpret_cast<double*>(chunk);  // chunk buffer is free here
+            TK_CUDA(cudaMemcpyAsync(xh, xa, h[0] * 8, cudaMemcpyDeviceToDevice, st));
+            TK_CUDA(cudaMemcpyAsync(xh + h[0], xa + n[0], h[1] * 8, cudaMemcpyDeviceToDevice, st));
+            TK_CUDA(cudaMemcpyAsync(xh + h[0] + h[1], xa + n[0] + n[1], h[2] * 8, cudaMemcpyDeviceToDevice, st));
+            k_i8_rowmax_gen<<<dim3((unsigned)h[0], (unsigned)ceil_div(h[1], jblk)), 256, 0, st>>>(
+                kp, gen.cheb, xh, h[0], h[1], h[2], m0, m1, m2, jblk);
             TK_CHECK_LAUNCH();
+            k_i8_mirror_max<<<(unsigned)ceil_div(n[0] + n[1] + n[2], 256), 256, 0, st>>>(m0, m1, m2, n[0], n[1], n[2]);
+            TK_CHECK_LAUNCH();
+        } else {  // general grid: one generation pass over i-plane chunks
+            const int64_t pc = f.Pc[1];
+            for (int64_t g0 = 0; g0 < n[0]; g0 += pc) {
+                ChunkGeo geo{0, mirror, n[0], n[1], n[2], g0, pc, n[0]};
+                TK_RC(launch_gen_chunk(geo, gen.kp, gen.cheb, gen.x2, chunk, st));
+                const int64_t valid = std::min(pc, n[0] - g0);
+                const int64_t nb =
+                    std::min<int64_t>(ceil_div(n[1], 32), std::max<int64_t>(1, ceil_div(4 * kNumSMs, valid)));
+                const int64_t jblk = ceil_div(ceil_div(n[1], nb), 32) * 32;
+                k_i8_rowmax<<<dim3((unsigned)valid, (unsigned)ceil_div(n[1], jblk)), 256, 0, st>>>(
+                    chunk, valid, n[1], n[2], mx + g0, mx + n[0], mx + n[0] + n[1], jblk);
+                TK_CHECK_LAUNCH();
+            }
         }
     }
     for (int m = m_first; m <= m_last; ++m) {
