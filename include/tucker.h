@@ -117,6 +117,10 @@ TUCKER_API int tucker_gram(const tucker_grid* grid, int32_t mode, const double* 
  * tucker_workspace_size_i8 (residues of up to 8 GiB of the unfolding at a time, partials).
  * TUCKER_ERR_UNSUPPORTED if some n_m > 16384. */
 TUCKER_API size_t tucker_workspace_size_i8(const tucker_grid* grid);
+/* The INT8 Gram's modular scheme for an unfolding with K columns (host only, no GPU): the 16
+ * moduli (moduli[16], host) and the integer width b (*b, host) used by tucker_gram_i8 —
+ * pairwise coprime odd p_l <= 253 with prod p_l > 2 K 2^(2b), b <= 50.  Returns TUCKER_OK. */
+TUCKER_API int tucker_i8_scheme(int64_t K, int32_t* moduli, int32_t* b);
 /* Gram engine of tucker_gram, tucker_hosvd and tucker_approximate (process-wide, not thread-safe;
  * set it before sizing workspaces: tucker_workspace_size depends on it).  TUCKER_GRAM_AUTO
  * (default): the INT8 emulation where supported (every n_m <= 16384), DMMA otherwise. */

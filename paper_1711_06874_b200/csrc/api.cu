@@ -363,6 +363,11 @@ size_t tucker_workspace_size_i8(const tucker_grid* grid) {
     return gram_i8_ws_bytes(grid->n);
 }
 
+int tucker_i8_scheme(int64_t K, int32_t* moduli, int32_t* b) {
+    if (K < 1 || !moduli || !b) return TUCKER_ERR_INVALID_ARG;
+    return gram_i8_scheme(K, moduli, b);
+}
+
 int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws, size_t ws_bytes,
                    void* stream) {
     launch_counter() = 0;

@@ -1010,6 +1010,12 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
 
 }  // namespace i8
 
+int gram_i8_scheme(int64_t K, int32_t* moduli, int32_t* b) {
+    for (int l = 0; l < i8::NMOD; ++l) moduli[l] = i8::kMod(l);
+    *b = i8::scale_bits(K);
+    return TUCKER_OK;
+}
+
 size_t gram_i8_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
 
 bool gram_i8_supported(const int64_t n[3]) {

@@ -42,6 +42,7 @@ int launch_gram(const int64_t n[3], int mode, const double* F, double* G, void* 
 
 // a-3 on the INT8 tensor cores (gram_i8.cu): modular emulation of the FP64 Gram.
 bool gram_i8_supported(const int64_t n[3]);
+int gram_i8_scheme(int64_t K, int32_t* moduli, int32_t* b);
 size_t gram_i8_ws_bytes(const int64_t n[3]);
 // Row maxima of the three unfoldings (n1 + n2 + n3 u64 bit patterns of non-negative doubles).
 int launch_gram_i8_rowmax(const int64_t n[3], const double* F, uint32_t* mx, cudaStream_t st);

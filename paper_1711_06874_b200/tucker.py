@@ -25,7 +25,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", 
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
-           "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8",
+           "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme",
            "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
            "tucker_last_launch_count", "tucker_strerror")
 
@@ -74,6 +74,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_workspace_size_i8": (sz, [pg]),
         "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
+        "tucker_i8_scheme": (ctypes.c_int, [i64, P(ctypes.c_int32), P(ctypes.c_int32)]),
         "tucker_set_gram_engine": (ctypes.c_int, [i32]),
         "tucker_get_gram_engine": (i32, []),
         "tucker_profile_enable": (ctypes.c_int, [i32]),
@@ -211,6 +212,13 @@ def profile_read() -> dict:
     ms, cnt = (ctypes.c_double * n)(), (ctypes.c_int64 * n)()
     _check(load().tucker_profile_read(ms, cnt), "tucker_profile_read")
     return {PROF_STAGES[i]: (ms[i], cnt[i]) for i in range(n)}
+
+
+def i8_scheme(K: int) -> tuple:
+    """(moduli, b) of the INT8 Gram's modular scheme for K unfolding columns (host query)."""
+    mod, b = (ctypes.c_int32 * 16)(), ctypes.c_int32()
+    _check(load().tucker_i8_scheme(int(K), mod, ctypes.byref(b)), "tucker_i8_scheme")
+    return list(mod), int(b.value)
 
 
 def workspace_i8(grid) -> torch.Tensor:
