@@ -221,3 +221,20 @@ def test_gram_i8_extreme_dynamic_range(T, orc):
         assert np.all(np.isfinite(G)), m
         A = unfold(F, m)
         assert np.all(np.abs(G - R) <= _bound(A, 50) + np.finfo(np.float64).tiny), m
+
+
+@pytest.mark.parametrize("shape", [(4096, 8, 6), (6, 2048, 16), (3, 5, 2049)])
+def test_gram_i8_extreme_aspect(T, orc, shape):
+    """Long modes next to tiny ones: 4096 rows with K = 48 (16 x 32 pair tiles, many merged units,
+    one K-block), and K = 4 x 2049 columns with 3 rows (one pair tile, ragged K-blocks)."""
+    g = GridSpec(shape, (-1.0,) * 3, (1.0,) * 3)
+    k = KernelSpec.matern(0.7, 0.4)
+    Fg = T.fill(g, k)
+    F = orc.fill(ogrid(orc, g), okern(orc, k))
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        G = to_np(T.gram_i8(g, m, Fg, ws))
+        R = orc.gram_mode(F, m)
+        A = unfold(F, m)
+        assert np.array_equal(G, G.T)
+        assert np.all(np.abs(G - R) <= _bound(A, 50)), (shape, m)
