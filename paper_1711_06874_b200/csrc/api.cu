@@ -121,7 +121,7 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
         for (int a = 0; a < 3; ++a) e = std::max(e, eig_ws_bytes(n[a], r[a]));
         L.eig = off;
         L.eig_bytes = align_up(e, 256);
-        off += L.eig_bytes;
+        off += 3 * L.eig_bytes;  // one per mode: the three eigensolves are in flight together
         L.t2 = off;
         off += align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
     }
@@ -162,8 +162,9 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         // runs on a side stream while the next Gram runs on `st` (one G per mode; the eigensolver is
         // latency-bound on one cluster); the last one (mode 0: U1) runs beside the core's first two
         // products (which need U2, U3 only); the third product waits for it.
-        cudaStream_t side = side_stream();
-        if (!side) return TUCKER_ERR_CUDA;
+        // side stream A: eigensolves of modes 2 and 1; side stream B: mode 0 (beside TTM1 + TTM2)
+        cudaStream_t sideA = side_stream(0), sideB = side_stream(1);
+        if (!sideA || !sideB) return TUCKER_ERR_CUDA;
         cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
         auto cleanup = [&]() {
             for (cudaEvent_t e : ev)
@@ -176,35 +177,37 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
             }
         double* Gm[3] = {G, reinterpret_cast<double*>(at(ws, L.G + L.g_bytes)),
                          reinterpret_cast<double*>(at(ws, L.G + 2 * L.g_bytes))};
-        void* escr = at(ws, L.eig);
+        void* escr[3] = {at(ws, L.eig), at(ws, L.eig + L.eig_bytes), at(ws, L.eig + 2 * L.eig_bytes)};
         double* T2 = reinterpret_cast<double*>(at(ws, L.t2));
-        auto eig_side = [&](int m) -> int {  // host waits here while `st` keeps running
-            if (cudaStreamWaitEvent(side, ev[m], 0) != cudaSuccess) return TUCKER_ERR_CUDA;
-            const int rc = launch_eig(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr, L.eig_bytes, side, info, m);
+        auto side_of = [&](int m) { return m == 0 ? sideB : sideA; };
+        auto eig_end = [&](int m) -> int {  // host waits for the solve (its first pass is long queued)
+            const int rc = launch_eig_end(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], side_of(m), info, m);
             if (rc == TUCKER_ERR_NOCONV) worst = rc;
             else if (rc != TUCKER_OK) return rc;
             return TUCKER_OK;
         };
-        int pend[3], npend = 0;  // Grams enqueued, eigensolves not yet issued
+        // each eigensolve's first pass is enqueued as soon as its Gram is: it runs beside the next
+        // Gram's residue kernels
         int rc = launch_gram_i8_hosvd(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, [&](const int* ms, int cnt) -> int {
-            for (int i = 0; i < cnt; ++i)
-                if (cudaEventRecord(ev[ms[i]], st) != cudaSuccess) return TUCKER_ERR_CUDA;
-            // the previous phase's modes: eigensolve now, beside this phase's Grams
-            for (int i = 0; i < npend; ++i)
-                if (pend[i] != 0) TK_RC(eig_side(pend[i]));
-            npend = 0;
-            for (int i = 0; i < cnt; ++i) pend[npend++] = ms[i];
+            for (int i = 0; i < cnt; ++i) {
+                const int m = ms[i];
+                if (cudaEventRecord(ev[m], st) != cudaSuccess || cudaStreamWaitEvent(side_of(m), ev[m], 0) != cudaSuccess)
+                    return TUCKER_ERR_CUDA;
+                TK_RC(launch_eig_begin(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], L.eig_bytes, side_of(m)));
+            }
             return TUCKER_OK;
         });
-        // U2, U3 ready on `side` -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve
-        if (rc == TUCKER_OK && (cudaEventRecord(ev[3], side) != cudaSuccess ||
+        if (rc == TUCKER_OK) rc = eig_end(2);
+        if (rc == TUCKER_OK) rc = eig_end(1);
+        // U2, U3 final on side A -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve on side B
+        if (rc == TUCKER_OK && (cudaEventRecord(ev[3], sideA) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
         if (rc == TUCKER_OK)
             rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
                                       nullptr, T2);
-        if (rc == TUCKER_OK) rc = eig_side(0);
-        if (rc == TUCKER_OK && (cudaEventRecord(ev[4], side) != cudaSuccess ||
+        if (rc == TUCKER_OK) rc = eig_end(0);
+        if (rc == TUCKER_OK && (cudaEventRecord(ev[4], sideB) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[4], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
         cleanup();

@@ -380,24 +380,43 @@ size_t eig_ws_bytes(int64_t n, int r) {
     return align_up(sizeof(State), 256) + 4 * align_up((size_t)p * n * sizeof(double), 256);
 }
 
-int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
-               size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot) {
+// Split form: launch_eig_begin enqueues the whole first pass (no host synchronisation; on the
+// cluster path: start basis, the power steps and the first batch of Rayleigh-Ritz iterations,
+// which usually converge — later launches of a converged solve exit at once), launch_eig_end
+// synchronises, continues in batches while not converged, and reports.  launch_eig = both.
+namespace eig {
+struct Plan {
+    int p;
+    State* dst;
+    double *Vt, *Wt, *VrT, *YT;
+};
+static Plan eig_plan(int64_t n, int r, void* ws) {
+    Plan q{};
+    q.p = block_width(n, r);
+    char* w = static_cast<char*>(ws);
+    q.dst = reinterpret_cast<State*>(w);
+    w += align_up(sizeof(State), 256);
+    const size_t blk = align_up((size_t)q.p * n * sizeof(double), 256);
+    q.Vt = reinterpret_cast<double*>(w);
+    q.Wt = reinterpret_cast<double*>(w + blk);
+    q.VrT = reinterpret_cast<double*>(w + 2 * blk);
+    q.YT = reinterpret_cast<double*>(w + 3 * blk);
+    return q;
+}
+}  // namespace eig
+
+int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
     TK_PROF(TUCKER_PROF_EIG, st);
     using namespace eig;
     if (r < 1 || r > n) return TUCKER_ERR_RANK;
     if (n > kDirectMax && r > kMaxP - 8) return TUCKER_ERR_UNSUPPORTED;
     if (ws_bytes < eig_ws_bytes(n, r)) return TUCKER_ERR_SIZE;
-    const int p = block_width(n, r);
-    char* w = static_cast<char*>(ws);
-    State* dst = reinterpret_cast<State*>(w);
-    w += align_up(sizeof(State), 256);
-    const size_t blk = align_up((size_t)p * n * sizeof(double), 256);
-    double* Vt = reinterpret_cast<double*>(w);
-    double* Wt = reinterpret_cast<double*>(w + blk);
-    double* VrT = reinterpret_cast<double*>(w + 2 * blk);
-    double* YT = reinterpret_cast<double*>(w + 3 * blk);
+    const Plan q = eig_plan(n, r, ws);
+    const int p = q.p;
+    State* dst = q.dst;
+    double *Vt = q.Vt, *Wt = q.Wt;
     TK_CUDA(cudaMemsetAsync(dst, 0, sizeof(State), st));
-
     if (n <= kDirectMax) {
         const size_t sm = direct_smem((int)n);
         TK_CUDA(cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -419,19 +438,10 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
             TK_CHECK_LAUNCH();
             TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
         }
-        int it = kMinIters - 1;
-        while (true) {
-            const int batch = it == kMinIters - 1 ? 4 : kBatch;
-            for (int b = 0; b < batch && it < kMaxIters; ++b, ++it) {
-                k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
-                TK_CHECK_LAUNCH();
-                TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst,
-                                        st));
-            }
-            State hs;
-            TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
-            TK_CUDA(cudaStreamSynchronize(st));
-            if (hs.done || it >= kMaxIters) break;
+        for (int it = kMinIters - 1; it < kMinIters + 3; ++it) {  // first batch: 4 Rayleigh-Ritz steps
+            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
+            TK_CHECK_LAUNCH();
+            TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst, st));
         }
     } else {
         const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
@@ -443,24 +453,53 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
         TK_CHECK_LAUNCH();
         const size_t sm = rr_smem(p);
         TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int it = 0;
-        while (true) {
-            for (int b = 0; b < kBatch && it < kMaxIters; ++b, ++it) {
-                k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
-                TK_CHECK_LAUNCH();
-                RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, Vt, Wt, VrT, YT, U, lambda, sigma, dst};
-                k_rr<<<1, kThreads, sm, st>>>(a);
-                TK_CHECK_LAUNCH();
-            }
-            State hs;
-            TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
-            TK_CUDA(cudaStreamSynchronize(st));
-            if (hs.done || it >= kMaxIters) break;
+        for (int it = 0; it < kBatch; ++it) {
+            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
+            TK_CHECK_LAUNCH();
+            RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, Vt, Wt, q.VrT, q.YT, U, lambda, sigma, dst};
+            k_rr<<<1, kThreads, sm, st>>>(a);
+            TK_CHECK_LAUNCH();
         }
     }
+    return TUCKER_OK;
+}
+
+int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                   cudaStream_t st, tucker_info* info, int slot) {
+    TK_PROF(TUCKER_PROF_EIG, st);
+    using namespace eig;
+    const Plan q = eig_plan(n, r, ws);
+    const int p = q.p;
+    State* dst = q.dst;
     State hs;
     TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
     TK_CUDA(cudaStreamSynchronize(st));
+    if (n > kDirectMax) {  // continue in batches while not converged
+        const bool cl = eig_cluster_supported(n);
+        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
+        int it = cl ? kMinIters + 3 : kBatch;
+        if (!cl) {
+            const size_t sm = rr_smem(p);
+            TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        }
+        while (!hs.done && it < kMaxIters) {
+            for (int b = 0; b < kBatch && it < kMaxIters; ++b, ++it) {
+                k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, p, n, dst);
+                TK_CHECK_LAUNCH();
+                if (cl) {
+                    TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, q.Vt, q.Wt, U, lambda, sigma,
+                                            dst, st));
+                } else {
+                    RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, dst};
+                    const size_t sm = rr_smem(p);
+                    k_rr<<<1, kThreads, sm, st>>>(a);
+                    TK_CHECK_LAUNCH();
+                }
+            }
+            TK_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(State), cudaMemcpyDeviceToHost, st));
+            TK_CUDA(cudaStreamSynchronize(st));
+        }
+    }
     if (info) {
         info->iters[slot] = hs.iters;
         info->converged[slot] = hs.converged;
@@ -470,6 +509,12 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
         info->lambda1[slot] = hs.lambda1;
     }
     return hs.converged ? TUCKER_OK : TUCKER_ERR_NOCONV;
+}
+
+int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+               size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot) {
+    TK_RC(launch_eig_begin(n, G, r, U, lambda, sigma, ws, ws_bytes, st));
+    return launch_eig_end(n, G, r, U, lambda, sigma, ws, st, info, slot);
 }
 
 }  // namespace tk

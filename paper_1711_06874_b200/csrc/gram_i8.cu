@@ -1073,14 +1073,15 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
 
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
 
-cudaStream_t side_stream() {
-    static cudaStream_t s[64] = {};
+cudaStream_t side_stream(int which) {
+    static cudaStream_t s[64][2] = {};
     static std::mutex mu;
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (which < 0 || which > 1 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     std::lock_guard<std::mutex> lk(mu);
-    if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) s[dev] = nullptr;
-    return s[dev];
+    cudaStream_t& x = s[dev][which];
+    if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
+    return x;
 }
 
 // G (n_m x n_m, both triangles) of one mode.  mx: row maxima (nullptr: computed into ws).

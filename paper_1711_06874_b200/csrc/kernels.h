@@ -67,8 +67,8 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
                          cudaStream_t st, const std::function<int(const int*, int)>& on_phase);
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
-// Per-device non-blocking side stream of the library (created once).
-cudaStream_t side_stream();
+// Per-device non-blocking side streams of the library (which = 0, 1; created once).
+cudaStream_t side_stream(int which);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
 bool gram_use_i8(const int64_t n[3]);
@@ -93,6 +93,12 @@ int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const dou
 // Top-r eigenpairs of a symmetric PSD n x n matrix (dev).  iters/resid/... reported in `info`
 // slot `slot`.
 size_t eig_ws_bytes(int64_t n, int r);
+// Split form: begin enqueues the first pass without host synchronisation, end synchronises,
+// continues while not converged and reports (launch_eig = begin + end).
+int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                     size_t ws_bytes, cudaStream_t st);
+int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                   cudaStream_t st, tucker_info* info, int slot);
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma,
                void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot);
 

@@ -165,7 +165,7 @@ def test_stage_profiler_and_engine_switch(T):
     finally:
         T.profile_enable(False)
     p = T.profile_read()
-    assert p["i8_gemm"][1] == 3 and p["i8_residues"][1] >= 2 and p["i8_rowmax"][1] == 1 and p["eig"][1] == 3
+    assert p["i8_gemm"][1] == 3 and p["i8_residues"][1] >= 2 and p["i8_rowmax"][1] == 1 and p["eig"][1] >= 3
     assert p["dmma_gram"][1] == 0 and all(v[0] >= 0.0 for v in p.values())
     assert p["i8_gemm"][0] > 0.0
     assert T.profile_read()["i8_gemm"] == (0.0, 0)  # cleared; disabled: nothing recorded
