@@ -8,7 +8,9 @@
 //   BCGS2    Q = orth(Y)                    (block classical Gram–Schmidt twice: blocks of 8
 //                                            columns, one pass over the earlier columns per
 //                                            block projection, CGS2 inside a block; fixed-order
-//                                            reductions)
+//                                            reductions; columns the Kahan–Parlett test finds
+//                                            dependent on earlier blocks are replaced by
+//                                            pseudo-random vectors and projected block-wise)
 //   pass 2   B = F_(m) Q                    (n_m x p, split-K partials + fixed-order reduce)
 //   SVD      B = U~ Sigma W^T               (one-sided Jacobi in a thread-block cluster: no
 //                                            squaring, small singular values keep their accuracy)
@@ -142,74 +144,109 @@ __global__ void __launch_bounds__(kNT) k_cgs_finish(double* __restrict__ Yt, int
     if (blockIdx.x == 0 && threadIdx.x == 0 && ok) *accepted = 1;
 }
 
+// Eight block sums at once, bitwise equal to eight block_sum() calls (same shuffle trees, same
+// warp order) with two barriers instead of sixteen.  red: >= 8 * 33 doubles.  Result in out[0..7]
+// (valid on thread 0).
+__device__ __forceinline__ void block_sum8(const double (&v)[8], double* red, double (&out)[8]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    double w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = warp_sum(v[u]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) red[u * 33 + warp] = w[u];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            double t = lane < nw ? red[u * 33 + lane] : 0.0;
+            out[u] = warp_sum(t);
+        }
+    }
+}
+
 // The column-by-column CGS2 of one block (columns k in [c0, c0 + bb)) in a single cooperative
 // launch: the same arithmetic as k_cgs_dots / k_reduce_h / k_cgs_update / k_cgs_finish (same row
 // ranges, same fixed-order block and shuffle reductions — bitwise the same result), with grid-wide
 // barriers instead of kernel boundaries.  Every CTA reduces the per-CTA partials itself (same
 // order), so the projection coefficients and the accept decision need no broadcast.
+// Three grid barriers per column (after each pass's dots, after the second update): a CTA's dots,
+// update and normalisation touch only its own rows, with the same thread-to-row mapping, so the
+// data needs no barrier; only the partials do.  They are double-buffered — part[] by pass,
+// npart[] by attempt parity — so a fast CTA never overwrites partials a slow one still sums:
+// part[pass] is rewritten only after the barrier that follows its last reader, and npart[par]
+// only after the next attempt's second-update barrier.  part: 2 x nblk x 64, npart: 2 x 2 x nblk.
 __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, int64_t M, int c0, int bb,
                                                       double* __restrict__ part, double* __restrict__ npart,
                                                       const int* __restrict__ jstart_all) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double red[40];
+    __shared__ double red[8 * 33];
     __shared__ double h[64];
     __shared__ double tot_s, tot1_s;
     const int nblk = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t b0, b1;
     row_range(M, b0, b1);
+    int seq = 0;  // attempts so far (npart parity)
     for (int k = c0; k < c0 + bb; ++k) {
         double* y = Yt + (size_t)k * M;
-        for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int attempt = 0; attempt < 2; ++attempt, ++seq) {
             const int js = attempt == 0 ? jstart_all[k] : 0;  // a replaced column: full projection
+            double* np = npart + (size_t)(seq & 1) * 2 * nblk;
             for (int pass = 0; pass < 2; ++pass) {
                 if (k > 0) {
-                    // dots: part[blk][j] over this CTA's rows (as k_cgs_dots)
+                    double* pp = part + (size_t)pass * nblk * 64;
+                    // dots: pp[blk][j] over this CTA's rows (as k_cgs_dots)
                     for (int j0 = js; j0 < k; j0 += 8) {
                         double acc[8];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 4
                         for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
                             const double yi = y[i];
 #pragma unroll
                             for (int u = 0; u < 8; ++u)
                                 if (j0 + u < k) acc[u] = fma(Yt[(size_t)(j0 + u) * M + i], yi, acc[u]);
                         }
+                        double sums[8];
+                        block_sum8(acc, red, sums);
+                        if (threadIdx.x == 0)
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const double sum = block_sum(acc[u], red);
-                            if (threadIdx.x == 0 && j0 + u < k) part[(size_t)blockIdx.x * 64 + j0 + u] = sum;
-                        }
+                            for (int u = 0; u < 8; ++u)
+                                if (j0 + u < k) pp[(size_t)blockIdx.x * 64 + j0 + u] = sums[u];
                     }
                     grid.sync();
                     // h[j] = sum over blocks (as k_reduce_h: warp per j, lanes strided, shuffle tree)
                     for (int j = js + warp; j < k; j += kNT / 32) {
                         double sum = 0.0;
-                        for (int b = lane; b < nblk; b += 32) sum += part[(size_t)b * 64 + j];
+                        for (int b = lane; b < nblk; b += 32) sum += pp[(size_t)b * 64 + j];
                         sum = warp_sum(sum);
                         if (lane == 0) h[j] = sum;
                     }
                     for (int j = threadIdx.x; j < js; j += kNT) h[j] = 0.0;
                     __syncthreads();
                 }
-                // update (as k_cgs_update): y -= Q h, npart[pass][blk] = ||y||^2 of this CTA's rows
+                // update (as k_cgs_update): y -= Q h, np[pass][blk] = ||y||^2 of this CTA's rows
                 double ss = 0.0;
+#pragma unroll 2
                 for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
                     double yi = y[i];
+#pragma unroll 4
                     for (int j = js; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
                     y[i] = yi;
                     ss = fma(yi, yi, ss);
                 }
                 ss = block_sum(ss, red);
-                if (threadIdx.x == 0) npart[pass * nblk + blockIdx.x] = ss;
-                grid.sync();
+                if (threadIdx.x == 0) np[pass * nblk + blockIdx.x] = ss;
             }
+            grid.sync();
             // finish (as k_cgs_finish): Kahan-Parlett acceptance, normalise or replace
             if (threadIdx.x < 32) {
                 double sum = 0.0, sum1 = 0.0;
                 for (int b = threadIdx.x; b < nblk; b += 32) {
-                    sum1 += npart[b];
-                    sum += npart[nblk + b];
+                    sum1 += np[b];
+                    sum += np[nblk + b];
                 }
                 sum = warp_sum(sum);
                 sum1 = warp_sum(sum1);
@@ -222,10 +259,13 @@ __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, i
             const double tot = tot_s, tot1 = tot1_s;
             const bool ok = (tot > 1e-300 && tot >= 0.5 * tot1) || attempt == 1;
             const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+#pragma unroll 4
             for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT)
                 y[i] = ok ? y[i] * inv : hash_u(0x5eedull * (k + 1) + i);
-            grid.sync();
-            if (ok) break;
+            if (ok) {
+                ++seq;
+                break;
+            }
         }
     }
 }
@@ -246,47 +286,74 @@ __global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const dou
 
 // Block projection coefficients, per-CTA partials: part[blk][j * bb + t] = sum over this CTA's rows
 // of Q_j[i] Y_{c0+t}[i], j < c0, t < bb.  Rows are staged 32 at a time in shared memory (all
-// column segments contiguous, coalesced); each thread owns (j, t) pairs.
-__global__ void __launch_bounds__(kNT) k_block_dots(const double* __restrict__ Yt, int64_t M, int c0, int bb,
-                                                    double* __restrict__ part) {
-    __shared__ double tile[32][64 + 8 + 1];
+// column segments contiguous, coalesced).  Lane l owns j = l and j = l + 32 for all bb block
+// columns (16 register accumulators), warp w the rows w, w + 8, ... of each tile: per row two
+// shared loads of Q and eight broadcast loads of Y feed 16 FMAs.  The 8 warps' partials are summed
+// in warp order at the end (fixed order).
+__global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                    double* __restrict__ part, const int* __restrict__ run) {
+    if (run && !*run) return;
+    constexpr int kLd = 64 + 8 + 1;
+    __shared__ double tile[8 * 16 * 32];  // [row][col] (32 x kLd); then the cross-warp sum [w][h][t][lane]
+    double* red = tile;
     int64_t b0, b1;
     row_range(M, b0, b1);
     const int ncol = c0 + bb, npair = c0 * bb;
-    double acc[2] = {0.0, 0.0};  // pairs threadIdx.x and threadIdx.x + 256 (npair <= 56 * 8 = 448)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[h][t] = 0.0;
     for (int64_t r0 = b0; r0 < b1; r0 += 32) {
         const int rows = (b1 - r0) < 32 ? (int)(b1 - r0) : 32;
         for (int e = threadIdx.x; e < 32 * ncol; e += kNT) {
             const int c = e / 32, i = e % 32;
-            tile[i][c] = i < rows ? Yt[(size_t)c * M + r0 + i] : 0.0;
+            tile[i * kLd + c] = i < rows ? Yt[(size_t)c * M + r0 + i] : 0.0;
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int pr = threadIdx.x + kNT * u;
-            if (pr < npair) {
-                const int j = pr / bb, t = pr % bb;
-                double a = acc[u];
-                for (int i = 0; i < 32; ++i) a = fma(tile[i][j], tile[i][c0 + t], a);
-                acc[u] = a;
+        for (int rr = 0; rr < 4; ++rr) {
+            const double* row = tile + (warp + 8 * rr) * kLd;
+            double y[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) y[t] = t < bb ? row[c0 + t] : 0.0;
+            const double q0 = lane < c0 ? row[lane] : 0.0;
+            const double q1 = lane + 32 < c0 ? row[lane + 32] : 0.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                acc[0][t] = fma(q0, y[t], acc[0][t]);
+                acc[1][t] = fma(q1, y[t], acc[1][t]);
             }
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int pr = threadIdx.x + kNT * u;
-        if (pr < npair) part[(size_t)blockIdx.x * npair + pr] = acc[u];
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) red[((warp * 2 + h) * 8 + t) * 32 + lane] = acc[h][t];
+    __syncthreads();
+    for (int pr = threadIdx.x; pr < npair; pr += kNT) {
+        const int j = pr / bb, t = pr % bb, h = j >> 5, l = j & 31;
+        double sum = 0.0;
+        for (int w = 0; w < 8; ++w) sum += red[((w * 2 + h) * 8 + t) * 32 + l];
+        part[(size_t)blockIdx.x * npair + pr] = sum;
     }
 }
 
 // Y_{c0+t}[i] -= sum_j Q_j[i] H[j][t] on this CTA's rows, then per-CTA partial squared norms of
-// the updated block columns (cnpart[blk][t]).
-__global__ void __launch_bounds__(kNT) k_block_update(double* __restrict__ Yt, int64_t M, int c0, int bb,
-                                                      const double* __restrict__ H, double* __restrict__ cnpart) {
-    __shared__ double h[64 * 8];
+// the updated block columns (cnpart[blk][t]).  H is held in shared memory with row stride 8
+// (16-byte aligned pairs: one LDS.128 serves two block columns).
+__global__ void __launch_bounds__(kNT, 4) k_block_update(double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                      const double* __restrict__ H, double* __restrict__ cnpart,
+                                                      const int* __restrict__ run) {
+    if (run && !*run) return;
+    __shared__ __align__(16) double h[64 * 8];
     __shared__ double red[40];
-    for (int e = threadIdx.x; e < c0 * bb; e += kNT) h[e] = H[e];
+    for (int e = threadIdx.x; e < c0 * 8; e += kNT) {
+        const int j = e >> 3, t = e & 7;
+        h[e] = t < bb ? H[j * bb + t] : 0.0;
+    }
     __syncthreads();
     int64_t b0, b1;
     row_range(M, b0, b1);
@@ -297,11 +364,16 @@ __global__ void __launch_bounds__(kNT) k_block_update(double* __restrict__ Yt, i
         double y[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) y[t] = t < bb ? Yt[(size_t)(c0 + t) * M + i] : 0.0;
+#pragma unroll 2
         for (int j = 0; j < c0; ++j) {
             const double qj = Yt[(size_t)j * M + i];
+            const double2* hj = reinterpret_cast<const double2*>(h + j * 8);
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-                if (t < bb) y[t] = fma(-qj, h[j * bb + t], y[t]);
+            for (int t2 = 0; t2 < 4; ++t2) {
+                const double2 hh = hj[t2];
+                y[2 * t2] = fma(-qj, hh.x, y[2 * t2]);
+                y[2 * t2 + 1] = fma(-qj, hh.y, y[2 * t2 + 1]);
+            }
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -318,21 +390,62 @@ __global__ void __launch_bounds__(kNT) k_block_update(double* __restrict__ Yt, i
 }
 
 // After the two inter-block passes: column t keeps its block-local projection start c0 when
-// ||y''||^2 >= ||y'||^2 / 2 (Kahan–Parlett), else it is treated as dependent on the earlier
-// blocks: start 0 (the intra-block step then projects it against every earlier column, and its
-// own acceptance test replaces it by a pseudo-random vector if needed).
+// ||y''||^2 >= ||y'||^2 / 2 (Kahan–Parlett), else it is numerically in the span of the earlier
+// blocks.  With dep != nullptr the failing columns are flagged (dep[t], dep[8] = any) for a
+// block-wise replacement (k_block_replace + two more inter-block passes on those columns only);
+// jstart[c0 + t] = 0 sends a column that fails anyway to the full column-by-column projection.
 __global__ void k_block_check(const double* __restrict__ part1, const double* __restrict__ part2, int nblk, int bb,
-                              int c0, int* __restrict__ jstart) {
+                              int c0, int* __restrict__ jstart, int* __restrict__ dep, const int* __restrict__ run) {
+    if (run && !*run) return;
     const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp per column, lanes over blocks
-    if (t >= bb) return;
-    double n1 = 0.0, n2 = 0.0;
-    for (int b = lane; b < nblk; b += 32) {
-        n1 += part1[(size_t)b * 8 + t];
-        n2 += part2[(size_t)b * 8 + t];
+    int bad = 0;
+    if (t < bb) {
+        double n1 = 0.0, n2 = 0.0;
+        for (int b = lane; b < nblk; b += 32) {
+            n1 += part1[(size_t)b * 8 + t];
+            n2 += part2[(size_t)b * 8 + t];
+        }
+        n1 = warp_sum(n1);
+        n2 = warp_sum(n2);
+        const bool ok = n2 > 1e-300 && n2 >= 0.5 * n1;
+        if (lane == 0) {
+            jstart[c0 + t] = ok ? c0 : 0;
+            if (dep) dep[t] = !ok;
+            bad = !ok;
+        }
     }
-    n1 = warp_sum(n1);
-    n2 = warp_sum(n2);
-    if (lane == 0) jstart[c0 + t] = (n2 > 1e-300 && n2 >= 0.5 * n1) ? c0 : 0;
+    const int any = __syncthreads_or(bad);
+    if (dep && threadIdx.x == 0) dep[8] = any;
+}
+
+// Replace the flagged columns of the block by deterministic pseudo-random vectors (their content
+// was dependent on the earlier blocks to working precision).
+__global__ void __launch_bounds__(kNT) k_block_replace(double* __restrict__ Yt, int64_t M, int c0, int bb,
+                                                       const int* __restrict__ dep) {
+    if (!dep[8]) return;
+    int64_t b0, b1;
+    row_range(M, b0, b1);
+    for (int t = 0; t < bb; ++t) {
+        if (!dep[t]) continue;
+        double* y = Yt + (size_t)(c0 + t) * M;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) y[i] = hash_u(0x7e91ull * (c0 + t + 1) + i);
+    }
+}
+
+// H[j][t] = sum_s part[s][j * bb + t] for the flagged columns t, 0 for the others (their update
+// y -= Q H is then the identity).
+__global__ void k_sum_partials_dep(const double* __restrict__ part, int S, int c0, int bb, const int* __restrict__ dep,
+                                   double* __restrict__ out) {
+    if (!dep[8]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t len = (int64_t)c0 * bb;
+    for (int64_t o = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; o < len;
+         o += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double s = 0.0;
+        for (int q = lane; q < S; q += 32) s += part[(size_t)q * len + o];
+        s = warp_sum(s);
+        if (lane == 0) out[o] = dep[o % bb] ? s : 0.0;
+    }
 }
 
 // out[o] = sum_s part[s][o] for short outputs and many partials: warp per output, lanes strided
@@ -381,10 +494,10 @@ RefLayout ref_plan(const int64_t n[3], int p) {
     off += align_up((size_t)std::max<int64_t>(kSplit, n[0]) * nmax * p * 8, 256);
     L.V = off;
     off += align_up((size_t)nmax * p * 8, 256);
-    L.dots = off;
-    off += align_up((size_t)kBlk * 64 * 8, 256);
+    L.dots = off;  // the cooperative CGS2 double-buffers both partial arrays
+    off += align_up((size_t)2 * kBlk * 64 * 8, 256);
     L.npart = off;
-    off += align_up((size_t)2 * kBlk * 8, 256);
+    off += align_up((size_t)4 * kBlk * 8, 256);
     L.flags = off;
     off += 256;
     L.H = off;
@@ -392,9 +505,9 @@ RefLayout ref_plan(const int64_t n[3], int p) {
     L.Hpart = off;
     off += align_up((size_t)std::max(kSplit, kBlk) * 64 * kBS * 8, 256);
     L.cn = off;
-    off += align_up((size_t)2 * kBlk * 8 * 8, 256);
-    L.jst = off;
-    off += align_up((size_t)(64 + 1) * sizeof(int), 256);
+    off += align_up((size_t)4 * kBlk * 8 * 8, 256);
+    L.jst = off;  // jstart[64], jzero, dep[9] (at +80)
+    off += align_up((size_t)(80 + 16) * sizeof(int), 256);
     L.total = off;
     return L;
 }
@@ -455,20 +568,35 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
         const int64_t Kc = M / S;
         int* jstart = reinterpret_cast<int*>(w + L.jst);
         int* jzero = jstart + 64;
+        int* dep = jstart + 80;
         TK_CUDA(cudaMemsetAsync(jstart, 0, 65 * sizeof(int), st));
         for (int c0 = 0; c0 < p; c0 += kBS) {
             const int bb = std::min(kBS, p - c0);
-            double* YB = Yt + (size_t)c0 * M;
             if (c0 > 0) {
                 for (int pass = 0; pass < 2; ++pass) {
-                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart);
+                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart, nullptr);
                     TK_CHECK_LAUNCH();
                     k_sum_partials_warp<<<48, 256, 0, st>>>(Hpart, kBlk, (int64_t)c0 * bb, H);
                     TK_CHECK_LAUNCH();
-                    k_block_update<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, H, cn + (size_t)pass * kBlk * 8);
+                    k_block_update<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, H, cn + (size_t)pass * kBlk * 8, nullptr);
                     TK_CHECK_LAUNCH();
                 }
-                k_block_check<<<1, 256, 0, st>>>(cn, cn + (size_t)kBlk * 8, kBlk, bb, c0, jstart);
+                k_block_check<<<1, 256, 0, st>>>(cn, cn + (size_t)kBlk * 8, kBlk, bb, c0, jstart, dep, nullptr);
+                TK_CHECK_LAUNCH();
+                // dependent columns: replaced and projected block-wise (each earlier column read
+                // once per pass for the whole block, not once per column); device-side skip
+                k_block_replace<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, dep);
+                TK_CHECK_LAUNCH();
+                for (int pass = 0; pass < 2; ++pass) {
+                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart, dep + 8);
+                    TK_CHECK_LAUNCH();
+                    k_sum_partials_dep<<<48, 256, 0, st>>>(Hpart, kBlk, c0, bb, dep, H);
+                    TK_CHECK_LAUNCH();
+                    k_block_update<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, H, cn + (size_t)(2 + pass) * kBlk * 8, dep + 8);
+                    TK_CHECK_LAUNCH();
+                }
+                k_block_check<<<1, 256, 0, st>>>(cn + (size_t)2 * kBlk * 8, cn + (size_t)3 * kBlk * 8, kBlk, bb, c0,
+                                                 jstart, nullptr, dep + 8);
                 TK_CHECK_LAUNCH();
             }
             if (coop_ok) {  // one cooperative launch for the block's column-by-column CGS2
