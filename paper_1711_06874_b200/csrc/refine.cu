@@ -166,6 +166,23 @@ __device__ __forceinline__ void block_sum8(const double (&v)[8], double* red, do
     }
 }
 
+// Lane-strided sum of nblk <= kBlk partials x[b * stride] (b = lane, lane + 32, ...) in the
+// same order as the plain loop, with every load issued before the first add (one L2 round trip).
+__device__ __forceinline__ double lane_sum_partials(const double* x, int nblk, int stride, int lane) {
+    constexpr int kPer = (kBlk + 31) / 32;
+    double v[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int b = lane + 32 * q;
+        v[q] = b < nblk ? x[(size_t)b * stride] : 0.0;
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+        if (lane + 32 * q < nblk) sum += v[q];
+    return sum;
+}
+
 // The column-by-column CGS2 of one block (columns k in [c0, c0 + bb)) in a single cooperative
 // launch: the same arithmetic as k_cgs_dots / k_reduce_h / k_cgs_update / k_cgs_finish (same row
 // ranges, same fixed-order block and shuffle reductions — bitwise the same result), with grid-wide
@@ -219,8 +236,7 @@ __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, i
                     grid.sync();
                     // h[j] = sum over blocks (as k_reduce_h: warp per j, lanes strided, shuffle tree)
                     for (int j = js + warp; j < k; j += kNT / 32) {
-                        double sum = 0.0;
-                        for (int b = lane; b < nblk; b += 32) sum += pp[(size_t)b * 64 + j];
+                        double sum = lane_sum_partials(pp + j, nblk, 64, lane);
                         sum = warp_sum(sum);
                         if (lane == 0) h[j] = sum;
                     }
@@ -228,14 +244,32 @@ __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, i
                     __syncthreads();
                 }
                 // update (as k_cgs_update): y -= Q h, np[pass][blk] = ||y||^2 of this CTA's rows
+                // four rows per thread at a time, every load before the first store (y aliases Yt,
+                // so the compiler cannot hoist loads across the stores itself); per-row FMA order and
+                // the row order of ss as in k_cgs_update
                 double ss = 0.0;
+                for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 4 * kNT) {
+                    double yr[4];
+                    bool in[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        in[r] = i0 + r * kNT < b1;
+                        yr[r] = in[r] ? y[i0 + r * kNT] : 0.0;
+                    }
 #pragma unroll 2
-                for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT) {
-                    double yi = y[i];
-#pragma unroll 4
-                    for (int j = js; j < k; ++j) yi = fma(-h[j], Yt[(size_t)j * M + i], yi);
-                    y[i] = yi;
-                    ss = fma(yi, yi, ss);
+                    for (int j = js; j < k; ++j) {
+                        const double* qj = Yt + (size_t)j * M + i0;
+                        const double hj = h[j];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            if (in[r]) yr[r] = fma(-hj, qj[r * kNT], yr[r]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (in[r]) {
+                            y[i0 + r * kNT] = yr[r];
+                            ss = fma(yr[r], yr[r], ss);
+                        }
                 }
                 ss = block_sum(ss, red);
                 if (threadIdx.x == 0) np[pass * nblk + blockIdx.x] = ss;
@@ -243,11 +277,8 @@ __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, i
             grid.sync();
             // finish (as k_cgs_finish): Kahan-Parlett acceptance, normalise or replace
             if (threadIdx.x < 32) {
-                double sum = 0.0, sum1 = 0.0;
-                for (int b = threadIdx.x; b < nblk; b += 32) {
-                    sum1 += np[b];
-                    sum += np[nblk + b];
-                }
+                double sum1 = lane_sum_partials(np, nblk, 1, lane);
+                double sum = lane_sum_partials(np + nblk, nblk, 1, lane);
                 sum = warp_sum(sum);
                 sum1 = warp_sum(sum1);
                 if (threadIdx.x == 0) {
@@ -259,9 +290,14 @@ __global__ void __launch_bounds__(kNT, 4) k_cgs_block(double* __restrict__ Yt, i
             const double tot = tot_s, tot1 = tot1_s;
             const bool ok = (tot > 1e-300 && tot >= 0.5 * tot1) || attempt == 1;
             const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
-#pragma unroll 4
-            for (int64_t i = b0 + threadIdx.x; i < b1; i += kNT)
-                y[i] = ok ? y[i] * inv : hash_u(0x5eedull * (k + 1) + i);
+            for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 4 * kNT) {
+                double yr[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) yr[r] = i0 + r * kNT < b1 ? y[i0 + r * kNT] : 0.0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (i0 + r * kNT < b1) y[i0 + r * kNT] = ok ? yr[r] * inv : hash_u(0x5eedull * (k + 1) + i0 + r * kNT);
+            }
             if (ok) {
                 ++seq;
                 break;
@@ -286,35 +322,53 @@ __global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const dou
 
 // Block projection coefficients, per-CTA partials: part[blk][j * bb + t] = sum over this CTA's rows
 // of Q_j[i] Y_{c0+t}[i], j < c0, t < bb.  Rows are staged 32 at a time in shared memory (all
-// column segments contiguous, coalesced).  Lane l owns j = l and j = l + 32 for all bb block
+// column segments contiguous, coalesced) through a kDotStages-deep cp.async ring, so several tiles'
+// loads are in flight while one is consumed.  Lane l owns j = l and j = l + 32 for all bb block
 // columns (16 register accumulators), warp w the rows w, w + 8, ... of each tile: per row two
 // shared loads of Q and eight broadcast loads of Y feed 16 FMAs.  The 8 warps' partials are summed
-// in warp order at the end (fixed order).
+// in warp order at the end (fixed order).  Dynamic shared memory: block_dots_smem(ncol).
+constexpr int kDotStages = 3;
+__host__ __device__ constexpr int block_dots_ld(int ncol) { return ncol + 1; }
+size_t block_dots_smem(int ncol) {
+    const size_t ring = (size_t)kDotStages * 32 * block_dots_ld(ncol);
+    return 8 * (ring > 8 * 16 * 32 ? ring : 8 * 16 * 32);
+}
 __global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict__ Yt, int64_t M, int c0, int bb,
-                                                    double* __restrict__ part, const int* __restrict__ run) {
+                                                       double* __restrict__ part, const int* __restrict__ run) {
     if (run && !*run) return;
-    constexpr int kLd = 64 + 8 + 1;
-    __shared__ double tile[8 * 16 * 32];  // [row][col] (32 x kLd); then the cross-warp sum [w][h][t][lane]
-    double* red = tile;
+    extern __shared__ double dsm[];  // ring [stage][row][ld]; then the cross-warp sum [w][h][t][lane]
     int64_t b0, b1;
     row_range(M, b0, b1);
-    const int ncol = c0 + bb, npair = c0 * bb;
+    const int ncol = c0 + bb, npair = c0 * bb, ld = block_dots_ld(ncol);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntile = (int)((b1 - b0 + 31) / 32);
+    auto issue = [&](int tt) {
+        if (tt < ntile) {
+            double* st = dsm + (size_t)(tt % kDotStages) * 32 * ld;
+            const int64_t r0 = b0 + (int64_t)tt * 32;
+            for (int e = threadIdx.x; e < 32 * ncol; e += kNT) {
+                const int c = e >> 5, i = e & 31;
+                const bool v = r0 + i < b1;
+                cp_async8(st + i * ld + c, Yt + (size_t)c * M + (v ? r0 + i : b0), v);
+            }
+        }
+        cp_async_commit();  // (empty groups keep the wait count uniform)
+    };
     double acc[2][8];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[h][t] = 0.0;
-    for (int64_t r0 = b0; r0 < b1; r0 += 32) {
-        const int rows = (b1 - r0) < 32 ? (int)(b1 - r0) : 32;
-        for (int e = threadIdx.x; e < 32 * ncol; e += kNT) {
-            const int c = e / 32, i = e % 32;
-            tile[i * kLd + c] = i < rows ? Yt[(size_t)c * M + r0 + i] : 0.0;
-        }
-        __syncthreads();
+#pragma unroll
+    for (int tt = 0; tt < kDotStages - 1; ++tt) issue(tt);
+    for (int tt = 0; tt < ntile; ++tt) {
+        cp_async_wait<kDotStages - 2>();
+        __syncthreads();  // tile tt landed for all threads; tile tt-1's stage is free
+        issue(tt + kDotStages - 1);
+        const double* tile = dsm + (size_t)(tt % kDotStages) * 32 * ld;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
-            const double* row = tile + (warp + 8 * rr) * kLd;
+            const double* row = tile + (warp + 8 * rr) * ld;
             double y[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) y[t] = t < bb ? row[c0 + t] : 0.0;
@@ -326,8 +380,10 @@ __global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict_
                 acc[1][t] = fma(q1, y[t], acc[1][t]);
             }
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();
+    double* red = dsm;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -364,15 +420,20 @@ __global__ void __launch_bounds__(kNT, 4) k_block_update(double* __restrict__ Yt
         double y[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) y[t] = t < bb ? Yt[(size_t)(c0 + t) * M + i] : 0.0;
-#pragma unroll 2
-        for (int j = 0; j < c0; ++j) {
-            const double qj = Yt[(size_t)j * M + i];
-            const double2* hj = reinterpret_cast<const double2*>(h + j * 8);
+        for (int j0 = 0; j0 < c0; j0 += 4) {  // four loads in flight, then the FMAs (same order)
+            double q[4];
 #pragma unroll
-            for (int t2 = 0; t2 < 4; ++t2) {
-                const double2 hh = hj[t2];
-                y[2 * t2] = fma(-qj, hh.x, y[2 * t2]);
-                y[2 * t2 + 1] = fma(-qj, hh.y, y[2 * t2 + 1]);
+            for (int u = 0; u < 4; ++u) q[u] = j0 + u < c0 ? Yt[(size_t)(j0 + u) * M + i] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (j0 + u >= c0) break;
+                const double2* hj = reinterpret_cast<const double2*>(h + (j0 + u) * 8);
+#pragma unroll
+                for (int t2 = 0; t2 < 4; ++t2) {
+                    const double2 hh = hj[t2];
+                    y[2 * t2] = fma(-q[u], hh.x, y[2 * t2]);
+                    y[2 * t2 + 1] = fma(-q[u], hh.y, y[2 * t2 + 1]);
+                }
             }
         }
 #pragma unroll
@@ -574,7 +635,11 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
             const int bb = std::min(kBS, p - c0);
             if (c0 > 0) {
                 for (int pass = 0; pass < 2; ++pass) {
-                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart, nullptr);
+                    static const bool dots_attr = cudaFuncSetAttribute(k_block_dots,
+                                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                       (int)block_dots_smem(64 + 8)) == cudaSuccess;
+                    if (!dots_attr) return TUCKER_ERR_CUDA;
+                    k_block_dots<<<kBlk, kNT, block_dots_smem(c0 + bb), st>>>(Yt, M, c0, bb, Hpart, nullptr);
                     TK_CHECK_LAUNCH();
                     k_sum_partials_warp<<<48, 256, 0, st>>>(Hpart, kBlk, (int64_t)c0 * bb, H);
                     TK_CHECK_LAUNCH();
@@ -588,7 +653,7 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
                 k_block_replace<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, dep);
                 TK_CHECK_LAUNCH();
                 for (int pass = 0; pass < 2; ++pass) {
-                    k_block_dots<<<kBlk, kNT, 0, st>>>(Yt, M, c0, bb, Hpart, dep + 8);
+                    k_block_dots<<<kBlk, kNT, block_dots_smem(c0 + bb), st>>>(Yt, M, c0, bb, Hpart, dep + 8);
                     TK_CHECK_LAUNCH();
                     k_sum_partials_dep<<<48, 256, 0, st>>>(Hpart, kBlk, c0, bb, dep, H);
                     TK_CHECK_LAUNCH();
