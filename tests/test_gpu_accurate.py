@@ -76,3 +76,33 @@ def test_accurate_beats_gram_floor_1024(T):
         assert np.max(np.abs(U.T @ U - np.eye(40))) <= 1e-12
         s = to_np(ac.sigma[m])
         assert np.all(np.diff(s) <= 0)
+
+
+@pytest.mark.parametrize("terms", [1, 3])
+def test_accurate_low_rank_forces_replacement(T, orc, terms):
+    """An exact low-rank tensor (sum of `terms` seeded rank-1 products) with p = r + q far above its
+    rank: after the first `terms` columns every Y column is dependent to working precision, so the
+    block-wise replacement (k_block_check / k_block_replace) and the in-block Kahan–Parlett
+    replacement both run.  The leading singular values match LAPACK's SVD of the unfoldings, the
+    rest are noise (<= 1e-13 sigma_1), the factors stay orthonormal and E is ~eps."""
+    rng = np.random.default_rng(1711 + terms)
+    n = (200, 150, 130)
+    Fo = np.zeros(n)
+    for _ in range(terms):
+        a, b, c = (rng.standard_normal(m) for m in n)
+        Fo += np.einsum("i,j,k->ijk", a, b, c)
+    g = GridSpec(n, (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    r = (20, 20, 20)
+    F = torch.from_numpy(Fo).cuda()
+    res = T.hosvd_accurate(g, r, F, iters=1)
+    assert res.rc == 0, res.info
+    hs = orc.hosvd_svd(Fo, r)
+    for m in range(3):
+        s_ref = np.sqrt(np.maximum(hs.lam[m], 0.0))
+        s = to_np(res.sigma[m])
+        assert np.max(np.abs(s[:terms] - s_ref[:terms])) <= 1e-13 * s_ref[0], m
+        assert np.max(np.abs(s[terms:])) <= 1e-13 * s_ref[0], m
+        U = to_np(res.U[m])
+        assert np.max(np.abs(U.T @ U - np.eye(r[m]))) <= 1e-12
+    e = to_np(T.error(g, r, F, res.U, res.core))
+    assert e[0] <= 1e-14, e
