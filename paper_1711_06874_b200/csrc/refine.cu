@@ -537,7 +537,7 @@ struct RefLayout {
     int S2;
 };
 
-constexpr int kSplit = 64;  // split-K factor of pass 2 and of the block projections
+constexpr int kSplit = 256;  // split-K factor of pass 2 (>= 6.9 waves of the skinny DMMA tiles at n_m = 1024)
 constexpr int kBS = 8;      // block width of the block Gram–Schmidt
 
 RefLayout ref_plan(const int64_t n[3], int p) {
@@ -624,7 +624,9 @@ int launch_refine_mode(const int64_t n[3], int m, const double* F, const double*
         // ---- block CGS2 of the p columns of Y (each column contiguous in Yt): blocks of kBS
         // columns; two inter-block passes (H = Q_<c0^T Y_B from per-CTA partials summed in a fixed
         // order, Y_B -= Q_<c0 H), then column-by-column CGS2 inside the block.
-        int S = kSplit;  // split of the M-long contractions: the largest divisor of M not above kSplit
+        // split of the M-long contractions: the largest divisor of M not above kSplit that keeps
+        // chunks of >= 512
+        int S = (int)std::min<int64_t>(kSplit, std::max<int64_t>(1, M / 512));
         while (M % S) --S;
         const int64_t Kc = M / S;
         int* jstart = reinterpret_cast<int*>(w + L.jst);
