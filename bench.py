@@ -249,6 +249,13 @@ def run_ours(args, rank, world, local):
             except Exception:
                 traffic = None
         gram_stage_ms = sum(st.get(s, 0.0) for s in ("i8_rowmax", "i8_residues", "i8_gemm", "i8_crt")) / 3
+        lib_i8 = None  # context: cuBLASLt's own sustained INT8 GEMM on this pool (tools/probe_int8_peak.py)
+        ip = os.path.join(ROOT, "profiles", "int8_peak_measured.json")
+        if os.path.exists(ip):
+            try:
+                lib_i8 = max(r["sustained_tops"] for r in json.load(open(ip))["runs"])
+            except Exception:
+                lib_i8 = None
         roof = {"bound": "tensor", "kernel": "k_i8_gemm (tcgen05 kind::i8, CTA pairs), per launch",
                 "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src, "ops_per_launch": ops_launch, "launch_ms": launch_ms,
@@ -256,6 +263,9 @@ def run_ours(args, rank, world, local):
                 "fp64_equivalent_gram_tflops": gram_flops_fp64 / (gram_stage_ms * 1e-3) / 1e12,
                 "fp64_equivalent_note": "FP64 SYRK flops of one mode / the whole emulated Gram stage (row maxima, "
                                         "residues, int8 Grams, CRT) vs the 37.2 TF/s FP64 (DMMA) peak"}
+        if lib_i8:
+            roof["cublaslt_int8_sustained_tops"] = lib_i8
+            roof["frac_of_cublaslt_int8_sustained"] = achieved / lib_i8
     else:
         launch_ms = prof["dmma_gram"][0] / prof["dmma_gram"][1]
         achieved = gram_flops_fp64 / (launch_ms * 1e-3) / 1e12
