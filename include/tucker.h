@@ -81,7 +81,8 @@ enum {
     TUCKER_ERR_SIZE = 4,        /* workspace too small / size overflow                       */
     TUCKER_ERR_NOCONV = 5,      /* eigensolver hit its iteration cap (best iterate returned) */
     TUCKER_ERR_CUDA = 6,        /* a CUDA runtime/driver call failed                         */
-    TUCKER_ERR_UNSUPPORTED = 7  /* e.g. r_m too large for the eigensolver block (r_m > 56)   */
+    TUCKER_ERR_UNSUPPORTED = 7, /* e.g. r_m too large for the eigensolver block (r_m > 56)   */
+    TUCKER_ERR_COLLECTIVE = 8   /* the caller's all-reduce callback reported a failure       */
 };
 
 /* Per-mode eigensolver report (host struct, optional). */
@@ -190,6 +191,39 @@ TUCKER_API int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* 
 TUCKER_API int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
                        const double* U1, const double* U2, const double* U3, const double* core, double* out3,
                        void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Row (e): ONE fused HOSVD (a-7, F never stored) sharded over `nshards` ranks,
+ * one process per GPU.  Every rank makes the same call with its own `shard` in [0, nshards).
+ * The work units — the residue super-chunks of each mode's unfolding (INT8 Gram route) and the
+ * i-slab chunks of the core and of the error — go round-robin to the ranks; the exchange steps
+ * (§8(e): "Grams: all-reduce of the n_m x n_m partials", "TTM1: ... all-reduce of r-sized
+ * intermediates", "Error: a scalar all-reduce") are all-reduces the CALLER performs through
+ * `allreduce` (e.g. torch.distributed over NCCL):
+ *   - per mode, the exact per-modulus residue sums of the Gram (int32, SUM; 16 x tiles x 512 x 256),
+ *     then folded mod p_l and reconstructed by the CRT on every rank;
+ *   - non-centred grids only: the row maxima of the three unfoldings (int32, MAX);
+ *   - T2 = F x2 U2^T x3 U3^T (n1 x r2 r3 doubles, SUM; rows off a rank's slabs are zero);
+ *   - with err3 != NULL, the per-tile error partials (doubles, SUM; zero off the rank's slabs).
+ * Integer sums are exact and the floating-point ones add zeros, so every rank returns the bitwise
+ * result of tucker_hosvd_fused (+ tucker_error_fused).  The eigensolves are replicated.
+ * allreduce(user, ws_offset, count, dtype, op): reduce `count` elements of `dtype` in place at
+ * byte offset `ws_offset` of `ws` (device memory of this rank) across the ranks; called from the
+ * calling host thread after `stream` has been synchronised, the same number of times and in the
+ * same order on every rank; must return 0 when the reduced data is in place.  nshards == 1 never
+ * calls it (it may then be NULL).
+ * Workspace >= tucker_workspace_size_fused(grid, r).  Requires the INT8 fused Gram route
+ * (n_m <= 16384, engine not forced to DMMA): else TUCKER_ERR_UNSUPPORTED.  Errors as
+ * tucker_hosvd_fused, plus INVALID_ARG (nshards < 1, shard out of range, nshards > 1 and no
+ * callback) and TUCKER_ERR_COLLECTIVE (the callback returned non-zero; the call stops there).
+ */
+enum { TUCKER_DT_INT32 = 0, TUCKER_DT_F64 = 1 };
+enum { TUCKER_RED_SUM = 0, TUCKER_RED_MAX = 1 };
+typedef int (*tucker_allreduce_fn)(void* user, int64_t ws_offset, int64_t count, int32_t dtype, int32_t op);
+TUCKER_API int tucker_hosvd_fused_sharded(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3],
+                       int32_t shard, int32_t nshards, tucker_allreduce_fn allreduce, void* user, double* U1,
+                       double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
+                       double* err3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
 /* ------------------------------------------------------------------------------------------
  * NEXT f1: Tucker-ALS (HOOI) sweeps, the paper's second stage after HOSVD: for each

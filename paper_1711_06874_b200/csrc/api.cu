@@ -534,6 +534,53 @@ int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* kernel, con
     return worst;
 }
 
+int tucker_hosvd_fused_sharded(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], int32_t shard,
+                               int32_t nshards, tucker_allreduce_fn allreduce, void* user, double* U1, double* U2,
+                               double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, double* err3,
+                               void* ws, size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    if (nshards < 1 || shard < 0 || shard >= nshards || (nshards > 1 && !allreduce)) return TUCKER_ERR_INVALID_ARG;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    const FusedLayout L = plan_fused(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    if (!L.i8_bytes) return TUCKER_ERR_UNSUPPORTED;  // the shardable Gram is the INT8 fused route
+    if (info) std::memset(info, 0, sizeof(*info));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Shard sh;
+    sh.index = shard;
+    sh.count = nshards;
+    char* const wsb = static_cast<char*>(ws);
+    sh.allreduce = [&](void* p, int64_t count, int dtype, int op) -> int {
+        const int64_t off = static_cast<char*>(p) - wsb;
+        return allreduce(user, off, count, dtype, op);
+    };
+    const KParams kp = fused_kparams(grid, kernel);
+    TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
+                           reinterpret_cast<double*>(at(ws, L.cheb)), st));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    double* G = reinterpret_cast<double*>(at(ws, L.G));
+    void* scr = at(ws, L.scratch);
+    int worst = TUCKER_OK;
+    auto eig_mode = [&](int m) -> int {  // replicated: the same G on every rank gives the same U_m
+        const int rc = launch_eig(grid->n[m], G, r[m], U[m], nullptr, S[m], scr, L.scratch_bytes, st, info, m);
+        if (rc == TUCKER_ERR_NOCONV) worst = rc;
+        else if (rc != TUCKER_OK) return rc;
+        return TUCKER_OK;
+    };
+    const I8Gen ig{kp, reinterpret_cast<const double*>(at(ws, L.cheb)), reinterpret_cast<const double*>(at(ws, L.nodes))};
+    TK_RC(launch_gram_i8_fused_modes(grid->n, ig, G, at(ws, L.i8), L.i8_bytes, st, 0, 2, eig_mode, &sh));
+    const FusedGen gen = fused_gen(grid, kp, L, ws);
+    TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st, nullptr, nullptr,
+                               &sh));
+    if (err3)
+        TK_RC(launch_error_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, err3, scr, L.scratch_bytes, st, &sh));
+    return worst;
+}
+
 int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], const double* U1,
                        const double* U2, const double* U3, const double* core, double* out3, void* ws,
                        size_t ws_bytes, void* stream) {
@@ -686,6 +733,7 @@ const char* tucker_strerror(int code) {
         case TUCKER_ERR_NOCONV: return "eigensolver did not converge (best iterate returned)";
         case TUCKER_ERR_CUDA: return "CUDA runtime/driver error";
         case TUCKER_ERR_UNSUPPORTED: return "unsupported configuration";
+        case TUCKER_ERR_COLLECTIVE: return "the caller's all-reduce callback failed";
         default: return "unknown error code";
     }
 }

@@ -935,7 +935,7 @@ struct ModeGemm {
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
-    int run(int64_t s, int64_t Kc) {
+    int run(bool first, int64_t Kc) {
         PFN_tmapEncodeTiled enc = tmap_encoder();
         if (!enc) return TUCKER_ERR_CUDA;
         // residues [NMOD][K-block][rows][128 B]: 4-D map (byte, row, K-block, modulus); a box of
@@ -959,7 +959,20 @@ struct ModeGemm {
         }
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
-        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, s == 0 ? 1 : 0);
+        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, first ? 1 : 0);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    }
+    // Row (e): combine the ranks' residue sums (each in [0, p)) by the caller's all-reduce, fold
+    // the sum (< ranks * p) back into [0, p); `have` = this rank ran a super-chunk (else its
+    // contribution is zero).
+    int combine(const Shard& sh, bool have) {
+        const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
+        if (!have) TK_CUDA(cudaMemsetAsync(Racc, 0, (size_t)tot * 4, st));
+        TK_CUDA(cudaStreamSynchronize(st));
+        if (sh.allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
+        TK_PROF(TUCKER_PROF_I8_CRT, st);
+        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(nullptr, Racc, p.ntiles, 0, 0);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -978,18 +991,23 @@ inline const uint32_t* mode_max(const uint32_t* mx, const int64_t n[3], int m) {
 
 // G_m (both triangles) on `st`; mx: row maxima of the three unfoldings.  produce(k0, Kc, R)
 // enqueues the residues of unfolding columns [k0, k0 + Kc) into R (K-block-major, column 0 = k0).
+// shard (row e): this rank's super-chunks only (s % count == index), then the combine step.
 template <class Produce>
 int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
-                   double* G, cudaStream_t st, Produce&& produce) {
+                   double* G, cudaStream_t st, Produce&& produce, const Shard* shard = nullptr) {
     ModeGemm g{n, m, p, mode_max(mx, n, m), reinterpret_cast<int8_t*>(base + w.off_R),
                reinterpret_cast<int16_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
                reinterpret_cast<int2*>(base + w.off_utab), 0, st};
     TK_RC(g.init());
+    bool first = true;
     for (int64_t s = 0; s < p.nsuper; ++s) {
+        if (shard && !shard->owns(s)) continue;
         const int64_t k0 = s * p.Ksc, Kc = std::min(p.Ksc, p.Kfull - k0);
         TK_RC(produce(k0, Kc, g.R));
-        TK_RC(g.run(s, Kc));
+        TK_RC(g.run(first, Kc));
+        first = false;
     }
+    if (shard && shard->sharded()) TK_RC(g.combine(*shard, !first));
     return g.crt(G);
 }
 
@@ -1152,7 +1170,9 @@ bool gram_i8_fused_supported(const int64_t n[3]) { return gram_i8_supported(n) &
 size_t gram_i8_fused_ws_bytes(const int64_t n[3]) { return i8::fused_i8_plan(n).total; }
 
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
-                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode) {
+                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
+                               const Shard* shard) {
+    const bool sharded = shard && shard->sharded();
     using namespace i8;
     if (!gram_i8_fused_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const FusedI8Plan f = fused_i8_plan(n);
@@ -1187,9 +1207,11 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
             TK_CHECK_LAUNCH();
             k_i8_mirror_max<<<(unsigned)ceil_div(n[0] + n[1] + n[2], 256), 256, 0, st>>>(m0, m1, m2, n[0], n[1], n[2]);
             TK_CHECK_LAUNCH();
-        } else {  // general grid: one generation pass over i-plane chunks
+        } else {  // general grid: one generation pass over i-plane chunks (sharded: this rank's
+                  // chunks, then a MAX all-reduce of the high words — all < 2^31, sign cleared)
             const int64_t pc = f.Pc[1];
             for (int64_t g0 = 0; g0 < n[0]; g0 += pc) {
+                if (sharded && !shard->owns(g0 / pc)) continue;
                 ChunkGeo geo{0, mirror, n[0], n[1], n[2], g0, pc, n[0]};
                 TK_RC(launch_gen_chunk(geo, gen.kp, gen.cheb, gen.x2, chunk, st));
                 const int64_t valid = std::min(pc, n[0] - g0);
@@ -1199,6 +1221,11 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
                 k_i8_rowmax<<<dim3((unsigned)valid, (unsigned)ceil_div(n[1], jblk)), 256, 0, st>>>(
                     chunk, valid, n[1], n[2], mx + g0, mx + n[0], mx + n[0] + n[1], jblk);
                 TK_CHECK_LAUNCH();
+            }
+            if (sharded) {
+                TK_CUDA(cudaStreamSynchronize(st));
+                if (shard->allreduce(mx, n[0] + n[1] + n[2], TUCKER_DT_INT32, TUCKER_RED_MAX) != 0)
+                    return TUCKER_ERR_COLLECTIVE;
             }
         }
     }
@@ -1221,7 +1248,7 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
                 TK_CHECK_LAUNCH();
             }
             return TUCKER_OK;
-        }));
+        }, shard));
         TK_RC(after_mode(m));
     }
     return TUCKER_OK;

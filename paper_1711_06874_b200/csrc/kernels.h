@@ -54,6 +54,19 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
 // disjoint from anything after_mode uses.
 int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* ws, size_t ws_bytes, cudaStream_t st,
                          const std::function<int(int)>& after_mode);
+// Row (e): one fused HOSVD sharded over `count` ranks.  Work units (residue super-chunks of a
+// mode's unfolding, i-slab chunks of the core and the error) go round-robin to the ranks; the
+// partial results are exact integer residue sums (Grams) or sums with zeros off the owner
+// (T2 rows, error partials), combined by the caller's all-reduce — so every rank ends with the
+// bitwise result of the single-GPU call.  allreduce(ptr, count, dtype, op) runs after the stream
+// has been synchronised (dtype TUCKER_DT_*, op TUCKER_RED_*).
+struct Shard {
+    int index = 0, count = 1;
+    std::function<int(void*, int64_t, int, int)> allreduce;
+    bool owns(int64_t unit) const { return count <= 1 || unit % count == index; }
+    bool sharded() const { return count > 1; }
+};
+
 // a-7 with the INT8 Gram (F never stored): generator of the plane chunks.
 struct I8Gen {
     KParams kp;
@@ -63,7 +76,8 @@ struct I8Gen {
 bool gram_i8_fused_supported(const int64_t n[3]);
 size_t gram_i8_fused_ws_bytes(const int64_t n[3]);
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
-                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode);
+                               cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
+                               const Shard* shard = nullptr);
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
                          cudaStream_t st, const std::function<int(const int*, int)>& on_phase);
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
@@ -134,13 +148,14 @@ struct FusedGen {
 };
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
-                         size_t ws_bytes, cudaStream_t st, double* t1_out = nullptr, double* t2_out = nullptr);
+                         size_t ws_bytes, cudaStream_t st, double* t1_out = nullptr, double* t2_out = nullptr,
+                         const Shard* shard = nullptr);
 // Tucker-ALS (f1): T1 = F x3 U3^T ((n1 n2) x r3) and Y1 = T1 x2 U2^T (n1 x r2 x r3), both stored.
 int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
                      double* T1, double* Y1, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen, const double* U1,
                       const double* U2, const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes,
-                      cudaStream_t st);
+                      cudaStream_t st, const Shard* shard = nullptr);
 size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs);
 
 // NEXT f1: Tucker-ALS sweeps from initial factors U (in/out); core and sigma of the last sweep.

@@ -389,7 +389,8 @@ int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, co
 // Core with F either materialised (F != nullptr) or generated slab-chunk by slab-chunk (gen).
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
-                         size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out) {
+                         size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out, const Shard* shard) {
+    const bool sharded = gen && shard && shard->sharded();
     TK_PROF(TUCKER_PROF_TTM, st);
     const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
     if (ws_bytes < ttm_ws_bytes(n, r) + chunk_b) return TUCKER_ERR_SIZE;
@@ -409,10 +410,13 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
                       st>>>(U3, n[2], r[2], RP, Bp);
     TK_CHECK_LAUNCH();
     ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT, 0, t1_out};
+    if (sharded)  // rows of the other ranks' slabs stay zero (the all-reduce adds zeros)
+        TK_CUDA(cudaMemsetAsync(JT > 1 ? part : T2, 0, JT > 1 ? JT * t2b : t2b, st));
     if (!gen) {
         TK_RC(launch_ttm12(a, n[0], st));
     } else {
         for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
+            if (sharded && !shard->owns(g0 / gen->Pc)) continue;
             const int64_t pc = std::min<int64_t>(gen->Pc, n[0] - g0);
             ChunkGeo geo = gen->geo;
             geo.g0 = g0;
@@ -428,6 +432,10 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
         k_t2_reduce<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(part, (int)JT, nout, total,
                                                                                               T2);
         TK_CHECK_LAUNCH();
+    }
+    if (sharded) {  // row (e): T2 rows are each computed by exactly one rank
+        TK_CUDA(cudaStreamSynchronize(st));
+        if (shard->allreduce(T2, n[0] * r[1] * r[2], TUCKER_DT_F64, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
     }
     if (!core) return TUCKER_OK;  // (Tucker-ALS: T1 / Y1 only)
     // TTM3: core (r1 x r2r3) = U1^T (r1 x n1) * T2 (n1 x r2r3)
@@ -725,7 +733,8 @@ int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const 
 
 int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen, const double* U1,
                       const double* U2, const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes,
-                      cudaStream_t st) {
+                      cudaStream_t st, const Shard* shard) {
+    const bool sharded = gen && shard && shard->sharded();
     const int64_t slabs = gen ? gen->Pc : n[0];
     const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
     if (ws_bytes < err_ws_bytes_slabs(n, r, slabs) + chunk_b) return TUCKER_ERR_SIZE;
@@ -761,10 +770,12 @@ int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, c
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     };
+    if (sharded) TK_CUDA(cudaMemsetAsync(partial, 0, (size_t)2 * nb * 8, st));  // others' tiles: zero
     if (!gen) {
         TK_RC(block(F, n[0], 0));
     } else {
         for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
+            if (sharded && !shard->owns(g0 / gen->Pc)) continue;
             const int64_t pc = std::min<int64_t>(gen->Pc, n[0] - g0);
             ChunkGeo geo = gen->geo;
             geo.g0 = g0;
@@ -772,6 +783,10 @@ int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, c
             TK_RC(launch_gen_chunk(geo, gen->kp, gen->cheb, gen->x2, chunk, st));
             TK_RC(block(chunk, pc, g0));
         }
+    }
+    if (sharded) {  // row (e): each (i, j-block) partial comes from exactly one rank
+        TK_CUDA(cudaStreamSynchronize(st));
+        if (shard->allreduce(partial, 2 * nb, TUCKER_DT_F64, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
     }
     errk::k_err_final<<<1, 1024, 0, st>>>(partial, nb, out3);
     TK_CHECK_LAUNCH();

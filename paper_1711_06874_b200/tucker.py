@@ -20,10 +20,12 @@ MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
 GRAM_AUTO, GRAM_DMMA, GRAM_INT8 = 0, 1, 2
 FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
-          4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED"}
+          4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED",
+          8: "TUCKER_ERR_COLLECTIVE"}
 EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
-           "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_workspace_size_als",
+           "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_hosvd_fused_sharded",
+           "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
            "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme",
            "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
@@ -57,6 +59,13 @@ class CInfo(ctypes.Structure):
 _lib = None
 
 
+# tucker_allreduce_fn(user, ws_offset, count, dtype, op) -> 0 on success
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                ctypes.c_int32)
+DT_INT32, DT_F64 = 0, 1
+RED_SUM, RED_MAX = 0, 1
+
+
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
     """Load the native library (raises if it has not been built)."""
     global _lib
@@ -88,6 +97,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_gram_fused": (ctypes.c_int, [pg, pk, i32, vp, vp, sz, vp]),
         "tucker_hosvd_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_error_fused": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "tucker_hosvd_fused_sharded": (ctypes.c_int, [pg, pk, pr, i32, i32, ALLREDUCE_FN, vp, vp, vp, vp, vp, vp,
+                                                      vp, vp, vp, vp, sz, vp, pi]),
         "tucker_workspace_size_als": (sz, [pg, pr]),
         "tucker_als": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
         "tucker_workspace_size_sym": (sz, [pg, pr]),
@@ -415,6 +426,59 @@ def hosvd_fused(grid, kernel, ranks, ws: torch.Tensor | None = None, stream=None
     if rc not in (0, 5):
         _check(rc, "tucker_hosvd_fused")
     return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+@dataclass
+class ShardedResult:
+    U: list
+    core: torch.Tensor
+    sigma: list
+    err: torch.Tensor | None
+    info: dict
+    rc: int
+    exchanges: list  # (ws_offset, count, dtype, op) of every all-reduce, in call order
+
+
+def hosvd_fused_sharded(grid, kernel, ranks, shard: int, nshards: int, group=None, with_error: bool = True,
+                        ws: torch.Tensor | None = None, stream=None) -> ShardedResult:
+    """Row (e): this rank's share of ONE fused HOSVD (+ error) sharded over `nshards` ranks
+    (tucker_hosvd_fused_sharded).  The exchange steps are torch.distributed all-reduces on views of
+    the workspace (`group`: the process group; NCCL over NVLink in production, gloo in the
+    one-GPU tests) — argument marshalling only, the arithmetic is the library's."""
+    lib = load()
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device="cuda") for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device="cuda") for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device="cuda")
+    err = torch.empty(3, dtype=torch.float64, device="cuda") if with_error else None
+    ws = ws if ws is not None else workspace_fused(grid, r)
+    exchanges, failure = [], []
+
+    def _allreduce(user, off, count, dtype, op):
+        try:
+            import torch.distributed as dist
+            tdt, esz = (torch.int32, 4) if dtype == DT_INT32 else (torch.float64, 8)
+            view = ws[off: off + count * esz].view(tdt)
+            dist.all_reduce(view, op=dist.ReduceOp.MAX if op == RED_MAX else dist.ReduceOp.SUM, group=group)
+            torch.cuda.synchronize()
+            exchanges.append((int(off), int(count), int(dtype), int(op)))
+            return 0
+        except Exception as e:  # reported to the library as TUCKER_ERR_COLLECTIVE
+            failure.append(e)
+            return 1
+
+    cb = ALLREDUCE_FN(_allreduce)
+    info = CInfo()
+    g, k = cgrid(grid), ckernel(kernel)
+    rc = lib.tucker_hosvd_fused_sharded(ctypes.byref(g), ctypes.byref(k), cranks(r), int(shard), int(nshards), cb,
+                                        None, _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core), _ptr(S[0]),
+                                        _ptr(S[1]), _ptr(S[2]), _ptr(err) if err is not None else None, _ptr(ws),
+                                        ws.numel(), _stream(stream), ctypes.byref(info))
+    if failure:
+        raise TuckerError(8, f"tucker_hosvd_fused_sharded: all-reduce failed: {failure[0]!r}")
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd_fused_sharded")
+    return ShardedResult(U, core, S, err, info.as_dict(), rc, exchanges)
 
 
 def error_fused(grid, kernel, ranks, U, core, ws=None, stream=None) -> torch.Tensor:

@@ -126,6 +126,16 @@ def test_validation_codes_next_rows(lib):
     assert lib.tucker_hosvd_accurate(ctypes.byref(g2), T.cranks((57, 4, 4)), d, d, d, d, d, d, d, d, 1, d, big, None,
                                      None) == 7
     assert lib.tucker_hosvd_accurate(ctypes.byref(g), r4, d, d, d, d, d, d, d, d, 1, d, 16, None, None) == 4
+    # row (e) sharded fused HOSVD: shard layout and the callback are validated first
+    cb, null_cb = T.ALLREDUCE_FN(lambda *a: 0), T.ALLREDUCE_FN()
+    for shard, nsh, fn in ((0, 0, cb), (2, 2, cb), (-1, 2, cb), (0, 2, null_cb)):
+        assert lib.tucker_hosvd_fused_sharded(ctypes.byref(g), ctypes.byref(k), r4, shard, nsh, fn, None, d, d, d, d,
+                                              d, d, d, None, d, big, None, None) == 1
+    assert lib.tucker_hosvd_fused_sharded(ctypes.byref(g), ctypes.byref(k), r_bad, 0, 1, null_cb, None, d, d, d, d,
+                                          d, d, d, None, d, big, None, None) == 3
+    assert lib.tucker_hosvd_fused_sharded(ctypes.byref(g), ctypes.byref(k), r4, 0, 1, null_cb, None, d, d, d, d,
+                                          d, d, d, None, d, 16, None, None) == 4
+    assert lib.tucker_strerror(8).decode().startswith("the caller")
     # spectral density domain
     sk = T.ckernel(KernelSpec.spectral(0.0, 0.4))
     assert lib.tucker_fill(ctypes.byref(g), ctypes.byref(sk), d, d, big, None) == 2
