@@ -152,9 +152,17 @@ def run_ours(args, rank, world, local):
     from paper_1711_06874_b200 import tucker as T
     from tucker_inputs import GridSpec, KernelSpec
 
+    # TUCKER_BENCH_BACKEND=gloo: a test mode for the N > 1 code paths on a one-GPU box (ranks share
+    # the GPU; no kernel waits on another rank; numbers from it are not bench values)
+    backend = os.environ.get("TUCKER_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T.load()
     T.set_gram_engine({"auto": T.GRAM_AUTO, "dmma": T.GRAM_DMMA, "int8": T.GRAM_INT8}[args.gram_engine])
     n, rr = args.n, args.r
@@ -393,6 +401,8 @@ def run_ours(args, rank, world, local):
         result["symmetric"] = [run_sym(T, nn, rr, stream) for nn in (n, 2 * n)]
     if not args.no_fused and world == 1:
         result["fused"] = run_fused(T, args.fused_n, rr, stream)
+    if not args.no_fused and world > 1:
+        result["fused_sharded"] = run_fused_sharded(T, args.fused_n, rr, stream, world)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
     if world > 1:
@@ -444,6 +454,44 @@ def run_fused(T, n: int, rr: int, stream) -> dict:
             "timed": "one hosvd_fused + error_fused call (CUDA events; stages from the library's stage timer), "
                      "after a warm-up Gram; gram_ms from three separate tucker_gram_fused calls (each INT8 call "
                      "includes its own row-maxima generation pass)"}
+
+
+def run_fused_sharded(T, n: int, rr: int, stream, world: int) -> dict:
+    """Row (e): ONE config-5f problem (n^3 fused HOSVD + error, F never stored) sharded over the
+    `world` ranks (tucker_hosvd_fused_sharded; exchanges = NCCL all-reduces of the Gram residue
+    sums, T2 and the error partials).  Strong scaling of one tensor; time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from tucker_inputs import GridSpec, KernelSpec
+    grid = GridSpec.cube(n, 1.0)
+    kern = KernelSpec.matern(1.5, 0.2)
+    ranks = (rr, rr, rr)
+    rank = dist.get_rank()
+    ws = T.workspace_fused(grid, ranks)
+    res = T.hosvd_fused_sharded(grid, kern, ranks, rank, world, ws=ws, stream=stream)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = T.hosvd_fused_sharded(grid, kern, ranks, rank, world, ws=ws, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    e = res.err.cpu().tolist()
+    eq = torch.tensor([e[0]], dtype=torch.float64, device="cuda")
+    emax, emin = eq.clone(), eq.clone()
+    dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(emin, op=dist.ReduceOp.MIN)
+    t = float(ms.item())
+    return {"workload": f"cfg5f_{n}cube_matern_nu1.5_ell0.2_fused_sharded", "grid": [n, n, n], "ranks": list(ranks),
+            "n_shards": world, "scaling": "strong", "value": grid.points / (t * 1e-3), "unit": UNIT, "ms": t,
+            "E": e[0], "E_identical_on_all_ranks": bool(emax.item() == emin.item()), "rc": res.rc,
+            "exchanges": len(res.exchanges),
+            "timed": "one tucker_hosvd_fused_sharded call with the error (CUDA events per rank, max over ranks) "
+                     "after a warm-up call; the exchanges are NCCL all-reduces issued from the library's callback"}
 
 
 def run_f4(T, grid, ranks, F, ws, stream) -> dict:
