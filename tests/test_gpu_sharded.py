@@ -113,3 +113,27 @@ def test_sharded_collective_failure_is_reported(T, knobs):
     with pytest.raises(T.TuckerError) as e:
         T.hosvd_fused_sharded(g, k, r, 0, 2)
     assert e.value.code == 8
+
+
+def test_bench_two_ranks_sharded_line(T, tmp_path):
+    """bench.py's N > 1 path (torchrun, 2 ranks) in its gloo test mode on the one GPU: the JSON line
+    reports n_gpus 2 and the sharded config-5f line (here 256^3) with the same E on both ranks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TUCKER_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--grid-n", "256", "--fused-n", "256", "--no-e2e", "--no-host-tensor"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    fs = d["fused_sharded"]
+    assert fs["n_shards"] == 2 and fs["rc"] == 0 and fs["E_identical_on_all_ranks"] and fs["exchanges"] == 5
+    ref = T.hosvd_fused(GridSpec.cube(256, 1.0), KernelSpec.matern(1.5, 0.2), (40, 40, 40))
+    e = T.error_fused(GridSpec.cube(256, 1.0), KernelSpec.matern(1.5, 0.2), (40, 40, 40), ref.U, ref.core)
+    assert fs["E"] == float(e[0].item())
