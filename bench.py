@@ -389,10 +389,10 @@ def run_ours(args, rank, world, local):
                                                      (x.cpu() for x in acc.sigma)]}
     if not args.no_f4 and world == 1:
         result["f4"] = run_f4(T, grid, ranks, F, ws, stream)
-    if not args.no_cfg4 and world == 1:
+    if not args.no_cfg4:
         del F
         torch.cuda.empty_cache()
-        result["config4"] = run_cfg4(T, stream)
+        result["config4"] = run_cfg4(T, stream, rank, world)
         F = None
     if not args.no_fused and world == 1 or not args.no_sym and world == 1:
         F = None
@@ -520,14 +520,17 @@ def run_f4(T, grid, ranks, F, ws, stream) -> dict:
     return {"grid": list(grid.n), "ranks": list(ranks), "unit": UNIT, "workloads": out}
 
 
-def run_cfg4(T, stream) -> dict:
+def run_cfg4(T, stream, rank: int = 0, world: int = 1) -> dict:
     """BASELINE config 4: 512^3, 16 seeded Matérn settings (R10), ranks 30 — the whole path per
-    setting (fill, 3 Grams, 3 eigensolves, core, error), timed over the batch."""
+    setting (fill, 3 Grams, 3 eigensolves, core, error), timed over the batch.  With world > 1 the
+    settings are replicas spread over the ranks (one setting set per GPU, settings
+    rank, rank + world, ...; time = max over ranks, strong scaling of the fixed batch)."""
     import torch
 
     from tucker_inputs import config4
     w = config4()
     g, r = w.grid, w.ranks
+    mine = w.kernels[rank::world]
     F = torch.empty(tuple(g.n), dtype=torch.float64, device="cuda")
     ws = T.workspace(g, r)
 
@@ -538,22 +541,33 @@ def run_cfg4(T, stream) -> dict:
 
     one(w.kernels[0])  # warm-up
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     errs, rcs = [], []
-    for k in w.kernels:
+    for k in mine:
         res, err = one(k)
         errs.append(err)
         rcs.append(res.rc)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    e_lo = min(float(e[0]) for e in errs) if errs else float("inf")
+    e_hi = max(float(e[0]) for e in errs) if errs else float("-inf")
+    if world > 1:
+        import torch.distributed as dist
+        red = torch.tensor([ms, -e_lo, e_hi], dtype=torch.float64, device="cuda")
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+        ms, e_lo, e_hi = float(red[0]), -float(red[1]), float(red[2])
     pts = len(w.kernels) * g.points
     del F, ws
     torch.cuda.empty_cache()
     return {"workload": w.name, "settings": len(w.kernels), "ranks": list(r), "value": pts / (ms * 1e-3),
-            "unit": UNIT, "ms_total": ms, "ms_per_setting": ms / len(w.kernels), "rc": rcs,
-            "E_range": [min(float(e[0]) for e in errs), max(float(e[0]) for e in errs)]}
+            "unit": UNIT, "ms_total": ms, "ms_per_setting": ms * world / len(w.kernels), "rc": rcs,
+            "n_gpus": world, "E_range": [e_lo, e_hi]}
 
 
 def run_sym(T, n: int, rr: int, stream, reps: int = 3) -> dict:
