@@ -238,3 +238,32 @@ def test_gram_i8_extreme_aspect(T, orc, shape):
         A = unfold(F, m)
         assert np.array_equal(G, G.T)
         assert np.all(np.abs(G - R) <= _bound(A, 50)), (shape, m)
+
+
+def test_gram_i8_maximum_rows(T, orc):
+    """The largest mode the INT8 route takes, n_m = 16384 (64 x 32 pair tiles, K = 12): sampled rows
+    of G against the oracle's fill and an FP64 product, within the R18 bound; exact symmetry.  One
+    row more (16385) leaves the INT8 route (UNSUPPORTED) and AUTO falls back to the DMMA Gram."""
+    g = GridSpec((16384, 4, 3), (-1.0,) * 3, (1.0,) * 3)
+    k = KernelSpec.matern(0.7, 0.4)
+    Fg = T.fill(g, k)
+    A = unfold(orc.fill(ogrid(orc, g), okern(orc, k)), 0)
+    G = T.gram_i8(g, 0, Fg, T.workspace_i8(g))
+    assert torch.equal(G, G.T)
+    rows = np.random.default_rng(16384).choice(16384, 256, replace=False)
+    Gs = to_np(G[torch.from_numpy(rows).cuda()])
+    m = np.max(np.abs(A), axis=1)
+    E = np.where(m > 0, np.frexp(m)[1], 0).astype(np.float64)
+    l1 = np.sum(np.abs(A), axis=1)
+    s = np.exp2(E - 50 - 1)
+    K = A.shape[1]
+    bound = (np.outer(s[rows], l1) + np.outer(l1[rows], s) + 3 * np.outer(s[rows], s) * K
+             + 2 * K * EPS * (np.abs(A[rows]) @ np.abs(A).T))
+    assert np.all(np.abs(Gs - A[rows] @ A.T) <= bound)
+    g2 = GridSpec((16385, 4, 3), (-1.0,) * 3, (1.0,) * 3)
+    F2 = T.fill(g2, k)
+    with pytest.raises(T.TuckerError) as e:
+        T.gram_i8(g2, 0, F2, T.workspace_i8(g))
+    assert e.value.code in (4, 7)
+    G2 = T.gram(g2, 0, F2)  # AUTO engine: the DMMA Gram
+    assert torch.equal(G2, G2.T) and G2.shape == (16385, 16385)
