@@ -70,7 +70,8 @@ int launch_als(const int64_t n[3], const int32_t r[3], const double* F, double* 
     auto solve = [&](int m, const double* Y, int64_t ra, int64_t rb) -> int {
         const int64_t v[3] = {n[m], ra, rb};
         TK_RC(launch_gram(v, 0, Y, G, scr, sb, st));
-        const int rc = launch_eig(n[m], G, r[m], U[m], nullptr, sigma[m], scr, sb, st, info, m);
+        // warm start from the current factor (the previous sweep's, or the caller's initial one)
+        const int rc = launch_eig(n[m], G, r[m], U[m], nullptr, sigma[m], scr, sb, st, info, m, U[m]);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
         return TUCKER_OK;

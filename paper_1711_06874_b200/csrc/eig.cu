@@ -151,6 +151,16 @@ __global__ void k_omega(double* Vt, int p, int64_t n) {
         Vt[t] = hash_uniform((uint64_t)t);
 }
 
+// Warm start block: Vt[j][i] = V0[i][j] (j < r), pseudo-random for r <= j < p.
+__global__ void k_seed_vt(double* Vt, const double* __restrict__ V0, int p, int r, int64_t n) {
+    const int64_t tot = (int64_t)p * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(t / n);
+        const int64_t i = t - (int64_t)j * n;
+        Vt[t] = j < r ? V0[i * r + j] : hash_uniform((uint64_t)t);
+    }
+}
+
 // Wt (p x n) = Vt (p x n) * G (n x n)   [= (G V)^T, G symmetric].  Tile 16 rows x 64 cols.
 __global__ void __launch_bounds__(256) k_gemm_vg(const double* __restrict__ Vt, const double* __restrict__ G,
                                                  double* __restrict__ Wt, int p, int64_t n, const State* st) {
@@ -406,7 +416,7 @@ static Plan eig_plan(int64_t n, int r, void* ws) {
 }  // namespace eig
 
 int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
+                     size_t ws_bytes, cudaStream_t st, const double* V0) {
     TK_PROF(TUCKER_PROF_EIG, st);
     using namespace eig;
     if (r < 1 || r > n) return TUCKER_ERR_RANK;
@@ -425,15 +435,19 @@ int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambd
     } else if (eig_cluster_supported(n)) {
         // cluster path (n <= 2048): W = G V on many CTAs, Rayleigh–Ritz + CGS2 in one cluster
         const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
-        k_omega<<<64, 256, 0, st>>>(Vt, p, n);
+        if (V0) {
+            k_seed_vt<<<64, 256, 0, st>>>(Vt, V0, p, r, n);
+        } else {
+            k_omega<<<64, 256, 0, st>>>(Vt, p, n);
+        }
         TK_CHECK_LAUNCH();
         k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
         TK_CHECK_LAUNCH();
         TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
         // iterations 1 .. kMinIters-2 are plain power steps (V <- CGS2(G V), no Rayleigh–Ritz):
         // the Ritz rotation does not change the subspace, and a single Jacobi solve of the dense
-        // H at the end replaces the per-iteration ones
-        for (int w = 1; w < kMinIters - 1; ++w) {
+        // H at the end replaces the per-iteration ones (a warm start skips them)
+        for (int w = 1; w < kMinIters - 1 && !V0; ++w) {
             k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
             TK_CHECK_LAUNCH();
             TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
@@ -512,8 +526,8 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
 }
 
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
-               size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot) {
-    TK_RC(launch_eig_begin(n, G, r, U, lambda, sigma, ws, ws_bytes, st));
+               size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot, const double* V0) {
+    TK_RC(launch_eig_begin(n, G, r, U, lambda, sigma, ws, ws_bytes, st, V0));
     return launch_eig_end(n, G, r, U, lambda, sigma, ws, st, info, slot);
 }
 

@@ -109,12 +109,16 @@ int launch_gram_fused(const int64_t n[3], int mode, const KParams& kp, const dou
 size_t eig_ws_bytes(int64_t n, int r);
 // Split form: begin enqueues the first pass without host synchronisation, end synchronises,
 // continues while not converged and reports (launch_eig = begin + end).
+// V0 (dev, n x r row-major, nullable): warm start (Tucker-ALS: the previous factor) — the start
+// block is [V0, pseudo-random columns] and the power steps before the first Rayleigh–Ritz step are
+// skipped (V0 already spans the target subspace approximately; convergence is still decided by
+// the Ritz residuals).
 int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
-                     size_t ws_bytes, cudaStream_t st);
+                     size_t ws_bytes, cudaStream_t st, const double* V0 = nullptr);
 int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
                    cudaStream_t st, tucker_info* info, int slot);
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma,
-               void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot);
+               void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot, const double* V0 = nullptr);
 
 // Cluster Rayleigh–Ritz step (eig_cluster.cu); n <= 2048.
 bool eig_cluster_supported(int64_t n);
