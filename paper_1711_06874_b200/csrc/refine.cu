@@ -321,26 +321,29 @@ __global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const dou
 }
 
 // Block projection coefficients, per-CTA partials: part[blk][j * bb + t] = sum over this CTA's rows
-// of Q_j[i] Y_{c0+t}[i], j < c0, t < bb.  Rows are staged 32 at a time in shared memory (all
-// column segments contiguous, coalesced) through a kDotStages-deep cp.async ring, so several tiles'
-// loads are in flight while one is consumed.  Lane l owns j = l and j = l + 32 for all bb block
-// columns (16 register accumulators), warp w the rows w, w + 8, ... of each tile: per row two
-// shared loads of Q and eight broadcast loads of Y feed 16 FMAs.  The 8 warps' partials are summed
-// in warp order at the end (fixed order).  Dynamic shared memory: block_dots_smem(ncol).
+// of Q_j[i] Y_{c0+t}[i], j < c0, t < bb: a (c0 x rows) x (rows x bb) product on the FP64 tensor
+// cores.  Rows are staged 32 at a time in shared memory (all column segments contiguous,
+// coalesced) through a kDotStages-deep cp.async ring; warp w owns rows 4w..4w+3 of every tile —
+// one m8n8k4 DMMA k-step per 8-row block of j (A = Q^T, B = Y_B), accumulators in registers
+// across the tiles; the 8 warps' accumulators are summed in warp order at the end (fixed order).
+// (A lane-per-j FMA version issued ~314 instructions per warp and tile — instruction-bound.)
+// Dynamic shared memory: block_dots_smem(ncol).
 constexpr int kDotStages = 3;
+constexpr int kMaxJB = 8;  // c0 <= 64
 __host__ __device__ constexpr int block_dots_ld(int ncol) { return ncol + 1; }
 size_t block_dots_smem(int ncol) {
     const size_t ring = (size_t)kDotStages * 32 * block_dots_ld(ncol);
-    return 8 * (ring > 8 * 16 * 32 ? ring : 8 * 16 * 32);
+    const size_t red = (size_t)8 * kMaxJB * 64;
+    return 8 * (ring > red ? ring : red);
 }
 __global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict__ Yt, int64_t M, int c0, int bb,
                                                        double* __restrict__ part, const int* __restrict__ run) {
     if (run && !*run) return;
-    extern __shared__ double dsm[];  // ring [stage][row][ld]; then the cross-warp sum [w][h][t][lane]
+    extern __shared__ double dsm[];  // ring [stage][row][ld]; then the cross-warp sum [w][jb][64]
     int64_t b0, b1;
     row_range(M, b0, b1);
-    const int ncol = c0 + bb, npair = c0 * bb, ld = block_dots_ld(ncol);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncol = c0 + bb, npair = c0 * bb, ld = block_dots_ld(ncol), njb = c0 / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
     const int ntile = (int)((b1 - b0 + 31) / 32);
     auto issue = [&](int tt) {
         if (tt < ntile) {
@@ -354,45 +357,36 @@ __global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict_
         }
         cp_async_commit();  // (empty groups keep the wait count uniform)
     };
-    double acc[2][8];
+    double acc[kMaxJB][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) acc[h][t] = 0.0;
+    for (int jb = 0; jb < kMaxJB; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
 #pragma unroll
     for (int tt = 0; tt < kDotStages - 1; ++tt) issue(tt);
     for (int tt = 0; tt < ntile; ++tt) {
         cp_async_wait<kDotStages - 2>();
         __syncthreads();  // tile tt landed for all threads; tile tt-1's stage is free
         issue(tt + kDotStages - 1);
-        const double* tile = dsm + (size_t)(tt % kDotStages) * 32 * ld;
+        const double* row = dsm + (size_t)(tt % kDotStages) * 32 * ld + (4 * warp + q) * ld;
+        const double bv = g < bb ? row[c0 + g] : 0.0;  // B[k = q][n = g] = Y_{c0+g}[row]
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-            const double* row = tile + (warp + 8 * rr) * ld;
-            double y[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) y[t] = t < bb ? row[c0 + t] : 0.0;
-            const double q0 = lane < c0 ? row[lane] : 0.0;
-            const double q1 = lane + 32 < c0 ? row[lane + 32] : 0.0;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                acc[0][t] = fma(q0, y[t], acc[0][t]);
-                acc[1][t] = fma(q1, y[t], acc[1][t]);
-            }
-        }
+        for (int jb = 0; jb < kMaxJB; ++jb)
+            if (jb < njb) dmma(acc[jb], row[jb * 8 + g], bv);  // A[m = g][k = q] = Q_{8jb+g}[row]
     }
     cp_async_wait<0>();
     __syncthreads();
-    double* red = dsm;
+    double* red = dsm;  // [w][jb][lane][2]
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) red[((warp * 2 + h) * 8 + t) * 32 + lane] = acc[h][t];
+    for (int jb = 0; jb < kMaxJB; ++jb)
+        if (jb < njb) {
+            red[((warp * kMaxJB + jb) * 32 + lane) * 2] = acc[jb][0];
+            red[((warp * kMaxJB + jb) * 32 + lane) * 2 + 1] = acc[jb][1];
+        }
     __syncthreads();
     for (int pr = threadIdx.x; pr < npair; pr += kNT) {
-        const int j = pr / bb, t = pr % bb, h = j >> 5, l = j & 31;
+        // H[j][t]: j = 8 jb + g', t = 2 q' + u  ->  lane' = 4 g' + q'
+        const int j = pr / bb, t = pr % bb, jb = j >> 3, gg = j & 7, qq = t >> 1, u = t & 1;
         double sum = 0.0;
-        for (int w = 0; w < 8; ++w) sum += red[((w * 2 + h) * 8 + t) * 32 + l];
+        for (int w = 0; w < 8; ++w) sum += red[((w * kMaxJB + jb) * 32 + 4 * gg + qq) * 2 + u];
         part[(size_t)blockIdx.x * npair + pr] = sum;
     }
 }
