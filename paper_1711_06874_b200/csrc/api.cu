@@ -145,7 +145,8 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
 inline char* at(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
 
 int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* const U[3], double* core,
-               double* const sig[3], void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info) {
+               double* const sig[3], void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info,
+               bool mx_ready = false) {
     const Layout L = plan(g, r);
     if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
     double* G = reinterpret_cast<double*>(at(ws, L.G));
@@ -196,7 +197,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
                 TK_RC(launch_eig_begin(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], L.eig_bytes, side_of(m)));
             }
             return TUCKER_OK;
-        });
+        }, mx_ready);
         if (rc == TUCKER_OK) rc = eig_end(2);
         if (rc == TUCKER_OK) rc = eig_end(1);
         // U2, U3 final on side A -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve on side B
@@ -447,10 +448,13 @@ int tucker_approximate(const tucker_grid* grid, const tucker_kernel* kernel, con
     o += align_up((size_t)r[0] * r[1] * r[2] * 8, 256);
     double* errd = reinterpret_cast<double*>(o);
 
+    // the INT8 route's row maxima come out of the fill on centred grids (one pass over F fewer)
+    const bool mx_fused = L.i8_bytes && fill_rowmax_supported(*grid);
     TK_RC(launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
-                      reinterpret_cast<double*>(at(ws, L.cheb)), st));
+                      reinterpret_cast<double*>(at(ws, L.cheb)), st,
+                      mx_fused ? gram_i8_rowmax_slot(grid->n, at(ws, L.i8)) : nullptr));
     const int64_t c0 = launch_counter();
-    const int rc = hosvd_impl(grid, r, F, Ud, cored, Sd, ws, ws_bytes, st, info);
+    const int rc = hosvd_impl(grid, r, F, Ud, cored, Sd, ws, ws_bytes, st, info, mx_fused);
     if (rc != TUCKER_OK && rc != TUCKER_ERR_NOCONV) return rc;
     const int64_t c1 = launch_counter();
     (void)c0;

@@ -60,19 +60,31 @@ __global__ void k_cheb_table(double nu, double pref, double* table) {
 
 // Octant fill with 8-fold mirrored 256-bit stores.  Requires lo = -hi on all axes and
 // n3 % 8 == 0.  Item = (i < h1, j < h2, quad t < n3/8); 4 consecutive k per thread.
+// mx (nullable; centred grids with n3 / 2 <= kFillMaxK): also the row maxima of the three
+// unfoldings as high words of |F| (the INT8 Gram's row scaling, bitwise what k_i8_rowmax computes
+// from the stored tensor) for the first half of every axis — rows i (mx[0..n1)), j (mx[n1..)),
+// k (mx[n1+n2..)); the caller mirrors them.  mode 2 through shared-memory maxima flushed once per
+// CTA, modes 0 and 1 through one global atomic per distinct row and warp.
+constexpr int kFillMaxK = 4096;
+template <bool kMax>
 __global__ void __launch_bounds__(256) k_fill_octant(KParams kp, const double* __restrict__ cheb_g,
                                                      const double* __restrict__ x2,
                                                      int64_t n1, int64_t n2, int64_t n3,
-                                                     double* __restrict__ F) {
+                                                     double* __restrict__ F, uint32_t* __restrict__ mx) {
     __shared__ double cheb[kChebIntervals * kChebN];
+    __shared__ uint32_t smk[kMax ? kFillMaxK : 1];
     if (kp.family == TUCKER_MATERN && kp.closed == 0)
         for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    if (kMax)
+        for (int t = threadIdx.x; t < n3 / 2; t += blockDim.x) smk[t] = 0u;
     __syncthreads();
     const double* xa = x2;
     const double* xb = x2 + n1;
     const double* xc = x2 + n1 + n2;
     const int64_t h1 = (n1 + 1) / 2, h2 = (n2 + 1) / 2, q3 = n3 / 8;
     const int64_t total = h1 * h2 * q3;
+    int64_t t_cur = -1;  // (kMax) k-chunk whose maxima km holds
+    uint32_t km[4] = {0u, 0u, 0u, 0u};
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
          it += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = it % q3;
@@ -91,7 +103,53 @@ __global__ void __launch_bounds__(256) k_fill_octant(KParams kp, const double* _
             st_v4(row + k0, v[0], v[1], v[2], v[3]);
             st_v4(row + (n3 - 4 - k0), v[3], v[2], v[1], v[0]);
         }
+        if (kMax) {
+            // mode 2: per-thread maxima of its 4 k's, kept in registers while its k-chunk stays
+            // the same (always, when q3 divides the grid stride) and flushed to shared memory
+            if (t != t_cur) {
+                if (t_cur >= 0)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) atomicMax(&smk[4 * t_cur + u], km[u]);
+                t_cur = t;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) km[u] = 0u;
+            }
+            uint32_t hm = 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t h = (uint32_t)__double2hiint(v[u]) & 0x7FFFFFFFu;
+                hm = max(hm, h);
+                km[u] = max(km[u], h);
+            }
+            // modes 0 and 1: one reduction and two atomics per distinct (i, j) and warp
+            const unsigned grp = __match_any_sync(__activemask(), ij);
+            const uint32_t m = __reduce_max_sync(grp, hm);
+            if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) {
+                atomicMax(mx + i, m);
+                atomicMax(mx + n1 + j, m);
+            }
+        }
     }
+    if (kMax) {
+        if (t_cur >= 0)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) atomicMax(&smk[4 * t_cur + u], km[u]);
+        __syncthreads();
+        for (int t = threadIdx.x; t < n3 / 2; t += blockDim.x)
+            if (smk[t]) atomicMax(mx + n1 + n2 + t, smk[t]);
+    }
+}
+
+// Mirror the first-half row maxima to the second half of every axis (centred grids).
+__global__ void k_fill_mirror_max(uint32_t* mx, int64_t n1, int64_t n2, int64_t n3) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t* m;
+    int64_t n, idx;
+    if (t < n1) { m = mx; n = n1; idx = t; }
+    else if (t < n1 + n2) { m = mx + n1; n = n2; idx = t - n1; }
+    else if (t < n1 + n2 + n3) { m = mx + n1 + n2; n = n3; idx = t - n1 - n2; }
+    else return;
+    if (idx >= (n + 1) / 2) m[idx] = m[n - 1 - idx];
 }
 
 // General fill: one point per thread (any grid, any n3).
@@ -173,16 +231,28 @@ int launch_fill_prep(const tucker_grid& g, const tucker_kernel& kn, const KParam
     return TUCKER_OK;
 }
 
+bool fill_rowmax_supported(const tucker_grid& g) {
+    return grid_centred(g) && g.n[2] % 8 == 0 && g.n[2] / 2 <= kFillMaxK;
+}
+
 int launch_fill(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
-                cudaStream_t st) {
+                cudaStream_t st, uint32_t* mx) {
     TK_PROF(TUCKER_PROF_FILL, st);
     const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
     const KParams kp = make_kparams(kn);
+    if (mx && !fill_rowmax_supported(g)) return TUCKER_ERR_UNSUPPORTED;
     TK_RC(launch_fill_prep(g, kn, kp, nodes_x2, cheb, st));
     if (grid_centred(g) && n3 % 8 == 0) {
         const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 8);
         const int64_t blocks = std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16);
-        k_fill_octant<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F);
+        if (mx) {
+            TK_CUDA(cudaMemsetAsync(mx, 0, (size_t)(n1 + n2 + n3) * 4, st));
+            k_fill_octant<true><<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F, mx);
+            TK_CHECK_LAUNCH();
+            k_fill_mirror_max<<<(unsigned)ceil_div(n1 + n2 + n3, 256), 256, 0, st>>>(mx, n1, n2, n3);
+        } else {
+            k_fill_octant<false><<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F, nullptr);
+        }
     } else {
         const int64_t blocks = std::min<int64_t>(ceil_div(n1 * n2 * n3, 256), (int64_t)kNumSMs * 16);
         k_fill_general<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F);

@@ -1074,14 +1074,14 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
 // next phase).  ws: gram_i8_hosvd_ws_bytes.  (A joint modes-1/2 residue pass reading F once was
 // measured: 12.3 ms against 12.6 ms for the two passes, for 8 GiB more workspace — not kept.)
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase) {
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, bool mx_ready) {
     using namespace i8;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const WsPlan w = ws_plan(n);
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
-    TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    if (!mx_ready) TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
     for (int m = 2; m >= 0; --m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
         TK_RC(on_phase(&m, 1));
@@ -1090,6 +1090,9 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
 }
 
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
+uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + i8::ws_plan(n).off_mx);
+}
 
 cudaStream_t side_stream(int which) {
     static cudaStream_t s[64][2] = {};

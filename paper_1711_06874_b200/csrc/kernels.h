@@ -33,7 +33,9 @@ struct ChunkGeo {
 };
 
 int launch_fill(const tucker_grid& g, const tucker_kernel& k, double* F, double* nodes_x2,
-                double* cheb, cudaStream_t st);
+                double* cheb, cudaStream_t st, uint32_t* mx = nullptr);
+// fill + row maxima (launch_fill with mx) is available on centred grids with n3 % 8 == 0, n3 <= 8192
+bool fill_rowmax_supported(const tucker_grid& g);
 
 // Gram G_m (n_m x n_m, both triangles) of the mode-m unfolding of F.
 size_t gram_ws_bytes(const int64_t n[3]);
@@ -78,9 +80,12 @@ size_t gram_i8_fused_ws_bytes(const int64_t n[3]);
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
                                cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
                                const Shard* shard = nullptr);
+// mx_ready: the row maxima are already in the workspace's slot (gram_i8_rowmax_slot; e.g. written
+// by the fill of the same call) — the row-maxima pass is skipped.
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase);
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, bool mx_ready = false);
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
+uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws);
 // Per-device non-blocking side streams of the library (which = 0, 1; created once).
 cudaStream_t side_stream(int which);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.

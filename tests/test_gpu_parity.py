@@ -248,3 +248,25 @@ def test_approximate_host_outputs(T, orc):
     E_o = orc.tucker_error(Fo, *h.U, h.core)[0]
     assert abs(out.err[0] - E_o) <= 1e-12
     assert T.last_launch_count() > 10
+
+
+@pytest.mark.parametrize("grid", [GridSpec.cube(256, 1.0), GridSpec((136, 144, 160), (-1.0,) * 3, (1.0,) * 3),
+                                  GridSpec((96, 80, 112), (-2.0, -1.0, -0.5), (2.0, 1.5, 1.0))])
+def test_approximate_equals_separate_calls(T, grid):
+    """tucker_approximate takes the INT8 route's row maxima out of the fill on centred grids (n3 % 8
+    == 0); the tensor, factors, core and error are bitwise those of tucker_fill + tucker_hosvd +
+    tucker_error (the maxima are the same numbers), also where the fusion does not apply."""
+    k, r = KernelSpec.matern(1.5, 0.3), (12, 12, 12)
+    F = torch.empty(tuple(grid.n), dtype=torch.float64, device="cuda")
+    ws = T.workspace(grid, r)
+    host = T.HostBuffers(grid, r)
+    out = T.approximate(grid, k, r, F, ws, host)
+    F2 = T.fill(grid, k)
+    assert torch.equal(F, F2)
+    res = T.hosvd(grid, r, F2)
+    e = T.error(grid, r, F2, res.U, res.core)
+    for m in range(3):
+        assert np.array_equal(out.U[m], to_np(res.U[m])), m
+        assert np.array_equal(out.sigma[m], to_np(res.sigma[m])), m
+    assert np.array_equal(out.core, to_np(res.core))
+    assert np.array_equal(out.err, to_np(e))
