@@ -1,4 +1,4 @@
-"""Row (e) on the GPU: ONE fused HOSVD (+ error) sharded over 2 and 3 ranks
+"""Row (e) on the GPU: ONE fused HOSVD (+ error) sharded over 2, 3 and 4 ranks
 (tucker_hosvd_fused_sharded).  The ranks are processes sharing the test box's one
 GPU and exchanging through gloo (a host-staged all-reduce: no kernel waits on another rank —
 B200_PROFILING.md); in production the same calls run one process per GPU over NCCL.
@@ -71,7 +71,7 @@ def knobs():
             os.environ[k] = v
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_sharded_fused_hosvd_bitwise(T, knobs, tmp_path, case, world):
     import torch.multiprocessing as mp
