@@ -34,23 +34,26 @@ int main() {
     cudaEventCreate(&b);
     int cfg[][2] = {{592, 256}, {296, 512}, {148, 1024}, {148, 256}};
     for (auto& c : cfg) {
-        for (int which = 0; which < 2; ++which) {
-            float best = 1e9;
-            for (int rep = 0; rep < 5; ++rep) {
-                unsigned int z = 0;
-                cudaMemcpyToSymbol(g_bar, &z, 4);
-                int n = 200;
-                void* args[] = {&n, &d};
-                cudaEventRecord(a);
-                cudaLaunchCooperativeKernel(which ? (void*)k_sync2 : (void*)k_sync, c[0], c[1], args, 0, 0);
-                cudaEventRecord(b);
-                cudaEventSynchronize(b);
-                float ms;
-                cudaEventElapsedTime(&ms, a, b);
-                if (ms < best) best = ms;
+        for (int n : {0, 200}) {
+            for (int coop = 0; coop < 2; ++coop) {
+                if (!coop && n) continue;  // grid.sync needs a cooperative launch
+                float best = 1e9;
+                for (int rep = 0; rep < 5; ++rep) {
+                    void* args[] = {&n, &d};
+                    cudaEventRecord(a);
+                    if (coop)
+                        cudaLaunchCooperativeKernel((void*)k_sync, c[0], c[1], args, 0, 0);
+                    else
+                        cudaLaunchKernel((void*)k_sync, c[0], c[1], args, 0, 0);
+                    cudaEventRecord(b);
+                    cudaEventSynchronize(b);
+                    float ms;
+                    cudaEventElapsedTime(&ms, a, b);
+                    if (ms < best) best = ms;
+                }
+                printf("%s grid %d x %d, %d syncs: %.1f us total (%s)\n", coop ? "cooperative" : "plain      ", c[0], c[1], n,
+                       best * 1000, cudaGetErrorString(cudaGetLastError()));
             }
-            printf("%s grid %d x %d: %.2f us per sync (%s)\n", which ? "red/ld.acquire" : "cg::grid.sync", c[0], c[1],
-                   best * 1000 / 200, cudaGetErrorString(cudaGetLastError()));
         }
     }
 }
