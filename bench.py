@@ -184,15 +184,25 @@ def run_ours(args, rank, world, local):
     sp = ctypes.c_void_p(stream.cuda_stream)
     wsp, wsn = ctypes.c_void_p(ws.data_ptr()), ws.numel()
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    # the fill also emits the INT8 route's row maxima (tucker_fill_rowmax) where it can: one pass
+    # over F fewer; tucker_hosvd_rowmax takes them (bitwise the plain calls' results)
+    rowmax = torch.empty(3 * n, dtype=torch.int32, device=dev)
+    use_rowmax = args.gram_engine != "dmma" and lib.tucker_fill_rowmax(
+        ctypes.byref(g_c), ctypes.byref(k_c), P(F), P(rowmax), wsp, wsn, sp) == 0
+    torch.cuda.synchronize()
 
     def step():
-        """One pass of the path as three ABI calls (fill, hosvd = 3 x (Gram + eig) + core, error);
-        returns the number of kernel launches."""
+        """One pass of the path as three ABI calls (fill [+ row maxima], hosvd = 3 x (Gram + eig) +
+        core, error); returns the number of kernel launches."""
         launches = 0
-        T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, sp), "fill")
+        if use_rowmax:
+            T._check(lib.tucker_fill_rowmax(ctypes.byref(g_c), ctypes.byref(k_c), P(F), P(rowmax), wsp, wsn, sp),
+                     "fill_rowmax")
+        else:
+            T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, sp), "fill")
         launches += lib.tucker_last_launch_count()
-        rc = lib.tucker_hosvd(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), P(S[0]), P(S[1]),
-                              P(S[2]), wsp, wsn, sp, None)
+        rc = lib.tucker_hosvd_rowmax(ctypes.byref(g_c), r_c, P(F), P(rowmax) if use_rowmax else None, P(U[0]), P(U[1]),
+                                     P(U[2]), P(core), P(S[0]), P(S[1]), P(S[2]), wsp, wsn, sp, None)
         if rc not in (0, 5):
             T._check(rc, "hosvd")
         launches += lib.tucker_last_launch_count()
@@ -303,6 +313,8 @@ def run_ours(args, rank, world, local):
                    "kernel": {"family": "matern", "nu": 1.5, "ell": 0.2, "sigma2": 1.0}, "ranks": list(ranks),
                    "gram_engine": "int8 emulation (tcgen05 kind::i8 + CRT)" if i8 else "dmma",
                    "l2": f"inputs larger than L2 (F = {8 * N / 1e9:.2f} GB per step, L2 = 126 MB)",
+                   "step_calls": ("tucker_fill_rowmax + tucker_hosvd_rowmax + tucker_error" if use_rowmax
+                                  else "tucker_fill + tucker_hosvd + tucker_error"),
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
         "stages_ms": st, "stage_calls_per_step": calls,
         "stages_note": "device time per stage from the library's stage timer (CUDA events on the launching "

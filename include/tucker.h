@@ -149,6 +149,22 @@ TUCKER_API int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const d
                  double* U2, double* U3, double* core, double* sigma1, double* sigma2,
                  double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
+/* a-2 + the INT8 route's row scaling in one pass: tucker_fill, and rowmax (dev, n1+n2+n3 uint32)
+ * <- per row of each unfolding the largest high 32-bit word of |F| (sign cleared): rows i of
+ * F_(1) at [0, n1), rows j of F_(2) at [n1, n1+n2), rows k of F_(3) at [n1+n2, n1+n2+n3) — the
+ * exponents R18 scales each row by.  Centred grids with n3 % 8 == 0 and n3 <= 8192 only (the
+ * octant fill), else TUCKER_ERR_UNSUPPORTED (use tucker_fill).  Workspace as tucker_fill. */
+TUCKER_API int tucker_fill_rowmax(const tucker_grid* grid, const tucker_kernel* kernel, double* F, uint32_t* rowmax,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* tucker_hosvd with the row maxima of F supplied (rowmax from tucker_fill_rowmax of this very F;
+ * the caller guarantees it): on the INT8 Gram route the row-maxima pass over F is skipped, the
+ * results are bitwise those of tucker_hosvd.  rowmax == NULL, or the DMMA route: tucker_hosvd. */
+TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], const double* F,
+                        const uint32_t* rowmax, double* U1, double* U2, double* U3, double* core,
+                        double* sigma1, double* sigma2, double* sigma3, void* ws, size_t ws_bytes,
+                        void* stream, tucker_info* info);
+
 /* a-6: out3 (dev, 3 doubles) <- {E, ||F||, ||F - Ft||} with Ft = core x1 U1 x2 U2 x3 U3
  * (P:1016-1025).  Deterministic (fixed-order reduction, no float atomics). */
 TUCKER_API int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1,

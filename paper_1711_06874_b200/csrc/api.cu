@@ -345,6 +345,19 @@ int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F,
                        reinterpret_cast<double*>(at(ws, L.cheb)), static_cast<cudaStream_t>(stream));
 }
 
+int tucker_fill_rowmax(const tucker_grid* grid, const tucker_kernel* kernel, double* F, uint32_t* rowmax, void* ws,
+                       size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    if (!F || !rowmax || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (!fill_rowmax_supported(*grid)) return TUCKER_ERR_UNSUPPORTED;
+    const Layout L = plan(grid, nullptr);
+    if (ws_bytes < L.scratch) return TUCKER_ERR_SIZE;
+    return launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                       reinterpret_cast<double*>(at(ws, L.cheb)), static_cast<cudaStream_t>(stream), rowmax);
+}
+
 int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws, size_t ws_bytes,
                 void* stream) {
     launch_counter() = 0;
@@ -410,6 +423,26 @@ int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const double* F, d
     double* const U[3] = {U1, U2, U3};
     double* const S[3] = {sigma1, sigma2, sigma3};
     return hosvd_impl(grid, r, F, U, core, S, ws, ws_bytes, static_cast<cudaStream_t>(stream), info);
+}
+
+int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], const double* F, const uint32_t* rowmax,
+                        double* U1, double* U2, double* U3, double* core, double* sigma1, double* sigma2,
+                        double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    if (info) std::memset(info, 0, sizeof(*info));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Layout L = plan(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    const bool use = rowmax && L.i8_bytes;
+    if (use)
+        TK_CUDA(cudaMemcpyAsync(gram_i8_rowmax_slot(grid->n, at(ws, L.i8)), rowmax,
+                                (size_t)(grid->n[0] + grid->n[1] + grid->n[2]) * 4, cudaMemcpyDeviceToDevice, st));
+    return hosvd_impl(grid, r, F, U, core, S, ws, ws_bytes, st, info, use);
 }
 
 int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1, const double* U2,

@@ -22,7 +22,7 @@ FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED",
           8: "TUCKER_ERR_COLLECTIVE"}
-EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_gram", "tucker_eig", "tucker_ttm_core",
+EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_fill_rowmax", "tucker_hosvd_rowmax", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_hosvd_fused_sharded",
            "tucker_workspace_size_als",
@@ -80,6 +80,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     sig = {
         "tucker_workspace_size": (sz, [pg, pr]),
         "tucker_fill": (ctypes.c_int, [pg, pk, vp, vp, sz, vp]),
+        "tucker_fill_rowmax": (ctypes.c_int, [pg, pk, vp, vp, vp, sz, vp]),
+        "tucker_hosvd_rowmax": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_workspace_size_i8": (sz, [pg]),
         "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
@@ -187,6 +189,22 @@ def fill(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | None = 
     return F
 
 
+def fill_rowmax(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """tucker_fill_rowmax: (F, rowmax) — the fill plus the INT8 route's per-row maxima (centred grids,
+    n3 % 8 == 0, n3 <= 8192; TuckerError UNSUPPORTED otherwise)."""
+    lib = load()
+    shape = tuple(int(v) for v in grid.n)
+    if F is None:
+        F = torch.empty(shape, dtype=torch.float64, device="cuda")
+    _dev(F, "F")
+    mx = torch.empty(int(sum(shape)), dtype=torch.int32, device=F.device)  # uint32 bit patterns (< 2^31)
+    ws = ws if ws is not None else workspace(grid)
+    g, k = cgrid(grid), ckernel(kernel)
+    _check(lib.tucker_fill_rowmax(ctypes.byref(g), ctypes.byref(k), _ptr(F), _ptr(mx), _ptr(ws), ws.numel(),
+                                  _stream(stream)), "tucker_fill_rowmax")
+    return F, mx
+
+
 def gram(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     lib = load()
     _dev(F, "F")
@@ -291,7 +309,9 @@ class HosvdResult:
     rc: int
 
 
-def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> HosvdResult:
+def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None,
+          rowmax: torch.Tensor | None = None) -> HosvdResult:
+    """tucker_hosvd, or tucker_hosvd_rowmax when `rowmax` (from fill_rowmax of this F) is given."""
     lib = load()
     _dev(F, "F")
     dev = F.device
@@ -302,9 +322,16 @@ def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=N
     ws = ws if ws is not None else workspace(grid, r)
     info = CInfo()
     g = cgrid(grid)
-    rc = lib.tucker_hosvd(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core),
-                          _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(), _stream(stream),
-                          ctypes.byref(info))
+    if rowmax is not None:
+        if not (rowmax.is_cuda and rowmax.dtype == torch.int32 and rowmax.is_contiguous()):
+            raise ValueError("rowmax must be a contiguous int32 CUDA tensor (from fill_rowmax)")
+        rc = lib.tucker_hosvd_rowmax(ctypes.byref(g), cranks(r), _ptr(F), _ptr(rowmax), _ptr(U[0]), _ptr(U[1]),
+                                     _ptr(U[2]), _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws),
+                                     ws.numel(), _stream(stream), ctypes.byref(info))
+    else:
+        rc = lib.tucker_hosvd(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core),
+                              _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(), _stream(stream),
+                              ctypes.byref(info))
     if rc not in (0, 5):
         _check(rc, "tucker_hosvd")
     return HosvdResult(U, core, S, info.as_dict(), rc)
