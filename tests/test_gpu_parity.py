@@ -272,10 +272,13 @@ def test_approximate_equals_separate_calls(T, grid):
     assert np.array_equal(out.err, to_np(e))
 
 
-def test_fill_rowmax_and_hosvd_rowmax(T):
+@pytest.mark.parametrize("g", [GridSpec.cube(256, 1.0), GridSpec((129, 131, 64), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0))])
+def test_fill_rowmax_and_hosvd_rowmax(T, g):
     """tucker_fill_rowmax: the same F as tucker_fill; tucker_hosvd_rowmax with those maxima: bitwise
-    tucker_hosvd (they are the row maxima the INT8 route would compute); unsupported grids refuse."""
-    g, k, r = GridSpec.cube(256, 1.0), KernelSpec.matern(0.7, 0.3), (16, 16, 16)
+    tucker_hosvd (they are the row maxima the INT8 route would compute); odd axes (a middle index);
+    unsupported grids refuse."""
+    k, r = KernelSpec.matern(0.7, 0.3), (16, 16, 16)
+    n1, n2, n3 = g.n
     F, mx = T.fill_rowmax(g, k)
     assert torch.equal(F, T.fill(g, k))
     a, b = T.hosvd(g, r, F), T.hosvd(g, r, F, rowmax=mx)
@@ -283,13 +286,13 @@ def test_fill_rowmax_and_hosvd_rowmax(T):
         assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m])
     assert torch.equal(a.core, b.core)
     # the maxima mirror on a centred grid and bound every |F| row from above in the exponent
-    for m, off in ((0, 0), (1, 256), (2, 512)):
-        seg = mx[off:off + 256]
+    for off, nn in ((0, n1), (n1, n2), (n1 + n2, n3)):
+        seg = mx[off:off + nn]
         assert torch.equal(seg, seg.flip(0))
     hw = (F.abs().view(torch.int64) >> 32).to(torch.int32)
-    assert torch.equal(mx[:256], hw.amax(dim=(1, 2)))
-    assert torch.equal(mx[256:512], hw.amax(dim=(0, 2)))
-    assert torch.equal(mx[512:], hw.amax(dim=(0, 1)))
+    assert torch.equal(mx[:n1], hw.amax(dim=(1, 2)))
+    assert torch.equal(mx[n1:n1 + n2], hw.amax(dim=(0, 2)))
+    assert torch.equal(mx[n1 + n2:], hw.amax(dim=(0, 1)))
     off_grid = GridSpec((64, 64, 64), (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0))
     with pytest.raises(T.TuckerError) as e:
         T.fill_rowmax(off_grid, k)
