@@ -414,7 +414,10 @@ def run_ours(args, rank, world, local):
     if not args.no_fused and world == 1:
         result["fused"] = run_fused(T, args.fused_n, rr, stream)
     if not args.no_fused and world > 1:
-        result["fused_sharded"] = run_fused_sharded(T, args.fused_n, rr, stream, world)
+        try:
+            result["fused_sharded"] = run_fused_sharded(T, args.fused_n, rr, stream, world)
+        except Exception as e:  # (symmetric failures, e.g. memory: every rank records it and goes on)
+            result["fused_sharded"] = {"unavailable": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
     if world > 1:
