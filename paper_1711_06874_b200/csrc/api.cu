@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "fill_eval.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace tk {
 
@@ -633,6 +634,7 @@ int tucker_error_fused(const tucker_grid* grid, const tucker_kernel* kernel, con
     TK_RC(launch_fill_prep(*grid, *kernel, kp, reinterpret_cast<double*>(at(ws, L.nodes)),
                            reinterpret_cast<double*>(at(ws, L.cheb)), st));
     const FusedGen gen = fused_gen(grid, kp, L, ws);
+    TK_PROF(TUCKER_PROF_ERROR, st);
     return launch_error_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, out3, at(ws, L.scratch), L.scratch_bytes,
                              st);
 }
