@@ -349,11 +349,13 @@ __global__ void __launch_bounds__(kNT, 4) k_block_dots(const double* __restrict_
         if (tt < ntile) {
             double* st = dsm + (size_t)(tt % kDotStages) * 32 * ld;
             const int64_t r0 = b0 + (int64_t)tt * 32;
-            for (int e = threadIdx.x; e < 32 * ncol; e += kNT) {
-                const int c = e >> 5, i = e & 31;
-                const bool v = r0 + i < b1;
-                cp_async8(st + i * ld + c, Yt + (size_t)c * M + (v ? r0 + i : b0), v);
-            }
+            // lane = row of the tile, warp = first column; columns step by 8 (strength-reduced)
+            const int i = threadIdx.x & 31, c0w = threadIdx.x >> 5;
+            const bool v = r0 + i < b1;
+            const double* src = Yt + (size_t)c0w * M + (v ? r0 + i : b0);
+            double* dst = st + i * ld + c0w;
+            for (int c = c0w; c < ncol; c += kNT / 32, src += (size_t)(kNT / 32) * M, dst += kNT / 32)
+                cp_async8(dst, src, v);
         }
         cp_async_commit();  // (empty groups keep the wait count uniform)
     };
