@@ -416,10 +416,14 @@ __global__ void __launch_bounds__(kNT, 4) k_block_update(double* __restrict__ Yt
         double y[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) y[t] = t < bb ? Yt[(size_t)(c0 + t) * M + i] : 0.0;
-        for (int j0 = 0; j0 < c0; j0 += 4) {  // four loads in flight, then the FMAs (same order)
-            double q[4];
+        // chunks of four Q values, the next chunk's loads issued before this chunk's FMAs (one
+        // chunk always in flight); FMA order as before
+        double q[4], qn[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = j0 + u < c0 ? Yt[(size_t)(j0 + u) * M + i] : 0.0;
+        for (int u = 0; u < 4; ++u) q[u] = u < c0 ? Yt[(size_t)u * M + i] : 0.0;
+        for (int j0 = 0; j0 < c0; j0 += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) qn[u] = j0 + 4 + u < c0 ? Yt[(size_t)(j0 + 4 + u) * M + i] : 0.0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (j0 + u >= c0) break;
@@ -431,6 +435,8 @@ __global__ void __launch_bounds__(kNT, 4) k_block_update(double* __restrict__ Yt
                     y[2 * t2 + 1] = fma(-q[u], hh.y, y[2 * t2 + 1]);
                 }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = qn[u];
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t)
