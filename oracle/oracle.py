@@ -68,6 +68,7 @@ def lib():
             "orc_unfold": (None, [pd, pi64, i32, pd]),
             "orc_gram": (None, [pd, i64, i64, pd]),
             "orc_gram_entry_fn": (d, [P(OrcGrid), P(OrcKernel), i32, i64, i64]),
+            "orc_row_stats_fn": (None, [P(OrcGrid), P(OrcKernel), i32, i64, pd]),
             "orc_jacobi_eig": (i32, [i64, pd, pd, pd, i32, P(i32)]),
             "orc_sign_fix": (None, [i64, i64, pd, i64]),
             "orc_ttm_core": (None, [pd, pi64, pi64, pd, pd, pd, pd]),
@@ -200,6 +201,14 @@ def gram_mode(F: np.ndarray, mode: int) -> np.ndarray:
 def gram_entry_fn(g: Grid, k: Kernel, mode: int, a: int, b: int) -> float:
     gc, kc = g.c(), k.c()
     return lib().orc_gram_entry_fn(ctypes.byref(gc), ctypes.byref(kc), mode, a, b)
+
+
+def row_stats_fn(g: Grid, k: Kernel, mode: int, a: int):
+    """(max_k |A_(m)[a,k]|, sum_k |A_(m)[a,k]|) of one unfolding row, from the kernel directly."""
+    gc, kc = g.c(), k.c()
+    out = np.empty(2)
+    lib().orc_row_stats_fn(ctypes.byref(gc), ctypes.byref(kc), mode, a, _pd(out))
+    return float(out[0]), float(out[1])
 
 
 def jacobi_eig(G: np.ndarray, max_sweeps: int = 100):

@@ -23,6 +23,7 @@
  *                       spectral density: exact values where alpha^2+rho^2 is a power of two)
  *   orc_fill            pinned (reflection symmetry, Gaussian separability, direct evaluation)
  *   orc_unfold/orc_gram pinned (numpy BLAS Gram, trace = ||F||^2, mode invariance on cubic grids)
+ *   orc_row_stats_fn    pinned (numpy max / sum of |unfolding row| of the filled tensor)
  *   orc_jacobi_eig      pinned (numpy.linalg.eigh on random SPD, residuals, orthonormality)
  *   orc_ttm_core        pinned (brute-force quadruple sum on tiny tensors, identity factors)
  *   orc_tucker_error    pinned (full-rank reconstruction, rank-1 Gaussian, ||F||^2=||b||^2+err^2)
@@ -340,6 +341,44 @@ double orc_gram_entry_fn(const orc_grid *g, const orc_kernel *k, int mode, int64
     }
     (void)outer;
     return total + totc;
+}
+
+/* Row statistics of the mode-m unfolding computed from the kernel directly (no F in memory):
+ * out[0] = max_k |A_(m)[a,k]|, out[1] = sum_k |A_(m)[a,k]| (compensated).  Test-only: the inputs of
+ * the INT8 Gram's element bound (R18) for sampled entries at sizes the oracle cannot fill. */
+void orc_row_stats_fn(const orc_grid *g, const orc_kernel *k, int mode, int64_t a, double *out) {
+    int64_t n1 = g->n[0], n2 = g->n[1], n3 = g->n[2];
+    int64_t outer = (mode == 0) ? n2 : n1;
+    int64_t inner = (mode == 2) ? n2 : n3;
+    double mx = 0.0, total = 0.0, totc = 0.0;
+#pragma omp parallel
+    {
+        double lmx = 0.0, s = 0.0, c = 0.0;
+#pragma omp for schedule(static)
+        for (int64_t u = 0; u < outer; ++u)
+            for (int64_t v = 0; v < inner; ++v) {
+                double f;
+                if (mode == 0) f = orc_fill_entry(g, k, a, u, v);
+                else if (mode == 1) f = orc_fill_entry(g, k, u, a, v);
+                else f = orc_fill_entry(g, k, u, v, a);
+                double af = fabs(f), t, e;
+                lmx = fmax(lmx, af);
+                two_sum(s, af, &t, &e);
+                s = t;
+                c += e;
+            }
+#pragma omp critical
+        {
+            double t, e;
+            mx = fmax(mx, lmx);
+            two_sum(total, s, &t, &e);
+            total = t;
+            totc += e + c;
+        }
+    }
+    (void)n3;
+    out[0] = mx;
+    out[1] = total + totc;
 }
 
 /* ------------------------------------------------------------------------------------------ */

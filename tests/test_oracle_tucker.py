@@ -51,6 +51,20 @@ def test_gram_entry_fn(orc):
             assert abs(orc.gram_entry_fn(g, k, m, a, b) - G[a, b]) <= 1e-15 * G[a, a]
 
 
+def test_row_stats_fn(orc):
+    """orc_row_stats_fn (inputs of the R18 element bound) = numpy's max / sum of |row| of the
+    filled tensor's unfolding."""
+    g = orc.Grid((10, 8, 6), (-2.0, -1.5, -0.5), (2.0, 1.5, 1.0))
+    k = orc.Kernel.matern(0.7, 0.5)
+    F = orc.fill(g, k)
+    for m in range(3):
+        A = np.abs(np.moveaxis(F, m, 0).reshape(F.shape[m], -1))
+        for a in (0, 3, g.n[m] - 1):
+            mx, l1 = orc.row_stats_fn(g, k, m, a)
+            assert mx == A[a].max()
+            assert abs(l1 - np.sum(A[a])) <= 1e-15 * l1
+
+
 # ---------------------------------------------------------------------------------- Jacobi --
 @pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 33, 64])
 def test_jacobi_vs_eigh(orc, n):
