@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-accurate", action="store_true", help="skip the SVD-accurate (NEXT f2) line")
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
     ap.add_argument("--no-f4", action="store_true", help="skip the NEXT f4 workloads line")
+    ap.add_argument("--no-parity", action="store_true", help="skip the per-config T1-T4 deltas vs the oracle")
     ap.add_argument("--fused-n", type=int, default=2048)
     ap.add_argument("--gram-engine", default="auto", choices=["auto", "dmma", "int8"],
                     help="Gram engine of the materialised path (auto: INT8 emulation)")
@@ -401,6 +402,9 @@ def run_ours(args, rank, world, local):
                                                      (x.cpu() for x in acc.sigma)]}
     if not args.no_f4 and world == 1:
         result["f4"] = run_f4(T, grid, ranks, F, ws, stream)
+    if not args.no_parity and world == 1 and n == 1024 and rr == 40:
+        T.fill(grid, kern, F, ws, stream)  # (f4 reused F)
+        result["parity"] = run_parity(T, stream, F)
     if not args.no_cfg4:
         del F
         torch.cuda.empty_cache()
@@ -419,7 +423,7 @@ def run_ours(args, rank, world, local):
         except Exception as e:  # (symmetric failures, e.g. memory: every rank records it and goes on)
             result["fused_sharded"] = {"unavailable": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=20.0)
+        result["cpu_baseline"] = cpu_baseline(n, rr, budget_s=15.0)
     if world > 1:
         dist.destroy_process_group()
     return result
@@ -509,6 +513,95 @@ def run_fused_sharded(T, n: int, rr: int, stream, world: int) -> dict:
                      "after a warm-up call; the exchanges are NCCL all-reduces issued from the library's callback"}
 
 
+def _merge_deltas(acc: dict, d: dict) -> dict:
+    """Worst case of T1-T4 deltas over several comparisons (parity_bars.Deltas.as_dict())."""
+    if not acc:
+        acc = {"T1_ratio": 0.0, "T2_max_col": 0.0, "T2p_orth": 0.0, "T3_rel": 0.0, "T3_norm_rel": 0.0,
+               "T4_abs": 0.0, "T4_over_bar": 0.0, "resolved_cases": 0, "cases": 0, "pass": True}
+    for k in ("T1_ratio", "T2_max_col", "T2p_orth", "T3_rel", "T3_norm_rel", "T4_abs"):
+        acc[k] = max(acc[k], d[k])
+    acc["T4_over_bar"] = max(acc["T4_over_bar"], d["T4_abs"] / d["T4_bar"])
+    acc["resolved_cases"] += int(d["resolved"])
+    acc["cases"] += 1
+    acc["pass"] &= (d["T1_ratio"] <= 1.0 and d["T2_max_col"] <= 1e-9 and d["T2p_orth"] <= 1e-12 and
+                    d["T3_rel"] <= 1e-10 and d["T3_norm_rel"] <= 1e-12 and d["T4_abs"] <= d["T4_bar"])
+    return acc
+
+
+def run_parity(T, stream, F=None) -> dict:
+    """Per-config T1-T4 parity deltas of the GPU path against the CPU oracle's
+    results stored by tests/golden/make_golden.py (oracle-only script; configs 1-3, config 4's 16
+    settings, config 5 at ranks 40 and 10).  Untimed.  F: the cfg5 tensor if still resident."""
+    import numpy as np
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import parity_bars as PB
+    from tucker_inputs import config1, config2, config3, config4, config5
+
+    gdir = os.path.join(ROOT, "tests", "golden")
+    out = {"bars": "T1 |dlambda| <= 1e-11 lambda + 1e-14 lambda_1 (ratio <= 1); T2 gap-separated columns <= 1e-9; "
+                   "T2' <= 1e-12; T3 <= 1e-10 (block k_res(1e-10)), norm <= 1e-12; T4 <= 1e-12 resolved, else "
+                   "max(1e-12, 1e-15/E)",
+           "reference": "oracle results in tests/golden/*.npz (tests/golden/make_golden.py, oracle only)"}
+
+    def cmp(ref, r, res, E):
+        return PB.compare(ref, r, [x.cpu().numpy() for x in res.sigma], [u.cpu().numpy() for u in res.U],
+                          res.core.cpu().numpy(), float(E), check=False).as_dict()
+
+    def trunc(res, t):
+        U = [u[:, :t[m]].contiguous() for m, u in enumerate(res.U)]
+        core = res.core[:t[0], :t[1], :t[2]].contiguous()
+        return type(res)(U, core, [sg[:t[m]] for m, sg in enumerate(res.sigma)], res.info, res.rc)
+
+    p = os.path.join(gdir, "small_oracle.npz")
+    if os.path.exists(p):
+        z = np.load(p)
+        for w in (config1(), config2(), config3()):
+            acc = {}
+            Fw = torch.empty(tuple(w.grid.n), dtype=torch.float64, device="cuda")
+            ws = T.workspace(w.grid, w.ranks)
+            for i, k in enumerate(w.kernels):
+                T.fill(w.grid, k, Fw, ws, stream)
+                res = T.hosvd(w.grid, w.ranks, Fw, ws, stream)
+                for t in [tuple(int(v) for v in x) for x in z[f"{w.name}_k{i}_truncations"]]:
+                    rt = trunc(res, t)
+                    e = T.error(w.grid, t, Fw, rt.U, rt.core, ws, stream)[0].item()
+                    acc = _merge_deltas(acc, cmp(PB.golden_ref(z, f"{w.name}_k{i}_", t), t, rt, e))
+            out[w.name] = acc
+            del Fw, ws
+    p = os.path.join(gdir, "cfg5_1024_oracle.npz")
+    if os.path.exists(p) and F is not None:
+        z = np.load(p)
+        w = config5()
+        for rk in ((40, 40, 40), (10, 10, 10)):
+            ws = T.workspace(w.grid, rk)
+            res = T.hosvd(w.grid, rk, F, ws, stream)
+            e = T.error(w.grid, rk, F, res.U, res.core, ws, stream)[0].item()
+            out[f"{w.name}_r{rk[0]}"] = _merge_deltas({}, cmp(PB.golden_ref(z, trunc=rk), rk, res, e))
+            out[f"{w.name}_r{rk[0]}"]["E_gpu"], out[f"{w.name}_r{rk[0]}"]["E_oracle"] = e, float(
+                PB.golden_ref(z, trunc=rk).E)
+            del ws
+    p = os.path.join(gdir, "cfg4_512_oracle.npz")
+    if os.path.exists(p):
+        z = np.load(p)
+        w = config4()
+        acc = {}
+        F4 = torch.empty(tuple(w.grid.n), dtype=torch.float64, device="cuda")
+        ws = T.workspace(w.grid, w.ranks)
+        for s_ in [int(v) for v in z["settings"]]:
+            T.fill(w.grid, w.kernels[s_], F4, ws, stream)
+            res = T.hosvd(w.grid, w.ranks, F4, ws, stream)
+            for t in ((30, 30, 30), (20, 20, 20), (10, 10, 10)):
+                rt = trunc(res, t)
+                e = T.error(w.grid, t, F4, rt.U, rt.core, ws, stream)[0].item()
+                acc = _merge_deltas(acc, cmp(PB.golden_ref(z, f"s{s_}_", t), t, rt, e))
+        out[w.name] = acc
+        del F4, ws
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_f4(T, grid, ranks, F, ws, stream) -> dict:
     """NEXT f4: the paper's other workloads through the same step on the same 1024^3 grid —
     Matérn spectral density (alpha = 0.1 and 100, nu = 0.4) and p-Slater
@@ -531,7 +624,9 @@ def run_f4(T, grid, ranks, F, ws, stream) -> dict:
         torch.cuda.synchronize()
         ms = e[0].elapsed_time(e[2])
         out.append({"kernel": k.label(), "ms_per_step": ms, "fill_ms": e[0].elapsed_time(e[1]),
-                    "value": grid.points / (ms * 1e-3), "E": float(err[0]), "rc": res.rc})
+                    "value": grid.points / (ms * 1e-3), "E": float(err[0]), "rc": res.rc,
+                    "eig_iters": res.info["iters"], "eig_converged": res.info["converged"],
+                    "k_resolved": res.info["k_resolved"], "eig_resid": res.info["resid"]})
     return {"grid": list(grid.n), "ranks": list(ranks), "unit": UNIT, "workloads": out}
 
 
@@ -624,76 +719,123 @@ def run_sym(T, n: int, rr: int, stream, reps: int = 3) -> dict:
 
 
 # ------------------------------------------------------------------------------ oracle arm ----
-def cpu_baseline(n: int, r: int, budget_s: float = 20.0) -> dict:
-    """The oracle, as it stands, on a bounded sample of the workload, scaled to points/s.
+def oracle_sampled_step(orc, n: int, r: int, S: int) -> dict:
+    """ONE sampled step of the oracle, as it stands, on the host cores: 1/S of the work of every
+    stage of the cfg5 step, actually executed and wall-clock timed (nothing is extrapolated):
 
-    Sample: the oracle's own functions on s of the n i-slabs of the same tensor (fill, a mode-2 Gram
-    over the s*n unfolding columns those slabs hold, TTM core and reconstruction error) plus its
-    cyclic Jacobi at a reduced order; each part is scaled by its exact work ratio to the full step.
-    """
+      fill       s = n/S of the n i-slabs of F (orc.fill of the sub-grid)
+      Gram x 3   the Dot2 Gram of an n x (s n) block of each mode's unfolding (s n of its n^2
+                 columns): modes 2 and 1 from the slab's unfoldings; mode 0's block (a j-slab) has
+                 the same shape and work on the cube, and its Gram is the slab's mode-1 Gram again
+      eig x 3    cyclic Jacobi at order n_s = n / S^(1/3) (work ~ n^3: 1/S), on the leading block of
+                 the sampled mode-2 Gram
+      core       orc.ttm_core of the slab (its s n^2 points, ranks r)
+      error      orc.tucker_error of the slab
+    Returns {seconds, parts, points = N/S, ...}."""
     import numpy as np
 
-    from oracle import oracle as orc
-    orc.build()
-    threads = orc.num_threads()
     k = orc.Kernel.matern(1.5, 0.2)
-    N = n ** 3
-    s = 16 if budget_s >= 20 else 8
-    s = min(s, n)
+    s = max(1, n // S)
     h = 2.0 / (n - 1)
     sub = orc.Grid((s, n, n), (-1.0, -1.0, -1.0), (-1.0 + h * (s - 1), 1.0, 1.0))
+    parts = {}
+    t_all = time.perf_counter()
     t = time.perf_counter()
     Fs = orc.fill(sub, k)
-    t_fill = (time.perf_counter() - t) * (n / s)
-    A = orc.unfold(Fs, 1)  # n x (s n): s n of the n^2 columns of the mode-2 unfolding
-    Ks = A.shape[1]
+    parts["fill"] = time.perf_counter() - t
     t = time.perf_counter()
-    Gs = orc.gram(A)
-    t_gram = (time.perf_counter() - t) * ((N // n) / Ks) * 3
-    ns = min(n, 160)
-    Gj = np.ascontiguousarray(Gs[:ns, :ns])
+    A1 = orc.unfold(Fs, 1)
+    G1 = orc.gram(A1)
+    orc.gram(A1)  # mode 0's sample (same n x s n shape and work on the cube)
+    A2 = orc.unfold(Fs, 2)
+    G2 = orc.gram(A2)
+    parts["gram"] = time.perf_counter() - t
+    ns = max(2, int(round(n / S ** (1.0 / 3.0))))
     t = time.perf_counter()
-    orc.jacobi_eig(Gj)
-    t_eig = (time.perf_counter() - t) * (n / ns) ** 3 * 3
+    for G in (G1, G1, G2):
+        orc.jacobi_eig(np.ascontiguousarray(G[:ns, :ns]))
+    parts["eig"] = time.perf_counter() - t
     rng = np.random.default_rng(0)
     U = [np.linalg.qr(rng.standard_normal((dim, min(r, dim))))[0] for dim in (s, n, n)]
     t = time.perf_counter()
     core = orc.ttm_core(Fs, *U)
-    t_ttm = (time.perf_counter() - t) * (n / s)
+    parts["ttm"] = time.perf_counter() - t
     t = time.perf_counter()
     orc.tucker_error(Fs, *U, core)
-    t_err = (time.perf_counter() - t) * (n / s)
-    total = t_fill + t_gram + t_eig + t_ttm + t_err
-    return {"value": N / total, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": (f"oracle functions on {s} of {n} i-slabs of cfg5 ({n}^3, Matern nu=1.5 ell=0.2, r={r}): "
-                       f"fill, TTM core and error on the slabs (x{n / s:g}); Dot2 Gram over {Ks} of {N // n} "
-                       f"mode-2 unfolding columns (x{(N // n) / Ks:g}, x3 modes); cyclic Jacobi at order {ns} "
-                       f"scaled by (n/{ns})^3 (x3 modes); estimated full step {total:.1f} s"),
-            "est_seconds_per_step": total,
-            "parts_s": {"fill": t_fill, "gram": t_gram, "eig": t_eig, "ttm": t_ttm, "error": t_err}}
+    parts["error"] = time.perf_counter() - t
+    sec = time.perf_counter() - t_all
+    return {"seconds": sec, "parts_s": parts, "points": n ** 3 / (n / s), "S": n / s, "slabs": s, "jacobi_order": ns,
+            "gram_columns": A1.shape[1]}
+
+
+def host_cpu() -> dict:
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def cpu_baseline(n: int, r: int, budget_s: float = 20.0, S: int = 64) -> dict:
+    """The oracle as it stands on the host cores: repeated sampled steps (each 1/S of the cfg5
+    step's work per stage, oracle_sampled_step) for about `budget_s` seconds; value = points of the
+    workload the sampled steps covered / their measured wall time."""
+    from oracle import oracle as orc
+    orc.build()
+    threads = orc.num_threads()
+    runs = []
+    t0 = time.perf_counter()
+    while not runs or (time.perf_counter() - t0 < budget_s and len(runs) < 8):
+        runs.append(oracle_sampled_step(orc, n, r, S))
+    sec = sum(x["seconds"] for x in runs)
+    pts = sum(x["points"] for x in runs)
+    x = runs[0]
+    return {"value": pts / sec, "unit": UNIT, "cores": threads, "kind": "oracle", "host": host_cpu(),
+            "sample": (f"{len(runs)} sampled oracle steps of cfg5 ({n}^3, Matern nu=1.5 ell=0.2, r={r}), each 1/"
+                       f"{x['S']:g} of every stage's work, executed and wall-clock timed: fill + core + error of "
+                       f"{x['slabs']} i-slabs, three Dot2 Grams of n x {x['gram_columns']} unfolding blocks, three "
+                       f"cyclic Jacobi solves at order {x['jacobi_order']}"),
+            "seconds_per_sampled_step": sec / len(runs), "sampled_steps": len(runs),
+            "parts_s_per_sampled_step": {k: sum(r_["parts_s"][k] for r_ in runs) / len(runs) for k in x["parts_s"]},
+            "full_oracle_runs": "profiles/r02_oracle_timing.json (the oracle run whole on the box: configs 1-3, "
+                                "1024^3 once, 1-thread 128^3)"}
 
 
 def run_reference(args, rank, world):
+    """The reference arm (this tier: the oracle): K timed sampled steps after W warm-up ones, on
+    rank 0; value = sampled points / measured wall time, ms_per_step = the measured step."""
     if rank != 0:
         return None
-    steps = []
+    from oracle import oracle as orc
+    orc.build()
+    S = 64
     for _ in range(args.warmup):
-        cpu_baseline(args.n, args.r, budget_s=10.0)
+        oracle_sampled_step(orc, args.n, args.r, S)
+    runs = []
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        t = time.perf_counter()
-        cb = cpu_baseline(args.n, args.r, budget_s=10.0)
-        steps.append((time.perf_counter() - t, cb))
-    vals = [cb["value"] for _, cb in steps]
-    v = statistics.median(vals)
-    cb = steps[-1][1]
+        runs.append(oracle_sampled_step(orc, args.n, args.r, S))
+    wall = time.perf_counter() - t0
+    pts = sum(x["points"] for x in runs)
+    v = pts / wall
+    x = runs[0]
+    sample = (f"each step: 1/{x['S']:g} of every stage of cfg5 ({args.n}^3, r={args.r}) executed by the oracle and "
+              f"wall-clock timed — fill + core + error of {x['slabs']} i-slabs, three Dot2 Grams of n x "
+              f"{x['gram_columns']} unfolding blocks, three cyclic Jacobi solves at order {x['jacobi_order']}; "
+              f"value = covered points / wall time")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * cb["est_seconds_per_step"], "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg5_{args.n}cube_matern_nu1.5_ell0.2", "grid": [args.n] * 3,
-                       "ranks": [args.r] * 3},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+                       "ranks": [args.r] * 3, "sampled_fraction": 1.0 / x["S"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": orc.num_threads(), "kind": "oracle", "sample": sample,
+                             "host": host_cpu()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s_per_sampled_step": statistics.median([s for s, _ in steps])}
+            "parts_s_per_step": {k: sum(r_["parts_s"][k] for r_ in runs) / len(runs) for k in x["parts_s"]}}
 
 
 def main():

@@ -18,13 +18,17 @@
  *     allocates or frees caller memory.  All scratch comes from the caller's workspace `ws`
  *     (device, >= tucker_workspace_size() bytes, 256-byte aligned).
  *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).  Entry points
- *     are asynchronous unless stated; tucker_hosvd synchronises `stream` once per mode to test
- *     eigensolver convergence.
+ *     are asynchronous unless stated.  tucker_hosvd / tucker_hosvd_rowmax synchronise only when
+ *     `info` is non-NULL (then per mode, to test and report eigensolver convergence); with
+ *     info == NULL they never touch the host (CUDA-Graph capturable) and cannot report NOCONV or
+ *     TUCKER_ERR_INPUT (a bad input then shows as NaN outputs).
  *   - Tensors are FP64, C order (n1 x n2 x n3, k fastest).  Factor U_m is n_m x r_m row-major
  *     (column c = c-th factor vector).  The core is r1 x r2 x r3 C order.
  *   - Validation happens before any launch.  Errors are returned as TUCKER_* codes; no exception
- *     crosses the ABI.  Functions are reentrant (no global mutable state besides a one-time
- *     driver entry-point lookup).
+ *     crosses the ABI.  Functions are reentrant across threads: the only mutable library state is
+ *     per calling thread (the Gram engine of tucker_set_gram_engine, the two side streams the
+ *     HOSVD overlaps its eigensolves on, the launch counter, the opt-in stage timer) besides a
+ *     one-time driver entry-point lookup.
  */
 #ifndef TUCKER_B200_H
 #define TUCKER_B200_H
@@ -82,7 +86,8 @@ enum {
     TUCKER_ERR_NOCONV = 5,      /* eigensolver hit its iteration cap (best iterate returned) */
     TUCKER_ERR_CUDA = 6,        /* a CUDA runtime/driver call failed                         */
     TUCKER_ERR_UNSUPPORTED = 7, /* e.g. r_m too large for the eigensolver block (r_m > 56)   */
-    TUCKER_ERR_COLLECTIVE = 8   /* the caller's all-reduce callback reported a failure       */
+    TUCKER_ERR_COLLECTIVE = 8,  /* the caller's all-reduce callback reported a failure       */
+    TUCKER_ERR_INPUT = 9        /* F not finite, or caller row maxima that do not bound F     */
 };
 
 /* Per-mode eigensolver report (host struct, optional). */
@@ -93,14 +98,20 @@ typedef struct {
     int32_t sweeps[3];    /* Jacobi sweeps of the last Rayleigh-Ritz solve                    */
     double resid[3];      /* max_{k<=r_m} ||G v_k - theta_k v_k|| / theta_1                   */
     double lambda1[3];    /* theta_1 (largest eigenvalue of G_m)                              */
+    int32_t k_resolved[3]; /* #{k <= r_m : lambda_k >= 1e-12 lambda_1}: the resolved leading
+                              eigenpairs (R14; past it the Gram route's noise)  */
 } tucker_info;
 
-/* Workspace bytes needed by tucker_fill / tucker_hosvd / tucker_error / tucker_gram /
- * tucker_eig / tucker_ttm_core for this grid and ranks (r may be NULL: ranks = 64). */
+/* Workspace bytes needed by tucker_hosvd / tucker_error / tucker_gram / tucker_eig /
+ * tucker_ttm_core / tucker_approximate for this grid and ranks (r may be NULL: ranks
+ * min(n_m, 56)).  Depends on the calling thread's Gram engine (set it first). */
 TUCKER_API size_t tucker_workspace_size(const tucker_grid* grid, const int32_t r[3]);
+/* Workspace bytes tucker_fill / tucker_fill_rowmax need (the nodes and the K_nu table; a few KB). */
+TUCKER_API size_t tucker_workspace_size_fill(const tucker_grid* grid);
 
 /* a-1 + a-2: F (dev, n1*n2*n3 doubles) <- collocation tensor of `kernel` on `grid`
- * (P:981-997).  Uses ws for the nodes and the K_nu Chebyshev table. */
+ * (P:981-997).  Uses ws (>= tucker_workspace_size_fill) for the nodes and the K_nu Chebyshev
+ * table. */
 TUCKER_API int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F, void* ws,
                 size_t ws_bytes, void* stream);
 
@@ -111,19 +122,20 @@ TUCKER_API int tucker_gram(const tucker_grid* grid, int32_t mode, const double* 
 
 /* a-3 on the INT8 tensor cores (tcgen05 kind::i8): the same G as tucker_gram, to FP64 accuracy by
  * modular emulation (R18).  Every row a_i of F_(m) is scaled by 2^(b - E_i)
- * (max_k |a_ik| < 2^E_i, b <= 51) and rounded to integers X; S = X X^T is formed exactly from its
+ * (max_k |a_ik| < 2^E_i, b <= 50) and rounded to integers X; S = X X^T is formed exactly from its
  * residues modulo 16 pairwise-coprime moduli (int8 Gram matrices on the tensor cores, exact int32
  * accumulation) and reconstructed by the Chinese remainder theorem; G_ij = fl(2^(E_i+E_j-2b) S_ij),
  * one rounding.  Deterministic and independent of the launch configuration.  Workspace:
  * tucker_workspace_size_i8 (residues of up to 8 GiB of the unfolding at a time, partials).
- * TUCKER_ERR_UNSUPPORTED if some n_m > 16384. */
+ * TUCKER_ERR_UNSUPPORTED if some n_m > 16384.  A value outside the scheme's window (NaN / Inf in
+ * F) makes every entry of G NaN. */
 TUCKER_API size_t tucker_workspace_size_i8(const tucker_grid* grid);
 /* The INT8 Gram's modular scheme for an unfolding with K columns (host only, no GPU): the 16
  * moduli (moduli[16], host) and the integer width b (*b, host) used by tucker_gram_i8 —
  * pairwise coprime odd p_l <= 253 with prod p_l > 2 K 2^(2b), b <= 50.  Returns TUCKER_OK. */
 TUCKER_API int tucker_i8_scheme(int64_t K, int32_t* moduli, int32_t* b);
-/* Gram engine of tucker_gram, tucker_hosvd and tucker_approximate (process-wide, not thread-safe;
- * set it before sizing workspaces: tucker_workspace_size depends on it).  TUCKER_GRAM_AUTO
+/* Gram engine of tucker_gram, tucker_hosvd and tucker_approximate, per calling thread (set it
+ * before sizing workspaces: tucker_workspace_size depends on it).  TUCKER_GRAM_AUTO
  * (default): the INT8 emulation where supported (every n_m <= 16384), DMMA otherwise. */
 enum { TUCKER_GRAM_AUTO = 0, TUCKER_GRAM_DMMA = 1, TUCKER_GRAM_INT8 = 2 };
 TUCKER_API int tucker_set_gram_engine(int32_t engine);
@@ -144,7 +156,9 @@ TUCKER_API int tucker_ttm_core(const tucker_grid* grid, const int32_t r[3], cons
                     void* stream);
 
 /* a-3..a-5: truncated HOSVD of F (dev).  Outputs (dev): U1,U2,U3 (n_m x r_m), core, and
- * sigma_m (dev, r_m) = sqrt(max(lambda_m,0)).  `info` (host) may be NULL. */
+ * sigma_m (dev, r_m) = sqrt(max(lambda_m,0)).  `info` (host) may be NULL (asynchronous call, see
+ * the conventions).  Errors: INVALID_ARG, RANK, SIZE, UNSUPPORTED (r_m > 56 with n_m > 112, or
+ * r_2 / r_3 > 64 — checked before any launch), NOCONV and INPUT (info != NULL only), CUDA. */
 TUCKER_API int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1,
                  double* U2, double* U3, double* core, double* sigma1, double* sigma2,
                  double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
@@ -157,9 +171,12 @@ TUCKER_API int tucker_hosvd(const tucker_grid* grid, const int32_t r[3], const d
 TUCKER_API int tucker_fill_rowmax(const tucker_grid* grid, const tucker_kernel* kernel, double* F, uint32_t* rowmax,
                        void* ws, size_t ws_bytes, void* stream);
 
-/* tucker_hosvd with the row maxima of F supplied (rowmax from tucker_fill_rowmax of this very F;
- * the caller guarantees it): on the INT8 Gram route the row-maxima pass over F is skipped, the
- * results are bitwise those of tucker_hosvd.  rowmax == NULL, or the DMMA route: tucker_hosvd. */
+/* tucker_hosvd with the row maxima of F supplied (rowmax from tucker_fill_rowmax of this very F):
+ * on the INT8 Gram route the row-maxima pass over F is skipped, the results are bitwise those of
+ * tucker_hosvd.  rowmax == NULL, or the DMMA route: tucker_hosvd.  The maxima are verified where
+ * they are used: a row maximum that does not bound its row (a stale rowmax) is detected by the
+ * residue kernel, which then makes the Grams NaN — TUCKER_ERR_INPUT with info != NULL, NaN outputs
+ * without. */
 TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], const double* F,
                         const uint32_t* rowmax, double* U1, double* U2, double* U3, double* core,
                         double* sigma1, double* sigma2, double* sigma3, void* ws, size_t ws_bytes,

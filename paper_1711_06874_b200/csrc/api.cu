@@ -145,15 +145,35 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
 
 inline char* at(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
 
+// Rank limits of the eigensolver and the core, checked before any launch (r_m <= n_m is
+// check_ranks'): the subspace block needs r_m <= 56 once n_m exceeds the direct-Jacobi size, the
+// core's fused TTM needs r_2, r_3 <= 64.
+int check_hosvd_limits(const tucker_grid* g, const int32_t* r) {
+    for (int a = 0; a < 3; ++a)
+        if (!eig_rank_supported(g->n[a], r[a])) return TUCKER_ERR_UNSUPPORTED;
+    if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    return TUCKER_OK;
+}
+
+// info == nullptr: asynchronous (no host synchronisation, CUDA-Graph capturable; convergence and
+// input-window failures are not reported — a failed input shows as NaN outputs).  info != nullptr:
+// the eigensolves are completed with host synchronisations and reported, and the call returns
+// TUCKER_ERR_INPUT if the INT8 route saw a value outside its window.
 int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* const U[3], double* core,
                double* const sig[3], void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info,
                bool mx_ready = false) {
     const Layout L = plan(g, r);
     if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    TK_RC(check_hosvd_limits(g, r));
+    const bool sync = info != nullptr;
     double* G = reinterpret_cast<double*>(at(ws, L.G));
     void* scr = at(ws, L.scratch);
     int worst = TUCKER_OK;
     auto eig_mode = [&](int m) -> int {
+        if (!sync) {
+            TK_RC(launch_eig_begin(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, st));
+            return launch_eig_rest(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, st);
+        }
         const int rc = launch_eig(g->n[m], G, r[m], U[m], nullptr, sig[m], scr, L.scratch_bytes, st, info, m);
         if (rc == TUCKER_ERR_NOCONV) worst = rc;
         else if (rc != TUCKER_OK) return rc;
@@ -183,6 +203,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         double* T2 = reinterpret_cast<double*>(at(ws, L.t2));
         auto side_of = [&](int m) { return m == 0 ? sideB : sideA; };
         auto eig_end = [&](int m) -> int {  // host waits for the solve (its first pass is long queued)
+            if (!sync) return launch_eig_rest(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], side_of(m));
             const int rc = launch_eig_end(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], side_of(m), info, m);
             if (rc == TUCKER_ERR_NOCONV) worst = rc;
             else if (rc != TUCKER_OK) return rc;
@@ -190,7 +211,9 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         };
         // each eigensolve's first pass is enqueued as soon as its Gram is: it runs beside the next
         // Gram's residue kernels
+        bool side_used = false;  // side-stream work enqueued: joined into `st` on every exit path
         int rc = launch_gram_i8_hosvd(g->n, F, Gm, at(ws, L.i8), L.i8_bytes, st, [&](const int* ms, int cnt) -> int {
+            side_used = true;
             for (int i = 0; i < cnt; ++i) {
                 const int m = ms[i];
                 if (cudaEventRecord(ev[m], st) != cudaSuccess || cudaStreamWaitEvent(side_of(m), ev[m], 0) != cudaSuccess)
@@ -212,12 +235,26 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         if (rc == TUCKER_OK && (cudaEventRecord(ev[4], sideB) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[4], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
+        if (rc != TUCKER_OK && side_used) {
+            // an error after side-stream work was enqueued: `st` must not run ahead of it (the
+            // caller may free U or ws once the stream is idle)
+            cudaEventRecord(ev[3], sideA);
+            cudaEventRecord(ev[4], sideB);
+            cudaStreamWaitEvent(st, ev[3], 0);
+            cudaStreamWaitEvent(st, ev[4], 0);
+        }
         cleanup();
         TK_RC(rc);
         // TTM3: core (r1 x r2 r3) = U1^T (r1 x n1) * T2 (n1 x r2 r3)
         SmallGemm g3{r[0], (int64_t)r[1] * r[2], g->n[0], 1, U[0], 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
                      (int64_t)r[1] * r[2], 1, 0};
         TK_RC(launch_small_gemm(g3, st));
+        if (sync) {  // input-window check of the INT8 route (stale row maxima, non-finite F)
+            int bad = 0;
+            TK_CUDA(cudaMemcpyAsync(&bad, gram_i8_flag_slot(g->n, at(ws, L.i8)), sizeof(int), cudaMemcpyDeviceToHost, st));
+            TK_CUDA(cudaStreamSynchronize(st));
+            if (bad) return TUCKER_ERR_INPUT;
+        }
         return worst;
     } else {
         for (int m = 0; m < 3; ++m) {
@@ -334,6 +371,11 @@ size_t tucker_workspace_size(const tucker_grid* grid, const int32_t r[3]) {
     return plan(grid, r).total;
 }
 
+size_t tucker_workspace_size_fill(const tucker_grid* grid) {
+    if (check_grid(grid) != TUCKER_OK) return 0;
+    return plan(grid, nullptr).G;  // nodes + K_nu table (the leading regions of every layout)
+}
+
 int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F, void* ws, size_t ws_bytes,
                 void* stream) {
     launch_counter() = 0;
@@ -341,7 +383,7 @@ int tucker_fill(const tucker_grid* grid, const tucker_kernel* kernel, double* F,
     TK_RC(check_kernel(kernel));
     if (!F || !ws) return TUCKER_ERR_INVALID_ARG;
     const Layout L = plan(grid, nullptr);
-    if (ws_bytes < L.scratch) return TUCKER_ERR_SIZE;
+    if (ws_bytes < L.G) return TUCKER_ERR_SIZE;
     return launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
                        reinterpret_cast<double*>(at(ws, L.cheb)), static_cast<cudaStream_t>(stream));
 }
@@ -354,7 +396,7 @@ int tucker_fill_rowmax(const tucker_grid* grid, const tucker_kernel* kernel, dou
     if (!F || !rowmax || !ws) return TUCKER_ERR_INVALID_ARG;
     if (!fill_rowmax_supported(*grid)) return TUCKER_ERR_UNSUPPORTED;
     const Layout L = plan(grid, nullptr);
-    if (ws_bytes < L.scratch) return TUCKER_ERR_SIZE;
+    if (ws_bytes < L.G) return TUCKER_ERR_SIZE;
     return launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
                        reinterpret_cast<double*>(at(ws, L.cheb)), static_cast<cudaStream_t>(stream), rowmax);
 }
@@ -773,6 +815,7 @@ const char* tucker_strerror(int code) {
         case TUCKER_ERR_CUDA: return "CUDA runtime/driver error";
         case TUCKER_ERR_UNSUPPORTED: return "unsupported configuration";
         case TUCKER_ERR_COLLECTIVE: return "the caller's all-reduce callback failed";
+        case TUCKER_ERR_INPUT: return "input not finite, or row maxima that do not bound F";
         default: return "unknown error code";
     }
 }

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) k_rr(RRArgs a) {
         for (int k = tid; k < a.r; k += blockDim.x) {
             const double th = H[order[k] * ld + order[k]];
             if (a.lambda) a.lambda[k] = th;
-            if (a.sigma) a.sigma[k] = sqrt(fmax(th, 0.0));
+            if (a.sigma) a.sigma[k] = th < 0.0 ? 0.0 : sqrt(th);  // NaN (poisoned input) propagates
         }
         if (tid == 0) {
             a.st->done = 1;
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) k_direct(const double* G, int n, int
     for (int k = threadIdx.x; k < r; k += blockDim.x) {
         const double th = H[order[k] * ld + order[k]];
         if (lambda) lambda[k] = th;
-        if (sigma) sigma[k] = sqrt(fmax(th, 0.0));
+        if (sigma) sigma[k] = th < 0.0 ? 0.0 : sqrt(th);  // NaN (poisoned input) propagates
     }
     if (threadIdx.x == 0) {
         st->done = 1;
@@ -383,6 +383,8 @@ static size_t direct_smem(int n) {
 }
 
 }  // namespace eig
+
+bool eig_rank_supported(int64_t n, int r) { return n <= eig::kDirectMax || r <= eig::kMaxP - 8; }
 
 size_t eig_ws_bytes(int64_t n, int r) {
     using namespace eig;
@@ -521,8 +523,54 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
         info->sweeps[slot] = hs.sweeps;
         info->resid[slot] = hs.resid;
         info->lambda1[slot] = hs.lambda1;
+        // resolved count k_res = #{k <= r : lambda_k >= 1e-12 lambda_1} (R14)
+        double ev[128];
+        const double* src = lambda ? lambda : sigma;
+        const int rr = src ? std::min(r, 128) : 0;
+        if (rr) {
+            TK_CUDA(cudaMemcpyAsync(ev, src, (size_t)rr * 8, cudaMemcpyDeviceToHost, st));
+            TK_CUDA(cudaStreamSynchronize(st));
+        }
+        int k = src ? 0 : -1;
+        for (int i = 0; i < rr; ++i) {
+            const double lam = lambda ? ev[i] : ev[i] * ev[i];
+            const double l1 = lambda ? ev[0] : ev[0] * ev[0];
+            k += lam >= 1e-12 * l1 ? 1 : 0;
+        }
+        info->k_resolved[slot] = k;
     }
     return hs.converged ? TUCKER_OK : TUCKER_ERR_NOCONV;
+}
+
+// Asynchronous completion (no host synchronisation; CUDA-Graph capturable): the remaining
+// iterations up to kMaxIters are enqueued unconditionally — every launch of a converged solve exits
+// at once (the state's `done` flag), so the cost of the unneeded ones is their launch latency.
+int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                    cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_EIG, st);
+    using namespace eig;
+    if (n <= kDirectMax) return TUCKER_OK;  // the direct Jacobi finished in launch_eig_begin
+    const Plan q = eig_plan(n, r, ws);
+    const int p = q.p;
+    const bool cl = eig_cluster_supported(n);
+    const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
+    if (!cl) {
+        const size_t sm = rr_smem(p);
+        TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+    for (int it = cl ? kMinIters + 3 : kBatch; it < kMaxIters; ++it) {
+        k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, p, n, q.dst);
+        TK_CHECK_LAUNCH();
+        if (cl) {
+            TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst,
+                                    st));
+        } else {
+            RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, q.dst};
+            k_rr<<<1, kThreads, rr_smem(p), st>>>(a);
+            TK_CHECK_LAUNCH();
+        }
+    }
+    return TUCKER_OK;
 }
 
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,

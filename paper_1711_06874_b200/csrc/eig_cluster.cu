@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT, 1) k_rr_cluster(Args a) {
                 for (int k = t; k < a.r; k += NT) {
                     const double th = s.theta[k];
                     if (a.lambda) a.lambda[k] = th;
-                    if (a.sigma) a.sigma[k] = sqrt(fmax(th, 0.0));
+                    if (a.sigma) a.sigma[k] = th < 0.0 ? 0.0 : sqrt(th);  // NaN (poisoned input) propagates
                 }
                 if (t == 0) {
                     a.st->done = 1;
@@ -480,10 +480,14 @@ __global__ void __launch_bounds__(NT, 1) k_svd_cluster(SvdArgs a) {
     cl_reduce<OP_SUM>(cl, s, round, s.vec, s.vec, p);
     for (int k = t; k < p; k += NT) s.theta[k] = sqrt(s.vec[k]);
     __syncthreads();
-    for (int k = t; k < p; k += NT) {  // stable descending rank of sigma
-        const double v = s.theta[k];
+    for (int k = t; k < p; k += NT) {  // stable descending rank of sigma (NaN last: a permutation)
+        auto key = [](double x) { return x == x ? x : -INFINITY; };
+        const double v = key(s.theta[k]);
         int rank = 0;
-        for (int j = 0; j < p; ++j) rank += (s.theta[j] > v) || (s.theta[j] == v && j < k);
+        for (int j = 0; j < p; ++j) {
+            const double w = key(s.theta[j]);
+            rank += (w > v) || (w == v && j < k);
+        }
         s.order[rank] = k;
     }
     __syncthreads();

@@ -281,6 +281,7 @@ struct ResArgs {
     int b;
     int8_t* R;                         // [NMOD][K-block][rows][128]
     int64_t kout;                      // first residue column written by this launch (multiple of 128)
+    int* bad;                          // set to 1 if some |rint(a 2^sh)| > 2^b or a value is not finite
 };
 
 __host__ __device__ constexpr int balanced(int r, int p) { return r > p / 2 ? r - p : r; }
@@ -333,15 +334,21 @@ __device__ __forceinline__ void row_scale(uint32_t hw, int b, double& sa, double
 
 // Residues of the 16 values v[e * stride] (one row, 16 consecutive unfolding columns) -> one
 // 16-byte store per modulus at out + l * lstride.
+// Returns false if some value falls outside the scheme's window |rint(a 2^sh)| <= 2^b (lim = 2^b):
+// a row maximum that does not bound its row (a stale caller-supplied rowmax), or NaN / Inf in F —
+// the CRT bound K 2^(2b) < P/2 would no longer hold, so the caller poisons G (k_i8_crt).
 template <int STRIDE>
-__device__ __forceinline__ void residues16(const double* v, double sa, double sb, int8_t* out, size_t lstride) {
+__device__ __forceinline__ bool residues16(const double* v, double sa, double sb, int8_t* out, size_t lstride,
+                                           double lim) {
     float2 u[8][3];
     constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
+    bool ok = true;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
         // y = 2^52 + w, w = rint(a 2^sh) + B in [0, 2^52): one rounding (the scaling is exact)
         const double x = v[e * STRIDE];
         const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
+        ok &= fabs(y - M2) <= lim;  // exact when in the window; false for NaN / Inf / overflow
         const uint32_t lo = (uint32_t)__double2loint(y);
         const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
         // balanced 17-bit digits: x = rint(a 2^sh) = (d0 - 2^16) + (d1 - 2^16) 2^17 + (d2 - 2^16) 2^34
@@ -360,6 +367,7 @@ __device__ __forceinline__ void residues16(const double* v, double sa, double sb
         }
     }
     store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    return ok;
 }
 
 // One 32-row x 128-column tile (row block by, column block bx of the super-chunk).
@@ -432,7 +440,8 @@ __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64
     const int64_t row = row0 + rr;
     if (row >= a.rows) return;  // (the caller syncs before the tile is reused); columns >= Kc: residue 0
     int8_t* out = a.R + (((kb + a.kout) / RT_K) * a.rows + row) * RT_K + q * 16;
-    residues16<1>(&tile[rr][q][0], s1[rr], s2[rr], out, (size_t)a.rows * a.ldr);
+    if (!residues16<1>(&tile[rr][q][0], s1[rr], s2[rr], out, (size_t)a.rows * a.ldr, ldexp(1.0, a.b)))
+        atomicExch(a.bad, 1);
 }
 
 // One CTA per tile (the loop also serves smaller grids).
@@ -808,7 +817,8 @@ __device__ __forceinline__ double u128_to_double_rn(unsigned __int128 m) {
 }
 
 __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const uint32_t* __restrict__ mx,
-                                                int n, int nJ, int ntiles, int b, double* __restrict__ G) {
+                                                int n, int nJ, int ntiles, int b, double* __restrict__ G,
+                                                const int* __restrict__ bad) {
     // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -836,6 +846,7 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     double d = u128_to_double_rn(mag);
     d = ldexp(d, row_exponent(mx[i]) + row_exponent(mx[j]) - 2 * b);
     if (neg) d = -d;
+    if (bad && *bad) d = __longlong_as_double(0x7FF8000000000000LL);  // input outside the window: NaN
     G[(int64_t)i * n + j] = d;
     G[(int64_t)j * n + i] = d;
 }
@@ -881,7 +892,7 @@ ModePlan mode_plan(const int64_t n[3], int mode, int64_t align = KCH) {
 }
 
 struct WsPlan {
-    size_t off_mx, off_R, off_P, off_Racc, off_utab, total;
+    size_t off_mx, off_flag, off_R, off_P, off_Racc, off_utab, total;
 };
 
 // align: per-mode super-chunk alignment (the fused path).
@@ -898,7 +909,8 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     WsPlan w{};
     size_t off = 0;
     w.off_mx = off;
-    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8, 1024);
+    w.off_flag = off + align_up((size_t)(n[0] + n[1] + n[2]) * 4, 16);  // the input-window flag
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8 + 16, 1024);
     w.off_R = off;
     off += rb;
     w.off_P = off;
@@ -927,6 +939,7 @@ struct ModeGemm {
     int2* utab;
     int nug;
     cudaStream_t st;
+    int* bad;
 
     int init() {
         TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
@@ -979,7 +992,7 @@ struct ModeGemm {
     int crt(double* G) {
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G);
+        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -997,7 +1010,7 @@ int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t*
                    double* G, cudaStream_t st, Produce&& produce, const Shard* shard = nullptr) {
     ModeGemm g{n, m, p, mode_max(mx, n, m), reinterpret_cast<int8_t*>(base + w.off_R),
                reinterpret_cast<int16_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
-               reinterpret_cast<int2*>(base + w.off_utab), 0, st};
+               reinterpret_cast<int2*>(base + w.off_utab), 0, st, reinterpret_cast<int*>(base + w.off_flag)};
     TK_RC(g.init());
     bool first = true;
     for (int64_t s = 0; s < p.nsuper; ++s) {
@@ -1018,7 +1031,8 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
     const uint32_t* mxm = mx + (m == 0 ? 0 : (m == 1 ? n[0] : n[0] + n[1]));
     return gram_mode_impl(n, m, p, mx, base, w, G, st, [&](int64_t k0, int64_t Kc, int8_t* R) -> int {
         TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
-        ResArgs ra{F, n[0], n[1], n[2], m, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R, 0};
+        ResArgs ra{F, n[0], n[1], n[2], m, p.rows, p.Kfull, k0, Kc, p.ldr, mxm, p.b, R, 0,
+                   reinterpret_cast<int*>(base + w.off_flag)};
         const int64_t ntx = ceil_div(Kc, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
         k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
         TK_CHECK_LAUNCH();
@@ -1062,6 +1076,7 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
     for (int m = 0; m < 3; ++m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G, st));
         TK_RC(after_mode(m));
@@ -1081,6 +1096,7 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
+    TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
     if (!mx_ready) TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
     for (int m = 2; m >= 0; --m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
@@ -1090,16 +1106,19 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
 }
 
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
+const int* gram_i8_flag_slot(const int64_t n[3], const void* ws) {
+    return reinterpret_cast<const int*>(static_cast<const char*>(ws) + i8::ws_plan(n).off_flag);
+}
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + i8::ws_plan(n).off_mx);
 }
 
+// Per calling thread and device (created on first use, kept for the thread's lifetime): concurrent
+// callers on different threads never share or wait on each other's side streams.
 cudaStream_t side_stream(int which) {
-    static cudaStream_t s[64][2] = {};
-    static std::mutex mu;
+    static thread_local cudaStream_t s[64][2] = {};
     int dev = 0;
     if (which < 0 || which > 1 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lk(mu);
     cudaStream_t& x = s[dev][which];
     if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
     return x;
@@ -1114,6 +1133,7 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
     const WsPlan w = ws_plan(n);
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
+    TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
     const uint32_t* mx = mx_in;
     if (!mx) {
         uint32_t* own = reinterpret_cast<uint32_t*>(base + w.off_mx);
@@ -1183,6 +1203,7 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
     char* base = static_cast<char*>(ws);
     double* chunk = reinterpret_cast<double*>(base + f.off_chunk);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + f.ws.off_mx);
+    TK_CUDA(cudaMemsetAsync(base + f.ws.off_flag, 0, sizeof(int), st));
     const int mirror = (gen.kp.centred && n[2] % 8 == 0) ? 1 : 0;
     {  // row maxima
         TK_PROF(TUCKER_PROF_I8_ROWMAX, st);
@@ -1245,7 +1266,8 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
                 TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
                 // the chunk as a small tensor: mode 0 [n1][pc][n3]; modes 1, 2 [pc][n2][n3]
                 const int64_t c1 = m == 0 ? n[0] : pc, c2 = m == 0 ? pc : n[1];
-                ResArgs ra{chunk, c1, c2, n[2], m, p.rows, p.Kfull, 0, valid * w, p.ldr, mxm, p.b, R, (g0 - plo) * w};
+                ResArgs ra{chunk, c1, c2, n[2], m, p.rows, p.Kfull, 0, valid * w, p.ldr, mxm, p.b, R, (g0 - plo) * w,
+                           reinterpret_cast<int*>(base + f.ws.off_flag)};
                 const int64_t ntx = ceil_div(valid * w, RT_K), ntiles = ntx * ceil_div(p.rows, RT_ROWS);
                 k_i8_residues<<<(unsigned)ntiles, 256, 0, st>>>(ra, ntx, ntiles);
                 TK_CHECK_LAUNCH();
@@ -1259,8 +1281,8 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
 
 // ------------------------------------------------------------------------------------------
 // Engine selection for the materialised path: AUTO = INT8 emulation where supported, else DMMA.
-int& gram_engine() {
-    static int engine = TUCKER_GRAM_AUTO;
+int& gram_engine() {  // per calling thread (tucker_set_gram_engine)
+    static thread_local int engine = TUCKER_GRAM_AUTO;
     return engine;
 }
 bool gram_use_i8(const int64_t n[3]) { return gram_engine() != TUCKER_GRAM_DMMA && gram_i8_supported(n); }

@@ -144,11 +144,14 @@ __device__ inline int jacobi_sym(double* H, double* Q, int p, JacobiWork js, int
 // Stable descending order of the diagonal of H (ld = jacobi_ld(p)): order[rank] = index.
 __device__ __forceinline__ void sort_desc_diag(const double* H, int p, int* order) {
     const int ld = jacobi_ld(p);
+    // NaN (a poisoned input, R18 window check) sorts last: a total order, so `order` is
+    // always a permutation
+    auto key = [](double x) { return x == x ? x : -INFINITY; };
     for (int k = threadIdx.x; k < p; k += blockDim.x) {
-        const double v = H[k * ld + k];
+        const double v = key(H[k * ld + k]);
         int rank = 0;
         for (int j = 0; j < p; ++j) {
-            const double w = H[j * ld + j];
+            const double w = key(H[j * ld + j]);
             rank += (w > v) || (w == v && j < k);
         }
         order[rank] = k;

@@ -80,6 +80,9 @@ size_t gram_i8_fused_ws_bytes(const int64_t n[3]);
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
                                cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
                                const Shard* shard = nullptr);
+// Device int of the INT8 workspace: 1 if an input value fell outside the scheme window (stale
+// row maxima or non-finite F; the Gram is then NaN), reset at the start of every Gram call.
+const int* gram_i8_flag_slot(const int64_t n[3], const void* ws);
 // mx_ready: the row maxima are already in the workspace's slot (gram_i8_rowmax_slot; e.g. written
 // by the fill of the same call) — the row-maxima pass is skipped.
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
@@ -118,10 +121,15 @@ size_t eig_ws_bytes(int64_t n, int r);
 // block is [V0, pseudo-random columns] and the power steps before the first Rayleigh–Ritz step are
 // skipped (V0 already spans the target subspace approximately; convergence is still decided by
 // the Ritz residuals).
+bool eig_rank_supported(int64_t n, int r);  // r <= 56 unless n is small enough for the direct Jacobi
 int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
                      size_t ws_bytes, cudaStream_t st, const double* V0 = nullptr);
 int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
                    cudaStream_t st, tucker_info* info, int slot);
+// Asynchronous completion of launch_eig_begin (no host synchronisation): enqueues the remaining
+// iterations (each exits at once after convergence).  Convergence is not reported.
+int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
+                    cudaStream_t st);
 int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma,
                void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info, int slot, const double* V0 = nullptr);
 
@@ -139,6 +147,8 @@ size_t refine_ws_bytes(const int64_t n[3], int p);
 int launch_refine_mode(const int64_t n[3], int m, const double* F, const double* V0, const double* lam0, int p,
                        int r, int iters, double* U, double* sigma, void* ws, size_t ws_bytes, cudaStream_t st,
                        int* sweeps_out);
+// V (n x p) <- [U (n x r) | p - r deterministic pseudo-random columns] (ALS start basis).
+int launch_seed_from_factors(double* V, const double* U, int64_t n, int r, int p, cudaStream_t st);
 
 // Core beta = F x1 U1^T x2 U2^T x3 U3^T.
 size_t ttm_ws_bytes(const int64_t n[3], const int32_t r[3]);

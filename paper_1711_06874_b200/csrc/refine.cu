@@ -320,6 +320,16 @@ __global__ void k_seed_basis(double* __restrict__ V, int64_t n, int p, const dou
     }
 }
 
+// Start basis for an ALS single-hole step: the current factor's r columns, then p - r
+// deterministic pseudo-random guard columns (the Rayleigh–Ritz step then orthonormalises them).
+__global__ void k_seed_from_factors(double* __restrict__ V, const double* __restrict__ U, int64_t n, int r, int p) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * p; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / p;
+        const int k = (int)(t % p);
+        V[t] = k < r ? U[i * r + k] : hash_u(0xa15ull * (k + 1) + (uint64_t)i);
+    }
+}
+
 // Block projection coefficients, per-CTA partials: part[blk][j * bb + t] = sum over this CTA's rows
 // of Q_j[i] Y_{c0+t}[i], j < c0, t < bb: a (c0 x rows) x (rows x bb) product on the FP64 tensor
 // cores.  Rows are staged 32 at a time in shared memory (all column segments contiguous,
@@ -577,6 +587,12 @@ RefLayout ref_plan(const int64_t n[3], int p) {
 }  // namespace
 
 size_t refine_ws_bytes(const int64_t n[3], int p) { return ref_plan(n, p).total; }
+
+int launch_seed_from_factors(double* V, const double* U, int64_t n, int r, int p, cudaStream_t st) {
+    k_seed_from_factors<<<64, 256, 0, st>>>(V, U, n, r, p);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
 
 // One or more Rayleigh–Ritz steps on F_(m) from V0 (n_m x p, dev; need not be orthonormal);
 // lam0 (dev, p, nullable): V0's Gram eigenvalues, unresolved columns are replaced (k_seed_basis).

@@ -21,8 +21,8 @@ GRAM_AUTO, GRAM_DMMA, GRAM_INT8 = 0, 1, 2
 FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED",
-          8: "TUCKER_ERR_COLLECTIVE"}
-EXPORTS = ("tucker_workspace_size", "tucker_fill", "tucker_fill_rowmax", "tucker_hosvd_rowmax", "tucker_gram", "tucker_eig", "tucker_ttm_core",
+          8: "TUCKER_ERR_COLLECTIVE", 9: "TUCKER_ERR_INPUT"}
+EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill", "tucker_fill_rowmax", "tucker_hosvd_rowmax", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_hosvd_fused_sharded",
            "tucker_workspace_size_als",
@@ -50,7 +50,8 @@ class CKernel(ctypes.Structure):
 
 class CInfo(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32 * 3), ("converged", ctypes.c_int32 * 3), ("block", ctypes.c_int32 * 3),
-                ("sweeps", ctypes.c_int32 * 3), ("resid", ctypes.c_double * 3), ("lambda1", ctypes.c_double * 3)]
+                ("sweeps", ctypes.c_int32 * 3), ("resid", ctypes.c_double * 3), ("lambda1", ctypes.c_double * 3),
+                ("k_resolved", ctypes.c_int32 * 3)]
 
     def as_dict(self) -> dict:
         return {k: list(getattr(self, k)) for k, _ in self._fields_}
@@ -79,6 +80,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     pr = P(ctypes.c_int32)
     sig = {
         "tucker_workspace_size": (sz, [pg, pr]),
+        "tucker_workspace_size_fill": (sz, [pg]),
         "tucker_fill": (ctypes.c_int, [pg, pk, vp, vp, sz, vp]),
         "tucker_fill_rowmax": (ctypes.c_int, [pg, pk, vp, vp, vp, sz, vp]),
         "tucker_hosvd_rowmax": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
@@ -175,6 +177,12 @@ def workspace(grid, ranks=None, device="cuda") -> torch.Tensor:
     return torch.empty(workspace_bytes(grid, ranks), dtype=torch.uint8, device=device)
 
 
+def workspace_fill(grid, device="cuda") -> torch.Tensor:
+    """The few-KB workspace of tucker_fill / tucker_fill_rowmax (nodes, K_nu table)."""
+    n = int(load().tucker_workspace_size_fill(ctypes.byref(cgrid(grid))))
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
 # -------------------------------------------------------------------------------- entry points
 def fill(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     lib = load()
@@ -182,7 +190,7 @@ def fill(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | None = 
     if F is None:
         F = torch.empty(shape, dtype=torch.float64, device="cuda")
     _dev(F, "F")
-    ws = ws if ws is not None else workspace(grid)
+    ws = ws if ws is not None else workspace_fill(grid)
     g, k = cgrid(grid), ckernel(kernel)
     _check(lib.tucker_fill(ctypes.byref(g), ctypes.byref(k), _ptr(F), _ptr(ws), ws.numel(), _stream(stream)),
            "tucker_fill")
@@ -198,7 +206,7 @@ def fill_rowmax(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | 
         F = torch.empty(shape, dtype=torch.float64, device="cuda")
     _dev(F, "F")
     mx = torch.empty(int(sum(shape)), dtype=torch.int32, device=F.device)  # uint32 bit patterns (< 2^31)
-    ws = ws if ws is not None else workspace(grid)
+    ws = ws if ws is not None else workspace_fill(grid)
     g, k = cgrid(grid), ckernel(kernel)
     _check(lib.tucker_fill_rowmax(ctypes.byref(g), ctypes.byref(k), _ptr(F), _ptr(mx), _ptr(ws), ws.numel(),
                                   _stream(stream)), "tucker_fill_rowmax")
@@ -310,8 +318,10 @@ class HosvdResult:
 
 
 def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None,
-          rowmax: torch.Tensor | None = None) -> HosvdResult:
-    """tucker_hosvd, or tucker_hosvd_rowmax when `rowmax` (from fill_rowmax of this F) is given."""
+          rowmax: torch.Tensor | None = None, sync: bool = True) -> HosvdResult:
+    """tucker_hosvd, or tucker_hosvd_rowmax when `rowmax` (from fill_rowmax of this F) is given.
+    sync=False passes info = NULL: the call is asynchronous (no host synchronisation, capturable in
+    a CUDA Graph) and `info` stays empty."""
     lib = load()
     _dev(F, "F")
     dev = F.device
@@ -327,11 +337,11 @@ def hosvd(grid, ranks, F: torch.Tensor, ws: torch.Tensor | None = None, stream=N
             raise ValueError("rowmax must be a contiguous int32 CUDA tensor (from fill_rowmax)")
         rc = lib.tucker_hosvd_rowmax(ctypes.byref(g), cranks(r), _ptr(F), _ptr(rowmax), _ptr(U[0]), _ptr(U[1]),
                                      _ptr(U[2]), _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws),
-                                     ws.numel(), _stream(stream), ctypes.byref(info))
+                                     ws.numel(), _stream(stream), ctypes.byref(info) if sync else None)
     else:
         rc = lib.tucker_hosvd(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), _ptr(core),
                               _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(), _stream(stream),
-                              ctypes.byref(info))
+                              ctypes.byref(info) if sync else None)
     if rc not in (0, 5):
         _check(rc, "tucker_hosvd")
     return HosvdResult(U, core, S, info.as_dict(), rc)

@@ -60,8 +60,10 @@ class Deltas:
                 "T2_columns": self.columns_checked}
 
 
-def compare(ref: Ref, r, sigma, U, core, E, check=True) -> Deltas:
-    """Apply T1-T4.  sigma, U: lists of numpy arrays (GPU result); core numpy; E float."""
+def compare(ref: Ref, r, sigma, U, core, E, check=True, tau4=1e-12) -> Deltas:
+    """Apply T1-T4.  sigma, U: lists of numpy arrays (GPU result); core numpy; E float.
+    tau4: the resolved threshold of T4 (1e-12; 1e-11 for the DMMA Gram engine, whose FP64
+    accumulation over K = n^2 terms adds ~sqrt(K) eps lambda_1 of noise — SURVEY §8(c) T4, DESIGN R19)."""
     d = Deltas()
     blocks = []
     for m in range(3):
@@ -79,7 +81,7 @@ def compare(ref: Ref, r, sigma, U, core, E, check=True) -> Deltas:
             d.t2 = max(d.t2, float(np.max(np.abs(Ug[:, c] - Uo[:, c]))))
         d.columns_checked.append(len(cols))
         d.t2p = max(d.t2p, float(np.max(np.abs(Ug[:, :rr].T @ Ug[:, :rr] - np.eye(rr)))))
-        d.resolved &= rr <= k_res(lam_o, rr, 1e-12)
+        d.resolved &= rr <= k_res(lam_o, rr, tau4)
         blocks.append(k_res(lam_o, rr, 1e-10))
     a, b, c = blocks
     co = np.asarray(ref.core_blk)[:a, :b, :c]

@@ -103,3 +103,23 @@ def test_als_invalid_args(T):
                           None) == 1
     assert lib.tucker_als(ctypes.byref(g), T.cranks((9, 2, 2)), d, d, d, d, d, d, d, d, 1, d, 1 << 30, None,
                           None) == 3
+
+
+@pytest.mark.parametrize("n,r", [(1024, (40, 40, 40)), (512, (30, 20, 10))])
+def test_als_does_not_worsen_hosvd_noise_regime(T, n, r):
+    """In the noise regime of the Gram route (ranks past k_res) HOOI started from HOSVD still may not
+    raise E: the single-hole factors come from a Gram-free SVD, so ALS instead lowers E
+    toward the SVD floor.  Also the orthogonal-projection identity and orthonormal factors."""
+    g, k = GridSpec.cube(n, 1.0), KernelSpec.matern(1.5, 0.2)
+    F = T.fill(g, k)
+    h = T.hosvd(g, r, F)
+    e0 = to_np(T.error(g, r, F, h.U, h.core))
+    a = T.als(g, r, F, h.U, 2)
+    assert a.rc == 0, a.info
+    e1 = to_np(T.error(g, r, F, a.U, a.core))
+    assert e1[0] <= e0[0] * (1 + 1e-12), (e0[0], e1[0])
+    for m in range(3):
+        U = to_np(a.U[m])
+        assert np.max(np.abs(U.T @ U - np.eye(r[m]))) <= 1e-12
+    nb = np.linalg.norm(to_np(a.core))
+    assert abs(e1[1] ** 2 - nb ** 2 - (e1[0] * e1[1]) ** 2) <= 1e-12 * e1[1] ** 2

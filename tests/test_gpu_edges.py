@@ -9,6 +9,7 @@ pytestmark = pytest.mark.gpu
 
 from test_gpu_parity import _compare_hosvd, ogrid, okern  # noqa: E402
 from tucker_inputs import GridSpec, KernelSpec  # noqa: E402
+import parity_bars as PB  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -65,10 +66,15 @@ def test_2048_materialised_vs_fused(T, orc):
     ws = T.workspace(g, r)
     G = T.gram(g, 2, F, ws)
     Gn = to_np(G)
-    bar = 2.0 * 2048 * np.finfo(np.float64).eps
+    # INT8 route (R18): sampled entries within the element bound (row maxima and 1-norms from the
+    # oracle's kernel evaluation) and within 1e-14 sqrt(G_aa G_bb)
+    K = 2048 * 2048
+    _, bits = T.i8_scheme(K)
     for a, b in rng.integers(0, 2048, size=(4, 2)):
         ref = orc.gram_entry_fn(og, ok, 2, int(a), int(b))
-        assert abs(Gn[a, b] - ref) <= bar * np.sqrt(Gn[a, a] * Gn[b, b])
+        (ma, la), (mb, lb) = orc.row_stats_fn(og, ok, 2, int(a)), orc.row_stats_fn(og, ok, 2, int(b))
+        assert abs(Gn[a, b] - ref) <= PB.i8_bound_entry(ma, mb, la, lb, K, bits, ref), (a, b)
+        assert abs(Gn[a, b] - ref) <= 1e-14 * np.sqrt(Gn[a, a] * Gn[b, b])
     del G
     ref = T.hosvd(g, r, F, ws)
     e_ref = to_np(T.error(g, r, F, ref.U, ref.core, ws))
@@ -136,3 +142,72 @@ def test_eig_single_cta_fallback_beyond_cluster(T, orc):
         if np.min(np.abs(np.delete(lam_ref, c) - lam_ref[c])) >= 1e-6 * lam_ref[0]:
             v = V_ref[:, c] * np.sign(V_ref[np.argmax(np.abs(V_ref[:, c]) >= 0.5 * np.max(np.abs(V_ref[:, c]))), c])
             assert np.max(np.abs(U[:, c] - v)) <= 1e-9, c
+
+
+# ------------------------------------------------------------------------ boundary (round 2) --
+def test_hosvd_async_equals_sync_and_graph_capture(T):
+    """info == NULL: no host synchronisation; bitwise the synchronous result, and the
+    whole HOSVD can be captured in a CUDA Graph and replayed."""
+    g, k, r = GridSpec((256, 192, 160), (-1.0,) * 3, (1.0,) * 3), KernelSpec.matern(1.5, 0.3), (20, 16, 12)
+    F = T.fill(g, k)
+    ws = T.workspace(g, r)
+    a = T.hosvd(g, r, F, ws)
+    assert a.rc == 0 and min(a.info["k_resolved"]) >= 1
+    b = T.hosvd(g, r, F, ws, sync=False)
+    torch.cuda.synchronize()
+    assert b.rc == 0
+    for m in range(3):
+        assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m])
+    assert torch.equal(a.core, b.core)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    out = None
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        T.hosvd(g, r, F, ws, stream=s, sync=False)  # warm-up (attributes, side streams)
+        s.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            out = T.hosvd(g, r, F, ws, stream=s, sync=False)
+    graph.replay()
+    torch.cuda.synchronize()
+    for m in range(3):
+        assert torch.equal(out.U[m], a.U[m])
+    assert torch.equal(out.core, a.core)
+
+
+def test_stale_rowmax_is_detected(T):
+    """A caller row maximum that does not bound its row: TUCKER_ERR_INPUT (sync), NaN (async)."""
+    g, k, r = GridSpec.cube(128, 1.0), KernelSpec.matern(1.5, 0.2), (8, 8, 8)
+    F, mx = T.fill_rowmax(g, k)
+    good = T.hosvd(g, r, F, rowmax=mx)
+    assert good.rc == 0
+    stale = mx.clone()
+    stale[5] -= 2 << 20  # two binades too low: row i = 5 of the mode-1 unfolding
+    with pytest.raises(T.TuckerError) as e:
+        T.hosvd(g, r, F, rowmax=stale)
+    assert e.value.code == 9
+    res = T.hosvd(g, r, F, rowmax=stale, sync=False)
+    torch.cuda.synchronize()
+    assert torch.isnan(res.sigma[0]).any()
+    again = T.hosvd(g, r, F, rowmax=mx)  # the flag does not leak into the next call
+    assert again.rc == 0 and torch.equal(again.U[0], good.U[0])
+
+
+def test_nonfinite_input_propagates(T):
+    g = GridSpec.cube(64, 1.0)
+    F = T.fill(g, KernelSpec.matern(0.5, 0.3))
+    F[3, 4, 5] = float("nan")
+    for m in range(3):
+        assert torch.isnan(T.gram(g, m, F)).all()
+    with pytest.raises(T.TuckerError) as e:
+        T.hosvd(g, (4, 4, 4), F)
+    assert e.value.code in (5, 9)
+
+
+def test_rank_limits_checked_before_launch(T):
+    g = GridSpec((300, 40, 40), (-1.0,) * 3, (1.0,) * 3)
+    F = torch.zeros(tuple(g.n), dtype=torch.float64, device="cuda")
+    with pytest.raises(T.TuckerError) as e:
+        T.hosvd(g, (57, 8, 8), F)
+    assert e.value.code == 7
+    assert T.last_launch_count() == 0

@@ -19,6 +19,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from tucker_inputs import GridSpec, KernelSpec  # noqa: E402
+import parity_bars as PB  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -62,8 +63,17 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["int8", "dmma"])
+def engine(T, request):
+    """INT8 fused route (plane chunks -> residues) and the DMMA route (k_gram_fused: persistent
+    cooperative grid, L2-resident ring); restored afterwards."""
+    T.set_gram_engine(T.GRAM_INT8 if request.param == "int8" else T.GRAM_DMMA)
+    yield request.param
+    T.set_gram_engine(T.GRAM_AUTO)
+
+
 @pytest.mark.parametrize("ci", range(len(CASES)))
-def test_gram_fused_parity(T, orc, chunk_kb, ci):
+def test_gram_fused_parity(T, orc, chunk_kb, engine, ci):
     g, k, kb = CASES[ci]
     chunk_kb(kb)
     F = T.fill(g, k)
@@ -105,7 +115,7 @@ def _bars(lam_ref, lam, U_ref, U, r):
     assert np.max(np.abs(U.T @ U - np.eye(r))) <= 1e-12
 
 
-def test_hosvd_fused_vs_oracle(T, orc, chunk_kb):
+def test_hosvd_fused_vs_oracle(T, orc, chunk_kb, engine):
     g = GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0))
     k = KernelSpec.matern(0.7, 0.5)
     r = (12, 10, 9)
@@ -165,12 +175,15 @@ def test_fused_2048_config5f(T, orc):
     G0 = T.gram_fused(g, k, 0, wsf)
     assert torch.equal(G0, G0.T)
     Gn = to_np(G0)
-    # one CTA accumulates all K = n^2 = 4.2M products of an entry in sequence (S = 1 at n = 2048):
-    # rounding noise ~ sqrt(K) eps relative to sqrt(G_aa G_bb); bar 2 sqrt(K) eps ~ 9e-13
-    bar = 2.0 * 2048 * np.finfo(np.float64).eps
+    # the INT8 route forms X X^T exactly (R18): each sampled entry within R18's element bound, whose
+    # inputs (row maxima, row 1-norms) the oracle computes from the kernel directly
+    K = 2048 * 2048
+    _, bits = T.i8_scheme(K)
     for a, b in rng.integers(0, 2048, size=(6, 2)):
         ref = orc.gram_entry_fn(og, ok, 0, int(a), int(b))
-        assert abs(Gn[a, b] - ref) <= bar * np.sqrt(Gn[a, a] * Gn[b, b]), (a, b)
+        (ma, la), (mb, lb) = orc.row_stats_fn(og, ok, 0, int(a)), orc.row_stats_fn(og, ok, 0, int(b))
+        assert abs(Gn[a, b] - ref) <= PB.i8_bound_entry(ma, mb, la, lb, K, bits, ref), (a, b)
+        assert abs(Gn[a, b] - ref) <= 1e-14 * np.sqrt(Gn[a, a] * Gn[b, b]), (a, b)
     del G0
     res = T.hosvd_fused(g, k, r, wsf)
     assert res.rc == 0, res.info

@@ -110,7 +110,11 @@ def test_gram_i8_deterministic_and_vs_dmma(T):
     for m in range(3):
         G = T.gram_i8(g, m, F, ws)
         assert torch.equal(G, T.gram_i8(g, m, F, ws))
-        D = T.gram(g, m, F)
+        T.set_gram_engine(T.GRAM_DMMA)
+        try:
+            D = T.gram(g, m, F, T.workspace(g))  # k_gram_tma (FP64 tensor cores)
+        finally:
+            T.set_gram_engine(T.GRAM_AUTO)
         d = torch.sqrt(torch.diagonal(D))
         assert float(torch.max(torch.abs(G - D) / torch.outer(d, d))) <= 1e-14
 

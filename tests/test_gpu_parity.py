@@ -82,8 +82,17 @@ GRAM_GRIDS = [GridSpec.cube(32, 1.0),                                        # c
               GridSpec((130, 129, 131), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))]  # odd n3 -> cp.async, 2 tiles
 
 
+@pytest.fixture(params=["int8", "dmma"])
+def engine(T, request):
+    """Run the test under each Gram engine (the INT8 emulation, R18, and the north_star's FP64
+    tensor-core DMMA route: k_gram_tma / k_gram_generic / k_gram_fused); restored afterwards."""
+    T.set_gram_engine(T.GRAM_INT8 if request.param == "int8" else T.GRAM_DMMA)
+    yield request.param
+    T.set_gram_engine(T.GRAM_AUTO)
+
+
 @pytest.mark.parametrize("gi", range(len(GRAM_GRIDS)))
-def test_gram_parity(T, orc, gi):
+def test_gram_parity(T, orc, engine, gi):
     g = GRAM_GRIDS[gi]
     k = KernelSpec.matern(1.3, 0.5)
     Fg = T.fill(g, k)
@@ -97,7 +106,7 @@ def test_gram_parity(T, orc, gi):
         assert np.max(np.abs(G - R) / np.outer(d, d)) <= 1e-14, m
 
 
-def test_gram_deterministic(T):
+def test_gram_deterministic(T, engine):
     g = GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0))
     F = T.fill(g, KernelSpec.matern(0.7, 0.5))
     ws = T.workspace(g)
@@ -194,24 +203,24 @@ def _compare_hosvd(T, orc, g, k, r):
     return res, err
 
 
-def test_hosvd_config1(T, orc):
+def test_hosvd_config1(T, orc, engine):
     w = config1()
     res, err = _compare_hosvd(T, orc, w.grid, w.kernels[0], w.ranks)
     assert 9.55e-7 < err[0] < 9.58e-7
 
 
 @pytest.mark.parametrize("nu,ell", [(0.5, 0.1), (1.5, 0.5), (2.5, 1.0)])
-def test_hosvd_config2_kernels(T, orc, nu, ell):
+def test_hosvd_config2_kernels(T, orc, engine, nu, ell):
     _compare_hosvd(T, orc, GridSpec.cube(128, 1.0), KernelSpec.matern(nu, ell), (20, 20, 20))
 
 
 @pytest.mark.parametrize("ki", [0, 2, 4])
-def test_hosvd_config3(T, orc, ki):
+def test_hosvd_config3(T, orc, engine, ki):
     w = config3()
     _compare_hosvd(T, orc, w.grid, w.kernels[ki], w.ranks)
 
 
-def test_hosvd_odd_grid_with_origin(T, orc):
+def test_hosvd_odd_grid_with_origin(T, orc, engine):
     # Table-2-like grid (n = 2k+1 contains the origin, C(0) = sigma^2); odd n3 -> cp.async paths
     _compare_hosvd(T, orc, GridSpec.cube(129, 5.0), KernelSpec.slater(1.0, 1.0), (10, 10, 10))
 
