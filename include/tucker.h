@@ -134,10 +134,18 @@ TUCKER_API size_t tucker_workspace_size_i8(const tucker_grid* grid);
  * moduli (moduli[16], host) and the integer width b (*b, host) used by tucker_gram_i8 —
  * pairwise coprime odd p_l <= 253 with prod p_l > 2 K 2^(2b), b <= 50.  Returns TUCKER_OK. */
 TUCKER_API int tucker_i8_scheme(int64_t K, int32_t* moduli, int32_t* b);
+/* Which INT8 residue layout the materialised Grams of `grid` use under the calling thread's engine
+ * (host only): *shared = 1 for the shared layout (R20: one residue pass serves the three
+ * modes, ONE exponent E = the largest row exponent scales the whole tensor, b = the scheme's width
+ * for the largest K), 0 for the per-mode row-scaled layout (R18; b of mode 0's K — each mode uses
+ * its own).  The shared layout applies when n3 % 16 == 0 and the 16 N-byte residue tensor fits the
+ * cap (40 GiB); TUCKER_GRAM_INT8_ROWSCALED forces the per-mode layout.  UNSUPPORTED if the INT8
+ * engine does not apply. */
+TUCKER_API int tucker_i8_layout(const tucker_grid* grid, int32_t* shared, int32_t* b);
 /* Gram engine of tucker_gram, tucker_hosvd and tucker_approximate, per calling thread (set it
  * before sizing workspaces: tucker_workspace_size depends on it).  TUCKER_GRAM_AUTO
  * (default): the INT8 emulation where supported (every n_m <= 16384), DMMA otherwise. */
-enum { TUCKER_GRAM_AUTO = 0, TUCKER_GRAM_DMMA = 1, TUCKER_GRAM_INT8 = 2 };
+enum { TUCKER_GRAM_AUTO = 0, TUCKER_GRAM_DMMA = 1, TUCKER_GRAM_INT8 = 2, TUCKER_GRAM_INT8_ROWSCALED = 3 };
 TUCKER_API int tucker_set_gram_engine(int32_t engine);
 TUCKER_API int32_t tucker_get_gram_engine(void);
 TUCKER_API int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,

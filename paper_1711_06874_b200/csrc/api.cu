@@ -410,7 +410,8 @@ int tucker_gram(const tucker_grid* grid, int32_t mode, const double* F, double* 
 }
 
 int tucker_set_gram_engine(int32_t engine) {
-    if (engine != TUCKER_GRAM_AUTO && engine != TUCKER_GRAM_DMMA && engine != TUCKER_GRAM_INT8)
+    if (engine != TUCKER_GRAM_AUTO && engine != TUCKER_GRAM_DMMA && engine != TUCKER_GRAM_INT8 &&
+        engine != TUCKER_GRAM_INT8_ROWSCALED)
         return TUCKER_ERR_INVALID_ARG;
     gram_engine() = engine;
     return TUCKER_OK;
@@ -421,6 +422,22 @@ int32_t tucker_get_gram_engine(void) { return gram_engine(); }
 size_t tucker_workspace_size_i8(const tucker_grid* grid) {
     if (check_grid(grid) != TUCKER_OK || !gram_i8_supported(grid->n)) return 0;
     return gram_i8_ws_bytes(grid->n);
+}
+
+int tucker_i8_layout(const tucker_grid* grid, int32_t* shared, int32_t* b) {
+    TK_RC(check_grid(grid));
+    if (!shared || !b) return TUCKER_ERR_INVALID_ARG;
+    if (!gram_use_i8(grid->n)) return TUCKER_ERR_UNSUPPORTED;
+    *shared = gram_i8_shared_layout(grid->n) ? 1 : 0;
+    int32_t mods[16];
+    const int64_t* n = grid->n;
+    const int64_t K0 = n[1] * n[2];
+    if (*shared) {
+        *b = gram_i8_shared_bits(n);
+    } else {
+        gram_i8_scheme(K0, mods, b);  // per mode: b of mode 0's K (each mode uses its own K)
+    }
+    return TUCKER_OK;
 }
 
 int tucker_i8_scheme(int64_t K, int32_t* moduli, int32_t* b) {

@@ -471,6 +471,10 @@ struct GemmArgs {
     int64_t Kc;      // K of this super-chunk
     int16_t* P;      // partials mod p_l, [(l * nchunks + c) * ntiles + t][PN][PM]
     const int2* utab;  // unit v of a group: tiles (ta, tb), tb = -1 unless two half tiles are merged
+    int lay;         // residue layout: 0 per-mode K-block-major [l][kb][row][128]; shared natural
+                     // layout [l][i][j][k] read as mode 0 (1), mode 1 (2), mode 2 MN-major (3)
+    int nb3;         // lay 2: K-blocks per i-slab (ceil(n3 / 128); the rest of the last is zero-filled)
+    int64_t nkb_total;  // K-blocks of this launch (the exact-int32 chunks hold KCH / BKB of them)
 };
 
 __host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
@@ -523,8 +527,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ uint32_t idesc_i8(int M, int N) {  // D s32, A/B signed 8-bit, both K-major
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+__device__ __forceinline__ uint32_t idesc_i8(int M, int N, bool mn = false) {  // D s32, A/B signed 8-bit
+    // K-major A and B, or (mn) both MN-major (bits 15, 16): the shared layout's mode-2 view
+    return (2u << 4) | (1u << 7) | (1u << 10) | (mn ? (3u << 15) : 0u) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void umma_i8_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -547,12 +553,29 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same smem o
     return r;
 }
 // Box (128 rows x 128 bytes) of modulus l, K-block kb, starting at `row` of the residue tensor.
+// Layout 0 (per-mode, K-block-major): {0, row, kb, l}.  Shared natural layout [l][i][j][k]:
+// mode 0 {kb * 128 (of the j k axis), row i, l}; mode 1 {(kb % nb3) * 128 (k), row j, kb / nb3 (i), l};
+// mode 2, MN-major {row k, kb * 128 (of the i j axis), l} — the box is 128 K-lines of 128 rows.
 __device__ __forceinline__ void tma_load_res_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int l, int kb,
-                                                  int row) {
+                                                  int row, int lay, int nb3) {
+    int c0 = 0, c1 = row, c2 = kb, c3 = l;
+    if (lay == 1) {
+        c0 = kb * BKB;
+        c2 = l;
+        c3 = 0;
+    } else if (lay == 2) {
+        c0 = (kb % nb3) * BKB;
+        c2 = kb / nb3;
+    } else if (lay == 3) {
+        c0 = row;
+        c1 = kb * BKB;
+        c2 = l;
+        c3 = 0;
+    }
     asm volatile(
         "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(0), "r"(row), "r"(kb), "r"(l)
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -644,11 +667,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             uint32_t ph = 0;
             for (int u = pair; u < g.nunits; u += npairs) {
                 const Unit x = unit_of(u, g);
-                const int64_t kbeg = (int64_t)x.c * KCH;
-                const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
+                const int64_t kbeg = (int64_t)x.c * (KCH / BKB);  // first K-block of the chunk
+                const int nkb = (int)min(KCH / BKB, g.nkb_total - kbeg);
                 const int nsub = x.merged ? 2 : 1;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    const int kx = (int)(kbeg / BKB) + kb;  // K-block index
+                    const int kx = (int)kbeg + kb;  // K-block index
                     for (int sub = 0; sub < nsub; ++sub) {
                         const Stream& s0 = x.s[sub];
                         mbar_wait(&empty[stage], ph ^ 1);
@@ -656,10 +679,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                         const uint32_t fl = leader_addr(&full[stage]);
                         const bool two_b = !x.merged && x.ns == 2;
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (two_b ? 3u : 2u) * BOX);
-                        tma_load_res_pair(sA, &map, fl, x.l, kx, s0.arow + (int)rank * 128);
-                        tma_load_res_pair(sA + BOX, &map, fl, x.l, kx, s0.brow + (int)rank * (s0.N / 2));
+                        tma_load_res_pair(sA, &map, fl, x.l, kx, s0.arow + (int)rank * 128, g.lay, g.nb3);
+                        tma_load_res_pair(sA + BOX, &map, fl, x.l, kx, s0.brow + (int)rank * (s0.N / 2), g.lay, g.nb3);
                         if (two_b)
-                            tma_load_res_pair(sA + 2 * BOX, &map, fl, x.l, kx, x.s[1].brow + (int)rank * (x.s[1].N / 2));
+                            tma_load_res_pair(sA + 2 * BOX, &map, fl, x.l, kx, x.s[1].brow + (int)rank * (x.s[1].N / 2),
+                                              g.lay, g.nb3);
                         if (++stage == STAGES) {
                             stage = 0;
                             ph ^= 1;
@@ -673,11 +697,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             int stage = 0;
             uint32_t ph = 0;
             int it = 0;
+            const bool mn = g.lay == 3;
+            // K-step of one MMA (K = 32 bytes): +32 B along the 128-B line (K-major) or +32 lines
+            // of 128 B (MN-major); both stay inside the 1024-B swizzle atoms' alignment
+            const uint32_t kstep = mn ? 32u * BKB : 32u;
             for (int u = pair; u < g.nunits; u += npairs, ++it) {
                 const Unit x = unit_of(u, g);
-                const int64_t kbeg = (int64_t)x.c * KCH;
-                const int nkb = (int)ceil_div(min(KCH, g.Kc - kbeg), (int64_t)BKB);
-                const uint32_t id0 = idesc_i8(PM, x.s[0].N), id1 = idesc_i8(PM, x.s[1].N);
+                const int64_t kbeg = (int64_t)x.c * (KCH / BKB);
+                const int nkb = (int)min(KCH / BKB, g.nkb_total - kbeg);
+                const uint32_t id0 = idesc_i8(PM, x.s[0].N, mn), id1 = idesc_i8(PM, x.s[1].N, mn);
                 const int nsub = x.merged ? 2 : 1;
                 mbar_wait_cluster(&tempty, (it & 1) ^ 1);
                 tc_fence_after();
@@ -689,14 +717,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 #pragma unroll
                         for (int k = 0; k < BKB / 32; ++k) {
                             const uint32_t acc = (kb | k) ? 1u : 0u;
-                            const uint64_t da = umma_desc_sw128(a0 + 32 * k);
+                            const uint64_t da = umma_desc_sw128(a0 + kstep * k);
                             if (x.merged) {
-                                umma_i8_pair(tmem + 256 * sub, da, umma_desc_sw128(a0 + BOX + 32 * k), sub ? id1 : id0,
+                                umma_i8_pair(tmem + 256 * sub, da, umma_desc_sw128(a0 + BOX + kstep * k), sub ? id1 : id0,
                                              acc);
                             } else {
-                                umma_i8_pair(tmem, da, umma_desc_sw128(a0 + BOX + 32 * k), id0, acc);
+                                umma_i8_pair(tmem, da, umma_desc_sw128(a0 + BOX + kstep * k), id0, acc);
                                 if (x.ns == 2)
-                                    umma_i8_pair(tmem + 256, da, umma_desc_sw128(a0 + 2 * BOX + 32 * k), id1, acc);
+                                    umma_i8_pair(tmem + 256, da, umma_desc_sw128(a0 + 2 * BOX + kstep * k), id1, acc);
                             }
                         }
                         umma_commit_pair(&empty[stage]);
@@ -818,7 +846,7 @@ __device__ __forceinline__ double u128_to_double_rn(unsigned __int128 m) {
 
 __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const uint32_t* __restrict__ mx,
                                                 int n, int nJ, int ntiles, int b, double* __restrict__ G,
-                                                const int* __restrict__ bad) {
+                                                const int* __restrict__ bad, int global_mx) {
     // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -844,7 +872,8 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     const bool neg = S > half;
     const unsigned __int128 mag = neg ? (Pp - S) : S;
     double d = u128_to_double_rn(mag);
-    d = ldexp(d, row_exponent(mx[i]) + row_exponent(mx[j]) - 2 * b);
+    // per-row exponents, or (shared layout) the one global exponent in mx[0]
+    d = ldexp(d, row_exponent(mx[global_mx ? 0 : i]) + row_exponent(mx[global_mx ? 0 : j]) - 2 * b);
     if (neg) d = -d;
     if (bad && *bad) d = __longlong_as_double(0x7FF8000000000000LL);  // input outside the window: NaN
     G[(int64_t)i * n + j] = d;
@@ -963,7 +992,8 @@ struct ModeGemm {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return TUCKER_ERR_CUDA;
         const int nchunks = (int)ceil_div(Kc, KCH);
-        GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nug, nchunks, NMOD * nchunks * nug, Kc, P, utab};
+        GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nug, nchunks, NMOD * nchunks * nug, Kc, P, utab, 0, 1,
+                    ceil_div(Kc, (int64_t)BKB)};
         const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
         {
             TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -992,7 +1022,7 @@ struct ModeGemm {
     int crt(double* G) {
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad);
+        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad, 0);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1040,6 +1070,198 @@ int gram_mode(const int64_t n[3], int m, const double* F, const uint32_t* mx, ch
     });
 }
 
+// ------------------------------------------------------------------------------------------
+// Shared residue layout (materialised F; R20).  One exponent for the whole tensor,
+// E = the largest row exponent, and b = scale_bits(max_m K_m): X = rint(F 2^(b-E)) is the same
+// integer tensor for every mode, so ONE streaming pass writes its residues R[l] (one byte plane per
+// modulus, in F's own C order) and all three Grams read them through mode-specific TMA maps:
+// mode 0 as [i][(j,k)] (K-major), mode 1 as [i][j][k] with K = (i,k) (K-major, K-blocks per
+// i-slab), mode 2 as [(i,j)][k] (MN-major operands).  G_m = fl(2^(2E-2b) X_(m) X_(m)^T), one
+// rounding; the input rounding is 2^(E-b-1) absolute instead of per row (norm-wise the same
+// accuracy, R20).  Requires n3 % 16 == 0 (TMA strides) and the 16 N-byte residue tensor
+// within the workspace cap.
+__global__ void k_i8_gmax(const uint32_t* __restrict__ mx, int64_t n, uint32_t* __restrict__ out) {
+    uint32_t m = 0;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) m = max(m, mx[t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ uint32_t w[32];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, w[i]);
+        out[0] = max(m, w[0]);
+    }
+}
+
+// Residues of the whole tensor: each warp takes chunks of 512 consecutive elements — coalesced
+// 16-byte loads into a per-warp shared buffer padded one double per 16 (conflict-free both ways),
+// then each lane converts its 16 consecutive elements and writes one 16-byte word per modulus
+// (512 contiguous bytes per warp and plane).  N % 16 == 0.
+constexpr int RA_CH = 512;
+__global__ void __launch_bounds__(256) k_i8_residues_all(const double* __restrict__ F, int64_t N,
+                                                         const uint32_t* __restrict__ gmax, int b,
+                                                         int8_t* __restrict__ R, int* __restrict__ bad) {
+    __shared__ double buf[8][RA_CH + RA_CH / 16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* sb = buf[warp];
+    double sa, sbb;
+    row_scale(*gmax, b, sa, sbb);
+    const double lim = ldexp(1.0, b);
+    const int64_t nch = ceil_div(N, (int64_t)RA_CH);
+    const int64_t wstride = (int64_t)gridDim.x * 8;
+    bool ok = true;
+    for (int64_t c = (int64_t)blockIdx.x * 8 + warp; c < nch; c += wstride) {
+        const int64_t base = c * RA_CH;
+        double2 v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int64_t e = base + 2 * lane + 64 * t;
+            v[t] = e < N ? __ldcs(reinterpret_cast<const double2*>(F + e)) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int e = 2 * lane + 64 * t;
+            sb[e + (e >> 4)] = v[t].x;
+            sb[e + 1 + (e >> 4)] = v[t].y;
+        }
+        __syncwarp();
+        if (base + 16 * lane < N)
+            ok &= residues16<1>(sb + 17 * lane, sa, sbb, R + base + 16 * lane, (size_t)N, lim);
+        __syncwarp();
+    }
+    if (!ok) atomicExch(bad, 1);
+}
+
+struct SharedPlan {
+    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc, off_utab, total;
+    int b;
+};
+
+inline size_t shared_cap() {  // residue tensor cap (env TUCKER_I8_SHARED_MB overrides; 0 disables)
+    const char* e = std::getenv("TUCKER_I8_SHARED_MB");
+    if (e) return (size_t)std::atoll(e) << 20;
+    return (size_t)40 << 30;
+}
+
+bool shared_ok(const int64_t n[3]) {
+    const int64_t N = n[0] * n[1] * n[2];
+    return gram_engine() != TUCKER_GRAM_INT8_ROWSCALED && n[2] % 16 == 0 && (size_t)NMOD * (size_t)N <= shared_cap();
+}
+
+inline int64_t shared_nkb(const int64_t n[3], int m) {  // K-blocks of mode m in the shared layout
+    if (m == 1) return n[0] * ceil_div(n[2], (int64_t)BKB);
+    return ceil_div(n[0] * n[1] * n[2] / n[m], (int64_t)BKB);
+}
+
+SharedPlan shared_plan(const int64_t n[3]) {
+    SharedPlan w{};
+    const int64_t N = n[0] * n[1] * n[2];
+    int64_t Kmax = 0;
+    size_t pb = 0, ab = 0, ub = 0;
+    for (int m = 0; m < 3; ++m) {
+        Kmax = std::max(Kmax, N / n[m]);
+        int nJ;
+        const int nt = count_tiles(n[m], nJ);
+        const int64_t nch = ceil_div(shared_nkb(n, m), KCH / BKB);
+        pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
+        ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
+        ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
+    }
+    w.b = scale_bits(Kmax);
+    size_t off = 0;
+    w.off_mx = off;  // same offsets as ws_plan: the row maxima slot and the flag are shared
+    w.off_flag = off + align_up((size_t)(n[0] + n[1] + n[2]) * 4, 16);
+    w.off_gmax = w.off_flag + 4;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8 + 16, 1024);
+    w.off_R = off;
+    off += align_up((size_t)NMOD * N, 1024);
+    w.off_P = off;
+    off += pb;
+    w.off_Racc = off;
+    off += ab;
+    w.off_utab = off;
+    off += ub;
+    w.total = off;
+    return w;
+}
+
+// TMA map over the shared residue tensor for mode m (4-D; unused trailing dims of extent 1).
+int shared_map(CUtensorMap* map, const int64_t n[3], int m, int8_t* R) {
+    PFN_tmapEncodeTiled enc = tmap_encoder();
+    if (!enc) return TUCKER_ERR_CUDA;
+    const int64_t N = n[0] * n[1] * n[2];
+    cuuint64_t dims[4], str[3];
+    if (m == 0) {
+        dims[0] = n[1] * n[2]; dims[1] = n[0]; dims[2] = NMOD; dims[3] = 1;
+        str[0] = n[1] * n[2]; str[1] = N; str[2] = N * NMOD;
+    } else if (m == 1) {
+        dims[0] = n[2]; dims[1] = n[1]; dims[2] = n[0]; dims[3] = NMOD;
+        str[0] = n[2]; str[1] = n[1] * n[2]; str[2] = N;
+    } else {
+        dims[0] = n[2]; dims[1] = n[0] * n[1]; dims[2] = NMOD; dims[3] = 1;
+        str[0] = n[2]; str[1] = N; str[2] = N * NMOD;
+    }
+    cuuint32_t box[4] = {BKB, 128, 1, 1}, es[4] = {1, 1, 1, 1};
+    if (enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, R, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+        return TUCKER_ERR_CUDA;
+    return TUCKER_OK;
+}
+
+// One pass: global exponent + residues of the whole tensor (mx: the row maxima of all modes).
+int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, char* base, const SharedPlan& w,
+                    cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+    uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
+    k_i8_gmax<<<1, 1024, 0, st>>>(mx, n[0], gw);  // the mode-0 row maxima cover every element
+    TK_CHECK_LAUNCH();
+    const int64_t N = n[0] * n[1] * n[2];
+    const int64_t nch = ceil_div(N, (int64_t)RA_CH);
+    const int grid = (int)std::min<int64_t>(ceil_div(nch, 8), (int64_t)kNumSMs * 8);
+    k_i8_residues_all<<<grid, 256, 0, st>>>(F, N, gw, w.b, reinterpret_cast<int8_t*>(base + w.off_R),
+                                            reinterpret_cast<int*>(base + w.off_flag));
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+// G_m from the shared residues: one k_i8_gemm launch over all K (exact int32 per KCH columns),
+// the fold, the CRT with the global exponent.
+int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
+    int nJ;
+    const int rows = (int)n[m];
+    const int ntiles = count_tiles(n[m], nJ);
+    int16_t* P = reinterpret_cast<int16_t*>(base + w.off_P);
+    int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
+    int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
+    TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    const int nug = build_units(rows, nJ, ntiles, nullptr);
+    k_i8_units<<<1, 1, 0, st>>>(rows, nJ, ntiles, utab);
+    TK_CHECK_LAUNCH();
+    CUtensorMap map;
+    TK_RC(shared_map(&map, n, m, reinterpret_cast<int8_t*>(base + w.off_R)));
+    const int64_t nkb = shared_nkb(n, m);
+    const int nchunks = (int)ceil_div(nkb, KCH / BKB);
+    GemmArgs ga{rows, nJ, ntiles, nug, nchunks, NMOD * nchunks * nug, nkb * BKB, P, utab, m + 1,
+                (int)ceil_div(n[2], (int64_t)BKB), nkb};
+    const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);
+    {
+        TK_PROF(TUCKER_PROF_I8_GEMM, st);
+        k_i8_gemm<<<grid, NT, GEMM_SMEM, st>>>(map, ga);
+        TK_CHECK_LAUNCH();
+    }
+    TK_PROF(TUCKER_PROF_I8_CRT, st);
+    const int64_t tot = (int64_t)NMOD * ntiles * PN * PM;
+    k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, 1);
+    TK_CHECK_LAUNCH();
+    const dim3 cg((unsigned)ceil_div(n[m], 32), (unsigned)ceil_div(n[m], 8));
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), rows, nJ, ntiles, w.b, G,
+                                 reinterpret_cast<const int*>(base + w.off_flag), 1);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
 }  // namespace i8
 
 int gram_i8_scheme(int64_t K, int32_t* moduli, int32_t* b) {
@@ -1048,7 +1270,9 @@ int gram_i8_scheme(int64_t K, int32_t* moduli, int32_t* b) {
     return TUCKER_OK;
 }
 
-size_t gram_i8_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
+size_t gram_i8_ws_bytes(const int64_t n[3]) {
+    return std::max(i8::ws_plan(n).total, i8::shared_ok(n) ? i8::shared_plan(n).total : (size_t)0);
+}
 
 bool gram_i8_supported(const int64_t n[3]) {
     // row counts up to 2^14 keep tile indices and the 2-D tensor map comfortably in range
@@ -1077,6 +1301,16 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
     TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
+    if (shared_ok(n)) {  // one residue pass for the three modes (R20)
+        const SharedPlan sp = shared_plan(n);
+        if (ws_bytes < sp.total) return TUCKER_ERR_SIZE;
+        TK_RC(shared_residues(n, F, mx, base, sp, st));
+        for (int m = 0; m < 3; ++m) {
+            TK_RC(shared_gram_mode(n, m, base, sp, G, st));
+            TK_RC(after_mode(m));
+        }
+        return TUCKER_OK;
+    }
     for (int m = 0; m < 3; ++m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G, st));
         TK_RC(after_mode(m));
@@ -1098,6 +1332,16 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
     TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
     if (!mx_ready) TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    if (shared_ok(n)) {  // one residue pass for the three modes (R20)
+        const SharedPlan sp = shared_plan(n);
+        if (ws_bytes < sp.total) return TUCKER_ERR_SIZE;
+        TK_RC(shared_residues(n, F, mx, base, sp, st));
+        for (int m = 2; m >= 0; --m) {
+            TK_RC(shared_gram_mode(n, m, base, sp, G[m], st));
+            TK_RC(on_phase(&m, 1));
+        }
+        return TUCKER_OK;
+    }
     for (int m = 2; m >= 0; --m) {
         TK_RC(gram_mode(n, m, F, mx, base, w, G[m], st));
         TK_RC(on_phase(&m, 1));
@@ -1105,7 +1349,7 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
     return TUCKER_OK;
 }
 
-size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return i8::ws_plan(n).total; }
+size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return gram_i8_ws_bytes(n); }
 const int* gram_i8_flag_slot(const int64_t n[3], const void* ws) {
     return reinterpret_cast<const int*>(static_cast<const char*>(ws) + i8::ws_plan(n).off_flag);
 }
@@ -1139,6 +1383,12 @@ int launch_gram_i8(const int64_t n[3], int mode, const double* F, double* G, con
         uint32_t* own = reinterpret_cast<uint32_t*>(base + w.off_mx);
         TK_RC(launch_gram_i8_rowmax(n, F, own, st));
         mx = own;
+    }
+    if (shared_ok(n)) {
+        const SharedPlan sp = shared_plan(n);
+        if (ws_bytes < sp.total) return TUCKER_ERR_SIZE;
+        TK_RC(shared_residues(n, F, mx, base, sp, st));
+        return shared_gram_mode(n, mode, base, sp, G, st);
     }
     return gram_mode(n, mode, F, mx, base, w, G, st);
 }
@@ -1286,6 +1536,8 @@ int& gram_engine() {  // per calling thread (tucker_set_gram_engine)
     return engine;
 }
 bool gram_use_i8(const int64_t n[3]) { return gram_engine() != TUCKER_GRAM_DMMA && gram_i8_supported(n); }
+bool gram_i8_shared_layout(const int64_t n[3]) { return gram_use_i8(n) && i8::shared_ok(n); }
+int gram_i8_shared_bits(const int64_t n[3]) { return i8::shared_plan(n).b; }
 size_t gram_auto_ws_bytes(const int64_t n[3]) { return gram_use_i8(n) ? gram_i8_ws_bytes(n) : gram_ws_bytes(n); }
 int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,
                      void* ws, size_t ws_bytes, cudaStream_t st) {

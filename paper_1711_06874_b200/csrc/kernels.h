@@ -94,6 +94,10 @@ cudaStream_t side_stream(int which);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
 bool gram_use_i8(const int64_t n[3]);
+// Materialised INT8 Grams of this grid use the shared residue layout (one residue pass, one global
+// exponent; R20) — and its integer width b.
+bool gram_i8_shared_layout(const int64_t n[3]);
+int gram_i8_shared_bits(const int64_t n[3]);
 size_t gram_auto_ws_bytes(const int64_t n[3]);
 int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,
                      void* ws, size_t ws_bytes, cudaStream_t st);

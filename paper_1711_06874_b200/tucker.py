@@ -17,7 +17,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libtucker_b200.so")
 
 MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
-GRAM_AUTO, GRAM_DMMA, GRAM_INT8 = 0, 1, 2
+GRAM_AUTO, GRAM_DMMA, GRAM_INT8, GRAM_INT8_ROWSCALED = 0, 1, 2, 3
 FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED",
@@ -27,7 +27,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_hosvd_fused_sharded",
            "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
-           "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme",
+           "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme", "tucker_i8_layout",
            "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
            "tucker_last_launch_count", "tucker_strerror")
 
@@ -88,6 +88,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_workspace_size_i8": (sz, [pg]),
         "tucker_gram_i8": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_i8_scheme": (ctypes.c_int, [i64, P(ctypes.c_int32), P(ctypes.c_int32)]),
+        "tucker_i8_layout": (ctypes.c_int, [pg, P(ctypes.c_int32), P(ctypes.c_int32)]),
         "tucker_set_gram_engine": (ctypes.c_int, [i32]),
         "tucker_get_gram_engine": (i32, []),
         "tucker_profile_enable": (ctypes.c_int, [i32]),
@@ -256,6 +257,14 @@ def i8_scheme(K: int) -> tuple:
     mod, b = (ctypes.c_int32 * 16)(), ctypes.c_int32()
     _check(load().tucker_i8_scheme(int(K), mod, ctypes.byref(b)), "tucker_i8_scheme")
     return list(mod), int(b.value)
+
+
+def i8_layout(grid) -> tuple:
+    """(shared, b): whether the materialised INT8 Grams of `grid` use the shared residue layout
+    (one global exponent, R20) and its integer width b (host query)."""
+    sh, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().tucker_i8_layout(ctypes.byref(cgrid(grid)), ctypes.byref(sh), ctypes.byref(b)), "tucker_i8_layout")
+    return bool(sh.value), int(b.value)
 
 
 def workspace_i8(grid) -> torch.Tensor:

@@ -182,7 +182,7 @@ def test_stale_rowmax_is_detected(T):
     good = T.hosvd(g, r, F, rowmax=mx)
     assert good.rc == 0
     stale = mx.clone()
-    stale[5] -= 2 << 20  # two binades too low: row i = 5 of the mode-1 unfolding
+    stale -= 2 << 20  # every row maximum two binades too low (also the global one, R20)
     with pytest.raises(T.TuckerError) as e:
         T.hosvd(g, r, F, rowmax=stale)
     assert e.value.code == 9

@@ -65,9 +65,10 @@ CASES = [
 
 @pytest.fixture(params=["int8", "dmma"])
 def engine(T, request):
-    """INT8 fused route (plane chunks -> residues) and the DMMA route (k_gram_fused: persistent
-    cooperative grid, L2-resident ring); restored afterwards."""
-    T.set_gram_engine(T.GRAM_INT8 if request.param == "int8" else T.GRAM_DMMA)
+    """INT8 fused route (plane chunks -> residues, per-mode row scaling; the materialised reference
+    Gram on the same row-scaled layout) and the DMMA route (k_gram_fused: persistent cooperative
+    grid, L2-resident ring); restored afterwards."""
+    T.set_gram_engine(T.GRAM_INT8_ROWSCALED if request.param == "int8" else T.GRAM_DMMA)
     yield request.param
     T.set_gram_engine(T.GRAM_AUTO)
 

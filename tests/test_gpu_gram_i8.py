@@ -60,8 +60,12 @@ def test_gram_i8_exact_on_integers(T, gi):
         assert np.array_equal(G, exact), (gi, m, np.max(np.abs(G - exact)))
 
 
-def _bound(A, b):
+def _bound(A, b, global_max=None):
+    """R18 element bound (per-row exponents), or R20's (global_max given: one exponent for all
+    rows, the shared residue layout)."""
     m = np.max(np.abs(A), axis=1)
+    if global_max is not None:
+        m = np.full_like(m, global_max)
     E = np.where(m > 0, np.frexp(m)[1], 0).astype(np.float64)
     l1 = np.sum(np.abs(A), axis=1)
     s = np.exp2(E - b - 1)
@@ -72,35 +76,63 @@ def _bound(A, b):
 
 @pytest.mark.parametrize("gi", range(len(GRIDS)))
 @pytest.mark.parametrize("kern", [KernelSpec.matern(1.3, 0.5), KernelSpec.matern(0.5, 0.1), KernelSpec.slater(1.0, 1.0)])
-def test_gram_i8_parity(T, orc, gi, kern):
+@pytest.mark.parametrize("layout", ["auto", "rowscaled"])
+def test_gram_i8_parity(T, orc, gi, kern, layout):
+    """Both residue layouts: per-mode row scaling (R18: element-wise within 1e-14 sqrt(G_aa G_bb))
+    and, where it applies (n3 % 16 == 0), the shared layout with one global exponent (R20: within its
+    element bound, norm-wise within 2e-15 ||G||_2)."""
     g = GRIDS[gi]
-    Fg = T.fill(g, kern)
-    F = orc.fill(ogrid(orc, g), okern(orc, kern))
-    ws = T.workspace_i8(g)
+    if layout == "rowscaled":
+        T.set_gram_engine(T.GRAM_INT8_ROWSCALED)
+    try:
+        shared, b = T.i8_layout(g)
+        Fg = T.fill(g, kern)
+        F = orc.fill(ogrid(orc, g), okern(orc, kern))
+        ws = T.workspace_i8(g)
+        Gs = [to_np(T.gram_i8(g, m, Fg, ws)) for m in range(3)]
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
+    assert shared == (layout == "auto" and g.n[2] % 16 == 0)
     for m in range(3):
-        G = to_np(T.gram_i8(g, m, Fg, ws))
+        G = Gs[m]
         R = orc.gram_mode(F, m)
         A = unfold(F, m)
         assert np.array_equal(G, G.T)
-        assert np.all(np.abs(G - R) <= _bound(A, 50)), (gi, m)
-        d = np.sqrt(np.diag(R))
-        assert np.max(np.abs(G - R) / np.outer(d, d)) <= 1e-14, (gi, m)
+        if shared:
+            assert np.all(np.abs(G - R) <= _bound(A, b, np.max(np.abs(F)))), (gi, m)
+            assert np.linalg.norm(G - R, 2) <= 2e-15 * np.linalg.norm(R, 2), (gi, m)
+        else:
+            assert np.all(np.abs(G - R) <= _bound(A, 50)), (gi, m)
+            d = np.sqrt(np.diag(R))
+            assert np.max(np.abs(G - R) / np.outer(d, d)) <= 1e-14, (gi, m)
 
 
 def test_gram_i8_chunks_and_superchunks(T, orc, monkeypatch):
     """K = 2^18: four exact-int32 K-chunks of 2^16; with a 16 MiB residue cap also four
-    super-chunks (residues rebuilt per K range, residue sums carried mod p)."""
+    super-chunks (residues rebuilt per K range, residue sums carried mod p) on the row-scaled layout;
+    the shared layout's modes 0 / 1 / 2 (K = 2^18 / 2^15 / 2^15: 4 / 1 / 1 chunks; mode 1 in
+    K-blocks per i-slab) within R20's bound."""
     g = GridSpec((64, 512, 512), (-1.0,) * 3, (1.0,) * 3)
     kern = KernelSpec.matern(1.5, 0.3)
     Fg = T.fill(g, kern)
     F = orc.fill(ogrid(orc, g), okern(orc, kern))
-    R = orc.gram_mode(F, 0)
-    A = unfold(F, 0)
-    G1 = to_np(T.gram_i8(g, 0, Fg))
-    assert np.all(np.abs(G1 - R) <= _bound(A, 50))
-    monkeypatch.setenv("TUCKER_I8_RESIDUE_MB", "16")
-    G2 = to_np(T.gram_i8(g, 0, Fg))
-    assert np.array_equal(G1, G2)  # the result does not depend on how K is split
+    T.set_gram_engine(T.GRAM_INT8_ROWSCALED)
+    try:
+        R = orc.gram_mode(F, 0)
+        A = unfold(F, 0)
+        G1 = to_np(T.gram_i8(g, 0, Fg))
+        assert np.all(np.abs(G1 - R) <= _bound(A, 50))
+        monkeypatch.setenv("TUCKER_I8_RESIDUE_MB", "16")
+        G2 = to_np(T.gram_i8(g, 0, Fg))
+        assert np.array_equal(G1, G2)  # the result does not depend on how K is split
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
+    shared, b = T.i8_layout(g)
+    assert shared
+    for m in range(3):
+        G = to_np(T.gram_i8(g, m, Fg))
+        R = orc.gram_mode(F, m)
+        assert np.all(np.abs(G - R) <= _bound(unfold(F, m), b, np.max(np.abs(F)))), m
 
 
 def test_gram_i8_deterministic_and_vs_dmma(T):
@@ -150,10 +182,14 @@ def test_gram_i8_fused_bitwise_equals_materialised(T, monkeypatch, g, k, kb, mb)
     if mb:
         monkeypatch.setenv("TUCKER_I8_RESIDUE_MB", str(mb))
     F = T.fill(g, k)
-    ws = T.workspace_i8(g)
-    wsf = T.workspace_fused(g)
-    for m in range(3):
-        assert torch.equal(T.gram_fused(g, k, m, wsf), T.gram_i8(g, m, F, ws)), m
+    T.set_gram_engine(T.GRAM_INT8_ROWSCALED)  # the fused route's layout (per-mode row scaling)
+    try:
+        ws = T.workspace_i8(g)
+        wsf = T.workspace_fused(g)
+        for m in range(3):
+            assert torch.equal(T.gram_fused(g, k, m, wsf), T.gram_i8(g, m, F, ws)), m
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
 
 
 def test_stage_profiler_and_engine_switch(T):
@@ -169,7 +205,7 @@ def test_stage_profiler_and_engine_switch(T):
     finally:
         T.profile_enable(False)
     p = T.profile_read()
-    assert p["i8_gemm"][1] == 3 and p["i8_residues"][1] >= 2 and p["i8_rowmax"][1] == 1 and p["eig"][1] >= 3
+    assert p["i8_gemm"][1] == 3 and p["i8_residues"][1] >= 1 and p["i8_rowmax"][1] == 1 and p["eig"][1] >= 3
     assert p["dmma_gram"][1] == 0 and all(v[0] >= 0.0 for v in p.values())
     assert p["i8_gemm"][0] > 0.0
     assert T.profile_read()["i8_gemm"] == (0.0, 0)  # cleared; disabled: nothing recorded
@@ -241,7 +277,9 @@ def test_gram_i8_extreme_aspect(T, orc, shape):
         R = orc.gram_mode(F, m)
         A = unfold(F, m)
         assert np.array_equal(G, G.T)
-        assert np.all(np.abs(G - R) <= _bound(A, 50)), (shape, m)
+        shared, b = T.i8_layout(g)
+        gm = np.max(np.abs(F)) if shared else None
+        assert np.all(np.abs(G - R) <= _bound(A, b if shared else 50, gm)), (shape, m)
 
 
 def test_gram_i8_maximum_rows(T, orc):
@@ -271,3 +309,26 @@ def test_gram_i8_maximum_rows(T, orc):
     assert e.value.code in (4, 7)
     G2 = T.gram(g2, 0, F2)  # AUTO engine: the DMMA Gram
     assert torch.equal(G2, G2.T) and G2.shape == (16385, 16385)
+
+
+@pytest.mark.parametrize("g", [GridSpec((96, 80, 48), (-1.0,) * 3, (1.0,) * 3),
+                               GridSpec((136, 144, 160), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)),
+                               GridSpec((40, 300, 272), (-1.0, -0.5, -1.0), (1.0, 1.5, 0.5))])
+def test_gram_i8_shared_layout_exact_on_integers(T, g):
+    """The shared residue layout (R20; one residue pass, mode 2 read as MN-major operands, mode 1
+    in K-blocks per i-slab with a zero-filled tail when n3 % 128 != 0): on integer-valued F the
+    three Grams are the exact integer Grams, bit for bit."""
+    shared, b = T.i8_layout(g)
+    assert shared
+    rng = np.random.default_rng(int(np.prod(g.n)))
+    Kmax = max(np.prod(g.n) // g.n[m] for m in range(3))
+    bits = min(20, (53 - int(np.ceil(np.log2(Kmax)))) // 2)
+    F = rng.integers(-(1 << bits), 1 << bits, size=tuple(g.n), dtype=np.int64)
+    F[:, 3, :] = 0
+    Fd = torch.from_numpy(F.astype(np.float64)).cuda()
+    ws = T.workspace_i8(g)
+    for m in range(3):
+        A = unfold(F, m)
+        exact = (A @ A.T).astype(np.float64)
+        G = to_np(T.gram_i8(g, m, Fd, ws))
+        assert np.array_equal(G, exact), (m, np.max(np.abs(G - exact)))
