@@ -27,6 +27,11 @@ constexpr int kDirectMax = 112;  // whole-matrix Jacobi fits in shared memory up
 constexpr int kThreads = 1024;
 constexpr int kBatch = 8;
 constexpr int kMaxIters = 96;
+// Asynchronous completion (info == NULL): the iterations are enqueued up front, each exiting at
+// once after convergence; 48 bounds the launches (the workloads converge in 3-8, the slowest
+// measured case in 55 before the R15 tolerance); a solve still unconverged there returns its
+// last iterate, as the synchronous path does at kMaxIters (where NOCONV is reported).
+constexpr int kMaxItersAsync = 48;
 constexpr int kMinIters = 3;
 // Residual tolerance relative to theta_1: 1e-14 (SURVEY a-4), floored at 4 sqrt(n) eps — the
 // rounding level of evaluating G v itself in FP64 (DESIGN reading R15); at n <= 1024 the floor
@@ -543,7 +548,7 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
 }
 
 // Asynchronous completion (no host synchronisation; CUDA-Graph capturable): the remaining
-// iterations up to kMaxIters are enqueued unconditionally — every launch of a converged solve exits
+// iterations up to kMaxItersAsync are enqueued unconditionally — every launch of a converged solve exits
 // at once (the state's `done` flag), so the cost of the unneeded ones is their launch latency.
 int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda, double* sigma, void* ws,
                     cudaStream_t st) {
@@ -558,14 +563,14 @@ int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda
         const size_t sm = rr_smem(p);
         TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
-    for (int it = cl ? kMinIters + 3 : kBatch; it < kMaxIters; ++it) {
+    for (int it = cl ? kMinIters + 3 : kBatch; it < kMaxItersAsync; ++it) {
+        const int last = it == kMaxItersAsync - 1 ? 1 : 0;
         k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, p, n, q.dst);
         TK_CHECK_LAUNCH();
         if (cl) {
-            TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst,
-                                    st));
+            TK_RC(launch_rr_cluster(n, p, r, it, last, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst, st));
         } else {
-            RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, q.dst};
+            RRArgs a{n, p, r, it, last, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, q.dst};
             k_rr<<<1, kThreads, rr_smem(p), st>>>(a);
             TK_CHECK_LAUNCH();
         }

@@ -319,6 +319,35 @@ __device__ __forceinline__ void store_all_residues(const float2 (&u)[8][3], int8
                                                    std::integer_sequence<int, L...>) {
     (store_residues<L>(u, out + L * lstride), ...);
 }
+// 8 elements -> one 8-byte store per modulus (the shared-layout residue kernel: half the live
+// limbs per thread, so more warps per SM keep more loads in flight)
+template <int L>
+__device__ __forceinline__ void store_residues8(const float2 (&u)[4][3], int8_t* out) {
+    constexpr int p = kMod(L);
+    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
+    constexpr float fp = (float)p, inv = 1.0f / (float)p;
+    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
+    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
+    const float2 NP = make_float2(-fp, -fp);
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));
+        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);
+        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);
+        w[2 * e] = (uint32_t)__float_as_int(r2.x);
+        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
+    }
+    uint2 v;
+    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
+    *reinterpret_cast<uint2*>(out) = v;
+}
+template <int... L>
+__device__ __forceinline__ void store_all_residues8(const float2 (&u)[4][3], int8_t* out, size_t lstride,
+                                                    std::integer_sequence<int, L...>) {
+    (store_residues8<L>(u, out + L * lstride), ...);
+}
 
 // Scale (2^sh as one or two exact factors) of a row with high-word maximum hw.
 __device__ __forceinline__ void row_scale(uint32_t hw, int b, double& sa, double& sb) {
@@ -367,6 +396,37 @@ __device__ __forceinline__ bool residues16(const double* v, double sa, double sb
         }
     }
     store_all_residues(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    return ok;
+}
+
+// residues16 for 8 values (one 8-byte store per modulus); same window check.
+__device__ __forceinline__ bool residues8(const double* v, double sa, double sb, int8_t* out, size_t lstride,
+                                          double lim) {
+    float2 u[4][3];
+    constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const double x = v[e];
+        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
+        ok &= fabs(y - M2) <= lim;
+        const uint32_t lo = (uint32_t)__double2loint(y);
+        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
+        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        if (e & 1) {
+            u[e >> 1][0].y = f0;
+            u[e >> 1][1].y = f1;
+            u[e >> 1][2].y = f2;
+        } else {
+            u[e >> 1][0].x = f0;
+            u[e >> 1][1].x = f1;
+            u[e >> 1][2].x = f2;
+        }
+    }
+    store_all_residues8(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
     return ok;
 }
 
@@ -1094,15 +1154,16 @@ __global__ void k_i8_gmax(const uint32_t* __restrict__ mx, int64_t n, uint32_t* 
     }
 }
 
-// Residues of the whole tensor: each warp takes chunks of 512 consecutive elements — coalesced
-// 16-byte loads into a per-warp shared buffer padded one double per 16 (conflict-free both ways),
-// then each lane converts its 16 consecutive elements and writes one 16-byte word per modulus
-// (512 contiguous bytes per warp and plane).  N % 16 == 0.
-constexpr int RA_CH = 512;
-__global__ void __launch_bounds__(256) k_i8_residues_all(const double* __restrict__ F, int64_t N,
-                                                         const uint32_t* __restrict__ gmax, int b,
-                                                         int8_t* __restrict__ R, int* __restrict__ bad) {
-    __shared__ double buf[8][RA_CH + RA_CH / 16];
+// Residues of the whole tensor: each warp takes chunks of 256 consecutive elements — coalesced
+// 16-byte loads into a per-warp shared buffer padded one double per 8 (conflict-free reads), then
+// each lane converts its 8 consecutive elements and writes one 8-byte word per modulus (256
+// contiguous bytes per warp and plane).  8 elements per lane keep the live limbs small enough for
+// 4 CTAs (32 warps) per SM: the loads of many warps in flight hide the DRAM latency.  N % 8 == 0.
+constexpr int RA_CH = 256;
+__global__ void __launch_bounds__(256, 4) k_i8_residues_all(const double* __restrict__ F, int64_t N,
+                                                            const uint32_t* __restrict__ gmax, int b,
+                                                            int8_t* __restrict__ R, int* __restrict__ bad) {
+    __shared__ double buf[8][RA_CH + RA_CH / 8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sb = buf[warp];
     double sa, sbb;
@@ -1113,21 +1174,20 @@ __global__ void __launch_bounds__(256) k_i8_residues_all(const double* __restric
     bool ok = true;
     for (int64_t c = (int64_t)blockIdx.x * 8 + warp; c < nch; c += wstride) {
         const int64_t base = c * RA_CH;
-        double2 v[8];
+        double2 v[4];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < 4; ++t) {
             const int64_t e = base + 2 * lane + 64 * t;
             v[t] = e < N ? __ldcs(reinterpret_cast<const double2*>(F + e)) : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < 4; ++t) {
             const int e = 2 * lane + 64 * t;
-            sb[e + (e >> 4)] = v[t].x;
-            sb[e + 1 + (e >> 4)] = v[t].y;
+            sb[e + (e >> 3)] = v[t].x;
+            sb[e + 1 + (e >> 3)] = v[t].y;
         }
         __syncwarp();
-        if (base + 16 * lane < N)
-            ok &= residues16<1>(sb + 17 * lane, sa, sbb, R + base + 16 * lane, (size_t)N, lim);
+        if (base + 8 * lane < N) ok &= residues8(sb + 9 * lane, sa, sbb, R + base + 8 * lane, (size_t)N, lim);
         __syncwarp();
     }
     if (!ok) atomicExch(bad, 1);
@@ -1219,7 +1279,7 @@ int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, cha
     TK_CHECK_LAUNCH();
     const int64_t N = n[0] * n[1] * n[2];
     const int64_t nch = ceil_div(N, (int64_t)RA_CH);
-    const int grid = (int)std::min<int64_t>(ceil_div(nch, 8), (int64_t)kNumSMs * 8);
+    const int grid = (int)std::min<int64_t>(ceil_div(nch, 8), (int64_t)kNumSMs * 4);
     k_i8_residues_all<<<grid, 256, 0, st>>>(F, N, gw, w.b, reinterpret_cast<int8_t*>(base + w.off_R),
                                             reinterpret_cast<int*>(base + w.off_flag));
     TK_CHECK_LAUNCH();
