@@ -120,6 +120,18 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def fp64_peak() -> tuple:
+    """(TF/s, source): the measured DMMA-pipe FP64 peak (tools/fp64_peak.py ->
+    profiles/fp64_peak_measured.json, sustained) or the spec-derived 37.2 TF/s."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_measured.json")))
+        return float(d["dmma"]["sustained_tflops"]), ("measured DMMA m8n8k4 f64 sustained (profiles/fp64_peak_measured."
+                                                       "json; cuBLAS DGEMM 8192^3 sustained "
+                                                       f"{d['cublas_dgemm']['sustained_tflops']:.2f})")
+    except (OSError, ValueError, KeyError):
+        return FP64_PEAK_SPEC_TFLOPS, "spec-derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+
+
 def measured_peaks() -> dict:
     """Driver-written MEASURED_PEAKS.json (HBM GB/s, dense bf16 TF/s burst and sustained), or {}."""
     try:
@@ -280,15 +292,16 @@ def run_ours(args, rank, world, local):
                 "peak_source": peak_src, "ops_per_launch": ops_launch, "launch_ms": launch_ms,
                 "launches_per_step": calls["i8_gemm"],
                 "fp64_equivalent_gram_tflops": gram_flops_fp64 / (gram_stage_ms * 1e-3) / 1e12,
-                "fp64_equivalent_note": "FP64 SYRK flops of one mode / the whole emulated Gram stage (row maxima, "
-                                        "residues, int8 Grams, CRT) vs the 37.2 TF/s FP64 (DMMA) peak"}
+                "fp64_peak_tflops": fp64_peak()[0],
+                "fp64_equivalent_note": "FP64 SYRK flops of one mode / the whole emulated Gram stage (residues, "
+                                        "int8 Grams, CRT; per mode) vs the measured FP64 (DMMA) peak"}
         if lib_i8:
             roof["cublaslt_int8_sustained_tops"] = lib_i8
             roof["frac_of_cublaslt_int8_sustained"] = achieved / lib_i8
     else:
         launch_ms = prof["dmma_gram"][0] / prof["dmma_gram"][1]
         achieved = gram_flops_fp64 / (launch_ms * 1e-3) / 1e12
-        peak = FP64_PEAK_SPEC_TFLOPS
+        peak, peak_src64 = fp64_peak()
         traffic = None
         tp = os.path.join(ROOT, "profiles", "gram_traffic.json")
         if os.path.exists(tp):
@@ -298,10 +311,20 @@ def run_ours(args, rank, world, local):
                 traffic = None
         roof = {"bound": "tensor", "kernel": "k_gram_tma (+k_gram_reduce), per mode",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": "FP64 tensor (DMMA) = FP64 FMA pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz "
-                               "(spec-derived; MEASURED_PEAKS.json has no FP64 entry)",
+                "peak_source": peak_src64,
                 "flops_per_launch": gram_flops_fp64}
     total_flops = 3 * gram_flops_fp64 + 2.0 * N * rr * 2  # FP64 Gram + TTM1 + error reconstruction (algorithmic)
+    p64, _ = fp64_peak()
+    hbm = float(measured_peaks().get("hbm_gbs", 6460.5))
+    stage_roof = {}
+    for name, fl in (("ttm", 2.0 * N * rr), ("error", 2.0 * N * rr)):
+        if name in st:
+            t_fp64 = fl / (p64 * 1e12) * 1e3
+            t_hbm = 8.0 * N / (hbm * 1e9) * 1e3
+            stage_roof[name] = {"ms": st[name], "fp64_roofline_ms": t_fp64, "hbm_roofline_ms": t_hbm,
+                                "binding": "fp64" if t_fp64 > t_hbm else "hbm",
+                                "frac_of_binding": max(t_fp64, t_hbm) / st[name],
+                                "algorithmic": f"2 N r3 = {fl:.3e} flop, 8 N = {8 * N / 1e9:.2f} GB"}
     result = {
         "metric": METRIC, "value": whole_job_rate(N, world, ms_step), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -323,6 +346,7 @@ def run_ours(args, rank, world, local):
                        "Gram of mode m+1 runs, so 'eig' spans that overlap and the stages sum past the step",
         "fp64_tflops_algorithmic": total_flops / (ms_step * 1e-3) / 1e12,
         "roofline": roof,
+        "stage_rooflines": stage_roof,
         "gpu_launches": launches,
         "error": {"E": E[0], "normF": E[1], "normDiff": E[2]},
     }
