@@ -311,6 +311,24 @@ TUCKER_API int tucker_hosvd_accurate(const tucker_grid* grid, const int32_t r[3]
                           double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
                           int32_t iters, void* ws, size_t ws_bytes, void* stream, tucker_info* info);
 
+/* ------------------------------------------------------------------------------------------
+ * Multigrid Tucker (the paper's alternative whose cost is linear in the tensor size):
+ * the function tensor of (grid, kernel) on a sequence of dyadically refined grids (n -> ceil(n/2)
+ * per axis, the same box) from the coarsest level with every n_m <= n0 (never below r_m or 4
+ * nodes) up to `grid`; HOSVD only at the coarsest level; at each finer level the previous level's
+ * factor columns are interpolated to the new nodes (4-point Lagrange in the node coordinate),
+ * orthonormalised (one-sided Jacobi SVD) and refined by `sweeps` (>= 1) Tucker-ALS sweeps on that
+ * level's tensor (tucker_als).  F (dev, n1 x n2 x n3) receives the finest tensor (the call fills
+ * it); outputs as tucker_als (U_m, core, sigma_m of the last single-hole unfoldings).
+ * levels_out (host, nullable) <- the number of levels.  Workspace >= tucker_workspace_size_multigrid.
+ * Errors: INVALID_ARG (null, sweeps < 1, n0 < 4), DOMAIN, RANK, SIZE, UNSUPPORTED (r_m > 56, r_2 or
+ * r_3 > 64), NOCONV (best iterate), CUDA. */
+TUCKER_API size_t tucker_workspace_size_multigrid(const tucker_grid* grid, const int32_t r[3], int32_t n0);
+TUCKER_API int tucker_multigrid(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], int32_t n0,
+                     int32_t sweeps, double* F, double* U1, double* U2, double* U3, double* core, double* sigma1,
+                     double* sigma2, double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info,
+                     int32_t* levels_out);
+
 /* Number of kernel launches enqueued by this thread's most recent entry-point call. */
 /* Opt-in per-stage device timing: while enabled, CUDA events are recorded on the launching stream
  * around each stage's launches (off by default: no events, no overhead).  tucker_profile_read

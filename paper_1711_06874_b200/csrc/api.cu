@@ -718,6 +718,143 @@ int tucker_als(const tucker_grid* grid, const int32_t r[3], const double* F, dou
     return launch_als(grid->n, r, F, U, core, S, sweeps, ws, ws_bytes, static_cast<cudaStream_t>(stream), info);
 }
 
+// ---------------------------------------------------------------- multigrid Tucker
+namespace {
+constexpr int kMgMaxLevels = 12;
+struct MgPlan {
+    int L;                      // levels, 0 = coarsest .. L-1 = the caller's grid
+    int64_t n[kMgMaxLevels][3];
+    size_t off_fill, off_x, off_Fc, off_U[2], off_V, off_sig, off_sub, sub_bytes, total;
+    int64_t nmax;
+};
+
+// Dyadic coarsening n -> ceil(n/2) per axis (n = 2m - 1 grids nest exactly), down to the first
+// level whose every n_m <= n0, never below r_m (the coarsest HOSVD needs r_m <= n_m) or 4 nodes.
+MgPlan mg_plan(const tucker_grid* g, const int32_t* r, int32_t n0) {
+    MgPlan P{};
+    int64_t lev[kMgMaxLevels][3];
+    int L = 0;
+    int64_t cur[3] = {g->n[0], g->n[1], g->n[2]};
+    for (;;) {
+        for (int a = 0; a < 3; ++a) lev[L][a] = cur[a];
+        ++L;
+        if (L == kMgMaxLevels || std::max(cur[0], std::max(cur[1], cur[2])) <= n0) break;
+        int64_t nx[3];
+        bool ok = true;
+        for (int a = 0; a < 3; ++a) {
+            nx[a] = (cur[a] + 1) / 2;
+            ok &= nx[a] >= std::max<int64_t>(r[a], 4);
+        }
+        if (!ok) break;
+        for (int a = 0; a < 3; ++a) cur[a] = nx[a];
+    }
+    P.L = L;
+    for (int l = 0; l < L; ++l)
+        for (int a = 0; a < 3; ++a) P.n[l][a] = lev[L - 1 - l][a];
+    const int64_t* nf = g->n;
+    P.nmax = std::max(nf[0], std::max(nf[1], nf[2]));
+    size_t off = 0;
+    P.off_fill = off;
+    off += align_up(plan(g, nullptr).G, 256);  // nodes + K_nu table of the finest grid (covers all)
+    P.off_x = off;
+    off += align_up((size_t)2 * P.nmax * 8, 256);
+    P.off_Fc = off;
+    size_t fc = 0;
+    for (int l = 0; l + 1 < L; ++l) fc = std::max(fc, (size_t)(P.n[l][0] * P.n[l][1] * P.n[l][2]) * 8);
+    off += align_up(fc, 256);
+    for (int s = 0; s < 2; ++s) {
+        P.off_U[s] = off;
+        for (int a = 0; a < 3; ++a) off += align_up((size_t)P.nmax * r[a] * 8, 256);
+    }
+    P.off_V = off;  // prolonged factor (SVD input) and the SVD's full output
+    off += 2 * align_up((size_t)P.nmax * 64 * 8, 256);
+    P.off_sig = off;
+    off += align_up((size_t)3 * 64 * 8, 256);
+    P.off_sub = off;
+    size_t sub = 0;
+    for (int l = 0; l < L; ++l) {
+        tucker_grid gl = *g;
+        for (int a = 0; a < 3; ++a) gl.n[a] = P.n[l][a];
+        sub = std::max(sub, l == 0 ? plan(&gl, r).total : als_ws_bytes(gl.n, r));
+    }
+    P.sub_bytes = align_up(sub, 256);
+    off += P.sub_bytes;
+    P.total = off;
+    return P;
+}
+}  // namespace
+
+size_t tucker_workspace_size_multigrid(const tucker_grid* grid, const int32_t r[3], int32_t n0) {
+    if (check_grid(grid) != TUCKER_OK || !r || check_ranks(grid, r) != TUCKER_OK || n0 < 4) return 0;
+    return mg_plan(grid, r, n0).total;
+}
+
+int tucker_multigrid(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], int32_t n0,
+                     int32_t sweeps, double* F, double* U1, double* U2, double* U3, double* core, double* sigma1,
+                     double* sigma2, double* sigma3, void* ws, size_t ws_bytes, void* stream, tucker_info* info,
+                     int32_t* levels_out) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws || sweeps < 1 || n0 < 4)
+        return TUCKER_ERR_INVALID_ARG;
+    if (r[1] > 64 || r[2] > 64) return TUCKER_ERR_UNSUPPORTED;
+    const MgPlan P = mg_plan(grid, r, n0);
+    if (ws_bytes < P.total) return TUCKER_ERR_SIZE;
+    for (int a = 0; a < 3; ++a)
+        if (r[a] > 56 || P.n[0][a] < r[a]) return TUCKER_ERR_UNSUPPORTED;
+    if (info) std::memset(info, 0, sizeof(*info));
+    if (levels_out) *levels_out = P.L;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* w = static_cast<char*>(ws);
+    double* nodes = reinterpret_cast<double*>(w + P.off_fill);
+    const Layout Lf = plan(grid, nullptr);
+    double* cheb = reinterpret_cast<double*>(w + P.off_fill + Lf.cheb);
+    double* xbuf = reinterpret_cast<double*>(w + P.off_x);
+    double* Fc = reinterpret_cast<double*>(w + P.off_Fc);
+    double* Ubuf[2][3];
+    for (int s = 0; s < 2; ++s) {
+        size_t o = P.off_U[s];
+        for (int a = 0; a < 3; ++a) {
+            Ubuf[s][a] = reinterpret_cast<double*>(w + o);
+            o += align_up((size_t)P.nmax * r[a] * 8, 256);
+        }
+    }
+    double* V = reinterpret_cast<double*>(w + P.off_V);
+    double* Vo = reinterpret_cast<double*>(w + P.off_V + align_up((size_t)P.nmax * 64 * 8, 256));
+    double* sig = reinterpret_cast<double*>(w + P.off_sig);
+    void* sub = w + P.off_sub;
+    double* const Uout[3] = {U1, U2, U3};
+    double* const Sout[3] = {sigma1, sigma2, sigma3};
+    int worst = TUCKER_OK;
+    double* const* Ucur = Ubuf[0];
+    for (int l = 0; l < P.L; ++l) {
+        tucker_grid gl = *grid;
+        for (int a = 0; a < 3; ++a) gl.n[a] = P.n[l][a];
+        const bool finest = l == P.L - 1;
+        double* Fl = finest ? F : Fc;
+        TK_RC(launch_fill(gl, *kernel, Fl, nodes, cheb, st));
+        double* const* Unext = finest ? Uout : Ubuf[(l + 1) & 1];
+        if (l == 0) {  // HOSVD at the coarsest level only
+            int rc = hosvd_impl(&gl, r, Fl, Unext, core, Sout, sub, P.sub_bytes, st, info);
+            if (rc == TUCKER_ERR_NOCONV) worst = rc;
+            else if (rc != TUCKER_OK) return rc;
+            if (P.L == 1) return worst;
+        } else {  // prolongate the previous level's subspaces, orthonormalise, ALS sweeps
+            for (int a = 0; a < 3; ++a) {
+                TK_RC(launch_prolong(Ucur[a], P.n[l - 1][a], grid->lo[a], grid->hi[a], V, gl.n[a], r[a], xbuf, st));
+                TK_RC(launch_svd_cluster(gl.n[a], r[a], r[a], V, Vo, Unext[a], sig + 64 * a, nullptr, st));
+            }
+            const int rc = launch_als(gl.n, r, Fl, Unext, core, Sout, sweeps, sub, P.sub_bytes, st, info);
+            if (rc == TUCKER_ERR_NOCONV) worst = rc;
+            else if (rc != TUCKER_OK) return rc;
+        }
+        Ucur = Unext;
+    }
+    return worst;
+}
+
 size_t tucker_workspace_size_sym(const tucker_grid* grid, const int32_t r[3]) {
     if (check_grid(grid) != TUCKER_OK || !r) return 0;
     return sym_ws_bytes(*grid, r);

@@ -146,6 +146,11 @@ int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, 
 int launch_svd_cluster(int64_t n, int p, int r, const double* B, double* Vout, double* U, double* sigma,
                        int* sweeps_out, cudaStream_t st);
 
+// Multigrid Tucker (multigrid.cu): Uf (nf x r) <- cubic interpolation of Uc's columns from the nc
+// nodes to the nf nodes of [lo, hi] (xbuf: nc + nf doubles of scratch).
+int launch_prolong(const double* Uc, int64_t nc, double lo, double hi, double* Uf, int64_t nf, int r, double* xbuf,
+                   cudaStream_t st);
+
 // NEXT f2: Rayleigh–Ritz steps on F_(m) from the Gram route's V (refine.cu).
 size_t refine_ws_bytes(const int64_t n[3], int p);
 int launch_refine_mode(const int64_t n[3], int m, const double* F, const double* V0, const double* lam0, int p,

@@ -29,7 +29,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
            "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme", "tucker_i8_layout",
            "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
-           "tucker_last_launch_count", "tucker_strerror")
+           "tucker_workspace_size_multigrid", "tucker_multigrid", "tucker_last_launch_count", "tucker_strerror")
 
 
 class TuckerError(RuntimeError):
@@ -110,6 +110,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_hosvd_sym": (ctypes.c_int, [pg, pk, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_workspace_size_accurate": (sz, [pg, pr]),
         "tucker_hosvd_accurate": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, sz, vp, pi]),
+        "tucker_workspace_size_multigrid": (sz, [pg, pr, i32]),
+        "tucker_multigrid": (ctypes.c_int, [pg, pk, pr, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi,
+                                            P(ctypes.c_int32)]),
         "tucker_last_launch_count": (i64, []),
         "tucker_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
@@ -388,6 +391,36 @@ def als(grid, ranks, F: torch.Tensor, U_init, sweeps: int, ws: torch.Tensor | No
     if rc not in (0, 5):
         _check(rc, "tucker_als")
     return HosvdResult(U, core, S, info.as_dict(), rc)
+
+
+# ------------------------------------------------------------------ multigrid Tucker
+def multigrid(grid, kernel, ranks, n0: int = 64, sweeps: int = 2, F: torch.Tensor | None = None,
+              ws: torch.Tensor | None = None, stream=None):
+    """tucker_multigrid: HOSVD on the coarsest dyadic level (every n_m <= n0), then per finer level
+    interpolated factors + `sweeps` ALS sweeps; returns (HosvdResult, F, levels)."""
+    lib = load()
+    r = tuple(int(v) for v in ranks)
+    shape = tuple(int(v) for v in grid.n)
+    if F is None:
+        F = torch.empty(shape, dtype=torch.float64, device="cuda")
+    _dev(F, "F")
+    U = [torch.empty((shape[m], r[m]), dtype=torch.float64, device=F.device) for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device=F.device) for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device=F.device)
+    g, k = cgrid(grid), ckernel(kernel)
+    if ws is None:
+        nb = int(lib.tucker_workspace_size_multigrid(ctypes.byref(g), cranks(r), int(n0)))
+        if nb == 0:
+            raise TuckerError(1, "tucker_workspace_size_multigrid")
+        ws = torch.empty(nb, dtype=torch.uint8, device=F.device)
+    info = CInfo()
+    lev = ctypes.c_int32()
+    rc = lib.tucker_multigrid(ctypes.byref(g), ctypes.byref(k), cranks(r), int(n0), int(sweeps), _ptr(F), _ptr(U[0]),
+                              _ptr(U[1]), _ptr(U[2]), _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws),
+                              ws.numel(), _stream(stream), ctypes.byref(info), ctypes.byref(lev))
+    if rc not in (0, 5):
+        _check(rc, "tucker_multigrid")
+    return HosvdResult(U, core, S, info.as_dict(), rc), F, int(lev.value)
 
 
 # ------------------------------------------------------------------ NEXT f2: SVD-accurate HOSVD
