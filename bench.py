@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-als", action="store_true", help="skip the Tucker-ALS (NEXT f1) line")
     ap.add_argument("--no-sym", action="store_true", help="skip the symmetry-exploiting (NEXT f3) line")
     ap.add_argument("--no-accurate", action="store_true", help="skip the SVD-accurate (NEXT f2) line")
+    ap.add_argument("--no-multigrid", action="store_true", help="skip the multigrid Tucker line")
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
     ap.add_argument("--no-f4", action="store_true", help="skip the NEXT f4 workloads line")
     ap.add_argument("--no-parity", action="store_true", help="skip the per-config T1-T4 deltas vs the oracle")
@@ -406,6 +407,8 @@ def run_ours(args, rank, world, local):
         result["als"] = {"what": "Tucker-ALS / HOOI sweep (NEXT f1, P:571-579) on the same 1024^3 tensor, ranks 40",
                          "ms_per_sweep": ms_als, "points_per_s_per_sweep": N / (ms_als * 1e-3),
                          "E_hosvd": eh[0], "E_after_2_sweeps": ea[0], "rc": al.rc}
+    if not args.no_multigrid and world == 1:
+        result["multigrid"] = run_multigrid(T, grid, kern, ranks, F, stream)
     if not args.no_accurate and world == 1:
         acc = T.hosvd_accurate(grid, ranks, F, 1, stream=stream)  # warm-up
         torch.cuda.synchronize()
@@ -451,6 +454,23 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.destroy_process_group()
     return result
+
+
+def run_multigrid(T, grid, kern, ranks, F, stream) -> dict:
+    """Multigrid Tucker on the same 1024^3 workload: HOSVD at 128^3, then interpolated
+    factors + 2 ALS sweeps at 256^3, 512^3, 1024^3 (fills of every level included)."""
+    import torch
+    res, _, lev = T.multigrid(grid, kern, ranks, n0=128, sweeps=2, F=F, stream=stream)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res, _, lev = T.multigrid(grid, kern, ranks, n0=128, sweeps=2, F=F, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    err = T.error(grid, ranks, F, res.U, res.core, stream=stream).cpu().tolist()
+    return {"what": "multigrid Tucker (P:587-596): HOSVD at 128^3, cubic prolongation + 2 ALS sweeps per level",
+            "levels": lev, "ms": ms, "value": grid.points / (ms * 1e-3), "unit": UNIT, "E": err[0], "rc": res.rc}
 
 
 def run_fused(T, n: int, rr: int, stream) -> dict:
