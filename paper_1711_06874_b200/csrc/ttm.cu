@@ -628,14 +628,13 @@ __global__ void __launch_bounds__(NT, 2) k_err(const ErrArgs g, const double* __
         mbar_wait(&bar[slot], (uint32_t)((tile >> 1) & 1));
         // 3. Ft tile on DMMA
         const uint32_t tB0 = sB32 + (uint32_t)(slot * KB * BN * 16 * 8);
-        double acc[4][4][2];  // starts at -F: the MMAs leave Ft - F (no separate subtraction)
+        // accumulators start at 0, not at -F: F's loads stay in flight under the MMAs (their
+        // values are first needed in step 4)
+        double acc[4][4][2];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                acc[mi][ni][0] = -f[mi][ni][0];
-                acc[mi][ni][1] = -f[mi][ni][1];
-            }
+            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
         for (int kb = 0; kb < KB; ++kb) {
             const uint32_t tA = sA32 + (uint32_t)(kb * BM * 16 * 8);
             const uint32_t tB = tB0 + (uint32_t)(kb * BN * 16 * 8);
@@ -668,7 +667,8 @@ __global__ void __launch_bounds__(NT, 2) k_err(const ErrArgs g, const double* __
             for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                    sd = fma(acc[mi][ni][u], acc[mi][ni][u], sd);
+                    const double d = f[mi][ni][u] - acc[mi][ni][u];
+                    sd = fma(d, d, sd);
                     sf = fma(f[mi][ni][u], f[mi][ni][u], sf);
                 }
     }
