@@ -139,3 +139,59 @@ def test_validation_codes_next_rows(lib):
     # spectral density domain
     sk = T.ckernel(KernelSpec.spectral(0.0, 0.4))
     assert lib.tucker_fill(ctypes.byref(g), ctypes.byref(sk), d, d, big, None) == 2
+
+
+def test_host_queries_round2(lib):
+    """Host-only queries added in round 2 (no GPU): the INT8 residue layout per grid (R20 shared
+    layout where n3 % 16 == 0 and 16 N bytes fit; R18 per-mode otherwise or when forced), the
+    fill-only workspace, the multigrid workspace, the new error code."""
+    from paper_1711_06874_b200 import tucker as T
+    from tucker_inputs import GridSpec
+    g = GridSpec.cube(1024, 1.0)
+    assert T.i8_layout(g) == (True, 50)
+    assert T.i8_layout(GridSpec((40, 36, 33), (-1.0,) * 3, (1.0,) * 3))[0] is False   # n3 % 16 != 0
+    assert T.i8_layout(GridSpec.cube(2048, 1.0))[0] is False                            # 137 GB > cap
+    T.set_gram_engine(T.GRAM_INT8_ROWSCALED)
+    try:
+        assert T.i8_layout(g)[0] is False
+        assert T.get_gram_engine() == T.GRAM_INT8_ROWSCALED
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
+    T.set_gram_engine(T.GRAM_DMMA)
+    try:
+        with pytest.raises(T.TuckerError):
+            T.i8_layout(g)
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
+    # fill needs only the nodes and the K_nu table (a few KB), not the HOSVD workspace
+    cg = T.cgrid(g)
+    nf = lib.tucker_workspace_size_fill(ctypes.byref(cg))
+    assert 0 < nf < 64 * 1024 < T.workspace_bytes(g, (40, 40, 40))
+    # multigrid: the finest level's ALS workspace dominates; invalid n0 -> 0
+    nm = lib.tucker_workspace_size_multigrid(ctypes.byref(cg), T.cranks((40, 40, 40)), 128)
+    assert nm > 8 * 512 ** 3
+    assert lib.tucker_workspace_size_multigrid(ctypes.byref(cg), T.cranks((40, 40, 40)), 2) == 0
+    assert lib.tucker_strerror(9).decode().startswith("input")
+
+
+def test_multigrid_and_hosvd_validation(lib):
+    """tucker_multigrid and tucker_hosvd reject bad arguments before any launch."""
+    from paper_1711_06874_b200 import tucker as T
+    from tucker_inputs import GridSpec, KernelSpec
+    g = T.cgrid(GridSpec.cube(64, 1.0))
+    k = T.ckernel(KernelSpec.matern(1.5, 0.2))
+    d = ctypes.c_void_p(1)
+    # sweeps < 1, n0 < 4, null F
+    assert lib.tucker_multigrid(ctypes.byref(g), ctypes.byref(k), T.cranks((4, 4, 4)), 16, 0, d, d, d, d, d, d, d, d,
+                                d, 1 << 40, None, None, None) == 1
+    assert lib.tucker_multigrid(ctypes.byref(g), ctypes.byref(k), T.cranks((4, 4, 4)), 2, 1, d, d, d, d, d, d, d, d,
+                                d, 1 << 40, None, None, None) == 1
+    assert lib.tucker_multigrid(ctypes.byref(g), ctypes.byref(k), T.cranks((4, 4, 4)), 16, 1, None, d, d, d, d, d, d,
+                                d, d, 1 << 40, None, None, None) == 1
+    assert lib.tucker_multigrid(ctypes.byref(g), ctypes.byref(k), T.cranks((65, 4, 4)), 16, 1, d, d, d, d, d, d, d, d,
+                                d, 1 << 40, None, None, None) == 3
+    # r_m > 56 with n_m > 112: UNSUPPORTED before any launch
+    g2 = T.cgrid(GridSpec((300, 64, 64), (-1.0,) * 3, (1.0,) * 3))
+    rc = lib.tucker_hosvd(ctypes.byref(g2), T.cranks((57, 8, 8)), d, d, d, d, d, d, d, d, d, 1 << 40, None, None)
+    assert rc == 7
+    assert lib.tucker_last_launch_count() == 0
