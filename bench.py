@@ -199,10 +199,13 @@ def run_ours(args, rank, world, local):
     sp = ctypes.c_void_p(stream.cuda_stream)
     wsp, wsn = ctypes.c_void_p(ws.data_ptr()), ws.numel()
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-    # the fill also emits the INT8 route's row maxima (tucker_fill_rowmax) where it can: one pass
-    # over F fewer; tucker_hosvd_rowmax takes them (bitwise the plain calls' results)
+    # the fill also writes the INT8 route's inputs where it can: the shared residues in the same octant
+    # pass (tucker_fill_prepare -> tucker_hosvd_prepared: the residue pass over F is gone), else the row
+    # maxima (tucker_fill_rowmax -> tucker_hosvd_rowmax); bitwise the plain calls' results
     rowmax = torch.empty(3 * n, dtype=torch.int32, device=dev)
-    use_rowmax = args.gram_engine != "dmma" and lib.tucker_fill_rowmax(
+    use_prepare = args.gram_engine != "dmma" and lib.tucker_fill_prepare(
+        ctypes.byref(g_c), ctypes.byref(k_c), r_c, P(F), wsp, wsn, sp) == 0
+    use_rowmax = not use_prepare and args.gram_engine != "dmma" and lib.tucker_fill_rowmax(
         ctypes.byref(g_c), ctypes.byref(k_c), P(F), P(rowmax), wsp, wsn, sp) == 0
     torch.cuda.synchronize()
 
@@ -214,15 +217,22 @@ def run_ours(args, rank, world, local):
         asynchronous, graph-capturable HOSVD); returns the number of kernel launches."""
         spp = sp if spp is None else spp
         launches = 0
-        if use_rowmax:
-            T._check(lib.tucker_fill_rowmax(ctypes.byref(g_c), ctypes.byref(k_c), P(F), P(rowmax), wsp, wsn, spp),
-                     "fill_rowmax")
+        pinfo = ctypes.byref(info) if sync else None
+        if use_prepare:
+            T._check(lib.tucker_fill_prepare(ctypes.byref(g_c), ctypes.byref(k_c), r_c, P(F), wsp, wsn, spp),
+                     "fill_prepare")
+            launches += lib.tucker_last_launch_count()
+            rc = lib.tucker_hosvd_prepared(ctypes.byref(g_c), r_c, P(F), P(U[0]), P(U[1]), P(U[2]), P(core), P(S[0]),
+                                           P(S[1]), P(S[2]), wsp, wsn, spp, pinfo)
         else:
-            T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, spp), "fill")
-        launches += lib.tucker_last_launch_count()
-        rc = lib.tucker_hosvd_rowmax(ctypes.byref(g_c), r_c, P(F), P(rowmax) if use_rowmax else None, P(U[0]), P(U[1]),
-                                     P(U[2]), P(core), P(S[0]), P(S[1]), P(S[2]), wsp, wsn, spp,
-                                     ctypes.byref(info) if sync else None)
+            if use_rowmax:
+                T._check(lib.tucker_fill_rowmax(ctypes.byref(g_c), ctypes.byref(k_c), P(F), P(rowmax), wsp, wsn,
+                                                spp), "fill_rowmax")
+            else:
+                T._check(lib.tucker_fill(ctypes.byref(g_c), ctypes.byref(k_c), P(F), wsp, wsn, spp), "fill")
+            launches += lib.tucker_last_launch_count()
+            rc = lib.tucker_hosvd_rowmax(ctypes.byref(g_c), r_c, P(F), P(rowmax) if use_rowmax else None, P(U[0]),
+                                         P(U[1]), P(U[2]), P(core), P(S[0]), P(S[1]), P(S[2]), wsp, wsn, spp, pinfo)
         if rc not in (0, 5):
             T._check(rc, "hosvd")
         launches += lib.tucker_last_launch_count()
@@ -384,7 +394,8 @@ def run_ours(args, rank, world, local):
                    "kernel": {"family": "matern", "nu": 1.5, "ell": 0.2, "sigma2": 1.0}, "ranks": list(ranks),
                    "gram_engine": "int8 emulation (tcgen05 kind::i8 + CRT)" if i8 else "dmma",
                    "l2": f"inputs larger than L2 (F = {8 * N / 1e9:.2f} GB per step, L2 = 126 MB)",
-                   "step_calls": ("tucker_fill_rowmax + tucker_hosvd_rowmax + tucker_error" if use_rowmax
+                   "step_calls": ("tucker_fill_prepare + tucker_hosvd_prepared + tucker_error" if use_prepare else
+                                  "tucker_fill_rowmax + tucker_hosvd_rowmax + tucker_error" if use_rowmax
                                   else "tucker_fill + tucker_hosvd + tucker_error"),
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
         "stages_ms": st, "stage_calls_per_step": calls,

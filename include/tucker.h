@@ -190,6 +190,24 @@ TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], 
                         double* sigma1, double* sigma2, double* sigma3, void* ws, size_t ws_bytes,
                         void* stream, tucker_info* info);
 
+/* a-2 + the INT8 route's inputs in one pass (centred grids with n3 % 16 == 0 under the shared
+ * residue layout, R20; else TUCKER_ERR_UNSUPPORTED): F (dev) <- the collocation tensor, and into
+ * ws — the tucker_hosvd workspace of (grid, r), the calling thread's engine — the global exponent
+ * and the 16 residue planes of F.  The octant fill evaluates N/8 values (F is even in every index)
+ * and converts each to its residues once, storing value and residue bytes at the 8 mirrored
+ * positions: the residue pass over F is gone.  Follow it with tucker_hosvd_prepared on the same
+ * F and ws. */
+TUCKER_API int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F,
+                        void* ws, size_t ws_bytes, void* stream);
+/* tucker_hosvd on a workspace prepared by tucker_fill_prepare for this very F (the caller guarantees
+ * it; nothing of F is re-read for the Grams): the row-maxima and residue passes are skipped, the
+ * results are those tucker_hosvd computes on the shared layout.  A value outside the scheme's window
+ * still trips the flag (TUCKER_ERR_INPUT with info, NaN without).  Same outputs and errors as
+ * tucker_hosvd, plus UNSUPPORTED where tucker_fill_prepare is. */
+TUCKER_API int tucker_hosvd_prepared(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1,
+                          double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
+                          void* ws, size_t ws_bytes, void* stream, tucker_info* info);
+
 /* a-6: out3 (dev, 3 doubles) <- {E, ||F||, ||F - Ft||} with Ft = core x1 U1 x2 U2 x3 U3
  * (P:1016-1025).  Deterministic (fixed-order reduction, no float atomics). */
 TUCKER_API int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1,

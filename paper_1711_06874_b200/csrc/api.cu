@@ -161,7 +161,7 @@ int check_hosvd_limits(const tucker_grid* g, const int32_t* r) {
 // TUCKER_ERR_INPUT if the INT8 route saw a value outside its window.
 int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* const U[3], double* core,
                double* const sig[3], void* ws, size_t ws_bytes, cudaStream_t st, tucker_info* info,
-               bool mx_ready = false) {
+               int prep = 0) {
     const Layout L = plan(g, r);
     if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
     TK_RC(check_hosvd_limits(g, r));
@@ -221,7 +221,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
                 TK_RC(launch_eig_begin(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], L.eig_bytes, side_of(m)));
             }
             return TUCKER_OK;
-        }, mx_ready);
+        }, prep);
         if (rc == TUCKER_OK) rc = eig_end(2);
         if (rc == TUCKER_OK) rc = eig_end(1);
         // U2, U3 final on side A -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve on side B
@@ -505,6 +505,37 @@ int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], const doubl
     return hosvd_impl(grid, r, F, U, core, S, ws, ws_bytes, st, info, use);
 }
 
+int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F, void* ws,
+                        size_t ws_bytes, void* stream) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_kernel(kernel));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !ws) return TUCKER_ERR_INVALID_ARG;
+    const Layout L = plan(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    if (!L.i8_bytes || !fill_prepare_supported(*grid)) return TUCKER_ERR_UNSUPPORTED;
+    return launch_fill_prepare(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                               reinterpret_cast<double*>(at(ws, L.cheb)), at(ws, L.i8), L.i8_bytes,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int tucker_hosvd_prepared(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1, double* U2,
+                          double* U3, double* core, double* sigma1, double* sigma2, double* sigma3, void* ws,
+                          size_t ws_bytes, void* stream, tucker_info* info) {
+    launch_counter() = 0;
+    TK_RC(check_grid(grid));
+    TK_RC(check_ranks(grid, r));
+    if (!F || !U1 || !U2 || !U3 || !core || !sigma1 || !sigma2 || !sigma3 || !ws) return TUCKER_ERR_INVALID_ARG;
+    const Layout L = plan(grid, r);
+    if (ws_bytes < L.total) return TUCKER_ERR_SIZE;
+    if (!L.i8_bytes || !fill_prepare_supported(*grid)) return TUCKER_ERR_UNSUPPORTED;
+    if (info) std::memset(info, 0, sizeof(*info));
+    double* const U[3] = {U1, U2, U3};
+    double* const S[3] = {sigma1, sigma2, sigma3};
+    return hosvd_impl(grid, r, F, U, core, S, ws, ws_bytes, static_cast<cudaStream_t>(stream), info, 2);
+}
+
 int tucker_error(const tucker_grid* grid, const int32_t r[3], const double* F, const double* U1, const double* U2,
                  const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, void* stream) {
     launch_counter() = 0;
@@ -541,13 +572,22 @@ int tucker_approximate(const tucker_grid* grid, const tucker_kernel* kernel, con
     o += align_up((size_t)r[0] * r[1] * r[2] * 8, 256);
     double* errd = reinterpret_cast<double*>(o);
 
-    // the INT8 route's row maxima come out of the fill on centred grids (one pass over F fewer)
-    const bool mx_fused = L.i8_bytes && fill_rowmax_supported(*grid);
-    TK_RC(launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
-                      reinterpret_cast<double*>(at(ws, L.cheb)), st,
-                      mx_fused ? gram_i8_rowmax_slot(grid->n, at(ws, L.i8)) : nullptr));
+    // on centred grids the fill also writes the INT8 route's inputs: the shared residues (one octant
+    // pass, R20) or at least the row maxima — one or two passes over F fewer
+    int prep = 0;
+    if (L.i8_bytes && fill_prepare_supported(*grid)) {
+        TK_RC(launch_fill_prepare(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                                  reinterpret_cast<double*>(at(ws, L.cheb)), at(ws, L.i8), L.i8_bytes, st));
+        prep = 2;
+    } else {
+        const bool mx_fused = L.i8_bytes && fill_rowmax_supported(*grid);
+        TK_RC(launch_fill(*grid, *kernel, F, reinterpret_cast<double*>(at(ws, L.nodes)),
+                          reinterpret_cast<double*>(at(ws, L.cheb)), st,
+                          mx_fused ? gram_i8_rowmax_slot(grid->n, at(ws, L.i8)) : nullptr));
+        prep = mx_fused ? 1 : 0;
+    }
     const int64_t c0 = launch_counter();
-    const int rc = hosvd_impl(grid, r, F, Ud, cored, Sd, ws, ws_bytes, st, info, mx_fused);
+    const int rc = hosvd_impl(grid, r, F, Ud, cored, Sd, ws, ws_bytes, st, info, prep);
     if (rc != TUCKER_OK && rc != TUCKER_ERR_NOCONV) return rc;
     const int64_t c1 = launch_counter();
     (void)c0;

@@ -430,6 +430,69 @@ __device__ __forceinline__ bool residues8(const double* v, double sa, double sb,
     return ok;
 }
 
+// residues of 8 values, each plane's 8-byte word stored at out[0..7] + l * lstride: even slots in
+// order, odd slots byte-reversed (the k-mirror side of the octant fill).
+template <int L>
+__device__ __forceinline__ void store_residues8_mirror(const float2 (&u)[4][3], int8_t* const (&out)[8],
+                                                       size_t off) {
+    constexpr int p = kMod(L);
+    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
+    constexpr float fp = (float)p, inv = 1.0f / (float)p;
+    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
+    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
+    const float2 NP = make_float2(-fp, -fp);
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));
+        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);
+        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);
+        w[2 * e] = (uint32_t)__float_as_int(r2.x);
+        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
+    }
+    uint2 v, m;
+    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
+    m.x = __byte_perm(v.y, 0, 0x0123);  // bytes 7..4 of v
+    m.y = __byte_perm(v.x, 0, 0x0123);  // bytes 3..0 of v
+#pragma unroll
+    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? m : v;
+}
+template <int... L>
+__device__ __forceinline__ void store_all_residues8_mirror(const float2 (&u)[4][3], int8_t* const (&out)[8],
+                                                           size_t lstride, std::integer_sequence<int, L...>) {
+    (store_residues8_mirror<L>(u, out, (size_t)L * lstride), ...);
+}
+__device__ __forceinline__ bool residues8_mirror(const double* v, double sa, double sb, int8_t* const (&out)[8],
+                                                 size_t lstride, double lim) {
+    float2 u[4][3];
+    constexpr double M2 = 5629508124213248.0;
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const double x = v[e];
+        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
+        ok &= fabs(y - M2) <= lim;
+        const uint32_t lo = (uint32_t)__double2loint(y);
+        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
+        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        if (e & 1) {
+            u[e >> 1][0].y = f0;
+            u[e >> 1][1].y = f1;
+            u[e >> 1][2].y = f2;
+        } else {
+            u[e >> 1][0].x = f0;
+            u[e >> 1][1].x = f1;
+            u[e >> 1][2].x = f2;
+        }
+    }
+    store_all_residues8_mirror(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    return ok;
+}
+
 // One 32-row x 128-column tile (row block by, column block bx of the super-chunk).
 __device__ __forceinline__ void residue_tile(const ResArgs& a, int64_t bx, int64_t by,
                                              double (&tile)[RT_ROWS][RT_K / 16][17], double* s1, double* s2) {
@@ -1296,6 +1359,99 @@ int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, cha
     return TUCKER_OK;
 }
 
+// ---- The fill and the shared residues in one pass (centred grids, n3 % 16 == 0).  F is even in
+// every index, so the octant's N/8 values carry the whole tensor: each is evaluated once, converted
+// to its 16 residues once, and stored (value and residue bytes) at its 8 mirrored positions — the
+// residue ALU work falls 8-fold and F is never re-read.  The global exponent comes first from the
+// smallest radius: C(r) (Matérn, p-Slater, spectral density) decreases in r, so max F = C(r_min)
+// evaluated bitwise as the fill evaluates it (any value beyond the window still trips the flag).
+__global__ void k_i8_gmax_eval(KParams kp, const double* __restrict__ cheb, const double* __restrict__ x2,
+                               int64_t n1, int64_t n2, int64_t n3, uint32_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double m[3] = {INFINITY, INFINITY, INFINITY};
+    const int64_t nn[3] = {n1, n2, n3};
+    const double* xa = x2;
+    for (int a = 0; a < 3; ++a) {
+        for (int64_t i = 0; i < nn[a]; ++i) m[a] = fmin(m[a], xa[i]);
+        xa += nn[a];
+    }
+    const double v = eval_point(kp, cheb, __dadd_rn(__dadd_rn(m[0], m[1]), m[2]));
+    out[0] = (uint32_t)__double2hiint(v) & 0x7FFFFFFFu;
+}
+
+// Item = (i < h1, j < h2, 8-block t < n3/16): 8 consecutive k per thread -> one 64-byte run of F
+// and one 8-byte word per residue plane at each of the 8 mirrored positions (byte-reversed on the
+// k-mirror side).
+__global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const double* __restrict__ cheb_g,
+                                                         const double* __restrict__ x2, int64_t n1, int64_t n2,
+                                                         int64_t n3, double* __restrict__ F, int8_t* __restrict__ R,
+                                                         const uint32_t* __restrict__ gmax, int b,
+                                                         int* __restrict__ bad) {
+    __shared__ double cheb[kChebIntervals * kChebN];
+    if (kp.family == TUCKER_MATERN && kp.closed == 0)
+        for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    __syncthreads();
+    double sa, sbb;
+    row_scale(*gmax, b, sa, sbb);
+    const double lim = ldexp(1.0, b);
+    const double* xa = x2;
+    const double* xb = x2 + n1;
+    const double* xc = x2 + n1 + n2;
+    const int64_t h1 = (n1 + 1) / 2, h2 = (n2 + 1) / 2, q3 = n3 / 16;
+    const int64_t total = h1 * h2 * q3;
+    const size_t N = (size_t)n1 * n2 * n3;
+    bool ok = true;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = it % q3;
+        const int64_t ij = it / q3;
+        const int64_t j = ij % h2, i = ij / h2;
+        const int64_t k0 = 8 * t;
+        const double sij = __dadd_rn(xa[i], xb[j]);
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = eval_point(kp, cheb, __dadd_rn(sij, xc[k0 + u]));
+        const int64_t rows[4] = {i * n2 + j, i * n2 + (n2 - 1 - j), (n1 - 1 - i) * n2 + j,
+                                 (n1 - 1 - i) * n2 + (n2 - 1 - j)};
+        // (the middle row of an odd axis is its own mirror: written twice with the same bytes)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            double* row = F + rows[w] * n3;
+            st_v4(row + k0, v[0], v[1], v[2], v[3]);
+            st_v4(row + k0 + 4, v[4], v[5], v[6], v[7]);
+            st_v4(row + (n3 - 8 - k0), v[7], v[6], v[5], v[4]);
+            st_v4(row + (n3 - 4 - k0), v[3], v[2], v[1], v[0]);
+        }
+        // residues of the 8 values once; the four row mirrors x two k sides get the words
+        int8_t* out[8];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            out[2 * w] = R + rows[w] * n3 + k0;
+            out[2 * w + 1] = R + rows[w] * n3 + (n3 - 8 - k0);
+        }
+        ok &= residues8_mirror(v, sa, sbb, out, N, lim);
+    }
+    if (!ok) atomicExch(bad, 1);
+}
+
+int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
+                         char* base, const SharedPlan& w, cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_FILL, st);
+    const int64_t n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    const KParams kp = make_kparams(kn);
+    TK_RC(launch_fill_prep(g, kn, kp, nodes_x2, cheb, st));
+    uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
+    k_i8_gmax_eval<<<1, 32, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, gw);
+    TK_CHECK_LAUNCH();
+    const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 16);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16));
+    k_fill_octant_res<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F,
+                                                         reinterpret_cast<int8_t*>(base + w.off_R), gw, w.b,
+                                                         reinterpret_cast<int*>(base + w.off_flag));
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
 // G_m from the shared residues: one k_i8_gemm launch over all K (exact int32 per KCH columns),
 // the fold, the CRT with the global exponent.
 int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
@@ -1393,19 +1549,20 @@ int launch_gram_i8_modes(const int64_t n[3], const double* F, double* G, void* w
 // next phase).  ws: gram_i8_hosvd_ws_bytes.  (A joint modes-1/2 residue pass reading F once was
 // measured: 12.3 ms against 12.6 ms for the two passes, for 8 GiB more workspace — not kept.)
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, bool mx_ready) {
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, int prep) {
     using namespace i8;
     if (!gram_i8_supported(n)) return TUCKER_ERR_UNSUPPORTED;
     const WsPlan w = ws_plan(n);
     if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);
     uint32_t* mx = reinterpret_cast<uint32_t*>(base + w.off_mx);
-    TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));
-    if (!mx_ready) TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
+    if (prep == 2 && !shared_ok(n)) return TUCKER_ERR_UNSUPPORTED;
+    if (prep != 2) TK_CUDA(cudaMemsetAsync(base + w.off_flag, 0, sizeof(int), st));  // (prepared: the fill's flag)
+    if (prep == 0) TK_RC(launch_gram_i8_rowmax(n, F, mx, st));
     if (shared_ok(n)) {  // one residue pass for the three modes (R20)
         const SharedPlan sp = shared_plan(n);
         if (ws_bytes < sp.total) return TUCKER_ERR_SIZE;
-        TK_RC(shared_residues(n, F, mx, base, sp, st));
+        if (prep != 2) TK_RC(shared_residues(n, F, mx, base, sp, st));
         for (int m = 2; m >= 0; --m) {
             TK_RC(shared_gram_mode(n, m, base, sp, G[m], st));
             TK_RC(on_phase(&m, 1));
@@ -1607,6 +1764,18 @@ int& gram_engine() {  // per calling thread (tucker_set_gram_engine)
 }
 bool gram_use_i8(const int64_t n[3]) { return gram_engine() != TUCKER_GRAM_DMMA && gram_i8_supported(n); }
 bool gram_i8_shared_layout(const int64_t n[3]) { return gram_use_i8(n) && i8::shared_ok(n); }
+bool fill_prepare_supported(const tucker_grid& g) {
+    return gram_i8_shared_layout(g.n) && grid_centred(g) && g.n[2] % 16 == 0;
+}
+int launch_fill_prepare(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
+                        void* i8ws, size_t i8ws_bytes, cudaStream_t st) {
+    if (!fill_prepare_supported(g)) return TUCKER_ERR_UNSUPPORTED;
+    const i8::SharedPlan sp = i8::shared_plan(g.n);
+    if (i8ws_bytes < sp.total) return TUCKER_ERR_SIZE;
+    char* base = static_cast<char*>(i8ws);
+    TK_CUDA(cudaMemsetAsync(base + sp.off_flag, 0, sizeof(int), st));
+    return i8::shared_fill_residues(g, kn, F, nodes_x2, cheb, base, sp, st);
+}
 int gram_i8_shared_bits(const int64_t n[3]) { return i8::shared_plan(n).b; }
 size_t gram_auto_ws_bytes(const int64_t n[3]) { return gram_use_i8(n) ? gram_i8_ws_bytes(n) : gram_ws_bytes(n); }
 int launch_gram_auto(const int64_t n[3], int mode, const double* F, double* G, const uint32_t* mx,

@@ -83,10 +83,17 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
 // Device int of the INT8 workspace: 1 if an input value fell outside the scheme window (stale
 // row maxima or non-finite F; the Gram is then NaN), reset at the start of every Gram call.
 const int* gram_i8_flag_slot(const int64_t n[3], const void* ws);
-// mx_ready: the row maxima are already in the workspace's slot (gram_i8_rowmax_slot; e.g. written
-// by the fill of the same call) — the row-maxima pass is skipped.
+// prep: 0 nothing precomputed; 1 the row maxima are already in the workspace's slot
+// (gram_i8_rowmax_slot; e.g. written by the fill) — the row-maxima pass is skipped; 2 the shared
+// layout's residues and global exponent are already in the workspace (launch_fill_prepare of this
+// F) — the row-maxima and residue passes are skipped.
 int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3], void* ws, size_t ws_bytes,
-                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, bool mx_ready = false);
+                         cudaStream_t st, const std::function<int(const int*, int)>& on_phase, int prep = 0);
+// The fill and the shared residues in one octant pass (centred grid, n3 % 16 == 0, shared layout):
+// F, the global exponent and the residue planes of the INT8 workspace i8ws (gram_i8_hosvd_ws_bytes).
+bool fill_prepare_supported(const tucker_grid& g);
+int launch_fill_prepare(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
+                        void* i8ws, size_t i8ws_bytes, cudaStream_t st);
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws);
 // Per-device non-blocking side streams of the library (which = 0, 1; created once).

@@ -22,7 +22,8 @@ FORCE_GENERAL_BESSEL = 2
 ERRORS = {0: "TUCKER_OK", 1: "TUCKER_ERR_INVALID_ARG", 2: "TUCKER_ERR_DOMAIN", 3: "TUCKER_ERR_RANK",
           4: "TUCKER_ERR_SIZE", 5: "TUCKER_ERR_NOCONV", 6: "TUCKER_ERR_CUDA", 7: "TUCKER_ERR_UNSUPPORTED",
           8: "TUCKER_ERR_COLLECTIVE", 9: "TUCKER_ERR_INPUT"}
-EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill", "tucker_fill_rowmax", "tucker_hosvd_rowmax", "tucker_gram", "tucker_eig", "tucker_ttm_core",
+EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill", "tucker_fill_prepare",
+           "tucker_hosvd_prepared", "tucker_fill_rowmax", "tucker_hosvd_rowmax", "tucker_gram", "tucker_eig", "tucker_ttm_core",
            "tucker_hosvd", "tucker_error", "tucker_approximate", "tucker_workspace_size_fused",
            "tucker_gram_fused", "tucker_hosvd_fused", "tucker_error_fused", "tucker_hosvd_fused_sharded",
            "tucker_workspace_size_als",
@@ -83,6 +84,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_workspace_size_fill": (sz, [pg]),
         "tucker_fill": (ctypes.c_int, [pg, pk, vp, vp, sz, vp]),
         "tucker_fill_rowmax": (ctypes.c_int, [pg, pk, vp, vp, vp, sz, vp]),
+        "tucker_fill_prepare": (ctypes.c_int, [pg, pk, pr, vp, vp, sz, vp]),
+        "tucker_hosvd_prepared": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_hosvd_rowmax": (ctypes.c_int, [pg, pr, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, pi]),
         "tucker_gram": (ctypes.c_int, [pg, i32, vp, vp, vp, sz, vp]),
         "tucker_workspace_size_i8": (sz, [pg]),
@@ -215,6 +218,39 @@ def fill_rowmax(grid, kernel, F: torch.Tensor | None = None, ws: torch.Tensor | 
     _check(lib.tucker_fill_rowmax(ctypes.byref(g), ctypes.byref(k), _ptr(F), _ptr(mx), _ptr(ws), ws.numel(),
                                   _stream(stream)), "tucker_fill_rowmax")
     return F, mx
+
+
+def fill_prepare(grid, kernel, ranks, F: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """tucker_fill_prepare: (F, ws) — the fill plus the INT8 route's shared residues written into the
+    HOSVD workspace `ws` of (grid, ranks); follow with hosvd_prepared(grid, ranks, F, ws)."""
+    lib = load()
+    shape = tuple(int(v) for v in grid.n)
+    if F is None:
+        F = torch.empty(shape, dtype=torch.float64, device="cuda")
+    _dev(F, "F")
+    ws = ws if ws is not None else workspace(grid, ranks)
+    g, k = cgrid(grid), ckernel(kernel)
+    _check(lib.tucker_fill_prepare(ctypes.byref(g), ctypes.byref(k), cranks(ranks), _ptr(F), _ptr(ws), ws.numel(),
+                                   _stream(stream)), "tucker_fill_prepare")
+    return F, ws
+
+
+def hosvd_prepared(grid, ranks, F: torch.Tensor, ws: torch.Tensor, stream=None, sync: bool = True) -> HosvdResult:
+    """tucker_hosvd_prepared on a workspace from fill_prepare of this F."""
+    lib = load()
+    _dev(F, "F")
+    r = tuple(int(v) for v in ranks)
+    U = [torch.empty((int(grid.n[m]), r[m]), dtype=torch.float64, device=F.device) for m in range(3)]
+    S = [torch.empty(r[m], dtype=torch.float64, device=F.device) for m in range(3)]
+    core = torch.empty(r, dtype=torch.float64, device=F.device)
+    info = CInfo()
+    g = cgrid(grid)
+    rc = lib.tucker_hosvd_prepared(ctypes.byref(g), cranks(r), _ptr(F), _ptr(U[0]), _ptr(U[1]), _ptr(U[2]),
+                                   _ptr(core), _ptr(S[0]), _ptr(S[1]), _ptr(S[2]), _ptr(ws), ws.numel(),
+                                   _stream(stream), ctypes.byref(info) if sync else None)
+    if rc not in (0, 5):
+        _check(rc, "tucker_hosvd_prepared")
+    return HosvdResult(U, core, S, info.as_dict(), rc)
 
 
 def gram(grid, mode: int, F: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:

@@ -332,3 +332,27 @@ def test_gram_i8_shared_layout_exact_on_integers(T, g):
         exact = (A @ A.T).astype(np.float64)
         G = to_np(T.gram_i8(g, m, Fd, ws))
         assert np.array_equal(G, exact), (m, np.max(np.abs(G - exact)))
+
+
+@pytest.mark.parametrize("g,k", [(GridSpec.cube(256, 1.0), KernelSpec.matern(1.5, 0.2)),
+                                 (GridSpec((129, 131, 64), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)), KernelSpec.matern(0.7, 0.3)),
+                                 (GridSpec((96, 80, 48), (-1.0,) * 3, (1.0,) * 3), KernelSpec.slater(1.0, 0.2)),
+                                 (GridSpec.cube(144, 1.0), KernelSpec.spectral(0.1, 0.4))])
+def test_fill_prepare_equals_separate_passes(T, g, k):
+    """tucker_fill_prepare (octant fill + shared residues in one pass, the global exponent from the
+    smallest radius) gives bitwise the tensor of tucker_fill, and tucker_hosvd_prepared bitwise the
+    factors, sigma and core of tucker_hosvd (which takes the exponent from the row maxima and
+    re-reads F for the residues); odd axes (middle rows), general nu, p-Slater, spectral density."""
+    r = (10, 9, 8)
+    F, ws = T.fill_prepare(g, k, r)
+    assert torch.equal(F, T.fill(g, k))
+    a = T.hosvd_prepared(g, r, F, ws)
+    b = T.hosvd(g, r, F)
+    assert a.rc == 0 and b.rc == 0
+    for m in range(3):
+        assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m]), m
+    assert torch.equal(a.core, b.core)
+    off = GridSpec((64, 64, 64), (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0))  # not centred: refused
+    with pytest.raises(T.TuckerError) as e:
+        T.fill_prepare(off, k, (4, 4, 4))
+    assert e.value.code == 7
