@@ -1452,25 +1452,24 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
     return TUCKER_OK;
 }
 
-// G_m from the shared residues: one k_i8_gemm launch over all K (exact int32 per KCH columns),
-// the fold, the CRT with the global exponent.
-int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
+// The int8 Grams of mode m over one residue tensor in the shared (natural) layout with dims c[3]
+// (the whole tensor, or a plane chunk of it whose mode-m rows are complete): one k_i8_gemm launch
+// over all its K (exact int32 per KCH columns) and the fold into Racc (first: Racc starts at 0).
+int shared_gemm(const int64_t c[3], int m, const int8_t* R, int16_t* P, int32_t* Racc, int2* utab, bool first,
+                cudaStream_t st) {
     int nJ;
-    const int rows = (int)n[m];
-    const int ntiles = count_tiles(n[m], nJ);
-    int16_t* P = reinterpret_cast<int16_t*>(base + w.off_P);
-    int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
-    int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
+    const int rows = (int)c[m];
+    const int ntiles = count_tiles(c[m], nJ);
     TK_CUDA(cudaFuncSetAttribute(k_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     const int nug = build_units(rows, nJ, ntiles, nullptr);
     k_i8_units<<<1, 1, 0, st>>>(rows, nJ, ntiles, utab);
     TK_CHECK_LAUNCH();
     CUtensorMap map;
-    TK_RC(shared_map(&map, n, m, reinterpret_cast<int8_t*>(base + w.off_R)));
-    const int64_t nkb = shared_nkb(n, m);
+    TK_RC(shared_map(&map, c, m, const_cast<int8_t*>(R)));
+    const int64_t nkb = shared_nkb(c, m);
     const int nchunks = (int)ceil_div(nkb, KCH / BKB);
     GemmArgs ga{rows, nJ, ntiles, nug, nchunks, NMOD * nchunks * nug, nkb * BKB, P, utab, m + 1,
-                (int)ceil_div(n[2], (int64_t)BKB), nkb};
+                (int)ceil_div(c[2], (int64_t)BKB), nkb};
     const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);
     {
         TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1479,12 +1478,268 @@ int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w,
     }
     TK_PROF(TUCKER_PROF_I8_CRT, st);
     const int64_t tot = (int64_t)NMOD * ntiles * PN * PM;
-    k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, 1);
+    k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, first ? 1 : 0);
     TK_CHECK_LAUNCH();
-    const dim3 cg((unsigned)ceil_div(n[m], 32), (unsigned)ceil_div(n[m], 8));
-    k_i8_crt<<<cg, 256, 0, st>>>(Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), rows, nJ, ntiles, w.b, G,
-                                 reinterpret_cast<const int*>(base + w.off_flag), 1);
+    return TUCKER_OK;
+}
+
+// G_m (n_m x n_m, both triangles) from the folded residue sums, with the global exponent.
+int shared_crt(int64_t nm, const int32_t* Racc, const uint32_t* gmax, int b, const int* flag, double* G,
+               cudaStream_t st) {
+    TK_PROF(TUCKER_PROF_I8_CRT, st);
+    int nJ;
+    const int ntiles = count_tiles(nm, nJ);
+    const dim3 cg((unsigned)ceil_div(nm, 32), (unsigned)ceil_div(nm, 8));
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, gmax, (int)nm, nJ, ntiles, b, G, flag, 1);
     TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
+// G_m from the shared residues of the whole tensor.
+int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
+    int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
+    TK_RC(shared_gemm(n, m, reinterpret_cast<const int8_t*>(base + w.off_R), reinterpret_cast<int16_t*>(base + w.off_P),
+                      Racc, reinterpret_cast<int2*>(base + w.off_utab), true, st));
+    return shared_crt(n[m], Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
+                      reinterpret_cast<const int*>(base + w.off_flag), G, st);
+}
+
+// ---- a-7 on the shared layout (F never stored): the residues of plane chunks generated straight
+// from the kernel — i-plane chunks serve modes 1 and 2 (their Grams sum over i), j-plane chunks
+// mode 0 — so the tensor is generated twice instead of three times, no F chunk is written or read,
+// and on centred grids every evaluation and residue conversion serves 4 mirrored positions (the
+// chunk's free axis and k).  Integer partial sums are exact in any order: the Grams are bitwise
+// those of the materialised shared route on the same values.
+template <int NS>
+__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
+                                                 std::integer_sequence<int>) {}
+template <int NS, int L, int... Ls>
+__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
+                                                 std::integer_sequence<int, L, Ls...>) {
+    constexpr int p = kMod(L);
+    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
+    constexpr float fp = (float)p, inv = 1.0f / (float)p;
+    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
+    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
+    const float2 NP = make_float2(-fp, -fp);
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));
+        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);
+        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);
+        w[2 * e] = (uint32_t)__float_as_int(r2.x);
+        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
+    }
+    uint2 v, mr;
+    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
+    mr.x = __byte_perm(v.y, 0, 0x0123);
+    mr.y = __byte_perm(v.x, 0, 0x0123);
+    const size_t off = (size_t)L * lstride;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? mr : v;
+    store_res8_slots<NS>(u, out, lstride, std::integer_sequence<int, Ls...>{});
+}
+
+// Residues of the 8 values v, stored at NS slots (odd slots byte-reversed).
+template <int NS>
+__device__ __forceinline__ bool residues8_slots(const double* v, double sa, double sb, int8_t* const (&out)[NS],
+                                                size_t lstride, double lim) {
+    float2 u[4][3];
+    constexpr double M2 = 5629508124213248.0;
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const double x = v[e];
+        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
+        ok &= fabs(y - M2) <= lim;
+        const uint32_t lo = (uint32_t)__double2loint(y);
+        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
+        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
+        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
+        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
+        if (e & 1) {
+            u[e >> 1][0].y = f0;
+            u[e >> 1][1].y = f1;
+            u[e >> 1][2].y = f2;
+        } else {
+            u[e >> 1][0].x = f0;
+            u[e >> 1][1].x = f1;
+            u[e >> 1][2].x = f2;
+        }
+    }
+    store_res8_slots<NS>(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    return ok;
+}
+
+// Residues of planes [p0, p0 + pc) of axis ax (0: i, 1: j) into the chunk tensor R (dims
+// c = (pc, n2, n3) or (n1, pc, n3), one byte plane per modulus of c0 c1 c2 bytes).  MIR (centred
+// grids, n3 % 16 == 0): items over half the free axis and half of k, 4 slots per evaluation.
+template <bool MIR>
+__global__ void __launch_bounds__(256) k_gen_res_chunk(KParams kp, const double* __restrict__ cheb_g,
+                                                       const double* __restrict__ x2, int64_t n1, int64_t n2,
+                                                       int64_t n3, int ax, int64_t p0, int64_t pc,
+                                                       int8_t* __restrict__ R, const uint32_t* __restrict__ gmax,
+                                                       int b, int* __restrict__ bad) {
+    __shared__ double cheb[kChebIntervals * kChebN];
+    if (kp.family == TUCKER_MATERN && kp.closed == 0)
+        for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    __syncthreads();
+    double sa, sbb;
+    row_scale(*gmax, b, sa, sbb);
+    const double lim = ldexp(1.0, b);
+    const double* xa = x2;
+    const double* xb = x2 + n1;
+    const double* xc = x2 + n1 + n2;
+    const int64_t c0 = ax == 0 ? pc : n1, c1 = ax == 0 ? n2 : pc;
+    const int64_t nfree = ax == 0 ? n2 : n1;                      // the chunk's complete (mirrorable) axis
+    const int64_t hfree = MIR ? (nfree + 1) / 2 : nfree;
+    const int64_t qk = MIR ? n3 / 16 : n3 / 8;
+    const int64_t total = pc * hfree * qk;
+    const size_t plane = (size_t)c0 * c1 * n3;
+    bool ok = true;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = it % qk;
+        const int64_t rest = it / qk;
+        const int64_t f = rest % hfree, a = rest / hfree;         // free-axis index, chunk plane
+        const int64_t i = ax == 0 ? p0 + a : f, j = ax == 0 ? f : p0 + a;
+        const int64_t k0 = 8 * t;
+        const double sij = __dadd_rn(xa[i], xb[j]);
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = eval_point(kp, cheb, __dadd_rn(sij, xc[k0 + u]));
+        // chunk row of (a, f) and of the mirrored free index
+        const int64_t row0 = ax == 0 ? a * n2 + f : f * pc + a;
+        if (MIR) {
+            const int64_t fm = nfree - 1 - f;
+            const int64_t row1 = ax == 0 ? a * n2 + fm : fm * pc + a;
+            int8_t* const out[4] = {R + row0 * n3 + k0, R + row0 * n3 + (n3 - 8 - k0), R + row1 * n3 + k0,
+                                    R + row1 * n3 + (n3 - 8 - k0)};
+            ok &= residues8_slots<4>(v, sa, sbb, out, plane, lim);
+        } else {
+            int8_t* const out[1] = {R + row0 * n3 + k0};
+            ok &= residues8_slots<1>(v, sa, sbb, out, plane, lim);
+        }
+    }
+    if (!ok) atomicExch(bad, 1);
+}
+
+struct FusedSharedPlan {
+    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc[2], off_utab, total;
+    int b;
+    int64_t pc[2];  // planes per chunk: i-chunks (modes 1, 2), j-chunks (mode 0)
+};
+
+FusedSharedPlan fused_shared_plan(const int64_t n[3]) {
+    FusedSharedPlan w{};
+    const int64_t N = n[0] * n[1] * n[2];
+    int64_t Kmax = 0;
+    for (int m = 0; m < 3; ++m) Kmax = std::max(Kmax, N / n[m]);
+    w.b = scale_bits(Kmax);
+    // residue chunks of <= 8 GiB (F-equivalent 4 GiB; the test knob TUCKER_FUSED_CHUNK_KB sets it)
+    const int64_t target = fused_chunk_target((int64_t)4 << 30);
+    w.pc[0] = std::min<int64_t>(n[0], std::max<int64_t>(1, target / (8 * n[1] * n[2])));
+    w.pc[1] = std::min<int64_t>(n[1], std::max<int64_t>(1, target / (8 * n[0] * n[2])));
+    size_t rb = 0, pb = 0, ab = 0, ub = 0;
+    for (int ax = 0; ax < 2; ++ax) {
+        const int64_t c[3] = {ax == 0 ? w.pc[0] : n[0], ax == 0 ? n[1] : w.pc[1], n[2]};
+        rb = std::max(rb, align_up((size_t)NMOD * c[0] * c[1] * c[2], 1024));
+        for (int m = 0; m < 3; ++m) {
+            if ((ax == 0) != (m != 0)) continue;
+            int nJ;
+            const int nt = count_tiles(c[m], nJ);
+            const int64_t nch = ceil_div(shared_nkb(c, m), KCH / BKB);
+            pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
+            ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
+            ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
+        }
+    }
+    size_t off = 0;
+    w.off_mx = off;
+    w.off_flag = off + align_up((size_t)(n[0] + n[1] + n[2]) * 4, 16);
+    w.off_gmax = w.off_flag + 4;
+    off += align_up((size_t)(n[0] + n[1] + n[2]) * 8 + 16, 1024);
+    w.off_R = off;
+    off += rb;
+    w.off_P = off;
+    off += pb;
+    for (int q = 0; q < 2; ++q) {
+        w.off_Racc[q] = off;
+        off += ab;
+    }
+    w.off_utab = off;
+    off += ub;
+    w.total = off;
+    return w;
+}
+
+bool fused_shared_ok(const int64_t n[3]) {
+    return gram_engine() != TUCKER_GRAM_INT8_ROWSCALED && n[2] % 16 == 0;
+}
+
+int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* base, const FusedSharedPlan& w,
+                        cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
+                        const Shard* shard) {
+    const bool sharded = shard && shard->sharded();
+    uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
+    int* flag = reinterpret_cast<int*>(base + w.off_flag);
+    TK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    k_i8_gmax_eval<<<1, 32, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2], gw);  // max F = C(r_min)
+    TK_CHECK_LAUNCH();
+    int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
+    int16_t* P = reinterpret_cast<int16_t*>(base + w.off_P);
+    int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
+    const bool mir = gen.kp.centred != 0;
+    for (int ax = 0; ax < 2; ++ax) {  // i-chunks for modes 1, 2; then j-chunks for mode 0
+        int modes[2], nm = 0;
+        for (int m = (ax == 0 ? 1 : 0); m <= (ax == 0 ? 2 : 0); ++m)
+            if (m >= m_first && m <= m_last) modes[nm++] = m;
+        if (!nm) continue;
+        const int64_t planes = ax == 0 ? n[0] : n[1], pc = w.pc[ax];
+        bool first[2] = {true, true};
+        for (int64_t p0 = 0, cidx = 0; p0 < planes; p0 += pc, ++cidx) {
+            if (sharded && !shard->owns(cidx)) continue;
+            const int64_t pcc = std::min(pc, planes - p0);
+            const int64_t c[3] = {ax == 0 ? pcc : n[0], ax == 0 ? n[1] : pcc, n[2]};
+            {
+                TK_PROF(TUCKER_PROF_I8_RESIDUES, st);
+                const int64_t hfree = mir ? ((ax == 0 ? n[1] : n[0]) + 1) / 2 : (ax == 0 ? n[1] : n[0]);
+                const int64_t items = pcc * hfree * (mir ? n[2] / 16 : n[2] / 8);
+                const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 8));
+                if (mir)
+                    k_gen_res_chunk<true><<<(unsigned)blocks, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2],
+                                                                           ax, p0, pcc, R, gw, w.b, flag);
+                else
+                    k_gen_res_chunk<false><<<(unsigned)blocks, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1],
+                                                                            n[2], ax, p0, pcc, R, gw, w.b, flag);
+                TK_CHECK_LAUNCH();
+            }
+            for (int q = 0; q < nm; ++q) {
+                TK_RC(shared_gemm(c, modes[q], R, P, reinterpret_cast<int32_t*>(base + w.off_Racc[q]), utab, first[q],
+                                  st));
+                first[q] = false;
+            }
+        }
+        for (int q = 0; q < nm; ++q) {
+            const int m = modes[q];
+            int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc[q]);
+            if (sharded) {  // combine the ranks' residue sums (each in [0, p)), fold, then the CRT
+                int nJ;
+                const int64_t tot = (int64_t)NMOD * count_tiles(n[m], nJ) * PN * PM;
+                if (first[q]) TK_CUDA(cudaMemsetAsync(Racc, 0, (size_t)tot * 4, st));
+                TK_CUDA(cudaStreamSynchronize(st));
+                if (shard->allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
+                TK_PROF(TUCKER_PROF_I8_CRT, st);
+                k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0);
+                TK_CHECK_LAUNCH();
+            }
+            TK_RC(shared_crt(n[m], Racc, gw, w.b, flag, G, st));
+            TK_RC(after_mode(m));
+        }
+    }
     return TUCKER_OK;
 }
 
@@ -1666,8 +1921,12 @@ FusedI8Plan fused_i8_plan(const int64_t n[3]) {
 
 }  // namespace i8
 
-bool gram_i8_fused_supported(const int64_t n[3]) { return gram_i8_supported(n) && i8::fused_i8_plan(n).ok; }
-size_t gram_i8_fused_ws_bytes(const int64_t n[3]) { return i8::fused_i8_plan(n).total; }
+bool gram_i8_fused_supported(const int64_t n[3]) {
+    return gram_i8_supported(n) && (i8::fused_shared_ok(n) || i8::fused_i8_plan(n).ok);
+}
+size_t gram_i8_fused_ws_bytes(const int64_t n[3]) {
+    return i8::fused_shared_ok(n) ? i8::fused_shared_plan(n).total : i8::fused_i8_plan(n).total;
+}
 
 int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, void* ws, size_t ws_bytes,
                                cudaStream_t st, int m_first, int m_last, const std::function<int(int)>& after_mode,
@@ -1675,6 +1934,11 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
     const bool sharded = shard && shard->sharded();
     using namespace i8;
     if (!gram_i8_fused_supported(n)) return TUCKER_ERR_UNSUPPORTED;
+    if (fused_shared_ok(n)) {  // shared layout: residues of plane chunks straight from the kernel (R20)
+        const FusedSharedPlan w = fused_shared_plan(n);
+        if (ws_bytes < w.total) return TUCKER_ERR_SIZE;
+        return launch_fused_shared(n, gen, G, static_cast<char*>(ws), w, st, m_first, m_last, after_mode, shard);
+    }
     const FusedI8Plan f = fused_i8_plan(n);
     if (ws_bytes < f.total) return TUCKER_ERR_SIZE;
     char* base = static_cast<char*>(ws);

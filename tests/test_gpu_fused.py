@@ -176,15 +176,18 @@ def test_fused_2048_config5f(T, orc):
     G0 = T.gram_fused(g, k, 0, wsf)
     assert torch.equal(G0, G0.T)
     Gn = to_np(G0)
-    # the INT8 route forms X X^T exactly (R18): each sampled entry within R18's element bound, whose
-    # inputs (row maxima, row 1-norms) the oracle computes from the kernel directly
+    # the INT8 route forms X X^T exactly: each sampled entry within the element bound of the fused
+    # route's shared layout (R20: one global exponent — max F is C at the centre-most node, from the
+    # oracle's kernel evaluation; row 1-norms from orc_row_stats_fn)
     K = 2048 * 2048
     _, bits = T.i8_scheme(K)
+    gmax = orc.fill_entry(og, ok, 1023, 1023, 1023)
     for a, b in rng.integers(0, 2048, size=(6, 2)):
         ref = orc.gram_entry_fn(og, ok, 0, int(a), int(b))
         (ma, la), (mb, lb) = orc.row_stats_fn(og, ok, 0, int(a)), orc.row_stats_fn(og, ok, 0, int(b))
-        assert abs(Gn[a, b] - ref) <= PB.i8_bound_entry(ma, mb, la, lb, K, bits, ref), (a, b)
-        assert abs(Gn[a, b] - ref) <= 1e-14 * np.sqrt(Gn[a, a] * Gn[b, b]), (a, b)
+        assert max(ma, mb) <= gmax
+        assert abs(Gn[a, b] - ref) <= PB.i8_bound_entry(gmax, gmax, la, lb, K, bits, ref), (a, b)
+        assert abs(Gn[a, b] - ref) <= 1e-13 * np.sqrt(Gn[a, a] * Gn[b, b]), (a, b)
     del G0
     res = T.hosvd_fused(g, k, r, wsf)
     assert res.rc == 0, res.info

@@ -232,12 +232,18 @@ def test_gram_i8_2048_materialised_equals_fused(T):
     fused one (F generated chunk by chunk, never stored) are bitwise equal (mode 0: K = 2^22 columns,
     two 8 GiB residue super-chunks, b = 50)."""
     g, k = GridSpec.cube(2048, 1.0), KernelSpec.matern(1.5, 0.2)
-    wsf = T.workspace_fused(g)
-    Gf = T.gram_fused(g, k, 0, wsf)
-    del wsf
-    torch.cuda.empty_cache()
-    F = T.fill(g, k)
-    G = T.gram_i8(g, 0, F)
+    # the row-scaled layout on both sides (at 2048^3 the materialised route cannot hold the shared
+    # residues next to F; the default fused route's shared layout is checked in test_gpu_fused.py)
+    T.set_gram_engine(T.GRAM_INT8_ROWSCALED)
+    try:
+        wsf = T.workspace_fused(g)
+        Gf = T.gram_fused(g, k, 0, wsf)
+        del wsf
+        torch.cuda.empty_cache()
+        F = T.fill(g, k)
+        G = T.gram_i8(g, 0, F)
+    finally:
+        T.set_gram_engine(T.GRAM_AUTO)
     assert torch.equal(G, Gf)
     d = torch.sqrt(torch.diagonal(G))
     assert bool(torch.all(d > 0)) and torch.equal(G, G.T)
