@@ -319,36 +319,6 @@ __device__ __forceinline__ void store_all_residues(const float2 (&u)[8][3], int8
                                                    std::integer_sequence<int, L...>) {
     (store_residues<L>(u, out + L * lstride), ...);
 }
-// 8 elements -> one 8-byte store per modulus (the shared-layout residue kernel: half the live
-// limbs per thread, so more warps per SM keep more loads in flight)
-template <int L>
-__device__ __forceinline__ void store_residues8(const float2 (&u)[4][3], int8_t* out) {
-    constexpr int p = kMod(L);
-    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
-    constexpr float fp = (float)p, inv = 1.0f / (float)p;
-    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
-    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
-    const float2 NP = make_float2(-fp, -fp);
-    uint32_t w[8];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));
-        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);
-        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);
-        w[2 * e] = (uint32_t)__float_as_int(r2.x);
-        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
-    }
-    uint2 v;
-    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
-    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
-    *reinterpret_cast<uint2*>(out) = v;
-}
-template <int... L>
-__device__ __forceinline__ void store_all_residues8(const float2 (&u)[4][3], int8_t* out, size_t lstride,
-                                                    std::integer_sequence<int, L...>) {
-    (store_residues8<L>(u, out + L * lstride), ...);
-}
-
 // Scale (2^sh as one or two exact factors) of a row with high-word maximum hw.
 __device__ __forceinline__ void row_scale(uint32_t hw, int b, double& sa, double& sb) {
     const int sh = b - row_exponent(hw);  // |a_ik| 2^sh < 2^b
@@ -399,42 +369,15 @@ __device__ __forceinline__ bool residues16(const double* v, double sa, double sb
     return ok;
 }
 
-// residues16 for 8 values (one 8-byte store per modulus); same window check.
-__device__ __forceinline__ bool residues8(const double* v, double sa, double sb, int8_t* out, size_t lstride,
-                                          double lim) {
-    float2 u[4][3];
-    constexpr double M2 = 5629508124213248.0;  // 2^52 + B, B = 2^50 + 2^33 + 2^16
-    bool ok = true;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const double x = v[e];
-        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
-        ok &= fabs(y - M2) <= lim;
-        const uint32_t lo = (uint32_t)__double2loint(y);
-        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
-        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
-        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
-        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
-        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
-        if (e & 1) {
-            u[e >> 1][0].y = f0;
-            u[e >> 1][1].y = f1;
-            u[e >> 1][2].y = f2;
-        } else {
-            u[e >> 1][0].x = f0;
-            u[e >> 1][1].x = f1;
-            u[e >> 1][2].x = f2;
-        }
-    }
-    store_all_residues8(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
-    return ok;
-}
-
-// residues of 8 values, each plane's 8-byte word stored at out[0..7] + l * lstride: even slots in
-// order, odd slots byte-reversed (the k-mirror side of the octant fill).
-template <int L>
-__device__ __forceinline__ void store_residues8_mirror(const float2 (&u)[4][3], int8_t* const (&out)[8],
-                                                       size_t off) {
+// Residues of 8 consecutive values -> one 8-byte word per modulus, stored at NS slots (odd slots
+// byte-reversed: the k-mirror side of the octant generators); the same window check as residues16.
+// 8 values per call keep the live limbs small (64 registers for the shared-layout residue kernel).
+template <int NS>
+__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
+                                                 std::integer_sequence<int>) {}
+template <int NS, int L, int... Ls>
+__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
+                                                 std::integer_sequence<int, L, Ls...>) {
     constexpr int p = kMod(L);
     constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
     constexpr float fp = (float)p, inv = 1.0f / (float)p;
@@ -450,21 +393,21 @@ __device__ __forceinline__ void store_residues8_mirror(const float2 (&u)[4][3], 
         w[2 * e] = (uint32_t)__float_as_int(r2.x);
         w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
     }
-    uint2 v, m;
+    uint2 v, mr;
     v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
     v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
-    m.x = __byte_perm(v.y, 0, 0x0123);  // bytes 7..4 of v
-    m.y = __byte_perm(v.x, 0, 0x0123);  // bytes 3..0 of v
+    mr.x = __byte_perm(v.y, 0, 0x0123);
+    mr.y = __byte_perm(v.x, 0, 0x0123);
+    const size_t off = (size_t)L * lstride;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? m : v;
+    for (int q = 0; q < NS; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? mr : v;
+    store_res8_slots<NS>(u, out, lstride, std::integer_sequence<int, Ls...>{});
 }
-template <int... L>
-__device__ __forceinline__ void store_all_residues8_mirror(const float2 (&u)[4][3], int8_t* const (&out)[8],
-                                                           size_t lstride, std::integer_sequence<int, L...>) {
-    (store_residues8_mirror<L>(u, out, (size_t)L * lstride), ...);
-}
-__device__ __forceinline__ bool residues8_mirror(const double* v, double sa, double sb, int8_t* const (&out)[8],
-                                                 size_t lstride, double lim) {
+
+// Residues of the 8 values v, stored at NS slots (odd slots byte-reversed).
+template <int NS>
+__device__ __forceinline__ bool residues8_slots(const double* v, double sa, double sb, int8_t* const (&out)[NS],
+                                                size_t lstride, double lim) {
     float2 u[4][3];
     constexpr double M2 = 5629508124213248.0;
     bool ok = true;
@@ -489,7 +432,7 @@ __device__ __forceinline__ bool residues8_mirror(const double* v, double sa, dou
             u[e >> 1][2].x = f2;
         }
     }
-    store_all_residues8_mirror(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    store_res8_slots<NS>(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
     return ok;
 }
 
@@ -1261,7 +1204,10 @@ __global__ void __launch_bounds__(256, 4) k_i8_residues_all(const double* __rest
         for (int u = 0; u < 8; ++u) x[u] = sb[ra_swz(8 * lane + u)];
         __syncwarp();
         const int64_t base = c * RA_CH;
-        if (base + 8 * lane < N) ok &= residues8(x, sa, sbb, R + base + 8 * lane, (size_t)N, lim);
+        if (base + 8 * lane < N) {
+            int8_t* const out[1] = {R + base + 8 * lane};
+            ok &= residues8_slots<1>(x, sa, sbb, out, (size_t)N, lim);
+        }
     }
     if (!ok) atomicExch(bad, 1);
 }
@@ -1429,7 +1375,7 @@ __global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const doubl
             out[2 * w] = R + rows[w] * n3 + k0;
             out[2 * w + 1] = R + rows[w] * n3 + (n3 - 8 - k0);
         }
-        ok &= residues8_mirror(v, sa, sbb, out, N, lim);
+        ok &= residues8_slots<8>(v, sa, sbb, out, N, lim);
     }
     if (!ok) atomicExch(bad, 1);
 }
@@ -1510,70 +1456,6 @@ int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w,
 // and on centred grids every evaluation and residue conversion serves 4 mirrored positions (the
 // chunk's free axis and k).  Integer partial sums are exact in any order: the Grams are bitwise
 // those of the materialised shared route on the same values.
-template <int NS>
-__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
-                                                 std::integer_sequence<int>) {}
-template <int NS, int L, int... Ls>
-__device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
-                                                 std::integer_sequence<int, L, Ls...>) {
-    constexpr int p = kMod(L);
-    constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
-    constexpr float fp = (float)p, inv = 1.0f / (float)p;
-    const float2 C1 = make_float2(c1, c1), C2 = make_float2(c2, c2), INV = make_float2(inv, inv);
-    const float2 MG = make_float2(12582912.f, 12582912.f), NMG = make_float2(-12582912.f, -12582912.f);
-    const float2 NP = make_float2(-fp, -fp);
-    uint32_t w[8];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const float2 s2 = __ffma2_rn(u[e][2], C2, __ffma2_rn(u[e][1], C1, u[e][0]));
-        const float2 q2 = __fadd2_rn(__ffma2_rn(s2, INV, MG), NMG);
-        const float2 r2 = __fadd2_rn(__ffma2_rn(q2, NP, s2), MG);
-        w[2 * e] = (uint32_t)__float_as_int(r2.x);
-        w[2 * e + 1] = (uint32_t)__float_as_int(r2.y);
-    }
-    uint2 v, mr;
-    v.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
-    v.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
-    mr.x = __byte_perm(v.y, 0, 0x0123);
-    mr.y = __byte_perm(v.x, 0, 0x0123);
-    const size_t off = (size_t)L * lstride;
-#pragma unroll
-    for (int q = 0; q < NS; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? mr : v;
-    store_res8_slots<NS>(u, out, lstride, std::integer_sequence<int, Ls...>{});
-}
-
-// Residues of the 8 values v, stored at NS slots (odd slots byte-reversed).
-template <int NS>
-__device__ __forceinline__ bool residues8_slots(const double* v, double sa, double sb, int8_t* const (&out)[NS],
-                                                size_t lstride, double lim) {
-    float2 u[4][3];
-    constexpr double M2 = 5629508124213248.0;
-    bool ok = true;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const double x = v[e];
-        const double y = (sb == 1.0) ? fma(x, sa, M2) : fma(x * sa, sb, M2);
-        ok &= fabs(y - M2) <= lim;
-        const uint32_t lo = (uint32_t)__double2loint(y);
-        const uint32_t hi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
-        const uint32_t d0 = lo & 0x1FFFFu, d1 = __funnelshift_r(lo, hi, 17) & 0x1FFFFu, d2 = hi >> 2;
-        const float f0 = __int_as_float(0x4B000000 | d0) - (8388608.f + 65536.f);
-        const float f1 = __int_as_float(0x4B000000 | d1) - (8388608.f + 65536.f);
-        const float f2 = __int_as_float(0x4B000000 | d2) - (8388608.f + 65536.f);
-        if (e & 1) {
-            u[e >> 1][0].y = f0;
-            u[e >> 1][1].y = f1;
-            u[e >> 1][2].y = f2;
-        } else {
-            u[e >> 1][0].x = f0;
-            u[e >> 1][1].x = f1;
-            u[e >> 1][2].x = f2;
-        }
-    }
-    store_res8_slots<NS>(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
-    return ok;
-}
-
 // Residues of planes [p0, p0 + pc) of axis ax (0: i, 1: j) into the chunk tensor R (dims
 // c = (pc, n2, n3) or (n1, pc, n3), one byte plane per modulus of c0 c1 c2 bytes).  MIR (centred
 // grids, n3 % 16 == 0): items over half the free axis and half of k, 4 slots per evaluation.
