@@ -1311,17 +1311,28 @@ int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, cha
 // residue ALU work falls 8-fold and F is never re-read.  The global exponent comes first from the
 // smallest radius: C(r) (Matérn, p-Slater, spectral density) decreases in r, so max F = C(r_min)
 // evaluated bitwise as the fill evaluates it (any value beyond the window still trips the flag).
-__global__ void k_i8_gmax_eval(KParams kp, const double* __restrict__ cheb, const double* __restrict__ x2,
-                               int64_t n1, int64_t n2, int64_t n3, uint32_t* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double m[3] = {INFINITY, INFINITY, INFINITY};
+__global__ void __launch_bounds__(256) k_i8_gmax_eval(KParams kp, const double* __restrict__ cheb,
+                                                      const double* __restrict__ x2, int64_t n1, int64_t n2,
+                                                      int64_t n3, uint32_t* __restrict__ out) {
+    __shared__ double red[3][8];
     const int64_t nn[3] = {n1, n2, n3};
     const double* xa = x2;
-    for (int a = 0; a < 3; ++a) {
-        for (int64_t i = 0; i < nn[a]; ++i) m[a] = fmin(m[a], xa[i]);
+    double m3[3];
+    for (int a = 0; a < 3; ++a) {  // min of each axis' squared nodes (block reduction)
+        double m = INFINITY;
+        for (int64_t i = threadIdx.x; i < nn[a]; i += blockDim.x) m = fmin(m, xa[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) red[a][threadIdx.x >> 5] = m;
         xa += nn[a];
     }
-    const double v = eval_point(kp, cheb, __dadd_rn(__dadd_rn(m[0], m[1]), m[2]));
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int a = 0; a < 3; ++a) {
+        m3[a] = red[a][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m3[a] = fmin(m3[a], red[a][w]);
+    }
+    const double v = eval_point(kp, cheb, __dadd_rn(__dadd_rn(m3[0], m3[1]), m3[2]));
     out[0] = (uint32_t)__double2hiint(v) & 0x7FFFFFFFu;
 }
 
@@ -1387,7 +1398,7 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
     const KParams kp = make_kparams(kn);
     TK_RC(launch_fill_prep(g, kn, kp, nodes_x2, cheb, st));
     uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
-    k_i8_gmax_eval<<<1, 32, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, gw);
+    k_i8_gmax_eval<<<1, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, gw);
     TK_CHECK_LAUNCH();
     const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 16);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16));
@@ -1569,7 +1580,7 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
     uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
     int* flag = reinterpret_cast<int*>(base + w.off_flag);
     TK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    k_i8_gmax_eval<<<1, 32, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2], gw);  // max F = C(r_min)
+    k_i8_gmax_eval<<<1, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2], gw);  // max F = C(r_min)
     TK_CHECK_LAUNCH();
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
     int16_t* P = reinterpret_cast<int16_t*>(base + w.off_P);

@@ -1,6 +1,6 @@
 """One small driver for the ncu captures under profiles/ (run under ncu on the GPU box):
 
-    python tools/profile_driver.py step [n] [r]        fill_rowmax + hosvd_rowmax + error (the bench step)
+    python tools/profile_driver.py step [n] [r]        fill_prepare + hosvd_prepared + error (the bench step)
     python tools/profile_driver.py fill NU [n]          the general-nu K_nu fill (Chebyshev table route)
     python tools/profile_driver.py als [n] [r]          HOSVD + one Tucker-ALS sweep
     python tools/profile_driver.py accurate [n] [r]     the SVD-accurate HOSVD (f2)
@@ -45,9 +45,9 @@ def main():
     F, mx = T.fill_rowmax(g, k)
     ws = T.workspace(g, rr)
     for _ in range(2 if warm else 1):
-        if what == "step":
-            T.fill_rowmax(g, k, F)
-            res = T.hosvd(g, rr, F, ws, rowmax=mx, sync=False)
+        if what == "step":  # the bench step: fill + shared residues, prepared HOSVD, error
+            T.fill_prepare(g, k, rr, F, ws)
+            res = T.hosvd_prepared(g, rr, F, ws)
             T.error(g, rr, F, res.U, res.core, ws)
         elif what == "als":
             res = T.hosvd(g, rr, F, ws)
