@@ -201,3 +201,22 @@ def test_fused_2048_config5f(T, orc):
     assert abs(np.trace(Gn) - nF ** 2) <= 1e-12 * nF ** 2
     # same function, twice the resolution: the relative truncation error is of the same size
     assert 1e-9 < e[0] < 1e-6, e
+
+
+@pytest.mark.parametrize("g,k,kb", [
+    (GridSpec((96, 80, 64), (-0.5, -2.0, 0.1), (1.5, 1.0, 0.9)), KernelSpec.matern(1.5, 0.2), 200),   # off-centre: no mirrors
+    (GridSpec((129, 131, 64), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)), KernelSpec.matern(0.7, 0.3), 300),  # odd free axes
+    (GridSpec((40, 24, 16), (-1.0,) * 3, (1.0,) * 3), KernelSpec.slater(1.0, 0.2), None),               # n3 = 16, 1 chunk
+    (GridSpec((2, 3, 32), (-1.0,) * 3, (1.0,) * 3), KernelSpec.spectral(0.1, 0.4), None)])              # tiny axes
+def test_gram_fused_shared_bitwise_equals_materialised(T, chunk_kb, g, k, kb):
+    """The default fused INT8 route on the shared layout (R20): plane chunks of residues generated
+    from the kernel (i-chunks for modes 1, 2; j-chunks for mode 0; mirrored on centred grids, plain
+    on off-centre ones) give bitwise the Grams of the materialised shared route on the same values
+    (the same global exponent, exact integer sums) — many chunks through the test knob."""
+    chunk_kb(kb)
+    assert T.i8_layout(g)[0]
+    F = T.fill(g, k)
+    ws = T.workspace_i8(g)
+    wsf = T.workspace_fused(g)
+    for m in range(3):
+        assert torch.equal(T.gram_fused(g, k, m, wsf), T.gram_i8(g, m, F, ws)), m

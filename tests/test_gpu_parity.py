@@ -306,3 +306,19 @@ def test_fill_rowmax_and_hosvd_rowmax(T, g):
     with pytest.raises(T.TuckerError) as e:
         T.fill_rowmax(off_grid, k)
     assert e.value.code == 7
+
+
+@pytest.mark.parametrize("g,k,r", [(GridSpec((2, 3, 16), (-1.0,) * 3, (1.0,) * 3), KernelSpec.matern(1.5, 0.5), (2, 3, 4)),
+                                   (GridSpec((5, 7, 32), (-1.0,) * 3, (1.0,) * 3), KernelSpec.matern(0.5, 0.3), (3, 4, 5)),
+                                   (GridSpec((33, 17, 48), (-2.0, -0.5, -1.0), (1.0, 1.5, 1.0)), KernelSpec.slater(5.0, 1.0), (6, 5, 7))])
+def test_shared_layout_tiny_and_offcentre_vs_oracle(T, orc, g, k, r):
+    """The shared INT8 residue layout (n3 % 16 == 0) on tiny and off-centre grids — through
+    tucker_fill_prepare where it applies (centred), tucker_hosvd otherwise — against the oracle."""
+    assert T.i8_layout(g)[0]
+    _compare_hosvd(T, orc, g, k, r)
+    centred = all(lo == -hi for lo, hi in zip(g.lo, g.hi))
+    if centred:
+        F, ws = T.fill_prepare(g, k, r)
+        a = T.hosvd_prepared(g, r, F, ws)
+        b = T.hosvd(g, r, F)
+        assert torch.equal(a.core, b.core)
