@@ -532,7 +532,7 @@ struct GemmArgs {
     int nJ;          // column blocks of PN
     int ntiles;      // lower-triangle pair tiles
     int nug;         // units per (modulus, K-chunk) group
-    int nchunks;     // K-chunks of KCH in this super-chunk
+    int nchunks;     // units' K-chunks (kbu K-blocks each) in this launch
     int nunits;      // NMOD * nchunks * nug
     int64_t Kc;      // K of this super-chunk
     int16_t* P;      // partials mod p_l, [(l * nchunks + c) * ntiles + t][PN][PM]
@@ -540,7 +540,8 @@ struct GemmArgs {
     int lay;         // residue layout: 0 per-mode K-block-major [l][kb][row][128]; shared natural
                      // layout [l][i][j][k] read as mode 0 (1), mode 1 (2), mode 2 MN-major (3)
     int nb3;         // lay 2: K-blocks per i-slab (ceil(n3 / 128); the rest of the last is zero-filled)
-    int64_t nkb_total;  // K-blocks of this launch (the exact-int32 chunks hold KCH / BKB of them)
+    int64_t nkb_total;  // K-blocks of this launch
+    int kbu;            // K-blocks per unit (<= KCH / BKB: one exact int32 chunk)
 };
 
 __host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
@@ -733,8 +734,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             uint32_t ph = 0;
             for (int u = pair; u < g.nunits; u += npairs) {
                 const Unit x = unit_of(u, g);
-                const int64_t kbeg = (int64_t)x.c * (KCH / BKB);  // first K-block of the chunk
-                const int nkb = (int)min(KCH / BKB, g.nkb_total - kbeg);
+                const int64_t kbeg = (int64_t)x.c * g.kbu;  // first K-block of the chunk
+                const int nkb = (int)min((int64_t)g.kbu, g.nkb_total - kbeg);
                 const int nsub = x.merged ? 2 : 1;
                 for (int kb = 0; kb < nkb; ++kb) {
                     const int kx = (int)kbeg + kb;  // K-block index
@@ -769,8 +770,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             const uint32_t kstep = mn ? 32u * BKB : 32u;
             for (int u = pair; u < g.nunits; u += npairs, ++it) {
                 const Unit x = unit_of(u, g);
-                const int64_t kbeg = (int64_t)x.c * (KCH / BKB);
-                const int nkb = (int)min(KCH / BKB, g.nkb_total - kbeg);
+                const int64_t kbeg = (int64_t)x.c * g.kbu;
+                const int nkb = (int)min((int64_t)g.kbu, g.nkb_total - kbeg);
                 const uint32_t id0 = idesc_i8(PM, x.s[0].N, mn), id1 = idesc_i8(PM, x.s[1].N, mn);
                 const int nsub = x.merged ? 2 : 1;
                 mbar_wait_cluster(&tempty, (it & 1) ^ 1);
@@ -1059,7 +1060,7 @@ struct ModeGemm {
             return TUCKER_ERR_CUDA;
         const int nchunks = (int)ceil_div(Kc, KCH);
         GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nug, nchunks, NMOD * nchunks * nug, Kc, P, utab, 0, 1,
-                    ceil_div(Kc, (int64_t)BKB)};
+                    ceil_div(Kc, (int64_t)BKB), (int)(KCH / BKB)};
         const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
         {
             TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1233,6 +1234,33 @@ inline int64_t shared_nkb(const int64_t n[3], int m) {  // K-blocks of mode m in
     return ceil_div(n[0] * n[1] * n[2] / n[m], (int64_t)BKB);
 }
 
+// K-blocks per k_i8_gemm unit over nkb K-blocks of `rows` rows: the largest of 512 / 256 / 128
+// (512 = one exact int32 chunk) within ~1 % of the best modelled time — whole rounds of the CTA
+// pairs, each a unit's K-blocks plus ~4 K-blocks of epilogue hand-over (the last round is mostly
+// idle when the unit count falls just past a multiple of the pairs).  Env TUCKER_I8_UNIT_KB fixes it.
+inline int unit_kblocks(int64_t nkb, int rows) {
+    static const int fixed = [] {
+        const char* e = std::getenv("TUCKER_I8_UNIT_KB");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (fixed == 128 || fixed == 256 || fixed == 512) return fixed;
+    int nJ;
+    const int nt = count_tiles(rows, nJ);
+    const int64_t nug = build_units(rows, nJ, nt, nullptr);
+    const int64_t npairs = kNumSMs / 2;
+    double t[3], best = 1e300;
+    for (int q = 0; q < 3; ++q) {
+        const int64_t kbu = 512 >> q;
+        const int64_t rounds = ceil_div(NMOD * ceil_div(nkb, kbu) * nug, npairs);
+        t[q] = (double)rounds * (double)(std::min(kbu, nkb) + 4);
+        best = std::min(best, t[q]);
+    }
+    int pick = 128;
+    for (int q = 2; q >= 0; --q)
+        if (t[q] <= 1.01 * best) pick = 512 >> q;
+    return pick;
+}
+
 SharedPlan shared_plan(const int64_t n[3]) {
     SharedPlan w{};
     const int64_t N = n[0] * n[1] * n[2];
@@ -1242,7 +1270,7 @@ SharedPlan shared_plan(const int64_t n[3]) {
         Kmax = std::max(Kmax, N / n[m]);
         int nJ;
         const int nt = count_tiles(n[m], nJ);
-        const int64_t nch = ceil_div(shared_nkb(n, m), KCH / BKB);
+        const int64_t nch = ceil_div(shared_nkb(n, m), (int64_t)unit_kblocks(shared_nkb(n, m), (int)n[m]));
         pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
         ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
         ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
@@ -1411,7 +1439,7 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
 
 // The int8 Grams of mode m over one residue tensor in the shared (natural) layout with dims c[3]
 // (the whole tensor, or a plane chunk of it whose mode-m rows are complete): one k_i8_gemm launch
-// over all its K (exact int32 per KCH columns) and the fold into Racc (first: Racc starts at 0).
+// over all its K (exact int32 per unit of <= KCH columns) and the fold into Racc (first: Racc starts at 0).
 int shared_gemm(const int64_t c[3], int m, const int8_t* R, int16_t* P, int32_t* Racc, int2* utab, bool first,
                 cudaStream_t st) {
     int nJ;
@@ -1424,9 +1452,10 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int16_t* P, int32_t*
     CUtensorMap map;
     TK_RC(shared_map(&map, c, m, const_cast<int8_t*>(R)));
     const int64_t nkb = shared_nkb(c, m);
-    const int nchunks = (int)ceil_div(nkb, KCH / BKB);
+    const int kbu = unit_kblocks(nkb, rows);
+    const int nchunks = (int)ceil_div(nkb, (int64_t)kbu);
     GemmArgs ga{rows, nJ, ntiles, nug, nchunks, NMOD * nchunks * nug, nkb * BKB, P, utab, m + 1,
-                (int)ceil_div(c[2], (int64_t)BKB), nkb};
+                (int)ceil_div(c[2], (int64_t)BKB), nkb, kbu};
     const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);
     {
         TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1537,14 +1566,18 @@ FusedSharedPlan fused_shared_plan(const int64_t n[3]) {
     w.pc[0] = std::min<int64_t>(n[0], std::max<int64_t>(1, target / (8 * n[1] * n[2])));
     w.pc[1] = std::min<int64_t>(n[1], std::max<int64_t>(1, target / (8 * n[0] * n[2])));
     size_t rb = 0, pb = 0, ab = 0, ub = 0;
-    for (int ax = 0; ax < 2; ++ax) {
-        const int64_t c[3] = {ax == 0 ? w.pc[0] : n[0], ax == 0 ? n[1] : w.pc[1], n[2]};
+    for (int q = 0; q < 4; ++q) {  // full chunks and the last (ragged) chunk of either axis: the
+        const int ax = q & 1;          // unit length (hence the partials' size) follows the chunk's K
+        const int64_t planes = ax == 0 ? n[0] : n[1];
+        const int64_t pcc = q < 2 ? w.pc[ax] : planes % w.pc[ax];
+        if (pcc == 0) continue;
+        const int64_t c[3] = {ax == 0 ? pcc : n[0], ax == 0 ? n[1] : pcc, n[2]};
         rb = std::max(rb, align_up((size_t)NMOD * c[0] * c[1] * c[2], 1024));
         for (int m = 0; m < 3; ++m) {
             if ((ax == 0) != (m != 0)) continue;
             int nJ;
             const int nt = count_tiles(c[m], nJ);
-            const int64_t nch = ceil_div(shared_nkb(c, m), KCH / BKB);
+            const int64_t nch = ceil_div(shared_nkb(c, m), (int64_t)unit_kblocks(shared_nkb(c, m), (int)c[m]));
             pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
             ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
             ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
