@@ -670,7 +670,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 // [tcol, tcol + N) and tile t of the partials.
 struct Stream {
     int arow, brow, N, tcol, t;
+    bool diag;  // B rows == A rows (a diagonal block, N = 256): each CTA's B box is its A box
 };
+__device__ __forceinline__ Stream make_stream(int arow, int brow, int N, int tcol, int t) {
+    return Stream{arow, brow, N, tcol, t, brow == arow && N == 256};
+}
 struct Unit {
     int l, c, ns, merged;
     Stream s[2];
@@ -687,14 +691,14 @@ __device__ __forceinline__ Unit unit_of(int u, const GemmArgs& g) {
     x.merged = tt.y >= 0;
     if (!x.merged) {
         x.ns = N > 256 ? 2 : 1;
-        x.s[0] = Stream{I * PM, J * PN, min(N, 256), 0, tt.x};
-        x.s[1] = Stream{I * PM, J * PN + 256, N > 256 ? N - 256 : 32, 256, tt.x};
+        x.s[0] = make_stream(I * PM, J * PN, min(N, 256), 0, tt.x);
+        x.s[1] = make_stream(I * PM, J * PN + 256, N > 256 ? N - 256 : 32, 256, tt.x);
     } else {
         int I2, J2;
         tile_of(tt.y, g.nJ, I2, J2);
         x.ns = 2;
-        x.s[0] = Stream{I * PM, J * PN, N, 0, tt.x};
-        x.s[1] = Stream{I2 * PM, J2 * PN, tile_cols(I2, J2, g.n), 256, tt.y};
+        x.s[0] = make_stream(I * PM, J * PN, N, 0, tt.x);
+        x.s[1] = make_stream(I2 * PM, J2 * PN, tile_cols(I2, J2, g.n), 256, tt.y);
     }
     return x;
 }
@@ -744,11 +748,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                         mbar_wait(&empty[stage], ph ^ 1);
                         uint8_t* sA = smem + stage * STAGE_BYTES;
                         const uint32_t fl = leader_addr(&full[stage]);
+                        // boxes: A, then B of stream 0 (or of this merged sub-stream) and B of
+                        // stream 1 — a diagonal block's B box is its A box and is not loaded again
                         const bool two_b = !x.merged && x.ns == 2;
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (two_b ? 3u : 2u) * BOX);
+                        const bool ld_b0 = !s0.diag, ld_b1 = two_b && !x.s[1].diag;
+                        if (rank == 0)
+                            mbar_arrive_expect_tx(&full[stage], 2u * (1u + (ld_b0 ? 1u : 0u) + (ld_b1 ? 1u : 0u)) * BOX);
                         tma_load_res_pair(sA, &map, fl, x.l, kx, s0.arow + (int)rank * 128, g.lay, g.nb3);
-                        tma_load_res_pair(sA + BOX, &map, fl, x.l, kx, s0.brow + (int)rank * (s0.N / 2), g.lay, g.nb3);
-                        if (two_b)
+                        if (ld_b0)
+                            tma_load_res_pair(sA + BOX, &map, fl, x.l, kx, s0.brow + (int)rank * (s0.N / 2), g.lay, g.nb3);
+                        if (ld_b1)
                             tma_load_res_pair(sA + 2 * BOX, &map, fl, x.l, kx, x.s[1].brow + (int)rank * (x.s[1].N / 2),
                                               g.lay, g.nb3);
                         if (++stage == STAGES) {
@@ -781,17 +790,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                         mbar_wait(&full[stage], ph);
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+                        const uint32_t b0 = x.s[x.merged ? sub : 0].diag ? a0 : a0 + BOX;
+                        const uint32_t b1 = x.s[1].diag ? a0 : a0 + 2 * BOX;
 #pragma unroll
                         for (int k = 0; k < BKB / 32; ++k) {
                             const uint32_t acc = (kb | k) ? 1u : 0u;
                             const uint64_t da = umma_desc_sw128(a0 + kstep * k);
                             if (x.merged) {
-                                umma_i8_pair(tmem + 256 * sub, da, umma_desc_sw128(a0 + BOX + kstep * k), sub ? id1 : id0,
-                                             acc);
+                                umma_i8_pair(tmem + 256 * sub, da, umma_desc_sw128(b0 + kstep * k), sub ? id1 : id0, acc);
                             } else {
-                                umma_i8_pair(tmem, da, umma_desc_sw128(a0 + BOX + kstep * k), id0, acc);
-                                if (x.ns == 2)
-                                    umma_i8_pair(tmem + 256, da, umma_desc_sw128(a0 + 2 * BOX + kstep * k), id1, acc);
+                                umma_i8_pair(tmem, da, umma_desc_sw128(b0 + kstep * k), id0, acc);
+                                if (x.ns == 2) umma_i8_pair(tmem + 256, da, umma_desc_sw128(b1 + kstep * k), id1, acc);
                             }
                         }
                         umma_commit_pair(&empty[stage]);
