@@ -535,7 +535,7 @@ struct GemmArgs {
     int nchunks;     // units' K-chunks (kbu K-blocks each) in this launch
     int nunits;      // NMOD * nchunks * nug
     int64_t Kc;      // K of this super-chunk
-    int16_t* P;      // partials mod p_l, [(l * nchunks + c) * ntiles + t][PN][PM]
+    int8_t* P;       // partials mod p_l in [-p/2, p/2], [(l * nchunks + c) * ntiles + t][PN][PM]
     const int2* utab;  // unit v of a group: tiles (ta, tb), tb = -1 unless two half tiles are merged
     int lay;         // residue layout: 0 per-mode K-block-major [l][kb][row][128]; shared natural
                      // layout [l][i][j][k] read as mode 0 (1), mode 1 (2), mode 2 MN-major (3)
@@ -832,7 +832,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                 const int t = x.s[sg].t;
                 const int N = x.merged ? x.s[sg].N : (x.ns == 2 ? 256 + x.s[1].N : x.s[0].N);
                 const uint32_t tc0 = x.merged ? 256u * sg : 0u;
-                int16_t* P = g.P + ((size_t)(x.l * g.nchunks + x.c) * g.ntiles + t) * (PN * PM);
+                int8_t* P = g.P + ((size_t)(x.l * g.nchunks + x.c) * g.ntiles + t) * (PN * PM);
                 for (int c0 = 0; c0 < N; c0 += 32) {
                     uint32_t v[32];
                     asm volatile(
@@ -845,13 +845,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                           "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(taddr + tc0 + c0));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    // exact int32 chunk sum -> a representative mod p in (-p, p) (int16: half the
-                    // partials traffic); v - p rint(v / p) with the quotient from FP64 (|v| < 2^31)
+                    // exact int32 chunk sum -> its balanced representative mod p, v - p rint(v / p)
+                    // in [-p/2, p/2] (|.| <= 126: one byte), the quotient from FP64 (|v| < 2^31)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int vi = (int)v[j];
                         const int q = __double2int_rn((double)vi * invp);
-                        P[(size_t)(c0 + j) * PM + row] = (int16_t)(vi - q * pmod);
+                        P[(size_t)(c0 + j) * PM + row] = (int8_t)(vi - q * pmod);
                     }
                 }
             }
@@ -871,19 +871,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 
 // ------------------------------------------------------------------------------------------
 // 2b. fold the chunk partials: Racc[l][t][col][row] = (Racc + sum_c P) mod p_l  (Racc in [0, p))
-__global__ void __launch_bounds__(256) k_i8_reduce(const int16_t* __restrict__ P, int32_t* __restrict__ Racc,
+__global__ void __launch_bounds__(256) k_i8_reduce(const int8_t* __restrict__ P, int32_t* __restrict__ Racc,
                                                    int ntiles, int nchunks, int first) {
-    const int64_t per = (int64_t)ntiles * PN * PM;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)ntiles * PN * PM;  // a multiple of 16
+    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16;  // 16 consecutive rows
     if (idx >= per * NMOD) return;
     const int l = (int)(idx / per);
     const int64_t e = idx - (int64_t)l * per;  // t * PN*PM + col*PM + row
-    int s = first ? 0 : Racc[idx];            // |s| <= p (nchunks + 1) << 2^31
-    for (int c = 0; c < nchunks; ++c) s += P[((int64_t)l * nchunks + c) * per + e];
+    int s[16];                                 // |s| <= p + 126 nchunks << 2^31
+    int4* ra = reinterpret_cast<int4*>(Racc + idx);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int4 v = first ? make_int4(0, 0, 0, 0) : ra[q];
+        s[4 * q] = v.x;
+        s[4 * q + 1] = v.y;
+        s[4 * q + 2] = v.z;
+        s[4 * q + 3] = v.w;
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const int4 w = *reinterpret_cast<const int4*>(P + ((int64_t)l * nchunks + c) * per + e);
+        const int wd[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s[q] += (int)(signed char)(wd[q >> 2] >> (8 * (q & 3)));
+    }
     const int p = c_mod[l];
-    int r = s - p * __double2int_rn((double)s * c_invmod[l]);  // in [-p/2 - 1, p/2 + 1]
-    r += r < 0 ? p : 0;
-    Racc[idx] = r >= p ? r - p : r;
+    const double ip = c_invmod[l];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        int r = s[q] - p * __double2int_rn((double)s[q] * ip);  // in [-p/2 - 1, p/2 + 1]
+        r += r < 0 ? p : 0;
+        s[q] = r >= p ? r - p : r;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ra[q] = make_int4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
 }
 
 template <int L, int Q>
@@ -1006,7 +1026,7 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     auto add = [&](const ModePlan& p) {
         rb = std::max(rb, align_up((size_t)NMOD * p.rows * p.ldr, 1024));
         const int64_t nch = ceil_div(p.Ksc, KCH);
-        pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM * 2, 256));
+        pb = std::max(pb, align_up((size_t)NMOD * nch * p.ntiles * PN * PM, 256));
         ab = std::max(ab, align_up((size_t)NMOD * p.ntiles * PN * PM * 4, 256));
         ub = std::max(ub, align_up((size_t)p.ntiles * sizeof(int2), 256));
     };
@@ -1039,7 +1059,7 @@ struct ModeGemm {
     ModePlan p;
     const uint32_t* mxm;
     int8_t* R;
-    int16_t* P;
+    int8_t* P;
     int32_t* Racc;
     int2* utab;
     int nug;
@@ -1078,7 +1098,7 @@ struct ModeGemm {
         }
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
-        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, first ? 1 : 0);
+        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, first ? 1 : 0);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1091,7 +1111,7 @@ struct ModeGemm {
         TK_CUDA(cudaStreamSynchronize(st));
         if (sh.allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
         TK_PROF(TUCKER_PROF_I8_CRT, st);
-        k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(nullptr, Racc, p.ntiles, 0, 0);
+        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, p.ntiles, 0, 0);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1115,7 +1135,7 @@ template <class Produce>
 int gram_mode_impl(const int64_t n[3], int m, const ModePlan& p, const uint32_t* mx, char* base, const WsPlan& w,
                    double* G, cudaStream_t st, Produce&& produce, const Shard* shard = nullptr) {
     ModeGemm g{n, m, p, mode_max(mx, n, m), reinterpret_cast<int8_t*>(base + w.off_R),
-               reinterpret_cast<int16_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
+               reinterpret_cast<int8_t*>(base + w.off_P), reinterpret_cast<int32_t*>(base + w.off_Racc),
                reinterpret_cast<int2*>(base + w.off_utab), 0, st, reinterpret_cast<int*>(base + w.off_flag)};
     TK_RC(g.init());
     bool first = true;
@@ -1280,7 +1300,7 @@ SharedPlan shared_plan(const int64_t n[3]) {
         int nJ;
         const int nt = count_tiles(n[m], nJ);
         const int64_t nch = ceil_div(shared_nkb(n, m), (int64_t)unit_kblocks(shared_nkb(n, m), (int)n[m]));
-        pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
+        pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM, 256));
         ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
         ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
     }
@@ -1449,7 +1469,7 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
 // The int8 Grams of mode m over one residue tensor in the shared (natural) layout with dims c[3]
 // (the whole tensor, or a plane chunk of it whose mode-m rows are complete): one k_i8_gemm launch
 // over all its K (exact int32 per unit of <= KCH columns) and the fold into Racc (first: Racc starts at 0).
-int shared_gemm(const int64_t c[3], int m, const int8_t* R, int16_t* P, int32_t* Racc, int2* utab, bool first,
+int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* Racc, int2* utab, bool first,
                 cudaStream_t st) {
     int nJ;
     const int rows = (int)c[m];
@@ -1473,7 +1493,7 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int16_t* P, int32_t*
     }
     TK_PROF(TUCKER_PROF_I8_CRT, st);
     const int64_t tot = (int64_t)NMOD * ntiles * PN * PM;
-    k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, first ? 1 : 0);
+    k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, first ? 1 : 0);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
@@ -1493,7 +1513,7 @@ int shared_crt(int64_t nm, const int32_t* Racc, const uint32_t* gmax, int b, con
 // G_m from the shared residues of the whole tensor.
 int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
     int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
-    TK_RC(shared_gemm(n, m, reinterpret_cast<const int8_t*>(base + w.off_R), reinterpret_cast<int16_t*>(base + w.off_P),
+    TK_RC(shared_gemm(n, m, reinterpret_cast<const int8_t*>(base + w.off_R), reinterpret_cast<int8_t*>(base + w.off_P),
                       Racc, reinterpret_cast<int2*>(base + w.off_utab), true, st));
     return shared_crt(n[m], Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
                       reinterpret_cast<const int*>(base + w.off_flag), G, st);
@@ -1587,7 +1607,7 @@ FusedSharedPlan fused_shared_plan(const int64_t n[3]) {
             int nJ;
             const int nt = count_tiles(c[m], nJ);
             const int64_t nch = ceil_div(shared_nkb(c, m), (int64_t)unit_kblocks(shared_nkb(c, m), (int)c[m]));
-            pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM * 2, 256));
+            pb = std::max(pb, align_up((size_t)NMOD * nch * nt * PN * PM, 256));
             ab = std::max(ab, align_up((size_t)NMOD * nt * PN * PM * 4, 256));
             ub = std::max(ub, align_up((size_t)nt * sizeof(int2), 256));
         }
@@ -1625,7 +1645,7 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
     k_i8_gmax_eval<<<1, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2], gw);  // max F = C(r_min)
     TK_CHECK_LAUNCH();
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
-    int16_t* P = reinterpret_cast<int16_t*>(base + w.off_P);
+    int8_t* P = reinterpret_cast<int8_t*>(base + w.off_P);
     int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
     const bool mir = gen.kp.centred != 0;
     for (int ax = 0; ax < 2; ++ax) {  // i-chunks for modes 1, 2; then j-chunks for mode 0
@@ -1668,7 +1688,7 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
                 TK_CUDA(cudaStreamSynchronize(st));
                 if (shard->allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
                 TK_PROF(TUCKER_PROF_I8_CRT, st);
-                k_i8_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0);
+                k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0);
                 TK_CHECK_LAUNCH();
             }
             TK_RC(shared_crt(n[m], Racc, gw, w.b, flag, G, st));
