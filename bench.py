@@ -353,6 +353,9 @@ def run_ours(args, rank, world, local):
         roof = {"bound": "tensor", "kernel": "k_i8_gemm (tcgen05 kind::i8, CTA pairs), per launch",
                 "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "traffic": traffic,
                 "executed_over_algorithmic_macs": exec_ratio, "frac_executed": achieved * exec_ratio / peak,
+                "frac_executed_note": "int8 ops the tensor cores execute (the diagonal pair tiles' upper halves "
+                                      "included) over the same peak; above 1 when the int8 MMAs hold a higher "
+                                      "power-capped clock than the bf16 cuBLAS loop behind the sustained figure",
                 "peak_source": peak_src, "ops_per_launch": ops_launch, "launch_ms": launch_ms,
                 "launches_per_step": calls["i8_gemm"],
                 "fp64_equivalent_gram_tflops": gram_flops_fp64 / (gram_stage_ms * 1e-3) / 1e12,
