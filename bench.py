@@ -67,59 +67,109 @@ def dist_env():
 
 # ----------------------------------------------------------------------------------- clocks ----
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and clock-event reasons sampled every ~10 ms through NVML (nvidia-smi's 100 ms loop
+    as the fallback).  Started before the warm-up, it keeps only the samples taken between
+    mark_start() and mark_end() (host clock; the step is host-synchronous) — the timed region."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.samples = []  # (host time, sm MHz, max MHz, set of reasons)
+        self.t_start = self.t_end = None
+        self.stop = threading.Event()
+        self.thread = None
+
+    def mark_start(self):
+        self.t_start = time.time()
+
+    def mark_end(self):
+        self.t_end = time.time()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        return pynvml, h
+
+    def _poll_nvml(self):
+        nv, h = self.nvml
+        bits = [(nv.nvmlClocksEventReasonHwSlowdown, "hw_slowdown"),
+                (nv.nvmlClocksEventReasonHwThermalSlowdown, "hw_thermal_slowdown"),
+                (nv.nvmlClocksEventReasonSwThermalSlowdown, "sw_thermal_slowdown"),
+                (nv.nvmlClocksEventReasonSwPowerCap, "sw_power_cap")]
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                m = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((time.time(), sm, mx, {nm for bit, nm in bits if m & bit}))
+            except Exception:
+                pass
+            self.stop.wait(0.01)
+
+    def _read_smi(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.strip().split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                self.samples.append((time.time(), float(p[0]), float(p[1]),
+                                     {nm for nm, v in zip(self.NAMES, p[3:7]) if v.lower().startswith("active")}))
+            except ValueError:
+                continue
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.nvml = self._nvml_handle()
+            self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                     "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                    stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._read_smi, daemon=True)
+            except OSError:
+                self.proc = None
+        if self.thread is not None:
             self.thread.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread is not None:
             self.thread.join(timeout=2)
 
     def summary(self):
+        lo = self.t_start if self.t_start is not None else -1e300
+        hi = self.t_end if self.t_end is not None else 1e300
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 7:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx = max(mx, float(p[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+        for ts, f, m, rs in self.samples:
+            if lo <= ts <= hi:
+                sm.append(f)
+                mx = max(mx, m)
+                reasons |= rs
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def fp64_peak() -> tuple:
@@ -241,6 +291,8 @@ def run_ours(args, rank, world, local):
         launches += lib.tucker_last_launch_count()
         return launches
 
+    clk = ClockSampler(local)
+    clk.__enter__()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -251,12 +303,16 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    try:
+        clk.mark_start()
         t0.record(stream)
         for k in range(K):
             launches += step()
         t1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
+    finally:
+        clk.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
     ms_total = max_over_ranks(t0.elapsed_time(t1), world, dev)
