@@ -248,7 +248,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         // TTM3: core (r1 x r2 r3) = U1^T (r1 x n1) * T2 (n1 x r2 r3)
         SmallGemm g3{r[0], (int64_t)r[1] * r[2], g->n[0], 1, U[0], 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
                      (int64_t)r[1] * r[2], 1, 0};
-        TK_RC(launch_small_gemm(g3, st));
+        TK_RC(launch_small_gemm_splitk(g3, static_cast<double*>(scr), L.scratch_bytes, st));  // scr is free again
         if (sync) {  // input-window check of the INT8 route (stale row maxima, non-finite F)
             int bad = 0;
             TK_CUDA(cudaMemcpyAsync(&bad, gram_i8_flag_slot(g->n, at(ws, L.i8)), sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -223,6 +223,9 @@ struct SmallGemm {
     int sub;  // 0: C = A B;  1: C = C - A B
 };
 int launch_small_gemm(const SmallGemm& p, cudaStream_t st);
+// The same for one long-K product with few output tiles: K split into slices (a batch into `scratch`),
+// then summed in slice order (deterministic); the plain kernel when it does not apply.
+int launch_small_gemm_splitk(const SmallGemm& p, double* scratch, size_t scratch_bytes, cudaStream_t st);
 // Same contract on the FP64 tensor cores (gemm.cu) when the contraction is large; falls back to
 // launch_small_gemm for small ones.
 int launch_gemm(const SmallGemm& p, cudaStream_t st);

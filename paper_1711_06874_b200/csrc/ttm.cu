@@ -78,6 +78,43 @@ int launch_small_gemm(const SmallGemm& p, cudaStream_t st) {
     return TUCKER_OK;
 }
 
+// C = sum_s P[s] in index order (the split-K slices of launch_small_gemm_splitk; deterministic).
+__global__ void __launch_bounds__(256) k_splitk_sum(const double* __restrict__ P, int S, int64_t MN,
+                                                    double* __restrict__ C) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = P[e];
+        for (int q = 1; q < S; ++q) s += P[(int64_t)q * MN + e];
+        C[e] = s;
+    }
+}
+
+// A single (batch = 1, sub = 0, C contiguous M x N) small GEMM with a long K and few output tiles
+// (the core's last product: r1 x r2 r3 over K = n1) split into S K-slices run as a batch into
+// `scratch` (S M N doubles), then summed in slice order.  S = the largest of 16, 8, 4, 2 that divides K
+// and leaves >= 64 per slice; otherwise the plain kernel.
+int launch_small_gemm_splitk(const SmallGemm& p, double* scratch, size_t scratch_bytes, cudaStream_t st) {
+    const int64_t tiles = ceil_div(p.N, 64) * ceil_div(p.M, 64);
+    int S = 1;
+    for (int c = 16; c >= 2 && S == 1; c /= 2)
+        if (p.K % c == 0 && p.K / c >= 64) S = c;
+    if (p.batch != 1 || p.sub || p.scn != 1 || p.scm != p.N || tiles >= 148 || S == 1 ||
+        (size_t)S * p.M * p.N * 8 > scratch_bytes || !scratch)
+        return launch_small_gemm(p, st);
+    const int64_t kc = p.K / S;
+    SmallGemm q = p;
+    q.K = kc;
+    q.batch = S;
+    q.sab = kc * p.sak;
+    q.sbb = kc * p.sbk;
+    q.C = scratch;
+    q.scb = p.M * p.N;
+    TK_RC(launch_small_gemm(q, st));
+    const int64_t MN = p.M * p.N;
+    k_splitk_sum<<<(unsigned)std::min<int64_t>(ceil_div(MN, 256), 1024), 256, 0, st>>>(scratch, S, MN, p.C);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
+}
+
 // ------------------------------------------------------------------------------- TTM1 + TTM2
 // Fused first two mode products over one slab F[i,:,:] (n2 x n3) per CTA row-tile:
 //   T1 tile (256 rows j x R) = F[i, j0:j0+256, :] U3            DMMA, streams F once
@@ -441,7 +478,8 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
     // TTM3: core (r1 x r2r3) = U1^T (r1 x n1) * T2 (n1 x r2r3)
     SmallGemm g3{r[0], (int64_t)r[1] * r[2], n[0], 1, U1, 1, r[0], 0, T2, (int64_t)r[1] * r[2], 1, 0, core,
                  (int64_t)r[1] * r[2], 1, 0};
-    TK_RC(launch_small_gemm(g3, st));
+    // split K = n1 over the (now free) TTM2 partials buffer
+    TK_RC(launch_small_gemm_splitk(g3, JT > 1 ? part : nullptr, JT > 1 ? JT * t2b : 0, st));
     return TUCKER_OK;
 }
 
