@@ -184,15 +184,17 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         // runs on a side stream while the next Gram runs on `st` (one G per mode; the eigensolver is
         // latency-bound on one cluster); the last one (mode 0: U1) runs beside the core's first two
         // products (which need U2, U3 only); the third product waits for it.
-        // side stream A: eigensolves of modes 2 and 1; side stream B: mode 0 (beside TTM1 + TTM2)
-        cudaStream_t sideA = side_stream(0), sideB = side_stream(1);
-        if (!sideA || !sideB) return TUCKER_ERR_CUDA;
-        cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        // one side stream per mode (A: mode 2, C: mode 1, B: mode 0 beside TTM1 + TTM2): the
+        // persistent int8 Gram holds every SM, so the solves of modes 2 and 1 mostly run after the
+        // last Gram — side by side, not one after the other
+        cudaStream_t sideA = side_stream(0), sideB = side_stream(1), sideC = side_stream(2);
+        if (!sideA || !sideB || !sideC) return TUCKER_ERR_CUDA;
+        cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
         auto cleanup = [&]() {
             for (cudaEvent_t e : ev)
                 if (e) cudaEventDestroy(e);
         };
-        for (int i = 0; i < 5; ++i)
+        for (int i = 0; i < 6; ++i)
             if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
                 cleanup();
                 return TUCKER_ERR_CUDA;
@@ -201,7 +203,7 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
                          reinterpret_cast<double*>(at(ws, L.G + 2 * L.g_bytes))};
         void* escr[3] = {at(ws, L.eig), at(ws, L.eig + L.eig_bytes), at(ws, L.eig + 2 * L.eig_bytes)};
         double* T2 = reinterpret_cast<double*>(at(ws, L.t2));
-        auto side_of = [&](int m) { return m == 0 ? sideB : sideA; };
+        auto side_of = [&](int m) { return m == 0 ? sideB : (m == 1 ? sideC : sideA); };
         auto eig_end = [&](int m) -> int {  // host waits for the solve (its first pass is long queued)
             if (!sync) return launch_eig_rest(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], side_of(m));
             const int rc = launch_eig_end(g->n[m], Gm[m], r[m], U[m], nullptr, sig[m], escr[m], side_of(m), info, m);
@@ -224,9 +226,11 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         }, prep);
         if (rc == TUCKER_OK) rc = eig_end(2);
         if (rc == TUCKER_OK) rc = eig_end(1);
-        // U2, U3 final on side A -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve on side B
+        // U3 final on side A, U2 on side C -> TTM1 + TTM2 on `st`, beside the mode-0 eigensolve on side B
         if (rc == TUCKER_OK && (cudaEventRecord(ev[3], sideA) != cudaSuccess ||
-                                cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess))
+                                cudaEventRecord(ev[5], sideC) != cudaSuccess ||
+                                cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess ||
+                                cudaStreamWaitEvent(st, ev[5], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
         if (rc == TUCKER_OK)
             rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
@@ -240,8 +244,10 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
             // caller may free U or ws once the stream is idle)
             cudaEventRecord(ev[3], sideA);
             cudaEventRecord(ev[4], sideB);
+            cudaEventRecord(ev[5], sideC);
             cudaStreamWaitEvent(st, ev[3], 0);
             cudaStreamWaitEvent(st, ev[4], 0);
+            cudaStreamWaitEvent(st, ev[5], 0);
         }
         cleanup();
         TK_RC(rc);

@@ -166,25 +166,29 @@ __global__ void k_seed_vt(double* Vt, const double* __restrict__ V0, int p, int 
     }
 }
 
-// Wt (p x n) = Vt (p x n) * G (n x n)   [= (G V)^T, G symmetric].  Tile 16 rows x 64 cols.
+// Wt (p x n) = Vt (p x n) * G (n x n)   [= (G V)^T, G symmetric].  Tile 16 rows x 64 cols; K split
+// into gridDim.z slices of kc (a multiple of 32): slice z writes Wt + z p n (k_vg_sum adds them).
 __global__ void __launch_bounds__(256) k_gemm_vg(const double* __restrict__ Vt, const double* __restrict__ G,
-                                                 double* __restrict__ Wt, int p, int64_t n, const State* st) {
+                                                 double* __restrict__ Wt, int p, int64_t n, const State* st,
+                                                 int64_t kc) {
     if (st && st->done) return;
     __shared__ double sV[16][33];
     __shared__ double sG[32][64];
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // ty 0..3 -> rows ty*4..ty*4+3
     const int64_t col = blockIdx.x * 64 + tx;
     const int row0 = blockIdx.y * 16;
+    const int64_t kbeg = blockIdx.z * kc, kend = min(n, kbeg + kc);
+    Wt += (size_t)blockIdx.z * p * n;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+    for (int64_t k0 = kbeg; k0 < kend; k0 += 32) {
         for (int t = threadIdx.x; t < 16 * 32; t += 256) {
             const int rr = t / 32, kk = t % 32;
-            sV[rr][kk] = (row0 + rr < p && k0 + kk < n) ? Vt[(size_t)(row0 + rr) * n + k0 + kk] : 0.0;
+            sV[rr][kk] = (row0 + rr < p && k0 + kk < kend) ? Vt[(size_t)(row0 + rr) * n + k0 + kk] : 0.0;
         }
         for (int t = threadIdx.x; t < 32 * 64; t += 256) {
             const int kk = t / 64, cc = t % 64;
             const int64_t gc = blockIdx.x * 64 + cc;
-            sG[kk][cc] = (k0 + kk < n && gc < n) ? G[(size_t)(k0 + kk) * n + gc] : 0.0;
+            sG[kk][cc] = (k0 + kk < kend && gc < n) ? G[(size_t)(k0 + kk) * n + gc] : 0.0;
         }
         __syncthreads();
 #pragma unroll 8
@@ -199,6 +203,27 @@ __global__ void __launch_bounds__(256) k_gemm_vg(const double* __restrict__ Vt, 
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (row0 + ty * 4 + u < p) Wt[(size_t)(row0 + ty * 4 + u) * n + col] = acc[u];
+}
+
+// Wt = sum_z part[z] in slice order (deterministic).
+__global__ void __launch_bounds__(256) k_vg_sum(const double* __restrict__ part, int S, int64_t pn,
+                                                double* __restrict__ Wt, const State* st) {
+    if (st && st->done) return;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pn; e += (int64_t)gridDim.x * blockDim.x) {
+        double a = part[e];
+        for (int z = 1; z < S; ++z) a += part[(int64_t)z * pn + e];
+        Wt[e] = a;
+    }
+}
+
+// K slices of W = G V: enough CTAs for the machine (the 16 x 64 output tiles of p x n are few),
+// each slice >= 128 columns of K.
+constexpr int kVgSlicesMax = 8;
+static int vg_slices(int64_t n, int p) {
+    const int64_t tiles = ceil_div(n, (int64_t)64) * ceil_div((int64_t)p, (int64_t)16);
+    int S = (int)std::min<int64_t>(kVgSlicesMax, std::max<int64_t>(1, ceil_div((int64_t)2 * 148, tiles)));
+    while (S > 1 && n / S < 128) --S;
+    return S;
 }
 
 __global__ void __launch_bounds__(kThreads) k_orth(const double* Yt, double* Vt, int p, int64_t n) {
@@ -394,7 +419,8 @@ bool eig_rank_supported(int64_t n, int r) { return n <= eig::kDirectMax || r <= 
 size_t eig_ws_bytes(int64_t n, int r) {
     using namespace eig;
     const int p = block_width(n, std::max(1, r));
-    return align_up(sizeof(State), 256) + 4 * align_up((size_t)p * n * sizeof(double), 256);
+    const int S = n > kDirectMax ? vg_slices(n, p) : 1;
+    return align_up(sizeof(State), 256) + (4 + (S > 1 ? S : 0)) * align_up((size_t)p * n * sizeof(double), 256);
 }
 
 // Split form: launch_eig_begin enqueues the whole first pass (no host synchronisation; on the
@@ -403,13 +429,16 @@ size_t eig_ws_bytes(int64_t n, int r) {
 // synchronises, continues in batches while not converged, and reports.  launch_eig = both.
 namespace eig {
 struct Plan {
-    int p;
+    int p, S;
+    int64_t n;
     State* dst;
-    double *Vt, *Wt, *VrT, *YT;
+    double *Vt, *Wt, *VrT, *YT, *part;
 };
 static Plan eig_plan(int64_t n, int r, void* ws) {
     Plan q{};
     q.p = block_width(n, r);
+    q.n = n;
+    q.S = n > kDirectMax ? vg_slices(n, q.p) : 1;
     char* w = static_cast<char*>(ws);
     q.dst = reinterpret_cast<State*>(w);
     w += align_up(sizeof(State), 256);
@@ -418,7 +447,27 @@ static Plan eig_plan(int64_t n, int r, void* ws) {
     q.Wt = reinterpret_cast<double*>(w + blk);
     q.VrT = reinterpret_cast<double*>(w + 2 * blk);
     q.YT = reinterpret_cast<double*>(w + 3 * blk);
+    q.part = reinterpret_cast<double*>(w + 4 * blk);  // S slices of p x n (blk apart: p n doubles each)
     return q;
+}
+// W = G V for the plan's Vt into its Wt (K-sliced when the output tiles are few); st_done: the
+// solve's state (launches of a converged solve exit at once), or nullptr.
+static int gemm_vg(const Plan& q, const double* G, const State* st_done, cudaStream_t st) {
+    const int64_t n = q.n;
+    const dim3 ggrid((unsigned)ceil_div(n, (int64_t)64), (unsigned)ceil_div((int64_t)q.p, (int64_t)16), (unsigned)q.S);
+    const int64_t kc = ceil_div(ceil_div(n, (int64_t)q.S), (int64_t)32) * 32;
+    if (q.S == 1) {
+        k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, q.p, n, st_done, kc);
+        TK_CHECK_LAUNCH();
+        return TUCKER_OK;
+    }
+    k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.part, q.p, n, st_done, kc);
+    TK_CHECK_LAUNCH();
+    const int64_t pn = (int64_t)q.p * n;
+    k_vg_sum<<<(unsigned)std::min<int64_t>(ceil_div(pn, (int64_t)256), 1024), 256, 0, st>>>(q.part, q.S, pn, q.Wt,
+                                                                                            st_done);
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
 }
 }  // namespace eig
 
@@ -441,42 +490,35 @@ int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambd
         TK_CHECK_LAUNCH();
     } else if (eig_cluster_supported(n)) {
         // cluster path (n <= 2048): W = G V on many CTAs, Rayleigh–Ritz + CGS2 in one cluster
-        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
         if (V0) {
             k_seed_vt<<<64, 256, 0, st>>>(Vt, V0, p, r, n);
         } else {
             k_omega<<<64, 256, 0, st>>>(Vt, p, n);
         }
         TK_CHECK_LAUNCH();
-        k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
-        TK_CHECK_LAUNCH();
+        TK_RC(gemm_vg(q, G, nullptr, st));
         TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
         // iterations 1 .. kMinIters-2 are plain power steps (V <- CGS2(G V), no Rayleigh–Ritz):
         // the Ritz rotation does not change the subspace, and a single Jacobi solve of the dense
         // H at the end replaces the per-iteration ones (a warm start skips them)
         for (int w = 1; w < kMinIters - 1 && !V0; ++w) {
-            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
-            TK_CHECK_LAUNCH();
+            TK_RC(gemm_vg(q, G, nullptr, st));
             TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
         }
         for (int it = kMinIters - 1; it < kMinIters + 3; ++it) {  // first batch: 4 Rayleigh-Ritz steps
-            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
-            TK_CHECK_LAUNCH();
+            TK_RC(gemm_vg(q, G, dst, st));
             TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst, st));
         }
     } else {
-        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
         k_omega<<<64, 256, 0, st>>>(Vt, p, n);
         TK_CHECK_LAUNCH();
-        k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, nullptr);
-        TK_CHECK_LAUNCH();
+        TK_RC(gemm_vg(q, G, nullptr, st));
         k_orth<<<1, kThreads, 0, st>>>(Wt, Vt, p, n);
         TK_CHECK_LAUNCH();
         const size_t sm = rr_smem(p);
         TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         for (int it = 0; it < kBatch; ++it) {
-            k_gemm_vg<<<ggrid, 256, 0, st>>>(Vt, G, Wt, p, n, dst);
-            TK_CHECK_LAUNCH();
+            TK_RC(gemm_vg(q, G, dst, st));
             RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, Vt, Wt, q.VrT, q.YT, U, lambda, sigma, dst};
             k_rr<<<1, kThreads, sm, st>>>(a);
             TK_CHECK_LAUNCH();
@@ -497,7 +539,6 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
     TK_CUDA(cudaStreamSynchronize(st));
     if (n > kDirectMax) {  // continue in batches while not converged
         const bool cl = eig_cluster_supported(n);
-        const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
         int it = cl ? kMinIters + 3 : kBatch;
         if (!cl) {
             const size_t sm = rr_smem(p);
@@ -505,8 +546,7 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
         }
         while (!hs.done && it < kMaxIters) {
             for (int b = 0; b < kBatch && it < kMaxIters; ++b, ++it) {
-                k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, p, n, dst);
-                TK_CHECK_LAUNCH();
+                TK_RC(gemm_vg(q, G, dst, st));
                 if (cl) {
                     TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, q.Vt, q.Wt, U, lambda, sigma,
                                             dst, st));
@@ -558,15 +598,13 @@ int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda
     const Plan q = eig_plan(n, r, ws);
     const int p = q.p;
     const bool cl = eig_cluster_supported(n);
-    const dim3 ggrid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(p, 16));
     if (!cl) {
         const size_t sm = rr_smem(p);
         TK_CUDA(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
     for (int it = cl ? kMinIters + 3 : kBatch; it < kMaxItersAsync; ++it) {
         const int last = it == kMaxItersAsync - 1 ? 1 : 0;
-        k_gemm_vg<<<ggrid, 256, 0, st>>>(q.Vt, G, q.Wt, p, n, q.dst);
-        TK_CHECK_LAUNCH();
+        TK_RC(gemm_vg(q, G, q.dst, st));
         if (cl) {
             TK_RC(launch_rr_cluster(n, p, r, it, last, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst, st));
         } else {

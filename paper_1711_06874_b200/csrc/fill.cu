@@ -38,23 +38,23 @@ __global__ void k_nodes(double c0, double s0, int64_t n0, double c1, double s1, 
     x2[t] = __dmul_rn(x, x);
 }
 
-// One block per dyadic interval j = kChebJmin + blockIdx.x; thread k < 21 computes the node
-// value at x_k = cos(pi (k+1/2)/21), then thread m the coefficient
+// One block per dyadic interval j = kChebJmin + blockIdx.x; warp k < 21 computes the node value at
+// x_k = cos(pi (k+1/2)/21) (warp-cooperative trapezoid), then thread m the coefficient
 // c_m = 2/21 sum_k g_k cos(pi m (k+1/2)/21).
-__global__ void k_cheb_table(double nu, double pref, double* table) {
+__global__ void __launch_bounds__(kChebN * 32) k_cheb_table(double nu, double pref, double* table) {
     __shared__ double g[kChebN];
     const int j = kChebJmin + blockIdx.x;
-    const int k = threadIdx.x;
-    if (k < kChebN) {
-        double xk = cospi((k + 0.5) / kChebN);
-        double z = ldexp(1.5 + 0.5 * xk, j);
-        g[k] = pref * pow(z, nu) * scaled_besselk_trapz(nu, z);
-    }
+    const int k = threadIdx.x >> 5;
+    const double xk = cospi((k + 0.5) / kChebN);
+    const double z = ldexp(1.5 + 0.5 * xk, j);
+    const double v = scaled_besselk_trapz_warp(nu, z);
+    if ((threadIdx.x & 31) == 0) g[k] = pref * pow(z, nu) * v;
     __syncthreads();
-    if (k < kChebN) {
+    if (threadIdx.x < kChebN) {
+        const int m = threadIdx.x;
         double c = 0.0;
-        for (int t = 0; t < kChebN; ++t) c += g[t] * cospi(k * (t + 0.5) / kChebN);
-        table[blockIdx.x * kChebN + k] = c * (2.0 / kChebN);
+        for (int t = 0; t < kChebN; ++t) c += g[t] * cospi(m * (t + 0.5) / kChebN);
+        table[blockIdx.x * kChebN + m] = c * (2.0 / kChebN);
     }
 }
 
@@ -225,7 +225,7 @@ int launch_fill_prep(const tucker_grid& g, const tucker_kernel& kn, const KParam
     k_nodes<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(c[0], s[0], n1, c[1], s[1], n2, c[2], s[2], n3, nodes_x2);
     TK_CHECK_LAUNCH();
     if (kn.family == TUCKER_MATERN && kp.closed == 0) {
-        k_cheb_table<<<kChebIntervals, 32, 0, st>>>(kn.nu, kp.pref, cheb);
+        k_cheb_table<<<kChebIntervals, kChebN * 32, 0, st>>>(kn.nu, kp.pref, cheb);
         TK_CHECK_LAUNCH();
     }
     return TUCKER_OK;

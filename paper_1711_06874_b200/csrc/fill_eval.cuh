@@ -11,7 +11,37 @@
 namespace tk {
 
 // ------------------------------------------------------------------------- K_nu Chebyshev table
-// e^z K_nu(z) = int_0^inf exp(-2 z sinh^2(t/2)) cosh(nu t) dt, trapezoid h = 1/32.
+// e^z K_nu(z) = int_0^inf exp(-2 z sinh^2(t/2)) cosh(nu t) dt, trapezoid h = 1/32, summed until a
+// node k has f_k < f_{k-1} and f_k < 1e-18 (running sum) (the last node counted is that k).
+// Warp-cooperative form (all 32 lanes call it with the same nu, z): lane L takes nodes 32 b + L + 1
+// of batch b; the stopping node is found with a warp prefix sum.  Returns the integral on every lane.
+__device__ inline double scaled_besselk_trapz_warp(double nu, double z) {
+    const double h = 1.0 / 32.0;
+    const int lane = threadIdx.x & 31;
+    double sum = 0.5, prev = 1.0;  // sum of the nodes counted so far, f of the last node of the batch before
+    for (int b = 0; b < 200000 / 32; ++b) {
+        const double t = (32 * b + lane + 1) * h;
+        const double sh = sinh(0.5 * t);
+        const double f = exp(-2.0 * z * sh * sh) * cosh(nu * t);
+        double pre = f;  // inclusive prefix sum over the lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const double fup = __shfl_up_sync(0xffffffffu, f, 1);  // every lane takes part
+        const double fprev = lane == 0 ? prev : fup;
+        const bool stop = f < fprev && f < 1e-18 * (sum + pre);
+        const unsigned m = __ballot_sync(0xffffffffu, stop);
+        if (m) {
+            const int ls = __ffs(m) - 1;  // first stopping node of the batch: nodes up to it count
+            return h * (sum + __shfl_sync(0xffffffffu, pre, ls));
+        }
+        sum += __shfl_sync(0xffffffffu, pre, 31);
+        prev = __shfl_sync(0xffffffffu, f, 31);
+    }
+    return h * sum;
+}
 __device__ inline double scaled_besselk_trapz(double nu, double z) {
     const double h = 1.0 / 32.0;
     double sum = 0.5, prev = 1.0;

@@ -542,6 +542,8 @@ struct GemmArgs {
     int nb3;         // lay 2: K-blocks per i-slab (ceil(n3 / 128); the rest of the last is zero-filled)
     int64_t nkb_total;  // K-blocks of this launch
     int kbu;            // K-blocks per unit (<= KCH / BKB: one exact int32 chunk)
+    int* sched;         // unit counter (0 at launch): pairs take units dynamically; nullptr: unit
+                        // u runs on pair u mod npairs
 };
 
 __host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
@@ -703,11 +705,29 @@ __device__ __forceinline__ Unit unit_of(int u, const GemmArgs& g) {
     return x;
 }
 
+__device__ __forceinline__ uint32_t peer_addr(const void* p) {  // same smem offset in cluster rank 1
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 1;\n" : "=r"(r) : "r"(smem_u32(p)));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, int v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+
+// Dynamic unit schedule of a CTA pair: the leader's producer takes the next unit from the global
+// counter and posts it in a UQ-deep ring (uq) in both CTAs; every other role of the pair (the peer's
+// producer, the MMA issuer, the eight epilogue warps) reads it from its own CTA's ring and releases
+// the slot on the leader's uq_empty.  A pair that starts late (SMs held by a concurrent kernel, e.g.
+// an eigensolve on a side stream) then takes fewer units instead of delaying the whole launch.
+constexpr int UQ = 4;
+constexpr int UQ_CONSUMERS = 10;  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     k_i8_gemm(const __grid_constant__ CUtensorMap map, const GemmArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty, uq_full[UQ], uq_empty[UQ];
+    __shared__ int uq[UQ];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint32_t rank;
@@ -720,9 +740,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         }
         mbar_init(&tfull, 1);
         mbar_init(&tempty, 8);  // 4 epilogue warps x 2 CTAs
+        for (int q = 0; q < UQ; ++q) {
+            mbar_init(&uq_full[q], 1);
+            mbar_init(&uq_empty[q], UQ_CONSUMERS);
+        }
         mbar_fence_init();
         tma_prefetch_desc(&map);
     }
+    // it-th unit of this pair (-1: none left).  Static: pair + it npairs.  Dynamic: see UQ above —
+    // `post` is the leader's producer (takes and posts), everyone else reads and releases.
+    auto next_unit = [&](int it, bool post) -> int {
+        if (!g.sched) {
+            const int u = pair + it * npairs;
+            return u < g.nunits ? u : -1;
+        }
+        const int slot = it % UQ;
+        const uint32_t par = (uint32_t)(it / UQ) & 1u;
+        if (post) {
+            mbar_wait_cluster(&uq_empty[slot], par ^ 1u);
+            int u = atomicAdd(g.sched, 1);
+            if (u >= g.nunits) u = -1;
+            uq[slot] = u;
+            st_cluster_u32(peer_addr(&uq[slot]), u);
+            mbar_arrive(&uq_full[slot]);
+            mbar_arrive_cluster(peer_addr(&uq_full[slot]));
+            return u;
+        }
+        mbar_wait_cluster(&uq_full[slot], par);
+        const int u = *reinterpret_cast<volatile int*>(&uq[slot]);
+        mbar_arrive_cluster(leader_addr(&uq_empty[slot]));
+        return u;
+    };
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
@@ -736,7 +784,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         if (lane == 0) {  // TMA producer (both CTAs): own A rows and own B halves, completion on the leader
             int stage = 0;
             uint32_t ph = 0;
-            for (int u = pair; u < g.nunits; u += npairs) {
+            for (int it = 0;; ++it) {
+                const int u = next_unit(it, rank == 0);
+                if (u < 0) break;
                 const Unit x = unit_of(u, g);
                 const int64_t kbeg = (int64_t)x.c * g.kbu;  // first K-block of the chunk
                 const int nkb = (int)min((int64_t)g.kbu, g.nkb_total - kbeg);
@@ -777,7 +827,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             // K-step of one MMA (K = 32 bytes): +32 B along the 128-B line (K-major) or +32 lines
             // of 128 B (MN-major); both stay inside the 1024-B swizzle atoms' alignment
             const uint32_t kstep = mn ? 32u * BKB : 32u;
-            for (int u = pair; u < g.nunits; u += npairs, ++it) {
+            for (;; ++it) {
+                const int u = next_unit(it, false);
+                if (u < 0) break;
                 const Unit x = unit_of(u, g);
                 const int64_t kbeg = (int64_t)x.c * g.kbu;
                 const int nkb = (int)min((int64_t)g.kbu, g.nkb_total - kbeg);
@@ -817,8 +869,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         const int lg = warp & 3;
         const int row = (int)rank * 128 + lg * 32 + lane;
         const uint32_t te = leader_addr(&tempty);
-        int it = 0;
-        for (int u = pair; u < g.nunits; u += npairs, ++it) {
+        for (int it = 0;; ++it) {
+            int u = 0;
+            if (lane == 0) u = next_unit(it, false);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u < 0) break;
             const Unit x = unit_of(u, g);
             mbar_wait(&tfull, it & 1);
             tc_fence_after();
@@ -1042,6 +1097,7 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
     off += pb;
     w.off_Racc = off;
     off += ab;
+    off += 256;  // the dynamic schedule's unit counter (unit_counter(utab))
     w.off_utab = off;
     off += ub;
     w.total = off;
@@ -1049,6 +1105,15 @@ WsPlan ws_plan(const int64_t n[3], const int64_t* align = nullptr) {
 }
 
 
+
+// k_i8_gemm's unit counter: every workspace plan reserves 256 bytes just before the unit table.
+inline int* unit_counter(int2* utab) { return reinterpret_cast<int*>(reinterpret_cast<char*>(utab) - 256); }
+inline int* gemm_sched(int2* utab, cudaStream_t st) {  // zeroed for one launch (nullptr: static schedule)
+    static const bool stat = std::getenv("TUCKER_I8_STATIC") != nullptr;
+    if (stat) return nullptr;
+    int* c = unit_counter(utab);
+    return cudaMemsetAsync(c, 0, sizeof(int), st) == cudaSuccess ? c : nullptr;
+}
 
 // One mode's int8 Grams, driven super-chunk by super-chunk: init() builds the unit table, run()
 // takes the residues of one super-chunk (K-block-major in R) through k_i8_gemm and folds its
@@ -1089,7 +1154,7 @@ struct ModeGemm {
             return TUCKER_ERR_CUDA;
         const int nchunks = (int)ceil_div(Kc, KCH);
         GemmArgs ga{(int)p.rows, p.nJ, p.ntiles, nug, nchunks, NMOD * nchunks * nug, Kc, P, utab, 0, 1,
-                    ceil_div(Kc, (int64_t)BKB), (int)(KCH / BKB)};
+                    ceil_div(Kc, (int64_t)BKB), (int)(KCH / BKB), gemm_sched(utab, st)};
         const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);  // CTA pairs, one CTA per SM
         {
             TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1316,6 +1381,7 @@ SharedPlan shared_plan(const int64_t n[3]) {
     off += pb;
     w.off_Racc = off;
     off += ab;
+    off += 256;  // the dynamic schedule's unit counter (unit_counter(utab))
     w.off_utab = off;
     off += ub;
     w.total = off;
@@ -1484,7 +1550,7 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* 
     const int kbu = unit_kblocks(nkb, rows);
     const int nchunks = (int)ceil_div(nkb, (int64_t)kbu);
     GemmArgs ga{rows, nJ, ntiles, nug, nchunks, NMOD * nchunks * nug, nkb * BKB, P, utab, m + 1,
-                (int)ceil_div(c[2], (int64_t)BKB), nkb, kbu};
+                (int)ceil_div(c[2], (int64_t)BKB), nkb, kbu, gemm_sched(utab, st)};
     const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);
     {
         TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1625,6 +1691,7 @@ FusedSharedPlan fused_shared_plan(const int64_t n[3]) {
         w.off_Racc[q] = off;
         off += ab;
     }
+    off += 256;  // the dynamic schedule's unit counter (unit_counter(utab))
     w.off_utab = off;
     off += ub;
     w.total = off;
@@ -1797,11 +1864,15 @@ uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
 // Per calling thread and device (created on first use, kept for the thread's lifetime): concurrent
 // callers on different threads never share or wait on each other's side streams.
 cudaStream_t side_stream(int which) {
-    static thread_local cudaStream_t s[64][2] = {};
+    static thread_local cudaStream_t s[64][3] = {};
     int dev = 0;
-    if (which < 0 || which > 1 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (which < 0 || which > 2 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     cudaStream_t& x = s[dev][which];
-    if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
+    // highest priority: the eigensolves' small launches take SMs ahead of the next wave of a large
+    // kernel on the caller's stream (e.g. the core's first product while the mode-0 solve runs)
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+    if (!x && cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi) != cudaSuccess) x = nullptr;
     return x;
 }
 

@@ -31,9 +31,11 @@ __device__ __forceinline__ void rr_pair(int s, int w, int m, int& a, int& b) {
         a = s;
         b = m - 1;
     } else {
-        const int mm = m - 1;
-        a = (s + w) % mm;
-        b = (s - w + mm) % mm;
+        const int mm = m - 1;  // 0 <= s < mm, 0 < w < mm: one conditional subtraction each
+        a = s + w;
+        a -= a >= mm ? mm : 0;
+        b = s - w + mm;
+        b -= b >= mm ? mm : 0;
     }
     if (a > b) { const int t = a; a = b; b = t; }
 }

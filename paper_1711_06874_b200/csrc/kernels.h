@@ -96,7 +96,7 @@ int launch_fill_prepare(const tucker_grid& g, const tucker_kernel& kn, double* F
                         void* i8ws, size_t i8ws_bytes, cudaStream_t st);
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]);
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws);
-// Per-device non-blocking side streams of the library (which = 0, 1; created once).
+// Per-device non-blocking side streams of the library (which = 0, 1, 2; created once per thread).
 cudaStream_t side_stream(int which);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
