@@ -371,10 +371,13 @@ def run_ours(args, rank, world, local):
     gram_flops_fp64 = N * (n + 1)  # SYRK count of one mode's FP64 Gram (n_m (n_m+1)/2 entries x 2K flops)
     i8 = "i8_gemm" in st
     if i8:
-        # k_i8_gemm: 16 residue Grams per mode, algorithmic int8 ops = 16 x n(n+1)/2 x K x 2 per mode
-        ops_mode = 16 * gram_flops_fp64
+        # k_i8_gemm: one residue Gram per modulus and mode, algorithmic int8 ops = moduli x n(n+1)/2 x K
+        # x 2 per mode (16 moduli, or 15 where the row-norm bound allows it: DESIGN.md R21)
+        mods = [int(x) for x in info.moduli]
+        if not all(mods):
+            mods = [16, 16, 16]
         launch_ms = prof["i8_gemm"][0] / prof["i8_gemm"][1]
-        ops_launch = ops_mode * 3 * K / prof["i8_gemm"][1]
+        ops_launch = sum(mods) * gram_flops_fp64 * K / prof["i8_gemm"][1]
         achieved = ops_launch / (launch_ms * 1e-3) / 1e12
         peaks = measured_peaks()
         if peaks.get("bf16_tflops_sustained"):
@@ -413,6 +416,7 @@ def run_ours(args, rank, world, local):
                                       "included) over the same peak; above 1 when the int8 MMAs hold a higher "
                                       "power-capped clock than the bf16 cuBLAS loop behind the sustained figure",
                 "peak_source": peak_src, "ops_per_launch": ops_launch, "launch_ms": launch_ms,
+                "moduli_per_mode": mods,
                 "launches_per_step": calls["i8_gemm"],
                 "fp64_equivalent_gram_tflops": gram_flops_fp64 / (gram_stage_ms * 1e-3) / 1e12,
                 "fp64_peak_tflops": fp64_peak()[0],
@@ -453,7 +457,8 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "dtype_note": ("FP64 path; the Grams are formed exactly from int8 residues on the tensor cores (tcgen05 "
-                       "kind::i8, 16 moduli) and reconstructed to FP64 by the CRT (DESIGN.md R18)") if i8 else
+                       "kind::i8, 16 moduli or 15 under the row-norm bound) and reconstructed to FP64 by the CRT (DESIGN.md R18, "
+                       "R21)") if i8 else
                       "FP64 path; Grams on the FP64 tensor cores (DMMA)",
         "data": "synthetic",
         "config": {"workload": f"cfg5_{n}cube_matern_nu1.5_ell0.2", "grid": [n, n, n], "box": [-1.0, 1.0],

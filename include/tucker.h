@@ -100,6 +100,10 @@ typedef struct {
     double lambda1[3];    /* theta_1 (largest eigenvalue of G_m)                              */
     int32_t k_resolved[3]; /* #{k <= r_m : lambda_k >= 1e-12 lambda_1}: the resolved leading
                               eigenpairs (R14; past it the Gram route's noise)  */
+    int32_t moduli[3];     /* INT8 Gram route: moduli the exact Gram of mode m was formed with
+                              (16, or 15 where the row-norm bound of DESIGN.md R21 allows it);
+                              0 for the FP64 DMMA engine.  Set by tucker_hosvd,
+                              tucker_hosvd_rowmax, tucker_hosvd_prepared (untouched elsewhere) */
 } tucker_info;
 
 /* Workspace bytes needed by tucker_hosvd / tucker_error / tucker_gram / tucker_eig /

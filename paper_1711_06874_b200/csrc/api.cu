@@ -257,12 +257,15 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
         TK_RC(launch_small_gemm_splitk(g3, static_cast<double*>(scr), L.scratch_bytes, st));  // scr is free again
         if (sync) {  // input-window check of the INT8 route (stale row maxima, non-finite F)
             int bad = 0;
+            TK_RC(gram_i8_moduli(g->n, at(ws, L.i8), info->moduli, st));
             TK_CUDA(cudaMemcpyAsync(&bad, gram_i8_flag_slot(g->n, at(ws, L.i8)), sizeof(int), cudaMemcpyDeviceToHost, st));
             TK_CUDA(cudaStreamSynchronize(st));
             if (bad) return TUCKER_ERR_INPUT;
         }
         return worst;
     } else {
+        if (info)
+            for (int m = 0; m < 3; ++m) info->moduli[m] = 0;  // FP64 DMMA Grams
         for (int m = 0; m < 3; ++m) {
             TK_RC(launch_gram(g->n, m, F, G, scr, L.scratch_bytes, st));
             TK_RC(eig_mode(m));

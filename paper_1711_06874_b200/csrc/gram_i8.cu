@@ -372,12 +372,14 @@ __device__ __forceinline__ bool residues16(const double* v, double sa, double sb
 // Residues of 8 consecutive values -> one 8-byte word per modulus, stored at NS slots (odd slots
 // byte-reversed: the k-mirror side of the octant generators); the same window check as residues16.
 // 8 values per call keep the live limbs small (64 registers for the shared-layout residue kernel).
+// nplanes: planes L >= nplanes are not written (no Gram of the launch reads them).
 template <int NS>
 __device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
-                                                 std::integer_sequence<int>) {}
+                                                 int nplanes, std::integer_sequence<int>) {}
 template <int NS, int L, int... Ls>
 __device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t* const (&out)[NS], size_t lstride,
-                                                 std::integer_sequence<int, L, Ls...>) {
+                                                 int nplanes, std::integer_sequence<int, L, Ls...>) {
+    if (L >= nplanes) return;
     constexpr int p = kMod(L);
     constexpr float c1 = (float)balanced(pow2mod(17, p), p), c2 = (float)balanced(pow2mod(34, p), p);
     constexpr float fp = (float)p, inv = 1.0f / (float)p;
@@ -401,13 +403,13 @@ __device__ __forceinline__ void store_res8_slots(const float2 (&u)[4][3], int8_t
     const size_t off = (size_t)L * lstride;
 #pragma unroll
     for (int q = 0; q < NS; ++q) *reinterpret_cast<uint2*>(out[q] + off) = (q & 1) ? mr : v;
-    store_res8_slots<NS>(u, out, lstride, std::integer_sequence<int, Ls...>{});
+    store_res8_slots<NS>(u, out, lstride, nplanes, std::integer_sequence<int, Ls...>{});
 }
 
 // Residues of the 8 values v, stored at NS slots (odd slots byte-reversed).
 template <int NS>
 __device__ __forceinline__ bool residues8_slots(const double* v, double sa, double sb, int8_t* const (&out)[NS],
-                                                size_t lstride, double lim) {
+                                                size_t lstride, double lim, int nplanes = NMOD) {
     float2 u[4][3];
     constexpr double M2 = 5629508124213248.0;
     bool ok = true;
@@ -432,7 +434,7 @@ __device__ __forceinline__ bool residues8_slots(const double* v, double sa, doub
             u[e >> 1][2].x = f2;
         }
     }
-    store_res8_slots<NS>(u, out, lstride, std::make_integer_sequence<int, NMOD>{});
+    store_res8_slots<NS>(u, out, lstride, nplanes, std::make_integer_sequence<int, NMOD>{});
     return ok;
 }
 
@@ -544,6 +546,8 @@ struct GemmArgs {
     int kbu;            // K-blocks per unit (<= KCH / BKB: one exact int32 chunk)
     int* sched;         // unit counter (0 at launch): pairs take units dynamically; nullptr: unit
                         // u runs on pair u mod npairs
+    const int* nmod;    // moduli this launch needs (device, set by k_i8_nmod; nullptr: NMOD): the
+                        // units of moduli l >= *nmod — the last ones, l is the outermost index — are skipped
 };
 
 __host__ __device__ __forceinline__ int tiles_in_row(int I, int nJ) { return min((I * PM + PM - 1) / PN + 1, nJ); }
@@ -749,17 +753,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
     // it-th unit of this pair (-1: none left).  Static: pair + it npairs.  Dynamic: see UQ above —
     // `post` is the leader's producer (takes and posts), everyone else reads and releases.
+    const int nunits = g.nmod ? min(g.nunits, *g.nmod * g.nchunks * g.nug) : g.nunits;
     auto next_unit = [&](int it, bool post) -> int {
         if (!g.sched) {
             const int u = pair + it * npairs;
-            return u < g.nunits ? u : -1;
+            return u < nunits ? u : -1;
         }
         const int slot = it % UQ;
         const uint32_t par = (uint32_t)(it / UQ) & 1u;
         if (post) {
             mbar_wait_cluster(&uq_empty[slot], par ^ 1u);
             int u = atomicAdd(g.sched, 1);
-            if (u >= g.nunits) u = -1;
+            if (u >= nunits) u = -1;
             uq[slot] = u;
             st_cluster_u32(peer_addr(&uq[slot]), u);
             mbar_arrive(&uq_full[slot]);
@@ -926,12 +931,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 
 // ------------------------------------------------------------------------------------------
 // 2b. fold the chunk partials: Racc[l][t][col][row] = (Racc + sum_c P) mod p_l  (Racc in [0, p))
+// nmod (device, nullptr: NMOD): moduli l >= *nmod were not formed and are not folded.
 __global__ void __launch_bounds__(256) k_i8_reduce(const int8_t* __restrict__ P, int32_t* __restrict__ Racc,
-                                                   int ntiles, int nchunks, int first) {
+                                                   int ntiles, int nchunks, int first, const int* __restrict__ nmod) {
     const int64_t per = (int64_t)ntiles * PN * PM;  // a multiple of 16
     const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16;  // 16 consecutive rows
     if (idx >= per * NMOD) return;
     const int l = (int)(idx / per);
+    if (nmod && l >= *nmod) return;
     const int64_t e = idx - (int64_t)l * per;  // t * PN*PM + col*PM + row
     int s[16];                                 // |s| <= p + 126 nchunks << 2^31
     int4* ra = reinterpret_cast<int4*>(Racc + idx);
@@ -969,18 +976,18 @@ __device__ __forceinline__ int garner_step(int vl, int vq) {
     d += (d < 0) ? p : 0;
     return (d * iv) % p;
 }
-template <int L, int... Q>
-__device__ __forceinline__ void garner_row(int (&v)[NMOD], std::integer_sequence<int, Q...>) {
+template <int NM, int L, int... Q>
+__device__ __forceinline__ void garner_row(int (&v)[NM], std::integer_sequence<int, Q...>) {
     ((v[L] = garner_step<L, Q>(v[L], v[Q])), ...);
 }
-template <int... L>
-__device__ __forceinline__ void garner_all(int (&v)[NMOD], std::integer_sequence<int, L...>) {
-    (garner_row<L>(v, std::make_integer_sequence<int, L>{}), ...);
+template <int NM, int... L>
+__device__ __forceinline__ void garner_all(int (&v)[NM], std::integer_sequence<int, L...>) {
+    (garner_row<NM, L>(v, std::make_integer_sequence<int, L>{}), ...);
 }
-__device__ __forceinline__ unsigned __int128 prod_moduli() {
+template <int NM>
+__host__ __device__ constexpr unsigned __int128 prod_moduli() {  // P of the first NM moduli
     unsigned __int128 P = 1;
-#pragma unroll
-    for (int l = 0; l < NMOD; ++l) P *= (uint64_t)kMod(l);
+    for (int l = 0; l < NM; ++l) P *= (uint64_t)kMod(l);
     return P;
 }
 
@@ -995,9 +1002,30 @@ __device__ __forceinline__ double u128_to_double_rn(unsigned __int128 m) {
     return ldexp(__ull2double_rn(top), 64 - lz);
 }
 
+// S_ij from its residues modulo the first NM moduli (Garner mixed radix, Horner in 128 bits,
+// symmetric range |S| <= (P - 1) / 2): the magnitude rounded once to FP64, and its sign.
+template <int NM>
+__device__ __forceinline__ double crt_value(const int32_t* __restrict__ Racc, int64_t per, int64_t e, bool& neg) {
+    int v[NM];
+#pragma unroll
+    for (int l = 0; l < NM; ++l) v[l] = Racc[l * per + e];
+    // Garner: v_l <- ((v_l - v_0) inv(p_0) - v_1) inv(p_1) ... mod p_l  (mixed-radix digits)
+    garner_all<NM>(v, std::make_integer_sequence<int, NM>{});
+    // S = v_0 + p_0 (v_1 + p_1 (v_2 + ...)), Horner from the top digit (exact in 128 bits)
+    unsigned __int128 S = (uint32_t)v[NM - 1];
+#pragma unroll
+    for (int l = NM - 2; l >= 0; --l) S = S * (uint64_t)kMod(l) + (uint32_t)v[l];
+    constexpr unsigned __int128 Pp = prod_moduli<NM>();
+    constexpr unsigned __int128 half = Pp >> 1;  // P odd: S in (P/2, P) represents S - P < 0
+    neg = S > half;
+    return u128_to_double_rn(neg ? (Pp - S) : S);
+}
+
+// nmod (device, nullptr: NMOD): the number of moduli the Grams were formed with (NMOD or NMOD - 1).
 __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const uint32_t* __restrict__ mx,
                                                 int n, int nJ, int ntiles, int b, double* __restrict__ G,
-                                                const int* __restrict__ bad, int global_mx) {
+                                                const int* __restrict__ bad, int global_mx,
+                                                const int* __restrict__ nmod) {
     // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -1009,20 +1037,8 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     t += J;
     const int64_t per = (int64_t)ntiles * PN * PM;
     const int64_t e = (int64_t)t * PN * PM + (int64_t)(j - J * PN) * PM + (i - I * PM);
-    int v[NMOD];
-#pragma unroll
-    for (int l = 0; l < NMOD; ++l) v[l] = Racc[l * per + e];
-    // Garner: v_l <- ((v_l - v_0) inv(p_0) - v_1) inv(p_1) ... mod p_l  (mixed-radix digits)
-    garner_all(v, std::make_integer_sequence<int, NMOD>{});
-    // S = v_0 + p_0 (v_1 + p_1 (v_2 + ...)), Horner from the top digit (exact in 128 bits)
-    unsigned __int128 S = (uint32_t)v[NMOD - 1];
-#pragma unroll
-    for (int l = NMOD - 2; l >= 0; --l) S = S * (uint64_t)kMod(l) + (uint32_t)v[l];
-    const unsigned __int128 Pp = prod_moduli();
-    const unsigned __int128 half = Pp >> 1;  // P odd: S in (P/2, P) represents S - P < 0
-    const bool neg = S > half;
-    const unsigned __int128 mag = neg ? (Pp - S) : S;
-    double d = u128_to_double_rn(mag);
+    bool neg;
+    double d = (nmod && *nmod == NMOD - 1) ? crt_value<NMOD - 1>(Racc, per, e, neg) : crt_value<NMOD>(Racc, per, e, neg);
     // per-row exponents, or (shared layout) the one global exponent in mx[0]
     d = ldexp(d, row_exponent(mx[global_mx ? 0 : i]) + row_exponent(mx[global_mx ? 0 : j]) - 2 * b);
     if (neg) d = -d;
@@ -1163,7 +1179,8 @@ struct ModeGemm {
         }
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const int64_t tot = (int64_t)NMOD * p.ntiles * PN * PM;
-        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, first ? 1 : 0);
+        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, p.ntiles, nchunks, first ? 1 : 0,
+                                                                          nullptr);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1176,14 +1193,14 @@ struct ModeGemm {
         TK_CUDA(cudaStreamSynchronize(st));
         if (sh.allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
         TK_PROF(TUCKER_PROF_I8_CRT, st);
-        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, p.ntiles, 0, 0);
+        k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, p.ntiles, 0, 0, nullptr);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
     int crt(double* G) {
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad, 0);
+        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad, 0, nullptr);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1308,7 +1325,7 @@ __global__ void __launch_bounds__(256, 4) k_i8_residues_all(const double* __rest
 }
 
 struct SharedPlan {
-    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc, off_utab, total;
+    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc, off_utab, off_rn, off_nmod, total;
     int b;
 };
 
@@ -1384,6 +1401,10 @@ SharedPlan shared_plan(const int64_t n[3]) {
     off += 256;  // the dynamic schedule's unit counter (unit_counter(utab))
     w.off_utab = off;
     off += ub;
+    w.off_rn = off;  // per mode: partial sums of a bound on the largest row sum of squares (k_i8_nmod)
+    off += align_up(3 * 64 * sizeof(double), 256);
+    w.off_nmod = off;  // moduli per mode (k_i8_nmod)
+    off += 256;
     w.total = off;
     return w;
 }
@@ -1412,6 +1433,8 @@ int shared_map(CUtensorMap* map, const int64_t n[3], int m, int8_t* R) {
     return TUCKER_OK;
 }
 
+int shared_nmod(const int64_t n[3], char* base, const SharedPlan& w, bool valid, cudaStream_t st);
+
 // One pass: global exponent + residues of the whole tensor (mx: the row maxima of all modes).
 int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, char* base, const SharedPlan& w,
                     cudaStream_t st) {
@@ -1425,7 +1448,7 @@ int shared_residues(const int64_t n[3], const double* F, const uint32_t* mx, cha
     k_i8_residues_all<<<grid, 256, 0, st>>>(F, N, gw, w.b, reinterpret_cast<int8_t*>(base + w.off_R),
                                             reinterpret_cast<int*>(base + w.off_flag));
     TK_CHECK_LAUNCH();
-    return TUCKER_OK;
+    return shared_nmod(n, base, w, false, st);  // no row norms on this route: every modulus
 }
 
 // ---- The fill and the shared residues in one pass (centred grids, n3 % 16 == 0).  F is even in
@@ -1466,7 +1489,7 @@ __global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const doubl
                                                          const double* __restrict__ x2, int64_t n1, int64_t n2,
                                                          int64_t n3, double* __restrict__ F, int8_t* __restrict__ R,
                                                          const uint32_t* __restrict__ gmax, int b,
-                                                         int* __restrict__ bad) {
+                                                         int* __restrict__ bad, const int* __restrict__ nmod) {
     __shared__ double cheb[kChebIntervals * kChebN];
     if (kp.family == TUCKER_MATERN && kp.closed == 0)
         for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
@@ -1474,6 +1497,8 @@ __global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const doubl
     double sa, sbb;
     row_scale(*gmax, b, sa, sbb);
     const double lim = ldexp(1.0, b);
+    // residue planes a Gram reads: all NMOD unless every mode takes NMOD - 1 moduli (k_i8_nmod)
+    const int nplanes = (nmod[0] == NMOD - 1 && nmod[1] == NMOD - 1 && nmod[2] == NMOD - 1) ? NMOD - 1 : NMOD;
     const double* xa = x2;
     const double* xb = x2 + n1;
     const double* xc = x2 + n1 + n2;
@@ -1509,9 +1534,104 @@ __global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const doubl
             out[2 * w] = R + rows[w] * n3 + k0;
             out[2 * w + 1] = R + rows[w] * n3 + (n3 - 8 - k0);
         }
-        ok &= residues8_slots<8>(v, sa, sbb, out, N, lim);
+        ok &= residues8_slots<8>(v, sa, sbb, out, N, lim, nplanes);
     }
     if (!ok) atomicExch(bad, 1);
+}
+
+// Row norms of the octant fill's tensor (R21).  C(r) is non-increasing in r for every
+// family the library evaluates (Matern, p-Slater, spectral density — the property k_i8_gmax_eval
+// already relies on), so on a centred grid the mode-m unfolding row nearest the centre dominates
+// every other row entry by entry (same offsets in the other two axes, larger radius elsewhere): its
+// norm is the largest of mode m.  Grid (kNormBlocks, 3): block (z, m) sums the squares of that row
+// over its share of the first halves of the other two axes (values evaluated bitwise as the fill
+// evaluates them) into part[m][z]; k_i8_nmod adds the partials in fixed order, each entry counted
+// 4 times (an upper bound when an axis is odd).  Runs before the fill, so the fill can skip the
+// residue plane no Gram reads.
+constexpr int kNormBlocks = 48;
+__global__ void __launch_bounds__(256) k_i8_central_norms(KParams kp, const double* __restrict__ cheb_g,
+                                                         const double* __restrict__ x2, int64_t n1, int64_t n2,
+                                                         int64_t n3, double* __restrict__ part) {
+    __shared__ double cheb[kChebIntervals * kChebN];
+    __shared__ double red[8];
+    __shared__ int64_t cidx;
+    if (kp.family == TUCKER_MATERN && kp.closed == 0)
+        for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    const int m = blockIdx.y;
+    const int64_t nn[3] = {n1, n2, n3};
+    const double* ax[3] = {x2, x2 + n1, x2 + n1 + n2};
+    if (threadIdx.x == 0) {  // the node nearest the centre (first minimum of x^2)
+        int64_t c = 0;
+        for (int64_t i = 1; i < nn[m]; ++i)
+            if (ax[m][i] < ax[m][c]) c = i;
+        cidx = c;
+    }
+    __syncthreads();
+    const double xm = ax[m][cidx];
+    const int p = m == 0 ? 1 : 0, q = m == 2 ? 1 : 2;  // the other two axes (p < q)
+    const int64_t hp = (nn[p] + 1) / 2, hq = (nn[q] + 1) / 2;
+    double s = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < hp * hq; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = e / hq, c = e % hq;  // index on axis p, on axis q
+        const double xi = m == 0 ? xm : ax[0][a];
+        const double yj = m == 1 ? xm : (m == 0 ? ax[1][a] : ax[1][c]);
+        const double zk = m == 2 ? xm : ax[2][c];
+        const double v = eval_point(kp, cheb, __dadd_rn(__dadd_rn(xi, yj), zk));  // the fill's association
+        s = fma(v, v, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[m * kNormBlocks + blockIdx.x] = t;
+    }
+}
+
+// Moduli per mode for the shared layout (R20 + DESIGN.md R21): |S_ij| <= ||x_i|| ||x_j|| with
+// ||x_i|| <= 2^(b-E) ||a_i|| + sqrt(K) / 2 (each rint moves an entry by <= 1/2), so NMOD - 1 moduli
+// recover S exactly when (2^(b-E) max_i ||a_i|| + sqrt(K) / 2)^2 < P' / 2, P' their product — for
+// a function tensor whose unfolding rows are far from flat (the Matern/Slater workloads with a
+// correlation length below the box) instead of the worst case K 2^(2b).  rn[m][0, kNormBlocks):
+// partial sums (k_i8_central_norms) of a bound on max_i ||a_i||^2 of mode m (valid != 0), else
+// NMOD for every mode.  A NaN / Inf bound keeps NMOD.
+__global__ void k_i8_nmod(const double* __restrict__ rn, int64_t n1, int64_t n2, int64_t n3,
+                          const uint32_t* __restrict__ gmax, int b, int valid, int* __restrict__ nmod) {
+    if (threadIdx.x != 0) return;
+    double P1 = 1.0;  // the product of the first NMOD - 1 moduli (rounded; the margins cover it)
+    for (int l = 0; l < NMOD - 1; ++l) P1 *= (double)kMod(l);
+    const double s = ldexp(1.0, b - row_exponent(*gmax));
+    const int64_t nn[3] = {n1, n2, n3};
+    const int64_t N = n1 * n2 * n3;
+    for (int a = 0; a < 3; ++a) {
+        double A2 = 0.0;
+        if (valid) {
+            for (int z = 0; z < kNormBlocks; ++z) A2 += rn[a * kNormBlocks + z];
+            A2 *= 4.0;  // each octant entry stands for 4 entries of its row
+        }
+        const double nx = s * sqrt(A2 * (1.0 + 1e-9)) + 0.5 * sqrt((double)(N / nn[a]));
+        const bool fewer = valid && nx * nx * (1.0 + 1e-9) < 0.5 * P1 * (1.0 - 1e-9);  // false for NaN
+        nmod[a] = fewer ? NMOD - 1 : NMOD;
+    }
+}
+
+inline bool nmod_forced_full() {  // env TUCKER_I8_NMOD=16: always every modulus (test knob)
+    static const bool f = [] {
+        const char* e = std::getenv("TUCKER_I8_NMOD");
+        return e && std::atoi(e) == NMOD;
+    }();
+    return f;
+}
+
+// k_i8_nmod on the plan's slots (valid: rn holds the three modes' row-norm bounds).
+int shared_nmod(const int64_t n[3], char* base, const SharedPlan& w, bool valid, cudaStream_t st) {
+    k_i8_nmod<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(base + w.off_rn), n[0], n[1], n[2],
+                                reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
+                                (valid && !nmod_forced_full()) ? 1 : 0, reinterpret_cast<int*>(base + w.off_nmod));
+    TK_CHECK_LAUNCH();
+    return TUCKER_OK;
 }
 
 int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* F, double* nodes_x2, double* cheb,
@@ -1523,11 +1643,17 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
     uint32_t* gw = reinterpret_cast<uint32_t*>(base + w.off_gmax);
     k_i8_gmax_eval<<<1, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, gw);
     TK_CHECK_LAUNCH();
+    // the moduli first (central-row norms, R21): the fill then skips a residue plane no Gram reads
+    k_i8_central_norms<<<dim3(kNormBlocks, 3), 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3,
+                                                             reinterpret_cast<double*>(base + w.off_rn));
+    TK_CHECK_LAUNCH();
+    TK_RC(shared_nmod(g.n, base, w, true, st));
     const int64_t items = ((n1 + 1) / 2) * ((n2 + 1) / 2) * (n3 / 16);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 16));
     k_fill_octant_res<<<(unsigned)blocks, 256, 0, st>>>(kp, cheb, nodes_x2, n1, n2, n3, F,
                                                          reinterpret_cast<int8_t*>(base + w.off_R), gw, w.b,
-                                                         reinterpret_cast<int*>(base + w.off_flag));
+                                                         reinterpret_cast<int*>(base + w.off_flag),
+                                                         reinterpret_cast<const int*>(base + w.off_nmod));
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
@@ -1536,7 +1662,7 @@ int shared_fill_residues(const tucker_grid& g, const tucker_kernel& kn, double* 
 // (the whole tensor, or a plane chunk of it whose mode-m rows are complete): one k_i8_gemm launch
 // over all its K (exact int32 per unit of <= KCH columns) and the fold into Racc (first: Racc starts at 0).
 int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* Racc, int2* utab, bool first,
-                cudaStream_t st) {
+                cudaStream_t st, const int* nmod = nullptr) {
     int nJ;
     const int rows = (int)c[m];
     const int ntiles = count_tiles(c[m], nJ);
@@ -1550,7 +1676,7 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* 
     const int kbu = unit_kblocks(nkb, rows);
     const int nchunks = (int)ceil_div(nkb, (int64_t)kbu);
     GemmArgs ga{rows, nJ, ntiles, nug, nchunks, NMOD * nchunks * nug, nkb * BKB, P, utab, m + 1,
-                (int)ceil_div(c[2], (int64_t)BKB), nkb, kbu, gemm_sched(utab, st)};
+                (int)ceil_div(c[2], (int64_t)BKB), nkb, kbu, gemm_sched(utab, st), nmod};
     const int grid = 2 * std::min(ga.nunits, kNumSMs / 2);
     {
         TK_PROF(TUCKER_PROF_I8_GEMM, st);
@@ -1559,30 +1685,32 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* 
     }
     TK_PROF(TUCKER_PROF_I8_CRT, st);
     const int64_t tot = (int64_t)NMOD * ntiles * PN * PM;
-    k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, first ? 1 : 0);
+    k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(P, Racc, ntiles, nchunks, first ? 1 : 0, nmod);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
 
 // G_m (n_m x n_m, both triangles) from the folded residue sums, with the global exponent.
 int shared_crt(int64_t nm, const int32_t* Racc, const uint32_t* gmax, int b, const int* flag, double* G,
-               cudaStream_t st) {
+               cudaStream_t st, const int* nmod = nullptr) {
     TK_PROF(TUCKER_PROF_I8_CRT, st);
     int nJ;
     const int ntiles = count_tiles(nm, nJ);
     const dim3 cg((unsigned)ceil_div(nm, 32), (unsigned)ceil_div(nm, 8));
-    k_i8_crt<<<cg, 256, 0, st>>>(Racc, gmax, (int)nm, nJ, ntiles, b, G, flag, 1);
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, gmax, (int)nm, nJ, ntiles, b, G, flag, 1, nmod);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
 
 // G_m from the shared residues of the whole tensor.
+// The number of moduli of mode m comes from k_i8_nmod (run by whoever wrote the residues).
 int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w, double* G, cudaStream_t st) {
     int32_t* Racc = reinterpret_cast<int32_t*>(base + w.off_Racc);
+    const int* nmod = reinterpret_cast<const int*>(base + w.off_nmod) + m;
     TK_RC(shared_gemm(n, m, reinterpret_cast<const int8_t*>(base + w.off_R), reinterpret_cast<int8_t*>(base + w.off_P),
-                      Racc, reinterpret_cast<int2*>(base + w.off_utab), true, st));
+                      Racc, reinterpret_cast<int2*>(base + w.off_utab), true, st, nmod));
     return shared_crt(n[m], Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
-                      reinterpret_cast<const int*>(base + w.off_flag), G, st);
+                      reinterpret_cast<const int*>(base + w.off_flag), G, st, nmod);
 }
 
 // ---- a-7 on the shared layout (F never stored): the residues of plane chunks generated straight
@@ -1755,7 +1883,8 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
                 TK_CUDA(cudaStreamSynchronize(st));
                 if (shard->allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
                 TK_PROF(TUCKER_PROF_I8_CRT, st);
-                k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0);
+                k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0,
+                                                                                  nullptr);
                 TK_CHECK_LAUNCH();
             }
             TK_RC(shared_crt(n[m], Racc, gw, w.b, flag, G, st));
@@ -1856,6 +1985,15 @@ int launch_gram_i8_hosvd(const int64_t n[3], const double* F, double* const G[3]
 size_t gram_i8_hosvd_ws_bytes(const int64_t n[3]) { return gram_i8_ws_bytes(n); }
 const int* gram_i8_flag_slot(const int64_t n[3], const void* ws) {
     return reinterpret_cast<const int*>(static_cast<const char*>(ws) + i8::ws_plan(n).off_flag);
+}
+int gram_i8_moduli(const int64_t n[3], const void* ws, int32_t* out, cudaStream_t st) {
+    if (i8::shared_ok(n)) {
+        TK_CUDA(cudaMemcpyAsync(out, static_cast<const char*>(ws) + i8::shared_plan(n).off_nmod, 3 * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+    } else {
+        for (int m = 0; m < 3; ++m) out[m] = i8::NMOD;
+    }
+    return TUCKER_OK;
 }
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + i8::ws_plan(n).off_mx);

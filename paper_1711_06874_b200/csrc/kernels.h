@@ -83,6 +83,9 @@ int launch_gram_i8_fused_modes(const int64_t n[3], const I8Gen& gen, double* G, 
 // Device int of the INT8 workspace: 1 if an input value fell outside the scheme window (stale
 // row maxima or non-finite F; the Gram is then NaN), reset at the start of every Gram call.
 const int* gram_i8_flag_slot(const int64_t n[3], const void* ws);
+// Moduli per mode of the INT8 Grams formed in ws (shared layout: k_i8_nmod's device slots, copied
+// asynchronously on st — valid after the stream synchronises; per-mode layout: 16).
+int gram_i8_moduli(const int64_t n[3], const void* ws, int32_t* out, cudaStream_t st);
 // prep: 0 nothing precomputed; 1 the row maxima are already in the workspace's slot
 // (gram_i8_rowmax_slot; e.g. written by the fill) — the row-maxima pass is skipped; 2 the shared
 // layout's residues and global exponent are already in the workspace (launch_fill_prepare of this

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtucker_b200.so")
+LIB_PATH = os.environ.get("TUCKER_LIB_PATH") or os.path.join(_PKG, "libtucker_b200.so")  # (env: A/B runs)
 
 MATERN, SLATER, MATERN_SPECTRAL = 0, 1, 2
 GRAM_AUTO, GRAM_DMMA, GRAM_INT8, GRAM_INT8_ROWSCALED = 0, 1, 2, 3
@@ -52,7 +52,7 @@ class CKernel(ctypes.Structure):
 class CInfo(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32 * 3), ("converged", ctypes.c_int32 * 3), ("block", ctypes.c_int32 * 3),
                 ("sweeps", ctypes.c_int32 * 3), ("resid", ctypes.c_double * 3), ("lambda1", ctypes.c_double * 3),
-                ("k_resolved", ctypes.c_int32 * 3)]
+                ("k_resolved", ctypes.c_int32 * 3), ("moduli", ctypes.c_int32 * 3)]
 
     def as_dict(self) -> dict:
         return {k: list(getattr(self, k)) for k, _ in self._fields_}

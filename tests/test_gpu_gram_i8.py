@@ -355,6 +355,13 @@ def test_fill_prepare_equals_separate_passes(T, g, k):
     a = T.hosvd_prepared(g, r, F, ws)
     b = T.hosvd(g, r, F)
     assert a.rc == 0 and b.rc == 0
+    # the prepared route bounds the unfoldings' row norms and forms the Grams with 15 moduli where
+    # (2^(b-E) max ||a_i|| + sqrt(K)/2)^2 < P_15 / 2 (R21); the plain route always takes 16 — the
+    # exact integer Grams, hence every output, are bitwise the same
+    assert b.info["moduli"] == [16, 16, 16]
+    assert all(x in (15, 16) for x in a.info["moduli"]), a.info["moduli"]
+    if tuple(g.n) == (256, 256, 256):
+        assert a.info["moduli"] == [15, 15, 15]
     for m in range(3):
         assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m]), m
     assert torch.equal(a.core, b.core)
@@ -362,3 +369,19 @@ def test_fill_prepare_equals_separate_passes(T, g, k):
     with pytest.raises(T.TuckerError) as e:
         T.fill_prepare(off, k, (4, 4, 4))
     assert e.value.code == 7
+
+
+def test_fill_prepare_flat_tensor_keeps_16_moduli(T):
+    """R21's bound must fall back to all 16 moduli when the unfolding rows are nearly flat at full
+    scale: sigma2 = 1.99 (max F just below 2^1, so |x| reaches ~2^50) and ell = 1000 on 384^3 —
+    (2^(b-E) ||a_i||)^2 ~ K 2^100 = 2^117.2 exceeds P_15 / 2 = 2^116.5.  The Grams are still exact
+    (bitwise those of the plain route)."""
+    g, k, r = GridSpec.cube(384, 1.0), KernelSpec.matern(0.5, 1000.0, 1.99), (4, 4, 4)
+    F, ws = T.fill_prepare(g, k, r)
+    a = T.hosvd_prepared(g, r, F, ws)
+    b = T.hosvd(g, r, F)
+    assert a.rc in (0, 5) and b.rc == a.rc  # (5: the noise-level trailing pairs of a near rank-1 G)
+    assert a.info["moduli"] == [16, 16, 16]
+    for m in range(3):
+        assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m]), m
+    assert torch.equal(a.core, b.core)
