@@ -197,10 +197,13 @@ TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], 
 /* a-2 + the INT8 route's inputs in one pass (centred grids with n3 % 16 == 0 under the shared
  * residue layout, R20; else TUCKER_ERR_UNSUPPORTED): F (dev) <- the collocation tensor, and into
  * ws — the tucker_hosvd workspace of (grid, r), the calling thread's engine — the global exponent
- * and the 16 residue planes of F.  The octant fill evaluates N/8 values (F is even in every index)
+ * and the residue planes of F.  The octant fill evaluates N/8 values (F is even in every index)
  * and converts each to its residues once, storing value and residue bytes at the 8 mirrored
- * positions: the residue pass over F is gone.  Follow it with tucker_hosvd_prepared on the same
- * F and ws. */
+ * positions: the residue pass over F is gone.  Before the fill, the unfoldings' largest row norms
+ * (the rows nearest the centre: C(r) is non-increasing in r) choose the moduli per mode (DESIGN.md
+ * R21): 15 where (2^(b-E) max ||a_i|| + sqrt(K)/2)^2 < P_15 / 2 — the Gram is still exact — else
+ * 16; the 16th plane is not written when no mode reads it.  Follow it with tucker_hosvd_prepared
+ * on the same F and ws. */
 TUCKER_API int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F,
                         void* ws, size_t ws_bytes, void* stream);
 /* tucker_hosvd on a workspace prepared by tucker_fill_prepare for this very F (the caller guarantees
