@@ -1554,20 +1554,14 @@ __global__ void __launch_bounds__(256) k_i8_central_norms(KParams kp, const doub
                                                          int64_t n3, double* __restrict__ part) {
     __shared__ double cheb[kChebIntervals * kChebN];
     __shared__ double red[8];
-    __shared__ int64_t cidx;
     if (kp.family == TUCKER_MATERN && kp.closed == 0)
         for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
+    __syncthreads();
     const int m = blockIdx.y;
     const int64_t nn[3] = {n1, n2, n3};
     const double* ax[3] = {x2, x2 + n1, x2 + n1 + n2};
-    if (threadIdx.x == 0) {  // the node nearest the centre (first minimum of x^2)
-        int64_t c = 0;
-        for (int64_t i = 1; i < nn[m]; ++i)
-            if (ax[m][i] < ax[m][c]) c = i;
-        cidx = c;
-    }
-    __syncthreads();
-    const double xm = ax[m][cidx];
+    // the node nearest the centre: (n - 1) / 2 on a centred grid (nodes mirror-exact, R2)
+    const double xm = ax[m][(nn[m] - 1) / 2];
     const int p = m == 0 ? 1 : 0, q = m == 2 ? 1 : 2;  // the other two axes (p < q)
     const int64_t hp = (nn[p] + 1) / 2, hq = (nn[q] + 1) / 2;
     double s = 0.0;
@@ -1727,7 +1721,8 @@ __global__ void __launch_bounds__(256) k_gen_res_chunk(KParams kp, const double*
                                                        const double* __restrict__ x2, int64_t n1, int64_t n2,
                                                        int64_t n3, int ax, int64_t p0, int64_t pc,
                                                        int8_t* __restrict__ R, const uint32_t* __restrict__ gmax,
-                                                       int b, int* __restrict__ bad) {
+                                                       int b, int* __restrict__ bad, const int* __restrict__ nmod,
+                                                       int mode_mask) {
     __shared__ double cheb[kChebIntervals * kChebN];
     if (kp.family == TUCKER_MATERN && kp.closed == 0)
         for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
@@ -1744,6 +1739,11 @@ __global__ void __launch_bounds__(256) k_gen_res_chunk(KParams kp, const double*
     const int64_t qk = MIR ? n3 / 16 : n3 / 8;
     const int64_t total = pc * hfree * qk;
     const size_t plane = (size_t)c0 * c1 * n3;
+    // planes the Grams of the modes in mode_mask read (k_i8_nmod): NMOD - 1 if every one skips the last
+    bool fewer = true;
+    for (int m = 0; m < 3; ++m)
+        if (mode_mask >> m & 1) fewer &= nmod[m] == NMOD - 1;
+    const int nplanes = fewer ? NMOD - 1 : NMOD;
     bool ok = true;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
          it += (int64_t)gridDim.x * blockDim.x) {
@@ -1763,17 +1763,17 @@ __global__ void __launch_bounds__(256) k_gen_res_chunk(KParams kp, const double*
             const int64_t row1 = ax == 0 ? a * n2 + fm : fm * pc + a;
             int8_t* const out[4] = {R + row0 * n3 + k0, R + row0 * n3 + (n3 - 8 - k0), R + row1 * n3 + k0,
                                     R + row1 * n3 + (n3 - 8 - k0)};
-            ok &= residues8_slots<4>(v, sa, sbb, out, plane, lim);
+            ok &= residues8_slots<4>(v, sa, sbb, out, plane, lim, nplanes);
         } else {
             int8_t* const out[1] = {R + row0 * n3 + k0};
-            ok &= residues8_slots<1>(v, sa, sbb, out, plane, lim);
+            ok &= residues8_slots<1>(v, sa, sbb, out, plane, lim, nplanes);
         }
     }
     if (!ok) atomicExch(bad, 1);
 }
 
 struct FusedSharedPlan {
-    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc[2], off_utab, total;
+    size_t off_mx, off_flag, off_gmax, off_R, off_P, off_Racc[2], off_utab, off_rn, off_nmod, total;
     int b;
     int64_t pc[2];  // planes per chunk: i-chunks (modes 1, 2), j-chunks (mode 0)
 };
@@ -1822,6 +1822,10 @@ FusedSharedPlan fused_shared_plan(const int64_t n[3]) {
     off += 256;  // the dynamic schedule's unit counter (unit_counter(utab))
     w.off_utab = off;
     off += ub;
+    w.off_rn = off;  // central-row norm partials (k_i8_central_norms, centred grids)
+    off += align_up(3 * 64 * sizeof(double), 256);
+    w.off_nmod = off;  // moduli per mode (k_i8_nmod)
+    off += 256;
     w.total = off;
     return w;
 }
@@ -1839,6 +1843,18 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
     TK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
     k_i8_gmax_eval<<<1, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2], gw);  // max F = C(r_min)
     TK_CHECK_LAUNCH();
+    // moduli per mode (R21): on centred grids from the central rows' norms, else all 16 (the
+    // chunk generator skips the residue plane no Gram of its chunk axis reads)
+    int* nmod = reinterpret_cast<int*>(base + w.off_nmod);
+    const bool cen = gen.kp.centred != 0 && !nmod_forced_full();
+    if (cen) {
+        k_i8_central_norms<<<dim3(kNormBlocks, 3), 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2],
+                                                                 reinterpret_cast<double*>(base + w.off_rn));
+        TK_CHECK_LAUNCH();
+    }
+    k_i8_nmod<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(base + w.off_rn), n[0], n[1], n[2], gw, w.b,
+                                cen ? 1 : 0, nmod);
+    TK_CHECK_LAUNCH();
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
     int8_t* P = reinterpret_cast<int8_t*>(base + w.off_P);
     int2* utab = reinterpret_cast<int2*>(base + w.off_utab);
@@ -1850,6 +1866,8 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
         if (!nm) continue;
         const int64_t planes = ax == 0 ? n[0] : n[1], pc = w.pc[ax];
         bool first[2] = {true, true};
+        // a residue plane every Gram of this chunk axis skips need not be written: NMOD - 1 planes
+        // when the centred bound holds for every mode served (the kernel reads nmod on the device)
         for (int64_t p0 = 0, cidx = 0; p0 < planes; p0 += pc, ++cidx) {
             if (sharded && !shard->owns(cidx)) continue;
             const int64_t pcc = std::min(pc, planes - p0);
@@ -1861,15 +1879,17 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
                 const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), (int64_t)kNumSMs * 8));
                 if (mir)
                     k_gen_res_chunk<true><<<(unsigned)blocks, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1], n[2],
-                                                                           ax, p0, pcc, R, gw, w.b, flag);
+                                                                           ax, p0, pcc, R, gw, w.b, flag,
+                                                                           nmod, ax == 0 ? 0x6 : 0x1);
                 else
                     k_gen_res_chunk<false><<<(unsigned)blocks, 256, 0, st>>>(gen.kp, gen.cheb, gen.x2, n[0], n[1],
-                                                                            n[2], ax, p0, pcc, R, gw, w.b, flag);
+                                                                            n[2], ax, p0, pcc, R, gw, w.b, flag,
+                                                                            nmod, ax == 0 ? 0x6 : 0x1);
                 TK_CHECK_LAUNCH();
             }
             for (int q = 0; q < nm; ++q) {
                 TK_RC(shared_gemm(c, modes[q], R, P, reinterpret_cast<int32_t*>(base + w.off_Racc[q]), utab, first[q],
-                                  st));
+                                  st, nmod + modes[q]));
                 first[q] = false;
             }
         }
@@ -1884,10 +1904,10 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
                 if (shard->allreduce(Racc, tot, TUCKER_DT_INT32, TUCKER_RED_SUM) != 0) return TUCKER_ERR_COLLECTIVE;
                 TK_PROF(TUCKER_PROF_I8_CRT, st);
                 k_i8_reduce<<<(unsigned)ceil_div(tot / 16, 256), 256, 0, st>>>(nullptr, Racc, count_tiles(n[m], nJ), 0, 0,
-                                                                                  nullptr);
+                                                                                  nmod + m);
                 TK_CHECK_LAUNCH();
             }
-            TK_RC(shared_crt(n[m], Racc, gw, w.b, flag, G, st));
+            TK_RC(shared_crt(n[m], Racc, gw, w.b, flag, G, st, nmod + m));
             TK_RC(after_mode(m));
         }
     }
