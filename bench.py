@@ -66,6 +66,9 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------------- clocks ----
+CLOCK_INTERVAL_S = float(os.environ.get("BENCH_CLOCK_INTERVAL_MS", "10")) / 1000.0
+
+
 class ClockSampler:
     """SM clock and clock-event reasons sampled every ~10 ms through NVML (nvidia-smi's 100 ms loop
     as the fallback).  Started before the warm-up, it keeps only the samples taken between
@@ -115,7 +118,7 @@ class ClockSampler:
                 self.samples.append((time.time(), sm, mx, {nm for bit, nm in bits if m & bit}))
             except Exception:
                 pass
-            self.stop.wait(0.01)
+            self.stop.wait(CLOCK_INTERVAL_S)
 
     def _read_smi(self):
         for line in self.proc.stdout:
