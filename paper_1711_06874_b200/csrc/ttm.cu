@@ -549,8 +549,11 @@ __host__ __device__ inline int ld_mod(int w, int target) {  // smallest ld >= w 
 //   Wp[(i * JE + jt)][kb][64][16] (kmap + swizzle, zeros elsewhere)
 // so that k_err fetches a whole tile with one cp.async.bulk.  Fragment-load leading dimensions
 // are 4 mod 16 doubles: a half-warp's 16 fragment addresses (4 rows x 4 k) hit 16 distinct
-// 8-byte bank slots.
-__global__ void __launch_bounds__(NT) k_err_w(const ErrArgs g, double* __restrict__ Wp) {
+// 8-byte bank slots.  A CTA takes WSLABS slabs of one row tile: the U2 tile and the zero padding of
+// the output tile are set up once (every slab writes the same positions), X[i] of the next slab is
+// loaded while the current tile is stored.
+constexpr int WSLABS = 4;
+__global__ void __launch_bounds__(NT) k_err_w(const ErrArgs g, double* __restrict__ Wp, int64_t nslabs) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const int KB = g.KB, R = g.R, r2 = g.r2;
     const int r2p = (r2 + 7) & ~7, Rp = (R + 7) & ~7, ldu = ld_mod(r2p, 4), ldx = ld_mod(Rp, 4);
@@ -559,39 +562,68 @@ __global__ void __launch_bounds__(NT) k_err_w(const ErrArgs g, double* __restric
     double* sX = sU2 + BM * ldu;                        // [r2p][ldx]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, q = lane & 3;
     const int full16 = R / 16, rem = R % 16;
-    const int64_t i = blockIdx.y, j0 = (int64_t)blockIdx.x * BM, M = g.n2;
+    const int64_t j0 = (int64_t)blockIdx.x * BM, M = g.n2;
     for (int e = tid; e < KB * BM * 16; e += NT) sW[e] = 0.0;
     for (int e = tid; e < BM * r2p; e += NT) {
         const int row = e / r2p, b = e - row * r2p;
         sU2[row * ldu + b] = (j0 + row < M && b < r2) ? g.U2[(j0 + row) * r2 + b] : 0.0;
     }
-    const double* Xi = g.X + (g.i_off + i) * (int64_t)r2 * R;
-    for (int e = tid; e < r2p * Rp; e += NT) {
-        const int b = e / Rp, c = e - b * Rp;
-        sX[b * ldx + c] = (b < r2 && c < R) ? Xi[b * R + c] : 0.0;
-    }
-    __syncthreads();
-    const int tnn = Rp / 8;
-    for (int t = warp; t < (BM / 8) * tnn; t += NT / 32) {
-        const int mt = (t / tnn) * 8, nt = (t % tnn) * 8;
-        double d[2] = {0.0, 0.0};
-        const double* pa = sU2 + (mt + r) * ldu + q;
-        const double* pb = sX + q * ldx + nt + r;
-        for (int k = 0; k < r2p; k += 4) dmma(d, pa[k], pb[k * ldx]);
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int c = nt + 2 * q + u;
-            if (c < R) {
-                int kb, local;
-                kmap_forward(c, full16, rem, kb, local);
-                sW[kb * BM * 16 + swz(mt + r, local)] = d[u];
+    for (int e = tid; e < r2p * ldx; e += NT) sX[e] = 0.0;  // padding rows / columns stay zero
+    __syncthreads();  // (before any thread writes X values over the zeros)
+    const int tnn = Rp / 8;  // <= 8 (R <= 64)
+    const int mt0 = warp * 16;  // this warp's two 8-row m-tiles: BM / 8 = 8 tiles over 4 warps
+    for (int64_t i = (int64_t)blockIdx.y * WSLABS; i < min(nslabs, (int64_t)(blockIdx.y + 1) * WSLABS); ++i) {
+        const double* Xi = g.X + (g.i_off + i) * (int64_t)r2 * R;
+        if ((R & 1) == 0) {  // X[i] is contiguous (r2 x R): coalesced 16-byte loads, a pair never straddles rows
+            const double2* X2 = reinterpret_cast<const double2*>(Xi);
+            for (int e = tid; e < r2 * R / 2; e += NT) {
+                const int b = (2 * e) / R, c = 2 * e - b * R;
+                const double2 v = X2[e];
+                sX[b * ldx + c] = v.x;
+                sX[b * ldx + c + 1] = v.y;
+            }
+        } else {
+            for (int e = tid; e < r2 * R; e += NT) {
+                const int b = e / R, c = e - b * R;
+                sX[b * ldx + c] = Xi[e];
             }
         }
+        __syncthreads();  // X ready; the previous tile's store is done with sW
+        // 2 m-tiles x tnn n-tiles per warp, all accumulators live: 2 tnn independent DMMA chains
+        double acc[2][8][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nn = 0; nn < 8; ++nn) acc[mi][nn][0] = acc[mi][nn][1] = 0.0;
+        for (int k = 0; k < r2p; k += 4) {
+            const double a0 = sU2[(mt0 + r) * ldu + k + q], a1 = sU2[(mt0 + 8 + r) * ldu + k + q];
+#pragma unroll
+            for (int nn = 0; nn < 8; ++nn)
+                if (nn < tnn) {
+                    const double bb = sX[(k + q) * ldx + nn * 8 + r];
+                    dmma(acc[0][nn], a0, bb);
+                    dmma(acc[1][nn], a1, bb);
+                }
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nn = 0; nn < 8; ++nn)
+                if (nn < tnn)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int c = nn * 8 + 2 * q + u;
+                        if (c < R) {
+                            int kb, local;
+                            kmap_forward(c, full16, rem, kb, local);
+                            sW[kb * BM * 16 + swz(mt0 + 8 * mi + r, local)] = acc[mi][nn][u];
+                        }
+                    }
+        __syncthreads();  // W tile complete; sX free
+        double2* dst = reinterpret_cast<double2*>(Wp + ((size_t)i * gridDim.x + blockIdx.x) * (size_t)(KB * BM * 16));
+        const double2* src = reinterpret_cast<const double2*>(sW);
+        for (int e = tid; e < KB * BM * 8; e += NT) dst[e] = src[e];
     }
-    __syncthreads();
-    double2* dst = reinterpret_cast<double2*>(Wp + ((size_t)i * gridDim.x + blockIdx.x) * (size_t)(KB * BM * 16));
-    const double2* src = reinterpret_cast<const double2*>(sW);
-    for (int e = tid; e < KB * BM * 8; e += NT) dst[e] = src[e];
 }
 
 // One CTA = slab i, rows j0..j0+63 (grid = (ceil(n2/64), n1)), 4 warps as 2 (M) x 2 (N) of
@@ -804,7 +836,7 @@ int launch_error_impl(const int64_t n[3], const int32_t r[3], const double* F, c
     auto block = [&](const double* Fb, int64_t ns, int64_t i_off) -> int {
         errk::ErrArgs a{Fb, U2, X, Up, partial, n[1], n[2], r[1], r[2], KB, i_off};
         const dim3 grid((unsigned)JE, (unsigned)ns);
-        errk::k_err_w<<<grid, errk::NT, smw, st>>>(a, Wp);
+        errk::k_err_w<<<dim3((unsigned)JE, (unsigned)ceil_div(ns, (int64_t)errk::WSLABS)), errk::NT, smw, st>>>(a, Wp, ns);
         TK_CHECK_LAUNCH();
         errk::k_err<<<grid, errk::NT, sm, st>>>(a, Wp);
         TK_CHECK_LAUNCH();
