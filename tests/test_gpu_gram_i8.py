@@ -385,3 +385,45 @@ def test_fill_prepare_flat_tensor_keeps_16_moduli(T):
     for m in range(3):
         assert torch.equal(a.U[m], b.U[m]) and torch.equal(a.sigma[m], b.sigma[m]), m
     assert torch.equal(a.core, b.core)
+
+
+MODULI = [253, 251, 249, 247, 245, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191]
+
+
+@pytest.mark.parametrize("g,k", [(GridSpec.cube(256, 1.0), KernelSpec.matern(1.5, 0.2)),
+                                 (GridSpec((129, 131, 64), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0)), KernelSpec.matern(0.7, 0.3)),
+                                 (GridSpec((96, 80, 48), (-1.0,) * 3, (1.0,) * 3), KernelSpec.slater(1.0, 0.2)),
+                                 (GridSpec.cube(144, 1.0), KernelSpec.spectral(0.1, 0.4)),
+                                 (GridSpec.cube(320, 1.0), KernelSpec.matern(0.5, 1000.0, 1.99)),
+                                 (GridSpec.cube(384, 1.0), KernelSpec.matern(0.5, 1000.0, 1.99))])
+def test_r21_modulus_count_against_true_row_norms(T, g, k):
+    """R21 checked against the tensor itself: from the TRUE row norms of every unfolding (numpy on
+    the filled tensor), (2^(b-E) max_i ||a_i|| + sqrt(K)/2)^2 is the bound that makes 15 moduli
+    exact.  Whenever the prepared route took 15 moduli for a mode, that bound must hold with the
+    true norms (the central-row shortcut may only be conservative: it takes 16 at most where the
+    true bound is within its 1e-9 margins), and where the true bound holds with room (factor 1.01)
+    it must have taken 15."""
+    r = (4, 4, 4)
+    F, ws = T.fill_prepare(g, k, r)
+    a = T.hosvd_prepared(g, r, F, ws)
+    assert a.rc in (0, 5)
+    A = F.cpu().numpy()
+    shared, b = T.i8_layout(g)
+    assert shared
+    E = int(np.frexp(np.max(np.abs(A)))[1])  # max |a| < 2^E
+    P15 = 1
+    for p in MODULI[:15]:
+        P15 *= p
+    for m in range(3):
+        U = unfold(A, m)
+        K = U.shape[1]
+        amax = float(np.sqrt(np.max(np.sum(U * U, axis=1))))
+        nx = 2.0 ** (b - E) * amax + 0.5 * np.sqrt(K)
+        ok15 = nx * nx < P15 / 2
+        got = a.info["moduli"][m]
+        assert got in (15, 16), got
+        if got == 15:
+            assert ok15, (m, np.log2(nx * nx), np.log2(P15 / 2))
+        elif nx * nx * 1.01 < P15 / 2:
+            pytest.fail(f"mode {m}: 16 moduli although the true bound holds ({np.log2(nx * nx):.3f} < "
+                        f"{np.log2(P15 / 2):.3f})")
