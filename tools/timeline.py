@@ -34,7 +34,7 @@ def main():
 
     def one(k):
         T.fill_prepare(g, k, rr, F, ws)
-        res = T.hosvd_prepared(g, rr, F, ws)
+        res = T.hosvd_prepared(g, rr, F, ws, sync=os.environ.get("TIMELINE_ASYNC") is None)
         return T.error(g, rr, F, res.U, res.core, ws)
 
     for k in kernels[:2]:
