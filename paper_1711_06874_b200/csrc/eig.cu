@@ -28,10 +28,12 @@ constexpr int kThreads = 1024;
 constexpr int kBatch = 8;
 constexpr int kMaxIters = 96;
 // Asynchronous completion (info == NULL): the iterations are enqueued up front, each exiting at
-// once after convergence; 48 bounds the launches (the workloads converge in 3-8, the slowest
-// measured case in 55 before the R15 tolerance); a solve still unconverged there returns its
-// last iterate, as the synchronous path does at kMaxIters (where NOCONV is reported).
-constexpr int kMaxItersAsync = 48;
+// once after convergence, but every launch of a converged solve still costs ~4 us on its side
+// stream, ahead of the core that waits for U.  24 bounds them: the workloads
+// converge in 3-8 iterations (tools/eig_iters_survey.py: at most 4 over configs 1-4, the f4
+// kernels and Table 2's grids); a solve still unconverged there returns its last iterate, as the
+// synchronous path does at kMaxIters (where NOCONV is reported).
+constexpr int kMaxItersAsync = 24;
 constexpr int kMinIters = 3;
 // Residual tolerance relative to theta_1: 1e-14 (SURVEY a-4), floored at 4 sqrt(n) eps — the
 // rounding level of evaluating G v itself in FP64 (DESIGN reading R15); at n <= 1024 the floor
