@@ -498,19 +498,16 @@ int launch_eig_begin(int64_t n, const double* G, int r, double* U, double* lambd
             k_omega<<<64, 256, 0, st>>>(Vt, p, n);
         }
         TK_CHECK_LAUNCH();
-        TK_RC(gemm_vg(q, G, nullptr, st));
-        TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
+        // one cluster launch per iteration: W = G V is formed inside it (the cluster's own SMs)
+        TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st, G));
         // iterations 1 .. kMinIters-2 are plain power steps (V <- CGS2(G V), no Rayleigh–Ritz):
         // the Ritz rotation does not change the subspace, and a single Jacobi solve of the dense
         // H at the end replaces the per-iteration ones (a warm start skips them)
-        for (int w = 1; w < kMinIters - 1 && !V0; ++w) {
-            TK_RC(gemm_vg(q, G, nullptr, st));
-            TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st));
-        }
-        for (int it = kMinIters - 1; it < kMinIters + 3; ++it) {  // first batch: 4 Rayleigh-Ritz steps
-            TK_RC(gemm_vg(q, G, dst, st));
-            TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst, st));
-        }
+        for (int w = 1; w < kMinIters - 1 && !V0; ++w)
+            TK_RC(launch_rr_cluster(n, p, r, 0, 0, 1, Vt, Wt, U, lambda, sigma, dst, st, G));
+        for (int it = kMinIters - 1; it < kMinIters + 3; ++it)  // first batch: 4 Rayleigh-Ritz steps
+            TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, Vt, Wt, U, lambda, sigma, dst, st,
+                                    G));
     } else {
         k_omega<<<64, 256, 0, st>>>(Vt, p, n);
         TK_CHECK_LAUNCH();
@@ -548,11 +545,11 @@ int launch_eig_end(int64_t n, const double* G, int r, double* U, double* lambda,
         }
         while (!hs.done && it < kMaxIters) {
             for (int b = 0; b < kBatch && it < kMaxIters; ++b, ++it) {
-                TK_RC(gemm_vg(q, G, dst, st));
                 if (cl) {
                     TK_RC(launch_rr_cluster(n, p, r, it, it == kMaxIters - 1 ? 1 : 0, 0, q.Vt, q.Wt, U, lambda, sigma,
-                                            dst, st));
+                                            dst, st, G));
                 } else {
+                    TK_RC(gemm_vg(q, G, dst, st));
                     RRArgs a{n, p, r, it, it == kMaxIters - 1 ? 1 : 0, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, dst};
                     const size_t sm = rr_smem(p);
                     k_rr<<<1, kThreads, sm, st>>>(a);
@@ -606,10 +603,10 @@ int launch_eig_rest(int64_t n, const double* G, int r, double* U, double* lambda
     }
     for (int it = cl ? kMinIters + 3 : kBatch; it < kMaxItersAsync; ++it) {
         const int last = it == kMaxItersAsync - 1 ? 1 : 0;
-        TK_RC(gemm_vg(q, G, q.dst, st));
         if (cl) {
-            TK_RC(launch_rr_cluster(n, p, r, it, last, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst, st));
+            TK_RC(launch_rr_cluster(n, p, r, it, last, 0, q.Vt, q.Wt, U, lambda, sigma, q.dst, st, G));
         } else {
+            TK_RC(gemm_vg(q, G, q.dst, st));
             RRArgs a{n, p, r, it, last, q.Vt, q.Wt, q.VrT, q.YT, U, lambda, sigma, q.dst};
             k_rr<<<1, kThreads, rr_smem(p), st>>>(a);
             TK_CHECK_LAUNCH();

@@ -2,7 +2,8 @@
 // thread-block cluster whose CTAs each own 128 rows of the n x p basis.
 //
 // The HOSVD factor U_m is the top-r_m eigenbasis of G_m.  Per iteration (see eig.cu
-// for the driver loop):  W = G V (k_gemm_vg, many CTAs), then this kernel:
+// for the driver loop) one launch of this kernel: W = G V for the CTA's rows (gv_rows, DMMA; or
+// from k_gemm_vg's Wt when G is not given), then:
 //   H = V^T W            local 4x4-blocked partial sums over the CTA's rows, cluster-summed in
 //                        rank order through distributed shared memory (deterministic; every
 //                        CTA ends with the bitwise same H)
@@ -72,7 +73,8 @@ struct Args {
     int64_t n;
     int p, r, it, last, orth_only;
     double* Vt;        // p x n (in: V; out: next V)
-    const double* Wt;  // p x n  (G V, or G Omega when orth_only)
+    const double* Wt;  // p x n  (G V, or G Omega when orth_only); unused when G is set
+    const double* G;   // n x n (nullable): W = G V formed here, each CTA its own rows (see k_rr_cluster)
     double* U;         // n x r
     double* lambda;    // r (nullable)
     double* sigma;     // r (nullable)
@@ -215,6 +217,74 @@ __device__ void cgs2_cluster(cg::cluster_group& cl, Smem& s, int& round, int p, 
     }
 }
 
+// W rows of this CTA, W[i][j] = sum_k G[i0 + i][k] V[k][j] (V = Vt^T: every CTA's rows, written by
+// the previous launch; no CTA overwrites Vt before the cluster barrier of its first reduction, so
+// all reads of this launch precede it), on DMMA (m8n8k4): warp w owns rows 8w .. 8w + 7 and all
+// p <= 64 columns; k in chunks of GV_KC staged through the Jacobi scratch (H, Q: two stages),
+// the next chunk's loads in flight under the current chunk's MMAs.  Forming W here, on the
+// cluster's own SMs, makes one launch per iteration that needs no SMs beyond the cluster's (a
+// persistent Gram on a concurrent stream holds every other SM).
+constexpr int GV_KC = 16, GV_LD = GV_KC + 4;  // row stride 20 doubles: fragment loads 2 wavefronts
+__device__ void gv_rows(const Args& a, Smem& s, int64_t i0, int nrows) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, r = lane >> 2, q = lane & 3;
+    const int64_t n = a.n;
+    const int p = a.p;
+    // two stages (s.H, s.Q), each: G chunk [RB][GV_LD] then V chunk [P][GV_LD]
+    // per thread: 4 G values (rows t/4 .. of the 128 x 16 chunk) and 2 V values (64 x 16)
+    double g4[4], v2[2];
+    auto load = [&](int64_t k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = t + u * NT, i = e / GV_KC, kk = e % GV_KC;
+            g4[u] = (i < nrows && k0 + kk < n) ? a.G[(i0 + i) * n + k0 + kk] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = t + u * NT, j = e / GV_KC, kk = e % GV_KC;
+            v2[u] = (j < p && k0 + kk < n) ? a.Vt[(int64_t)j * n + k0 + kk] : 0.0;
+        }
+    };
+    auto store = [&](double* b) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = t + u * NT;
+            b[(e / GV_KC) * GV_LD + e % GV_KC] = g4[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = t + u * NT;
+            b[RB * GV_LD + (e / GV_KC) * GV_LD + e % GV_KC] = v2[u];
+        }
+    };
+    double acc[8][2];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    const int64_t nch = (n + GV_KC - 1) / GV_KC;
+    load(0);
+    store(s.H);
+    __syncthreads();
+    for (int64_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) load((c + 1) * GV_KC);
+        const double* b = (c & 1) ? s.Q : s.H;
+#pragma unroll
+        for (int kq = 0; kq < GV_KC; kq += 4) {
+            const double av = b[(8 * warp + r) * GV_LD + kq + q];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt)
+                if (8 * nt < p) dmma(acc[nt], av, b[RB * GV_LD + (8 * nt + r) * GV_LD + kq + q]);
+        }
+        if (c + 1 < nch) store((c & 1) ? s.H : s.Q);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = 8 * nt + 2 * q + u;
+            s.Y[sw(8 * warp + r, j)] = j < p ? acc[nt][u] : 0.0;
+        }
+}
+
 __global__ void __launch_bounds__(NT, 1) k_rr_cluster(Args a) {
     cg::cluster_group cl = cg::this_cluster();
     if (a.st->done) return;  // uniform across the cluster (written by an earlier launch)
@@ -232,9 +302,10 @@ __global__ void __launch_bounds__(NT, 1) k_rr_cluster(Args a) {
     for (int e = t; e < RB * P; e += NT) {
         const int j = e / RB, i = e % RB;
         const bool ok = i < nrows && j < p;
-        s.Y[sw(i, j)] = ok ? a.Wt[(size_t)j * n + i0 + i] : 0.0;
+        if (!a.G) s.Y[sw(i, j)] = ok ? a.Wt[(size_t)j * n + i0 + i] : 0.0;
         if (!a.orth_only) s.V[sw(i, j)] = ok ? a.Vt[(size_t)j * n + i0 + i] : 0.0;
     }
+    if (a.G) gv_rows(a, s, i0, nrows);  // W rows = G[i0 .., :] V (V of every CTA, from global)
     __syncthreads();
 
     if (!a.orth_only) {
@@ -612,9 +683,9 @@ int launch_svd_cluster(int64_t n, int p, int r, const double* B, double* Vout, d
 }
 
 int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
-                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st) {
+                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st, const double* G) {
     const int cs = eig_cluster_size(n);
-    eigc::Args a{n, p, r, it, last, orth_only, Vt, Wt, U, lambda, sigma, static_cast<eigc::State*>(state)};
+    eigc::Args a{n, p, r, it, last, orth_only, Vt, Wt, G, U, lambda, sigma, static_cast<eigc::State*>(state)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(eigc::NT);

@@ -149,8 +149,10 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
 
 // Cluster Rayleigh–Ritz step (eig_cluster.cu); n <= 2048.
 bool eig_cluster_supported(int64_t n);
+// G (nullable): W = G V formed inside the cluster kernel (Wt unused) — one launch per iteration.
 int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
-                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st);
+                      double* U, double* lambda, double* sigma, void* state, cudaStream_t st,
+                      const double* G = nullptr);
 
 // NEXT f2: left singular vectors of B (n x p, n <= 2048, p <= 64) by one-sided Jacobi in a cluster.
 int launch_svd_cluster(int64_t n, int p, int r, const double* B, double* Vout, double* U, double* sigma,
