@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-Graph replay of the step")
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 (512^3 x 16 settings) line")
     ap.add_argument("--no-f4", action="store_true", help="skip the NEXT f4 workloads line")
+    ap.add_argument("--no-lowrank", action="store_true", help="skip the TTM / error stages at ranks 10 and 20")
     ap.add_argument("--no-parity", action="store_true", help="skip the per-config T1-T4 deltas vs the oracle")
     ap.add_argument("--fused-n", type=int, default=2048)
     ap.add_argument("--gram-engine", default="auto", choices=["auto", "dmma", "int8"],
@@ -573,6 +574,9 @@ def run_ours(args, rank, world, local):
                                                      (x.cpu() for x in acc.sigma)]}
     if not args.no_f4 and world == 1:
         result["f4"] = run_f4(T, grid, ranks, F, ws, stream)
+    if not args.no_lowrank and world == 1:
+        result["lowrank"] = run_lowrank(T, grid, kern, F, stream, p64=fp64_peak()[0],
+                                        hbm=float(measured_peaks().get("hbm_gbs", 6460.5)))
     if not args.no_parity and world == 1 and n == 1024 and rr == 40:
         T.fill(grid, kern, F, ws, stream)  # (f4 reused F)
         result["parity"] = run_parity(T, stream, F)
@@ -788,6 +792,50 @@ def run_parity(T, stream, F=None) -> dict:
         del F4, ws
         torch.cuda.empty_cache()
     return out
+
+
+def run_lowrank(T, grid, kern, F, stream, p64: float, hbm: float) -> dict:
+    """The TTM and error stages where HBM binds them (2 r3 flop per 8 B below the FP64 ridge: r3 <= 23,
+    SURVEY §8(d)): the headline step at ranks (10,10,10) and (20,20,20), asynchronous HOSVD, stage
+    times from the library's stage timer over five steps after three warm-up steps."""
+    import torch
+    N = grid.points
+    out = []
+    for r in (10, 20):
+        rr3 = (r, r, r)
+        ws = T.workspace(grid, rr3)
+        results = []
+
+        def step():
+            T.fill_prepare(grid, kern, rr3, F, ws, stream)
+            res = T.hosvd_prepared(grid, rr3, F, ws, stream, sync=False)
+            results.append(res)  # (outputs stay alive until the synchronisation below)
+            return T.error(grid, rr3, F, res.U, res.core, ws, stream)
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        T.profile_read()
+        T.profile_enable(True)
+        for _ in range(5):
+            e = step()
+        torch.cuda.synchronize()
+        T.profile_enable(False)
+        prof = T.profile_read()
+        st = {name: ms / 5 for name, (ms, cnt) in prof.items() if cnt}
+        t_hbm = 8.0 * N / (hbm * 1e9) * 1e3
+        t_fp = 2.0 * N * r / (p64 * 1e12) * 1e3
+        row = {"ranks": list(rr3), "E": float(e.cpu()[0]), "hbm_roofline_ms": t_hbm, "fp64_roofline_ms": t_fp,
+               "binding": "hbm" if t_hbm >= t_fp else "fp64"}
+        for name in ("ttm", "error"):
+            if name in st:
+                row[name + "_ms"] = st[name]
+                row[name + "_frac_of_binding"] = max(t_hbm, t_fp) / st[name]
+        out.append(row)
+        del ws, results
+        torch.cuda.empty_cache()
+    return {"grid": list(grid.n), "what": "TTM and error stages at ranks where HBM binds them (in-step, stage timer)",
+            "rows": out}
 
 
 def run_f4(T, grid, ranks, F, ws, stream) -> dict:
