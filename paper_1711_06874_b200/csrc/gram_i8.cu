@@ -54,9 +54,18 @@ constexpr int RT_ROWS = 32, RT_K = 128;  // residue tile
 
 // run-time modulus tables for the k_i8_gemm epilogue (index l is not a compile-time constant there)
 __constant__ int c_mod[NMOD] = {253, 251, 249, 247, 245, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191};
-__constant__ double c_invmod[NMOD] = {1.0 / 253, 1.0 / 251, 1.0 / 249, 1.0 / 247, 1.0 / 245, 1.0 / 241, 1.0 / 239,
-                                      1.0 / 233, 1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 211, 1.0 / 199, 1.0 / 197,
-                                      1.0 / 193, 1.0 / 191};
+// Integer reduction mod p_l (Barrett, 32-bit): for a 32-bit sum v with |v| < 2^30, v' = v + c_off[l]
+// (c_off = p ceil(2^30 / p), a multiple of p, so v' is in [0, 2^32) and v' = v mod p), then
+// q = umulhi(v', c_mg[l]) with c_mg = floor(2^32 / p) is floor(v' / p) or one less: v' - q p is in
+// [0, 2p), one conditional subtraction.  All on the integer pipe (the FP64 route cost two FP64
+// conversions per element in the int8 Gram's epilogue).
+__constant__ uint32_t c_off[NMOD] = {1073741867u, 1073741856u, 1073742033u, 1073741851u, 1073741900u, 1073742001u, 1073741916u, 1073742055u, 1073741841u, 1073742007u, 1073741878u, 1073741864u, 1073741912u, 1073741999u, 1073741990u, 1073741835u};
+__constant__ uint32_t c_mg[NMOD] = {16976155u, 17111423u, 17248864u, 17388531u, 17530478u, 17821441u, 17970574u, 18433336u, 18755315u, 18920560u, 19259943u, 20355295u, 21582750u, 21801864u, 22253716u, 22486739u};
+__device__ __forceinline__ uint32_t mod_p(int v, uint32_t p, uint32_t off, uint32_t mg) {  // v mod p in [0, p)
+    const uint32_t w = (uint32_t)v + off;
+    const uint32_t r = w - __umulhi(w, mg) * p;
+    return r >= p ? r - p : r;
+}
 
 __host__ __device__ constexpr int pow2mod(int e, int p) {
     int64_t r = 1;
@@ -886,8 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             // output segments: a full/half tile is columns [0, N) at TMEM column c; merged tiles
             // are two segments at TMEM columns 0.. and 256..
             const int nseg = x.merged ? 2 : 1;
-            const int pmod = c_mod[x.l];
-            const double invp = c_invmod[x.l];
+            const uint32_t pmod = (uint32_t)c_mod[x.l], poff = c_off[x.l], pmg = c_mg[x.l];
             for (int sg = 0; sg < nseg; ++sg) {
                 const int t = x.s[sg].t;
                 const int N = x.merged ? x.s[sg].N : (x.ns == 2 ? 256 + x.s[1].N : x.s[0].N);
@@ -905,13 +913,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
                           "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(taddr + tc0 + c0));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    // exact int32 chunk sum -> its balanced representative mod p, v - p rint(v / p)
-                    // in [-p/2, p/2] (|.| <= 126: one byte), the quotient from FP64 (|v| < 2^31)
+                    // exact int32 chunk sum (|v| <= 126^2 2^16 < 2^30) -> a representative mod p in
+                    // [-127, 127] (one byte): r = v mod p in [0, p), minus p when r >= 128
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const int vi = (int)v[j];
-                        const int q = __double2int_rn((double)vi * invp);
-                        P[(size_t)(c0 + j) * PM + row] = (int8_t)(vi - q * pmod);
+                        const uint32_t r = mod_p((int)v[j], pmod, poff, pmg);
+                        P[(size_t)(c0 + j) * PM + row] = (int8_t)((int)r - (r >= 128u ? (int)pmod : 0));
                     }
                 }
             }
@@ -956,14 +963,9 @@ __global__ void __launch_bounds__(256) k_i8_reduce(const int8_t* __restrict__ P,
 #pragma unroll
         for (int q = 0; q < 16; ++q) s[q] += (int)(signed char)(wd[q >> 2] >> (8 * (q & 3)));
     }
-    const int p = c_mod[l];
-    const double ip = c_invmod[l];
+    const uint32_t p = (uint32_t)c_mod[l], poff = c_off[l], pmg = c_mg[l];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        int r = s[q] - p * __double2int_rn((double)s[q] * ip);  // in [-p/2 - 1, p/2 + 1]
-        r += r < 0 ? p : 0;
-        s[q] = r >= p ? r - p : r;
-    }
+    for (int q = 0; q < 16; ++q) s[q] = (int)mod_p(s[q], p, poff, pmg);  // |s| <= p + 127 nchunks
 #pragma unroll
     for (int q = 0; q < 4; ++q) ra[q] = make_int4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
 }
