@@ -779,7 +779,8 @@ static size_t err_w_smem(const int32_t r[3]) {
 }
 static size_t err_smem(const int32_t r[3]) {
     const int KB = (int)ceil_div(r[2], 16);
-    return (size_t)KB * (errk::BM + 2 * errk::BN) * 16 * 8 + 3 * 8;
+    // (rounded up to 1 KB: mbarriers at the end of an odd-sized region were seen to fault)
+    return align_up((size_t)KB * (errk::BM + 2 * errk::BN) * 16 * 8 + 3 * 8, 1024);
 }
 
 static size_t packed_err_bytes(const int64_t n[3], const int32_t r[3]) {
