@@ -152,6 +152,16 @@ TUCKER_API int tucker_i8_layout(const tucker_grid* grid, int32_t* shared, int32_
 enum { TUCKER_GRAM_AUTO = 0, TUCKER_GRAM_DMMA = 1, TUCKER_GRAM_INT8 = 2, TUCKER_GRAM_INT8_ROWSCALED = 3 };
 TUCKER_API int tucker_set_gram_engine(int32_t engine);
 TUCKER_API int32_t tucker_get_gram_engine(void);
+/* TTM engine of the core on the INT8 hosvd route (tucker_hosvd, tucker_hosvd_rowmax,
+ * tucker_hosvd_prepared, tucker_approximate with INT8 Grams in the shared layout), per calling
+ * thread.  TUCKER_TTM_AUTO (default): the first product T1 = F x3 U3^T (P:578-579, 2 N r3 flops)
+ * on the INT8 tensor cores by six balanced base-256 digits per operand, the 26 digit pairs of
+ * weight >= 256^-6 (R22: input rounding 2^-47 of max|F| and of each column's max|U3|,
+ * truncation <= 2^-52 per term), where r3 <= 48, n3 % 16 == 0 and n3 <= 16384; the FP64 DMMA TTM
+ * otherwise.  TUCKER_TTM_DMMA forces the DMMA TTM.  INVALID_ARG for other values. */
+enum { TUCKER_TTM_AUTO = 0, TUCKER_TTM_DMMA = 1 };
+TUCKER_API int tucker_set_ttm_engine(int32_t engine);
+TUCKER_API int32_t tucker_get_ttm_engine(void);
 TUCKER_API int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,
                 size_t ws_bytes, void* stream);
 

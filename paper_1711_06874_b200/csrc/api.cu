@@ -232,9 +232,17 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
                                 cudaStreamWaitEvent(st, ev[3], 0) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[5], 0) != cudaSuccess))
             rc = TUCKER_ERR_CUDA;
-        if (rc == TUCKER_OK)
-            rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
-                                      nullptr, T2);
+        if (rc == TUCKER_OK) {  // TTM1 on the INT8 tensor cores where it applies (R22), else DMMA
+            rc = TUCKER_ERR_UNSUPPORTED;
+            const uint32_t* gm = nullptr;
+            void* reg = nullptr;
+            size_t rb = 0;
+            if (ttm_engine() != TUCKER_TTM_DMMA && gram_i8_ttm_scratch(g->n, at(ws, L.i8), &gm, &reg, &rb))
+                rc = launch_ttm12_i8(g->n, r, F, U[1], U[2], gm, T2, reg, rb, st);
+            if (rc == TUCKER_ERR_UNSUPPORTED)
+                rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
+                                          nullptr, T2);
+        }
         if (rc == TUCKER_OK) rc = eig_end(0);
         if (rc == TUCKER_OK && (cudaEventRecord(ev[4], sideB) != cudaSuccess ||
                                 cudaStreamWaitEvent(st, ev[4], 0) != cudaSuccess))
@@ -427,6 +435,14 @@ int tucker_set_gram_engine(int32_t engine) {
 }
 
 int32_t tucker_get_gram_engine(void) { return gram_engine(); }
+
+int tucker_set_ttm_engine(int32_t engine) {
+    if (engine != TUCKER_TTM_AUTO && engine != TUCKER_TTM_DMMA) return TUCKER_ERR_INVALID_ARG;
+    ttm_engine() = engine;
+    return TUCKER_OK;
+}
+
+int32_t tucker_get_ttm_engine(void) { return ttm_engine(); }
 
 size_t tucker_workspace_size_i8(const tucker_grid* grid) {
     if (check_grid(grid) != TUCKER_OK || !gram_i8_supported(grid->n)) return 0;

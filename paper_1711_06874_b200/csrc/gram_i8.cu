@@ -2017,6 +2017,15 @@ int gram_i8_moduli(const int64_t n[3], const void* ws, int32_t* out, cudaStream_
     }
     return TUCKER_OK;
 }
+bool gram_i8_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes) {
+    if (!i8::shared_ok(n)) return false;
+    const i8::SharedPlan sp = i8::shared_plan(n);
+    char* base = static_cast<char*>(ws);
+    *gmax = reinterpret_cast<const uint32_t*>(base + sp.off_gmax);
+    *region = base + sp.off_R;
+    *bytes = sp.off_P - sp.off_R;
+    return true;
+}
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + i8::ws_plan(n).off_mx);
 }

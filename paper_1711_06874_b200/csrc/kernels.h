@@ -103,6 +103,17 @@ uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws);
 cudaStream_t side_stream(int which);
 // Engine selection (tucker_set_gram_engine): TUCKER_GRAM_AUTO / _DMMA / _INT8.
 int& gram_engine();
+// TTM engine of the INT8 hosvd route (tucker_set_ttm_engine): TUCKER_TTM_AUTO / _DMMA.
+int& ttm_engine();
+// a-5 with T1 = F x3 U3^T on the INT8 tensor cores (ttm_i8.cu, R22): T2 out; UNSUPPORTED
+// when the shape does not apply or `region` is too small (the caller then runs the DMMA TTM).
+bool ttm_i8_applies(const int64_t n[3], const int32_t r[3], const double* F);
+size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]);
+int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
+                    const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st);
+// The INT8 shared route's global exponent word and its residue region (free once the three Grams
+// are enqueued): false when the materialised Grams do not use the shared layout.
+bool gram_i8_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes);
 bool gram_use_i8(const int64_t n[3]);
 // Materialised INT8 Grams of this grid use the shared residue layout (one residue pass, one global
 // exponent; R20) — and its integer width b.

@@ -29,7 +29,7 @@ EXPORTS = ("tucker_workspace_size", "tucker_workspace_size_fill", "tucker_fill",
            "tucker_workspace_size_als",
            "tucker_als", "tucker_workspace_size_sym", "tucker_hosvd_sym", "tucker_workspace_size_accurate",
            "tucker_hosvd_accurate", "tucker_workspace_size_i8", "tucker_gram_i8", "tucker_i8_scheme", "tucker_i8_layout",
-           "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_profile_enable", "tucker_profile_read",
+           "tucker_set_gram_engine", "tucker_get_gram_engine", "tucker_set_ttm_engine", "tucker_get_ttm_engine", "tucker_profile_enable", "tucker_profile_read",
            "tucker_workspace_size_multigrid", "tucker_multigrid", "tucker_last_launch_count", "tucker_strerror")
 
 
@@ -94,6 +94,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "tucker_i8_layout": (ctypes.c_int, [pg, P(ctypes.c_int32), P(ctypes.c_int32)]),
         "tucker_set_gram_engine": (ctypes.c_int, [i32]),
         "tucker_get_gram_engine": (i32, []),
+        "tucker_set_ttm_engine": (ctypes.c_int, [i32]),
+        "tucker_get_ttm_engine": (i32, []),
         "tucker_profile_enable": (ctypes.c_int, [i32]),
         "tucker_profile_read": (ctypes.c_int, [P(ctypes.c_double), P(ctypes.c_int64)]),
         "tucker_eig": (ctypes.c_int, [i64, vp, i32, vp, vp, vp, sz, vp, pi]),
@@ -273,6 +275,19 @@ def set_gram_engine(engine: int) -> None:
 
 def get_gram_engine() -> int:
     return int(load().tucker_get_gram_engine())
+
+
+TTM_AUTO, TTM_DMMA = 0, 1
+
+
+def set_ttm_engine(engine: int) -> None:
+    """TTM engine of the INT8 hosvd route's core: TTM_AUTO (T1 = F x3 U3^T on the INT8 tensor cores
+    by base-256 digits where it applies, R22) or TTM_DMMA (the FP64 tensor-core TTM)."""
+    _check(load().tucker_set_ttm_engine(int(engine)), "tucker_set_ttm_engine")
+
+
+def get_ttm_engine() -> int:
+    return int(load().tucker_get_ttm_engine())
 
 
 PROF_STAGES = ("fill", "i8_rowmax", "i8_residues", "i8_gemm", "i8_crt", "dmma_gram", "eig", "ttm", "error")
