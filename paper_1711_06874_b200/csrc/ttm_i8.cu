@@ -24,9 +24,9 @@
 //               edges) per K-step into a 5-stage ring (160 KB per SM), each stage converted in
 //               place into its K-step's digit tiles and freed by the MMAs' commit;
 //   warps 2-5   epilogue: tcgen05.ld of the 7 groups, Horner in FP64, T1 rows to HBM;
-//   warp 6      B loader: the U3 digit image of each 64-k block (6 NB rows x 64 B, pre-swizzled
-//               SWIZZLE_64B) by one cp.async.bulk into a 2-stage ring;
-//   warps 7-14  converters: a fibre row's 16 doubles from the F stage (conflict-free through the
+//   warp 6      B loader: the U3 digit image of each 128-k block (6 NB rows x 128 B, pre-swizzled
+//               SWIZZLE_128B) by one cp.async.bulk into a 2-stage ring;
+//   warps 7-22  converters (two groups of 8 warps taking alternate K-steps): a fibre row's 16 doubles from the F stage (conflict-free through the
 //               swizzle), one DFMA + byte permutes per element, digit words stored over the same
 //               stage in the SWIZZLE_128B K-major A layout (two 128 x 128 B tiles per K-step:
 //               digits 0-3 and 4-5 as the four 32-byte K chunks of a row).
@@ -51,23 +51,27 @@ constexpr int NS = 5;
 constexpr uint32_t ATILE = 128 * 128;      // one SWIZZLE_128B tile / F box: 128 rows x 128 bytes
 constexpr uint32_t FBOX = ATILE;
 constexpr uint32_t STAGE = 2 * ATILE;
-constexpr int NCONV = 8;                   // converter warps
-constexpr int NT = 32 * (7 + NCONV);       // warps 0 MMA, 1 F loader, 2-5 epilogue, 6 B loader, 7.. converters
+constexpr int NCONV = 8;                   // converter warps per K-step (one per 16 fibre rows)
+constexpr int NGC = 2;                     // converter groups, alternating K-steps
+constexpr int NT = 32 * (7 + NGC * NCONV); // warps 0 MMA, 1 F loader, 2-5 epilogue, 6 B loader, 7.. converters
 constexpr uint64_t BIAS = 0x808080808080ull;
+constexpr int TQ = 4;                                        // tile-id ring depth
+constexpr int TQ_CONSUMERS = 1 + 1 + 4 + NGC * NCONV;        // MMA, B loader, epilogue and converter warps
 constexpr int MAX_R = 40;  // NB = r3 rounded up to 8, one MMA per digit (N = 6 NB <= 256)
-constexpr int SB = 2, BK = 64;             // B ring: 64-k blocks (SWIZZLE_64B rows of 64 bytes)
+constexpr int SB = 2, BK = 128;            // B ring: 128-k blocks (SWIZZLE_128B rows of 128 bytes)
 constexpr size_t smem_bytes(int NB) {
     return (size_t)NS * STAGE + (size_t)SB * ND * NB * BK + 1024;
 }
 
 struct Args {
     const double* F;         // M x n3 (fibre-major, k contiguous)
-    const uint8_t* Bimg;     // [nkb][ND * NB rows][64 B], SWIZZLE_64B image
+    const uint8_t* Bimg;     // [nkb][ND * NB rows][128 B], SWIZZLE_128B image
     const double* colscale;  // [R]: 2^(E_c - 12)
     const uint32_t* gmax;    // high word of max |F| (the INT8 route's global exponent)
     double* T1;              // T1t: n2 x n1 x R (the TTM2 GEMM's K-major operand)
     int64_t M, n1, n2, n3;
     int R, NB, nks, nkb, ntiles;
+    int* sched;  // tile counter (zero at launch): CTAs take tiles dynamically
 };
 
 __device__ __forceinline__ int exp_of(uint32_t hw) {  // E with max |F| < 2^E (gram_i8.cu row_exponent)
@@ -86,7 +90,7 @@ __device__ __forceinline__ uint32_t idesc_s8(int N) {  // D s32, A/B s8, K-major
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 __device__ __forceinline__ void mma_s8(uint32_t tmem, uint32_t a, uint32_t b, int N, uint32_t acc) {
-    const uint64_t da = desc_sw128(a), db = desc_sw64(b);
+    const uint64_t da = desc_sw128(a), db = desc_sw128(b);
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
@@ -129,13 +133,28 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
     uint8_t* sB = smem + NS * STAGE;
     // ffull: F landed (TMA); afull: digits written (converters); sempty: MMAs done (commit)
     __shared__ __align__(8) uint64_t ffull[NS], afull[NS], sempty[NS], bfull[SB], bempty[SB], tfull, tempty;
+    __shared__ __align__(8) uint64_t tq_full[TQ], tq_empty[TQ];
+    __shared__ int tq[TQ];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NB = g.NB;
     const uint32_t bstage = (uint32_t)(ND * NB * BK);
     const int nks = g.nks;
-    const int64_t ntile_cta = g.ntiles > (int)blockIdx.x ? (g.ntiles - 1 - (int)blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t nq = ntile_cta * nks;  // K-steps of this CTA (its tiles one after another)
+    // Dynamic tile schedule: the F loader takes the next tile from the global counter and posts
+    // it in a TQ-deep ring; every other role reads it there (a CTA whose SM is held by a
+    // concurrent kernel — the mode-0 eigensolve on its side stream — then takes fewer tiles).
+    auto next_tile = [&](int it) -> int {  // consumers: one thread per role unit
+        const int slot = it % TQ;
+        mbar_wait(&tq_full[slot], (uint32_t)(it / TQ) & 1u);
+        const int t = *reinterpret_cast<volatile int*>(&tq[slot]);
+        mbar_arrive(&tq_empty[slot]);
+        return t;
+    };
+    auto next_tile_warp = [&](int it) -> int {
+        int t = 0;
+        if (lane == 0) t = next_tile(it);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&ffull[s], 1);
@@ -148,6 +167,10 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
         }
         mbar_init(&tfull, 1);
         mbar_init(&tempty, 4);
+        for (int s = 0; s < TQ; ++s) {
+            mbar_init(&tq_full[s], 1);
+            mbar_init(&tq_empty[s], TQ_CONSUMERS);
+        }
         mbar_fence_init();
         tma_prefetch_desc(&mapF);
     }
@@ -165,12 +188,12 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
             const uint32_t tb = (uint32_t)(NB * BK);  // one digit block of B rows
-            int it = 0;
-            for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x, ++it) {
+            for (int it = 0;; ++it) {
+                if (next_tile(it) < 0) break;
                 mbar_wait(&tempty, it & 1);  // drained and zeroed by the epilogue
                 fence_after();
                 for (int ks = 0; ks < nks; ++ks) {
-                    const int j = ks & 1;  // K-step within the 64-k B block
+                    const int j = ks & 3;  // K-step within the 128-k B block
                     if (j == 0) mbar_wait(&bfull[bs], bph);
                     mbar_wait(&afull[as], aph);
                     fence_after();
@@ -190,7 +213,7 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
                         as = 0;
                         aph ^= 1;
                     }
-                    if (j == 1 || ks == nks - 1) {
+                    if (j == 3 || ks == nks - 1) {
                         commit(&bempty[bs]);
                         if (++bs == SB) {
                             bs = 0;
@@ -205,17 +228,25 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
         if (lane == 0) {  // F loader: two SWIZZLE_128B boxes (16 k x 128 fibres) per K-step
             int fs = 0;
             uint32_t fph = 0;
-            for (int64_t q = 0; q < nq; ++q) {
-                const int tile = (int)(blockIdx.x + (q / nks) * gridDim.x);
-                const int k0 = (int)(q % nks) * 32;
-                mbar_wait(&sempty[fs], fph ^ 1);
-                mbar_arrive_expect_tx(&ffull[fs], STAGE);
-                uint8_t* dst = sS + fs * STAGE;
-                tma_load_2d(dst, &mapF, &ffull[fs], k0, tile * 128);
-                tma_load_2d(dst + FBOX, &mapF, &ffull[fs], k0 + 16, tile * 128);
-                if (++fs == NS) {
-                    fs = 0;
-                    fph ^= 1;
+            for (int it = 0;; ++it) {
+                const int slot = it % TQ;
+                mbar_wait(&tq_empty[slot], ((uint32_t)(it / TQ) & 1u) ^ 1u);
+                int tile = atomicAdd(g.sched, 1);
+                if (tile >= g.ntiles) tile = -1;
+                tq[slot] = tile;
+                mbar_arrive(&tq_full[slot]);
+                if (tile < 0) break;
+                for (int ks = 0; ks < nks; ++ks) {
+                    const int k0 = ks * 32;
+                    mbar_wait(&sempty[fs], fph ^ 1);
+                    mbar_arrive_expect_tx(&ffull[fs], STAGE);
+                    uint8_t* dst = sS + fs * STAGE;
+                    tma_load_2d(dst, &mapF, &ffull[fs], k0, tile * 128);
+                    tma_load_2d(dst + FBOX, &mapF, &ffull[fs], k0 + 16, tile * 128);
+                    if (++fs == NS) {
+                        fs = 0;
+                        fph ^= 1;
+                    }
                 }
             }
         }
@@ -223,7 +254,7 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
         if (lane == 0) {  // B loader
             int bs = 0;
             uint32_t bph = 0;
-            for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x)
+            for (int it = 0; next_tile(it) >= 0; ++it)
                 for (int kb = 0; kb < g.nkb; ++kb) {
                     mbar_wait(&bempty[bs], bph ^ 1);
                     mbar_arrive_expect_tx(&bfull[bs], bstage);
@@ -247,8 +278,9 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
             if (lane == 0) mbar_arrive(&tempty);
         };
         zero_tmem();
-        int it = 0;
-        for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x, ++it) {
+        for (int it = 0;; ++it) {
+            const int tile = next_tile_warp(it);
+            if (tile < 0) break;
             mbar_wait(&tfull, it & 1);
             fence_after();
             const int64_t p = (int64_t)tile * 128 + row;  // fibre (i, j): T1t[j][i][:] (n2 x n1 R)
@@ -277,16 +309,21 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
     } else {  // converters: thread -> fibre row (ct / 2), k half (ct % 2) of each 32-k K-step
         // a quarter warp (one 16-byte access phase) = 8 consecutive rows of one half: distinct
         // swizzled chunks, conflict-free loads and stores
-        const int ct = tid - 224, row = (ct & 7) | ((ct >> 4) << 3), h = (ct >> 3) & 1;
+        const int gc = (tid - 224) / (32 * NCONV);  // converter group: K-steps q = gc (mod NGC)
+        const int ct = (tid - 224) % (32 * NCONV), row = (ct & 7) | ((ct >> 4) << 3), h = (ct >> 3) & 1;
         const int E = exp_of(*g.gmax);
         const double sc = ldexp(1.0, 46 - E);
         const double magic = 4503599627370496.0 + (double)BIAS;  // 2^52 + bias
         // this thread's row of F box h (128 B, 16-byte chunk u at u ^ (row % 8)) and its 16-byte
         // unit of digit s in the A tiles (unit 2 (s % 4) + h of its row, same swizzle)
         const uint32_t rbase = (uint32_t)((row >> 3) * 1024 + (row & 7) * 128);
-        int fs = 0;
-        uint32_t fph = 0;
-        for (int64_t q = 0; q < nq; ++q) {
+        for (int it = 0;; ++it) {
+          if (next_tile_warp(it) < 0) break;
+          for (int ks = 0; ks < nks; ++ks) {
+            const int64_t q = (int64_t)it * nks + ks;  // this CTA's K-step sequence
+            if ((int)(q % NGC) != gc) continue;
+            const int fs = (int)(q % NS);
+            const uint32_t fph = (uint32_t)(q / NS) & 1u;
             mbar_wait(&ffull[fs], fph);
             const uint32_t st0 = smem_u32(sS + fs * STAGE) + rbase;
             const uint32_t f0 = st0 + h * FBOX;
@@ -326,10 +363,7 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[fs]);
-            if (++fs == NS) {
-                fs = 0;
-                fph ^= 1;
-            }
+          }
         }
     }
     fence_before();
@@ -340,9 +374,9 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
     }
 }
 
-// U3 (n3 x R, row-major) -> column exponents and the SWIZZLE_64B digit image of B:
-// block kb (64 k) holds rows NB t + c (digit t of column c, most significant first), 64 bytes each
-// (k = 64 kb .. + 63), 16-byte unit u of row r at unit u ^ ((r / 2) % 4).  One CTA per column.
+// U3 (n3 x R, row-major) -> column exponents and the SWIZZLE_128B digit image of B:
+// block kb (128 k) holds rows NB t + c (digit t of column c, most significant first), 128 bytes
+// each (k = 128 kb .. + 127), 16-byte unit u of row r at unit u ^ (r % 8).  One CTA per column.
 __global__ void __launch_bounds__(256) k_u3_digits(const double* __restrict__ U3, int64_t n3, int R, int NB,
                                                    uint8_t* __restrict__ img, double* __restrict__ colscale) {
     const int c = blockIdx.x;
@@ -369,21 +403,24 @@ __global__ void __launch_bounds__(256) k_u3_digits(const double* __restrict__ U3
         const int kc = (int)(k % BK);
         for (int t = 0; t < ND; ++t) {
             const int r = NB * t + c;
-            const size_t off = (size_t)kb * bstage + (size_t)(r >> 3) * 512 + (size_t)(r & 7) * 64 +
-                               (size_t)((((kc >> 4) ^ ((r >> 1) & 3)) << 4) | (kc & 15));
+            const size_t off = (size_t)kb * bstage + (size_t)(r >> 3) * 1024 + (size_t)(r & 7) * 128 +
+                               (size_t)((((kc >> 4) ^ (r & 7)) << 4) | (kc & 15));
             img[off] = (uint8_t)(((w >> (8 * (5 - t))) & 255u) ^ 0x80u);
         }
     }
 }
 
-// T2[i][b][c] = T2p[b][i][c]
-__global__ void __launch_bounds__(256) k_t2_transpose(const double* __restrict__ T2p, int64_t n1, int r2, int R,
-                                                      double* __restrict__ T2) {
+// T2[i][b][c] = sum over the S K-slices of T2p[sl][b][i][c] (slice order)
+__global__ void __launch_bounds__(256) k_t2_transpose(const double* __restrict__ T2p, int S, int64_t n1, int r2,
+                                                      int R, double* __restrict__ T2) {
     const int64_t total = n1 * r2 * R;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / ((int64_t)r2 * R), o = t - i * r2 * R;
         const int b = (int)(o / R), c = (int)(o - (int64_t)b * R);
-        T2[t] = T2p[((int64_t)b * n1 + i) * R + c];
+        const double* p = T2p + ((int64_t)b * n1 + i) * R + c;
+        double v = p[0];
+        for (int sl = 1; sl < S; ++sl) v += p[sl * total];
+        T2[t] = v;
     }
 }
 
@@ -398,7 +435,7 @@ size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]) {
     const int NB = ((r[2] + 7) / 8) * 8;
     const int64_t nkb = ceil_div(n[2], (int64_t)t8::BK);
     return align_up((size_t)n[0] * n[1] * r[2] * 8, 1024) + align_up((size_t)nkb * t8::ND * NB * t8::BK, 1024) +
-           align_up((size_t)r[2] * 8, 256) + align_up((size_t)n[0] * r[1] * r[2] * 8, 256);
+           align_up((size_t)r[2] * 8, 256) + 256 + align_up((size_t)8 * n[0] * r[1] * r[2] * 8, 256);
 }
 
 // T2 (n1 x r2 x r3) = (F x3 U3^T) x2 U2^T with the first product on the INT8 tensor cores.
@@ -421,12 +458,15 @@ int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, con
     w += align_up(img_bytes, 1024);
     double* colscale = reinterpret_cast<double*>(w);
     w += align_up((size_t)R * 8, 256);
+    int* sched = reinterpret_cast<int*>(w);
+    w += 256;
+    TK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
     double* part = reinterpret_cast<double*>(w);
     TK_CUDA(cudaMemsetAsync(img, 0, img_bytes, st));
     k_u3_digits<<<R, 256, 0, st>>>(U3, n[2], R, NB, img, colscale);
     TK_CHECK_LAUNCH();
     Args a{F, img, colscale, gmax, T1, M, n[0], n[1], n[2], R, NB, (int)ceil_div(n[2], (int64_t)32), (int)nkb,
-           (int)ceil_div(M, (int64_t)128)};
+           (int)ceil_div(M, (int64_t)128), sched};
     CUtensorMap map;  // F as M rows x n3 doubles, boxes of 16 k x 128 fibres (SWIZZLE_128B; zero fill)
     std::memset(&map, 0, sizeof(map));
     const uint64_t dims[2] = {(uint64_t)n[2], (uint64_t)M};
@@ -438,12 +478,15 @@ int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, con
     const int grid = (int)std::min<int64_t>(a.ntiles, kNumSMs);
     k_ttm1_i8<<<grid, NT, sm, st>>>(map, a);
     TK_CHECK_LAUNCH();
-    // TTM2 as one GEMM over the transposed T1: T2p (r2 x n1 R) = U2^T (r2 x n2) T1t (n2 x n1 R),
-    // then T2[i][b][c] = T2p[b][i][c]
-    const SmallGemm g2{r[1], n[0] * R, n[1], 1, U2, 1, r[1], 0, T1, n[0] * R, 1, 0, part, n[0] * R, 1, 0, 0};
+    // TTM2 as one GEMM over the transposed T1, K = n2 split into S slices (a batch):
+    // T2p[sl] (r2 x n1 R) = U2[slice]^T T1t[slice], then T2[i][b][c] = sum_sl T2p[sl][b][i][c] in
+    // slice order (fixed, deterministic)
+    const int S = n[1] % 8 == 0 ? 8 : 1;
+    const int64_t Ks = n[1] / S, plane = n[0] * r[1] * R;
+    const SmallGemm g2{r[1], n[0] * R, Ks, S, U2, 1, r[1], Ks * r[1], T1, n[0] * R, 1, Ks * n[0] * R,
+                       part, n[0] * R, 1, plane, 0};
     TK_RC(launch_gemm(g2, st));
-    const int64_t total = n[0] * r[1] * R;
-    k_t2_transpose<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(part, n[0], r[1], R, T2);
+    k_t2_transpose<<<(unsigned)std::min<int64_t>(ceil_div(plane, 256), 4096), 256, 0, st>>>(part, S, n[0], r[1], R, T2);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
