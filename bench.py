@@ -176,6 +176,21 @@ class ClockSampler:
                 "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+def ttm_on_int8(r3: int, args) -> bool:
+    """The core's first product runs on the INT8 tensor cores (R22) on this configuration: the INT8
+    shared-layout Gram route, the default TTM engine and r3 <= 40 (n3 % 16 == 0 on every bench grid)."""
+    from paper_1711_06874_b200 import tucker as T
+    return getattr(args, "gram_engine", "auto") != "dmma" and T.get_ttm_engine() == T.TTM_AUTO and 1 <= r3 <= 40
+
+
+def ttm_i8_note(r3: int) -> str:
+    nb = (r3 + 7) // 8 * 8
+    cols = sum(((6 if s < 2 else 7 - s) * nb + 15) // 16 * 16 for s in range(6))
+    return (f"T1 = F x3 U3^T on the INT8 tensor cores (k_ttm1_i8, six base-256 digits per operand, 26 digit "
+            f"pairs; {2 * cols} int8 ops per F element executed, below the HBM time at the measured INT8 "
+            f"peak): bound by the 8 N bytes of F")
+
+
 def fp64_peak() -> tuple:
     """(TF/s, source): the measured DMMA-pipe FP64 peak (tools/fp64_peak.py ->
     profiles/fp64_peak_measured.json, sustained) or the spec-derived 37.2 TF/s."""
@@ -459,10 +474,13 @@ def run_ours(args, rank, world, local):
         if name in st:
             t_fp64 = fl / (p64 * 1e12) * 1e3
             t_hbm = 8.0 * N / (hbm * 1e9) * 1e3
+            i8 = name == "ttm" and ttm_on_int8(rr, args)
             stage_roof[name] = {"ms": st[name], "fp64_roofline_ms": t_fp64, "hbm_roofline_ms": t_hbm,
-                                "binding": "fp64" if t_fp64 > t_hbm else "hbm",
-                                "frac_of_binding": max(t_fp64, t_hbm) / st[name],
+                                "binding": "hbm" if (i8 or t_hbm >= t_fp64) else "fp64",
+                                "frac_of_binding": (t_hbm if i8 else max(t_fp64, t_hbm)) / st[name],
                                 "algorithmic": f"2 N r3 = {fl:.3e} flop, 8 N = {8 * N / 1e9:.2f} GB"}
+            if i8:
+                stage_roof[name]["engine"] = ttm_i8_note(rr)
     result = {
         "metric": METRIC, "value": whole_job_rate(N, world, ms_step), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -829,8 +847,11 @@ def run_lowrank(T, grid, kern, F, stream, p64: float, hbm: float) -> dict:
                "binding": "hbm" if t_hbm >= t_fp else "fp64"}
         for name in ("ttm", "error"):
             if name in st:
+                i8 = name == "ttm" and ttm_on_int8(r, None) and T.get_gram_engine() != T.GRAM_DMMA
                 row[name + "_ms"] = st[name]
-                row[name + "_frac_of_binding"] = max(t_hbm, t_fp) / st[name]
+                row[name + "_frac_of_binding"] = (t_hbm if i8 else max(t_hbm, t_fp)) / st[name]
+                if i8:
+                    row[name + "_engine"] = ttm_i8_note(r)
         out.append(row)
         del ws, results
         torch.cuda.empty_cache()

@@ -9,11 +9,20 @@
 #include "kernels.h"
 #include "prof.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace tk {
 
 int64_t& launch_counter() {
     static thread_local int64_t c = 0;
     return c;
+}
+
+int report_cuda(cudaError_t e, const char* file, int line) {
+    static const bool dbg = std::getenv("TUCKER_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "tucker: CUDA error at %s:%d: %s\n", file, line, cudaGetErrorString(e));
+    return TUCKER_ERR_CUDA;
 }
 
 PFN_tmapEncodeTiled tmap_encoder() {

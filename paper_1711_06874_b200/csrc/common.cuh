@@ -17,17 +17,20 @@ namespace tk {
 int64_t& launch_counter();  // per-thread count of kernel launches of the current ABI call
 #define TK_LAUNCHED() (++::tk::launch_counter())
 
-#define TK_CUDA(call)                                \
-    do {                                             \
-        cudaError_t e_ = (call);                     \
-        if (e_ != cudaSuccess) return TUCKER_ERR_CUDA; \
+// TUCKER_DEBUG=1 in the environment: a failing CUDA call is reported on stderr (file:line, error)
+int report_cuda(cudaError_t e, const char* file, int line);
+
+#define TK_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) return ::tk::report_cuda(e_, __FILE__, __LINE__);   \
     } while (0)
 
-#define TK_CHECK_LAUNCH()                                        \
-    do {                                                         \
-        TK_LAUNCHED();                                           \
-        cudaError_t e_ = cudaGetLastError();                     \
-        if (e_ != cudaSuccess) return TUCKER_ERR_CUDA;           \
+#define TK_CHECK_LAUNCH()                                                          \
+    do {                                                                           \
+        TK_LAUNCHED();                                                             \
+        cudaError_t e_ = cudaGetLastError();                                       \
+        if (e_ != cudaSuccess) return ::tk::report_cuda(e_, __FILE__, __LINE__);   \
     } while (0)
 
 #define TK_RC(call)                   \

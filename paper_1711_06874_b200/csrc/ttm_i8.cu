@@ -26,7 +26,7 @@
 //   warps 2-5   epilogue: tcgen05.ld of the 7 groups, Horner in FP64, T1 rows to HBM;
 //   warp 6      B loader: the U3 digit image of each 128-k block (6 NB rows x 128 B, pre-swizzled
 //               SWIZZLE_128B) by one cp.async.bulk into a 2-stage ring;
-//   warps 7-22  converters (two groups of 8 warps taking alternate K-steps): a fibre row's 16 doubles from the F stage (conflict-free through the
+//   warps 7-22  converters (each K-step over all 16 warps, 8 k of one fibre row per thread): a fibre row's 16 doubles from the F stage (conflict-free through the
 //               swizzle), one DFMA + byte permutes per element, digit words stored over the same
 //               stage in the SWIZZLE_128B K-major A layout (two 128 x 128 B tiles per K-step:
 //               digits 0-3 and 4-5 as the four 32-byte K chunks of a row).
@@ -51,12 +51,11 @@ constexpr int NS = 5;
 constexpr uint32_t ATILE = 128 * 128;      // one SWIZZLE_128B tile / F box: 128 rows x 128 bytes
 constexpr uint32_t FBOX = ATILE;
 constexpr uint32_t STAGE = 2 * ATILE;
-constexpr int NCONV = 8;                   // converter warps per K-step (one per 16 fibre rows)
-constexpr int NGC = 2;                     // converter groups, alternating K-steps
-constexpr int NT = 32 * (7 + NGC * NCONV); // warps 0 MMA, 1 F loader, 2-5 epilogue, 6 B loader, 7.. converters
+constexpr int NCONV = 16;                  // converter warps (each K-step: 8 fibre rows x 32 k per warp)
+constexpr int NT = 32 * (7 + NCONV);       // warps 0 MMA, 1 F loader, 2-5 epilogue, 6 B loader, 7.. converters
 constexpr uint64_t BIAS = 0x808080808080ull;
 constexpr int TQ = 4;                                        // tile-id ring depth
-constexpr int TQ_CONSUMERS = 1 + 1 + 4 + NGC * NCONV;        // MMA, B loader, epilogue and converter warps
+constexpr int TQ_CONSUMERS = 1 + 1 + 4 + NCONV;              // MMA, B loader, epilogue and converter warps
 constexpr int MAX_R = 40;  // NB = r3 rounded up to 8, one MMA per digit (N = 6 NB <= 256)
 constexpr int SB = 2, BK = 128;            // B ring: 128-k blocks (SWIZZLE_128B rows of 128 bytes)
 constexpr size_t smem_bytes(int NB) {
@@ -306,64 +305,63 @@ __global__ void __launch_bounds__(NT, 1) k_ttm1_i8(const __grid_constant__ CUten
             }
             zero_tmem();
         }
-    } else {  // converters: thread -> fibre row (ct / 2), k half (ct % 2) of each 32-k K-step
-        // a quarter warp (one 16-byte access phase) = 8 consecutive rows of one half: distinct
-        // swizzled chunks, conflict-free loads and stores
-        const int gc = (tid - 224) / (32 * NCONV);  // converter group: K-steps q = gc (mod NGC)
-        const int ct = (tid - 224) % (32 * NCONV), row = (ct & 7) | ((ct >> 4) << 3), h = (ct >> 3) & 1;
+    } else {  // converters: every K-step is split over all 16 warps (thread -> fibre row, 8-k quarter),
+              // so every converter warp consumes every stage in order and its parity waits are exact
+        // a quarter warp (one 16-byte access phase) = 8 consecutive rows of one quarter: distinct
+        // swizzled chunks; a warp holds 8 whole rows (both boxes), which it alone reads and rewrites
+        const int ct = tid - 224, qt = (ct >> 3) & 3, row = (ct & 7) | ((ct >> 5) << 3), h = qt >> 1;
         const int E = exp_of(*g.gmax);
         const double sc = ldexp(1.0, 46 - E);
         const double magic = 4503599627370496.0 + (double)BIAS;  // 2^52 + bias
-        // this thread's row of F box h (128 B, 16-byte chunk u at u ^ (row % 8)) and its 16-byte
-        // unit of digit s in the A tiles (unit 2 (s % 4) + h of its row, same swizzle)
+        // this thread's 8 doubles: chunks 4 (qt % 2) .. +3 of its row in F box h (chunk u at u ^ (row % 8));
+        // its digit bytes: 8 bytes at byte 8 (qt % 2) of unit 2 (s % 4) + h of its row (same swizzle)
         const uint32_t rbase = (uint32_t)((row >> 3) * 1024 + (row & 7) * 128);
+        int fs = 0;
+        uint32_t fph = 0;
         for (int it = 0;; ++it) {
-          if (next_tile_warp(it) < 0) break;
-          for (int ks = 0; ks < nks; ++ks) {
-            const int64_t q = (int64_t)it * nks + ks;  // this CTA's K-step sequence
-            if ((int)(q % NGC) != gc) continue;
-            const int fs = (int)(q % NS);
-            const uint32_t fph = (uint32_t)(q / NS) & 1u;
-            mbar_wait(&ffull[fs], fph);
-            const uint32_t st0 = smem_u32(sS + fs * STAGE) + rbase;
-            const uint32_t f0 = st0 + h * FBOX;
-            double x[16];
+            if (next_tile_warp(it) < 0) break;
+            for (int ks = 0; ks < nks; ++ks) {
+                mbar_wait(&ffull[fs], fph);
+                const uint32_t st0 = smem_u32(sS + fs * STAGE) + rbase;
+                const uint32_t f0 = st0 + h * FBOX;
+                double x[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
-                             : "=d"(x[2 * u]), "=d"(x[2 * u + 1])
-                             : "r"(f0 + (((uint32_t)u ^ (uint32_t)(row & 7)) << 4))
-                             : "memory");
-            // the digits overwrite the F rows just read: a warp reads and writes only its own 16
-            // rows (both halves), so the warp's own reads must be done first
-            __syncwarp();
-            uint32_t w[ND][4];  // [digit s][group of 4 k]
+                for (int u = 0; u < 4; ++u)
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
+                                 : "=d"(x[2 * u]), "=d"(x[2 * u + 1])
+                                 : "r"(f0 + (((uint32_t)(4 * (qt & 1) + u) ^ (uint32_t)(row & 7)) << 4))
+                                 : "memory");
+                __syncwarp();  // the digits overwrite the rows just read (this warp's own rows)
+                uint32_t w[ND][2];  // [digit s][group of 4 k]
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint32_t lo[4], hi[4];
+                for (int u = 0; u < 2; ++u) {
+                    uint32_t lo[4], hi[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const long long b = __double_as_longlong(fma(x[4 * u + e], sc, magic));
-                    lo[e] = (uint32_t)b;
-                    hi[e] = (uint32_t)(b >> 32);
+                    for (int e = 0; e < 4; ++e) {
+                        const long long b = __double_as_longlong(fma(x[4 * u + e], sc, magic));
+                        lo[e] = (uint32_t)b;
+                        hi[e] = (uint32_t)(b >> 32);
+                    }
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) w[5 - m][u] = digit_word(lo[0], lo[1], lo[2], lo[3], m);
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) w[1 - m][u] = digit_word(hi[0], hi[1], hi[2], hi[3], m);
                 }
 #pragma unroll
-                for (int m = 0; m < 4; ++m) w[5 - m][u] = digit_word(lo[0], lo[1], lo[2], lo[3], m);
-#pragma unroll
-                for (int m = 0; m < 2; ++m) w[1 - m][u] = digit_word(hi[0], hi[1], hi[2], hi[3], m);
+                for (int sd = 0; sd < ND; ++sd) {
+                    const uint32_t qq = (uint32_t)(2 * (sd & 3) + h) ^ (uint32_t)(row & 7);
+                    const uint32_t addr = st0 + (uint32_t)(sd >> 2) * ATILE + (qq << 4) + 8u * (uint32_t)(qt & 1);
+                    asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(w[sd][0]), "r"(w[sd][1])
+                                 : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[fs]);
+                if (++fs == NS) {
+                    fs = 0;
+                    fph ^= 1;
+                }
             }
-#pragma unroll
-            for (int s = 0; s < ND; ++s) {
-                const uint32_t qq = (uint32_t)(2 * (s & 3) + h) ^ (uint32_t)(row & 7);
-                const uint32_t addr = st0 + (uint32_t)(s >> 2) * ATILE + (qq << 4);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(w[s][0]), "r"(w[s][1]),
-                             "r"(w[s][2]), "r"(w[s][3])
-                             : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[fs]);
-          }
         }
     }
     fence_before();
@@ -472,7 +470,7 @@ int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, con
     const uint64_t dims[2] = {(uint64_t)n[2], (uint64_t)M};
     const uint64_t strides[1] = {(uint64_t)n[2] * 8};
     const uint32_t box[2] = {16, 128};
-    if (!make_tmap_f64(&map, F, 2, dims, strides, box)) return TUCKER_ERR_CUDA;
+    if (!make_tmap_f64(&map, F, 2, dims, strides, box)) return ::tk::report_cuda(cudaErrorInvalidValue, __FILE__, __LINE__);
     const size_t sm = smem_bytes(NB);
     TK_CUDA(cudaFuncSetAttribute(k_ttm1_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int grid = (int)std::min<int64_t>(a.ntiles, kNumSMs);
