@@ -158,8 +158,11 @@ TUCKER_API int32_t tucker_get_gram_engine(void);
  * on the INT8 tensor cores by six balanced base-256 digits per operand, the 26 digit pairs of
  * weight >= 256^-6 (R22: input rounding 2^-47 of max|F| and of each column's max|U3|,
  * truncation <= 2^-52 per term), where r3 <= 48, n3 % 16 == 0 and n3 <= 16384; the FP64 DMMA TTM
- * otherwise.  TUCKER_TTM_DMMA forces the DMMA TTM.  INVALID_ARG for other values. */
-enum { TUCKER_TTM_AUTO = 0, TUCKER_TTM_DMMA = 1 };
+ * otherwise.  TUCKER_TTM_DMMA forces the DMMA TTM.  TUCKER_TTM_INT8_ERROR = AUTO plus the error
+ * pass's reconstruction Ft = W U3^T on the INT8 tensor cores (tucker_error; R23: the same
+ * digit scheme, E within 2^-46 of the FP64 pass) — opt-in: measured slower than the DMMA error pass.
+ * INVALID_ARG for other values. */
+enum { TUCKER_TTM_AUTO = 0, TUCKER_TTM_DMMA = 1, TUCKER_TTM_INT8_ERROR = 2 };
 TUCKER_API int tucker_set_ttm_engine(int32_t engine);
 TUCKER_API int32_t tucker_get_ttm_engine(void);
 TUCKER_API int tucker_gram_i8(const tucker_grid* grid, int32_t mode, const double* F, double* G, void* ws,

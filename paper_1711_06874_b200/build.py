@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtucker_b200.so")
-SOURCES = ["api.cu", "fill.cu", "gram.cu", "gram_i8.cu", "eig.cu", "eig_cluster.cu", "ttm.cu", "ttm_i8.cu", "als.cu", "sym.cu", "refine.cu", "gemm.cu", "prof.cu", "multigrid.cu"]
+SOURCES = ["api.cu", "fill.cu", "gram.cu", "gram_i8.cu", "eig.cu", "eig_cluster.cu", "ttm.cu", "ttm_i8.cu", "err_i8.cu", "als.cu", "sym.cu", "refine.cu", "gemm.cu", "prof.cu", "multigrid.cu"]
 HEADERS = ["common.cuh", "fill_eval.cuh", "jacobi.cuh", "kernels.h", "prof.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

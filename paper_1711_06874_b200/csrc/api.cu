@@ -140,7 +140,7 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
     if (!i8)
         for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
     s = std::max(s, ttm_ws_bytes(n, r));
-    s = std::max(s, err_ws_bytes(n, r));
+    s = std::max(s, std::max(err_ws_bytes(n, r), err_i8_ws_bytes(n, r)));
     L.scratch_bytes = align_up(s, 256);
     off += L.scratch_bytes;
     L.outs = off;
@@ -446,7 +446,8 @@ int tucker_set_gram_engine(int32_t engine) {
 int32_t tucker_get_gram_engine(void) { return gram_engine(); }
 
 int tucker_set_ttm_engine(int32_t engine) {
-    if (engine != TUCKER_TTM_AUTO && engine != TUCKER_TTM_DMMA) return TUCKER_ERR_INVALID_ARG;
+    if (engine != TUCKER_TTM_AUTO && engine != TUCKER_TTM_DMMA && engine != TUCKER_TTM_INT8_ERROR)
+        return TUCKER_ERR_INVALID_ARG;
     ttm_engine() = engine;
     return TUCKER_OK;
 }

@@ -113,6 +113,12 @@ int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, con
                     const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st);
 // The INT8 shared route's global exponent word and its residue region (free once the three Grams
 // are enqueued): false when the materialised Grams do not use the shared layout.
+// a-6 with the reconstruction W U3^T on the INT8 tensor cores (err_i8.cu, R23); UNSUPPORTED
+// when the shape does not apply or ws is too small (the caller then runs the DMMA error pass).
+bool err_i8_applies(const int64_t n[3], const int32_t r[3], const double* F);
+size_t err_i8_ws_bytes(const int64_t n[3], const int32_t r[3]);
+int launch_error_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
+                    const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, cudaStream_t st);
 bool gram_i8_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes);
 bool gram_use_i8(const int64_t n[3]);
 // Materialised INT8 Grams of this grid use the shared residue layout (one residue pass, one global

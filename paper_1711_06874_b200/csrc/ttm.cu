@@ -801,6 +801,10 @@ size_t err_ws_bytes_slabs(const int64_t n[3], const int32_t r[3], int64_t slabs)
 int launch_error(const int64_t n[3], const int32_t r[3], const double* F, const double* U1, const double* U2,
                  const double* U3, const double* core, double* out3, void* ws, size_t ws_bytes, cudaStream_t st) {
     TK_PROF(TUCKER_PROF_ERROR, st);
+    if (ttm_engine() == TUCKER_TTM_INT8_ERROR) {  // opt-in: the reconstruction on the INT8 tensor cores (R23)
+        const int rc = launch_error_i8(n, r, F, U1, U2, U3, core, out3, ws, ws_bytes, st);
+        if (rc != TUCKER_ERR_UNSUPPORTED) return rc;
+    }
     return launch_error_impl(n, r, F, nullptr, U1, U2, U3, core, out3, ws, ws_bytes, st);
 }
 

@@ -277,12 +277,13 @@ def get_gram_engine() -> int:
     return int(load().tucker_get_gram_engine())
 
 
-TTM_AUTO, TTM_DMMA = 0, 1
+TTM_AUTO, TTM_DMMA, TTM_INT8_ERROR = 0, 1, 2
 
 
 def set_ttm_engine(engine: int) -> None:
     """TTM engine of the INT8 hosvd route's core: TTM_AUTO (T1 = F x3 U3^T on the INT8 tensor cores
-    by base-256 digits where it applies, R22) or TTM_DMMA (the FP64 tensor-core TTM)."""
+    by base-256 digits where it applies, R22), TTM_DMMA (the FP64 tensor-core TTM) or
+    TTM_INT8_ERROR (AUTO plus the error pass's reconstruction on the INT8 tensor cores, R23; opt-in)."""
     _check(load().tucker_set_ttm_engine(int(engine)), "tucker_set_ttm_engine")
 
 

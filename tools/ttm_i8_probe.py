@@ -23,7 +23,7 @@ def main():
     for r in ranks:
         rr = (r, r, r)
         ws = T.workspace(g, rr)
-        for eng in (T.TTM_AUTO, T.TTM_DMMA):
+        for eng in (T.TTM_AUTO, T.TTM_DMMA) + ((T.TTM_INT8_ERROR,) if os.environ.get("PROBE_ERR_I8") else ()):
             T.set_ttm_engine(eng)
 
             def step():
@@ -43,7 +43,7 @@ def main():
             torch.cuda.synchronize()
             T.profile_enable(False)
             prof = T.profile_read()
-            out[f"r{r}_{'int8' if eng == T.TTM_AUTO else 'dmma'}"] = {
+            out[f"r{r}_{ {T.TTM_AUTO: 'int8', T.TTM_DMMA: 'dmma'}.get(eng, 'int8_err')}"] = {
                 "stages_ms": {s: v[0] / 5 for s, v in prof.items() if v[1]}, "E": float(e[0])}
         T.set_ttm_engine(T.TTM_AUTO)
         del ws
