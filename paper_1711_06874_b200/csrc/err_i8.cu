@@ -18,7 +18,7 @@
 // of the chunk stacked by digit along N (N = 32 x digits paired), D group d at TMEM columns 32 d,
 // two TMEM buffers (224 columns each).  Warps: 0 TMEM owner + MMA issuer, 1 loader (unit schedule,
 // A image, F box {128 k, 32 fibres} by TMA and the chunk's W digit image by cp.async.bulk into a
-// 3-stage ring), 2-9 epilogue (warp -> TMEM lane quarter and 16 of the 32 fibre columns).
+// 4-stage ring; units are posted 6 ahead and their F boxes prefetched to L2), 2-9 epilogue (warp -> TMEM lane quarter and 16 of the 32 fibre columns).
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -29,7 +29,7 @@ namespace tk {
 namespace e8 {
 
 constexpr int ND = 6, NGRP = 7;
-constexpr int NS = 3;                       // stage ring
+constexpr int NS = 4;                       // stage ring
 constexpr int FC = 32;                      // fibres per unit (MMA N per digit block)
 constexpr int KT = 128;                     // k per unit (MMA M)
 constexpr uint32_t ABLK = KT * 64;          // one U3 digit: 128 rows x 64 B (SWIZZLE_64B)
@@ -41,7 +41,8 @@ constexpr uint32_t STAGE = FBYTES + WIMG;
 constexpr int NEPI = 8;                     // epilogue warps: 2 per TMEM lane quarter, 16 fibre columns each
 constexpr int UG = 1024;                     // chunks per unit block (the block's W digits stay in L2 across its k-tiles)
 constexpr int NT = 32 * (2 + NEPI);
-constexpr int TQ = 4, TQ_CONSUMERS = 1 + NEPI;
+constexpr int TQ = 8, TQ_CONSUMERS = 1 + NEPI;
+constexpr int LA = 6;                        // units posted (and their F boxes prefetched to L2) ahead of the loads
 constexpr uint64_t BIAS = 0x808080808080ull;
 constexpr int MAX_R = 40;
 constexpr size_t smem_bytes() { return (size_t)AIMG + (size_t)NS * STAGE + 1024; }
@@ -183,18 +184,34 @@ __global__ void __launch_bounds__(NT, 1) k_err_i8(const __grid_constant__ CUtens
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // loader: unit schedule, A image, F box + W digits per unit
-            int cur_kt = -1;
+        if (lane == 0) {  // loader: unit schedule (posted LA units ahead, their F boxes prefetched to
+                          // L2), A image, F box + W digits per unit
+            int cur_kt = -1, posted = 0;
+            bool done = false;
+            long long ahead[TQ];
             for (int it = 0;; ++it) {
-                const int slot = it % TQ;
-                mbar_wait(&tq_empty[slot], ((uint32_t)(it / TQ) & 1u) ^ 1u);
-                long long u = atomicAdd(g.sched, 1);
-                int kt = 0, fc = 0;
-                if (u >= g.nunits) u = -1;
-                else unit_of((int)u, g.nkt, g.nfc, kt, fc);
-                tq[slot] = u < 0 ? -1 : (u << 40) | ((long long)kt << 24) | fc;  // unit, k-tile, chunk
-                mbar_arrive(&tq_full[slot]);
-                if (u < 0) break;
+                while (!done && posted <= it + LA) {
+                    const int slot = posted % TQ;
+                    mbar_wait(&tq_empty[slot], ((uint32_t)(posted / TQ) & 1u) ^ 1u);
+                    long long u = atomicAdd(g.sched, 1);
+                    int kt = 0, fc = 0;
+                    if (u >= g.nunits) u = -1;
+                    else unit_of((int)u, g.nkt, g.nfc, kt, fc);
+                    const long long pk = u < 0 ? -1 : (u << 40) | ((long long)kt << 24) | fc;  // unit, k-tile, chunk
+                    tq[slot] = pk;
+                    mbar_arrive(&tq_full[slot]);
+                    ahead[slot] = pk;
+                    ++posted;
+                    if (u < 0) done = true;
+                    else
+                        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                         reinterpret_cast<uint64_t>(&mapF)),
+                                     "r"(kt * KT), "r"(fc * FC)
+                                     : "memory");
+                }
+                const long long pk = ahead[it % TQ];
+                if (pk < 0) break;
+                const int kt = (int)((pk >> 24) & 0xFFFF), fc = (int)(pk & 0xFFFFFF);
                 if (kt != cur_kt) {  // every MMA on the old A image done (unit it-1's stage released)
                     if (it > 0) mbar_wait(&sempty[(it - 1) % NS], (uint32_t)((it - 1) / NS) & 1u);
                     mbar_arrive_expect_tx(&afull, AIMG);
