@@ -195,3 +195,28 @@ def test_multigrid_and_hosvd_validation(lib):
     rc = lib.tucker_hosvd(ctypes.byref(g2), T.cranks((57, 8, 8)), d, d, d, d, d, d, d, d, d, 1 << 40, None, None)
     assert rc == 7
     assert lib.tucker_last_launch_count() == 0
+
+
+def test_ttm_engine_switch_host_only(lib):
+    """tucker_set_ttm_engine: per-thread, AUTO / DMMA / INT8_ERROR accepted, anything else rejected
+    (host only, no device work)."""
+    from paper_1711_06874_b200 import tucker as T
+    assert T.get_ttm_engine() == T.TTM_AUTO
+    for e in (T.TTM_DMMA, T.TTM_INT8_ERROR, T.TTM_AUTO):
+        T.set_ttm_engine(e)
+        assert T.get_ttm_engine() == e
+    for bad in (-1, 3, 7):
+        with pytest.raises(Exception):
+            T.set_ttm_engine(bad)
+    assert T.get_ttm_engine() == T.TTM_AUTO
+
+
+def test_sass_uses_int8_tensor_cores_for_ttm():
+    """k_ttm1_i8 (R22) and k_err_i8 (R23) are tcgen05 kind::i8 kernels fed by TMA."""
+    import subprocess
+    from paper_1711_06874_b200 import build
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    for name in ("9k_ttm1_i8E", "8k_err_i8E"):  # (mangled: the kernels themselves, not k_err_i8_final)
+        i = next(k for k, part in enumerate(sass.split("Function : ")) if part.split("\n", 1)[0].find(name) >= 0)
+        body = sass.split("Function : ")[i]
+        assert "UTCIMMA" in body and "UTMALDG" in body, name
