@@ -247,7 +247,10 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
             void* reg = nullptr;
             size_t rb = 0;
             if (ttm_engine() != TUCKER_TTM_DMMA && gram_i8_ttm_scratch(g->n, at(ws, L.i8), &gm, &reg, &rb))
-                rc = launch_ttm12_i8(g->n, r, F, U[1], U[2], gm, T2, reg, rb, st);
+                // the mode-0 eigensolve runs beside it on side stream B: leave it its SMs (one CTA,
+                // or one thread-block cluster per iteration)
+                rc = launch_ttm12_i8(g->n, r, F, U[1], U[2], gm, T2, reg, rb, st,
+                                     g->n[0] <= 112 ? 1 : (eig_cluster_supported(g->n[0]) ? eig_cluster_size(g->n[0]) : 0));
             if (rc == TUCKER_ERR_UNSUPPORTED)
                 rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,
                                           nullptr, T2);

@@ -110,7 +110,8 @@ int& ttm_engine();
 bool ttm_i8_applies(const int64_t n[3], const int32_t r[3], const double* F);
 size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
-                    const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st);
+                    const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st,
+                    int reserve_sms = 0);
 // The INT8 shared route's global exponent word and its residue region (free once the three Grams
 // are enqueued): false when the materialised Grams do not use the shared layout.
 // a-6 with the reconstruction W U3^T on the INT8 tensor cores (err_i8.cu, R23); UNSUPPORTED
@@ -166,6 +167,7 @@ int launch_eig(int64_t n, const double* G, int r, double* U, double* lambda, dou
 
 // Cluster Rayleigh–Ritz step (eig_cluster.cu); n <= 2048.
 bool eig_cluster_supported(int64_t n);
+int eig_cluster_size(int64_t n);
 // G (nullable): W = G V formed inside the cluster kernel (Wt unused) — one launch per iteration.
 int launch_rr_cluster(int64_t n, int p, int r, int it, int last, int orth_only, double* Vt, const double* Wt,
                       double* U, double* lambda, double* sigma, void* state, cudaStream_t st,

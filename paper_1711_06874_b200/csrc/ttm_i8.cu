@@ -440,7 +440,8 @@ size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]) {
 // gmax: the INT8 route's global exponent word (device); region: device scratch of
 // ttm_i8_region_bytes.  UNSUPPORTED when the shape does not apply (the caller uses the DMMA TTM).
 int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
-                    const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st) {
+                    const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st,
+                    int reserve_sms) {
     using namespace t8;
     if (!ttm_i8_applies(n, r, F)) return TUCKER_ERR_UNSUPPORTED;
     if (region_bytes < ttm_i8_region_bytes(n, r)) return TUCKER_ERR_UNSUPPORTED;
@@ -473,7 +474,9 @@ int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, con
     if (!make_tmap_f64(&map, F, 2, dims, strides, box)) return ::tk::report_cuda(cudaErrorInvalidValue, __FILE__, __LINE__);
     const size_t sm = smem_bytes(NB);
     TK_CUDA(cudaFuncSetAttribute(k_ttm1_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int grid = (int)std::min<int64_t>(a.ntiles, kNumSMs);
+    // one CTA per SM; `reserve_sms` SMs are left to a concurrent kernel (the mode-0 eigensolve's cluster,
+    // which would otherwise wait for the whole persistent grid): the dynamic schedule absorbs it
+    const int grid = (int)std::min<int64_t>(a.ntiles, std::max(kNumSMs - reserve_sms, kNumSMs / 2));
     k_ttm1_i8<<<grid, NT, sm, st>>>(map, a);
     TK_CHECK_LAUNCH();
     // TTM2 as one GEMM over the transposed T1, K = n2 split into S slices (a batch):
