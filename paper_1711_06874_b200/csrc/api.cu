@@ -705,7 +705,11 @@ int tucker_hosvd_fused(const tucker_grid* grid, const tucker_kernel* kernel, con
         }
     }
     const FusedGen gen = fused_gen(grid, kp, L, ws);
-    TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st));
+    TtmI8 ti{nullptr, nullptr, 0};
+    const bool i8t = L.i8_bytes && ttm_engine() != TUCKER_TTM_DMMA &&
+                     gram_i8_fused_ttm_scratch(grid->n, at(ws, L.i8), &ti.gmax, &ti.region, &ti.bytes);
+    TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st, nullptr, nullptr,
+                               nullptr, i8t ? &ti : nullptr));
     return worst;
 }
 
@@ -749,8 +753,11 @@ int tucker_hosvd_fused_sharded(const tucker_grid* grid, const tucker_kernel* ker
     const I8Gen ig{kp, reinterpret_cast<const double*>(at(ws, L.cheb)), reinterpret_cast<const double*>(at(ws, L.nodes))};
     TK_RC(launch_gram_i8_fused_modes(grid->n, ig, G, at(ws, L.i8), L.i8_bytes, st, 0, 2, eig_mode, &sh));
     const FusedGen gen = fused_gen(grid, kp, L, ws);
+    TtmI8 ti{nullptr, nullptr, 0};  // the same INT8 TTM as tucker_hosvd_fused (bitwise the same T2 rows)
+    const bool i8t = L.i8_bytes && ttm_engine() != TUCKER_TTM_DMMA &&
+                     gram_i8_fused_ttm_scratch(grid->n, at(ws, L.i8), &ti.gmax, &ti.region, &ti.bytes);
     TK_RC(launch_ttm_core_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, scr, L.scratch_bytes, st, nullptr, nullptr,
-                               &sh));
+                               &sh, i8t ? &ti : nullptr));
     if (err3)
         TK_RC(launch_error_impl(grid->n, r, nullptr, &gen, U1, U2, U3, core, err3, scr, L.scratch_bytes, st, &sh));
     return worst;

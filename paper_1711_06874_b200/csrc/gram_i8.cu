@@ -2026,6 +2026,15 @@ bool gram_i8_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, vo
     *bytes = sp.off_P - sp.off_R;
     return true;
 }
+bool gram_i8_fused_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes) {
+    if (!i8::fused_shared_ok(n)) return false;
+    const i8::FusedSharedPlan fp = i8::fused_shared_plan(n);
+    char* base = static_cast<char*>(ws);
+    *gmax = reinterpret_cast<const uint32_t*>(base + fp.off_gmax);
+    *region = base + fp.off_R;  // the residue super-chunks: free once the Grams are enqueued
+    *bytes = fp.off_P - fp.off_R;
+    return true;
+}
 uint32_t* gram_i8_rowmax_slot(const int64_t n[3], void* ws) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + i8::ws_plan(n).off_mx);
 }

@@ -111,7 +111,15 @@ bool ttm_i8_applies(const int64_t n[3], const int32_t r[3], const double* F);
 size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]);
 int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
                     const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st,
-                    int reserve_sms = 0);
+                    int reserve_sms = 0, bool profile = true);
+// INT8 TTM context for the fused route's slab chunks (launch_ttm_core_impl): the route's global
+// exponent word and a free device region.
+struct TtmI8 {
+    const uint32_t* gmax;
+    void* region;
+    size_t bytes;
+};
+bool gram_i8_fused_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes);
 // The INT8 shared route's global exponent word and its residue region (free once the three Grams
 // are enqueued): false when the materialised Grams do not use the shared layout.
 // a-6 with the reconstruction W U3^T on the INT8 tensor cores (err_i8.cu, R23); UNSUPPORTED
@@ -208,7 +216,7 @@ struct FusedGen {
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
                          size_t ws_bytes, cudaStream_t st, double* t1_out = nullptr, double* t2_out = nullptr,
-                         const Shard* shard = nullptr);
+                         const Shard* shard = nullptr, const TtmI8* i8 = nullptr);
 // Tucker-ALS (f1): T1 = F x3 U3^T ((n1 n2) x r3) and Y1 = T1 x2 U2^T (n1 x r2 x r3), both stored.
 int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
                      double* T1, double* Y1, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -36,6 +36,7 @@ cudaEvent_t take(State& s) {
 }  // namespace
 
 ProfScope::ProfScope(int tag, cudaStream_t st) : tag_(tag), st_(st), a_(nullptr) {
+    if (tag < 0) return;  // (a nested scope that must not count twice)
     State& s = state();
     std::lock_guard<std::mutex> g(s.mu);
     if (!s.on) return;

@@ -426,7 +426,8 @@ int launch_ttm_t1_y1(const int64_t n[3], const int32_t r[3], const double* F, co
 // Core with F either materialised (F != nullptr) or generated slab-chunk by slab-chunk (gen).
 int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F, const FusedGen* gen,
                          const double* U1, const double* U2, const double* U3, double* core, void* ws,
-                         size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out, const Shard* shard) {
+                         size_t ws_bytes, cudaStream_t st, double* t1_out, double* t2_out, const Shard* shard,
+                         const TtmI8* i8) {
     const bool sharded = gen && shard && shard->sharded();
     TK_PROF(TUCKER_PROF_TTM, st);
     const size_t chunk_b = gen ? align_up((size_t)gen->Pc * n[1] * n[2] * 8, 256) : 0;
@@ -447,9 +448,26 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
                       st>>>(U3, n[2], r[2], RP, Bp);
     TK_CHECK_LAUNCH();
     ttm1::Args12 a{F, Bp, U2, JT > 1 ? part : T2, n[1], n[2], r[2], r[1], (int)JT, 0, t1_out};
+    // fused route: TTM1 of every generated slab chunk on the INT8 tensor cores (R22) when the caller
+    // passes the route's exponent and a region large enough for the biggest chunk (T2 rows direct)
+    int64_t nci[3] = {gen ? gen->Pc : 0, n[1], n[2]};
+    const bool use_i8 = gen && i8 && !t1_out && ttm_i8_applies(nci, r, chunk) &&
+                        i8->bytes >= ttm_i8_region_bytes(nci, r);
     if (sharded)  // rows of the other ranks' slabs stay zero (the all-reduce adds zeros)
-        TK_CUDA(cudaMemsetAsync(JT > 1 ? part : T2, 0, JT > 1 ? JT * t2b : t2b, st));
-    if (!gen) {
+        TK_CUDA(cudaMemsetAsync(JT > 1 && !use_i8 ? part : T2, 0, JT > 1 && !use_i8 ? JT * t2b : t2b, st));
+    if (use_i8) {
+        for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
+            if (sharded && !shard->owns(g0 / gen->Pc)) continue;
+            const int64_t pc = std::min<int64_t>(gen->Pc, n[0] - g0);
+            ChunkGeo geo = gen->geo;
+            geo.g0 = g0;
+            geo.Pc = pc;
+            TK_RC(launch_gen_chunk(geo, gen->kp, gen->cheb, gen->x2, chunk, st));
+            const int64_t nc[3] = {pc, n[1], n[2]};
+            TK_RC(launch_ttm12_i8(nc, r, chunk, U2, U3, i8->gmax, T2 + g0 * r[1] * r[2], i8->region, i8->bytes, st, 0,
+                                  false));
+        }
+    } else if (!gen) {
         TK_RC(launch_ttm12(a, n[0], st));
     } else {
         for (int64_t g0 = 0; g0 < n[0]; g0 += gen->Pc) {
@@ -464,7 +482,7 @@ int launch_ttm_core_impl(const int64_t n[3], const int32_t r[3], const double* F
             TK_RC(launch_ttm12(a, pc, st));
         }
     }
-    if (JT > 1) {
+    if (JT > 1 && !use_i8) {
         const int64_t nout = (int64_t)r[1] * r[2], total = n[0] * nout;
         k_t2_reduce<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(part, (int)JT, nout, total,
                                                                                               T2);

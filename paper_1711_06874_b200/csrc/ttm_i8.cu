@@ -441,11 +441,11 @@ size_t ttm_i8_region_bytes(const int64_t n[3], const int32_t r[3]) {
 // ttm_i8_region_bytes.  UNSUPPORTED when the shape does not apply (the caller uses the DMMA TTM).
 int launch_ttm12_i8(const int64_t n[3], const int32_t r[3], const double* F, const double* U2, const double* U3,
                     const uint32_t* gmax, double* T2, void* region, size_t region_bytes, cudaStream_t st,
-                    int reserve_sms) {
+                    int reserve_sms, bool profile) {
     using namespace t8;
     if (!ttm_i8_applies(n, r, F)) return TUCKER_ERR_UNSUPPORTED;
     if (region_bytes < ttm_i8_region_bytes(n, r)) return TUCKER_ERR_UNSUPPORTED;
-    TK_PROF(TUCKER_PROF_TTM, st);
+    ProfScope prof(profile ? TUCKER_PROF_TTM : -1, st);
     const int R = r[2], NB = ((R + 7) / 8) * 8;
     const int64_t M = n[0] * n[1];
     const int64_t nkb = ceil_div(n[2], (int64_t)BK);
