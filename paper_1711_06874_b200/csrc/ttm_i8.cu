@@ -16,20 +16,23 @@
 // So T1 carries the input rounding 2^-47 max|F| (and 2^-47 max|U3[:, c]|) plus ~2^-52 per term —
 // at the level of the FP64 DMMA product's own accumulation error (n3 2^-53).  DESIGN.md R22.
 //
-// k_ttm1_i8: persistent, one CTA per SM, 128-fibre tiles (M = 128 TMEM lanes), warp-specialised:
-//   warp 0      TMEM owner + MMA issuer (one thread): per K-step (32 k) eight MMAs
-//               (M = 128, N = NB x digit count, K = 32) covering the 26 pairs, TMEM group d at
-//               columns [d NB, d NB + NB);
-//   warp 1      F loader: two TMA boxes (16 k x 128 fibres, SWIZZLE_128B, zero fill past the
-//               edges) per K-step into a 5-stage ring (160 KB per SM), each stage converted in
-//               place into its K-step's digit tiles and freed by the MMAs' commit;
+// k_ttm1_i8: persistent, one CTA per SM (minus the SMs a concurrent eigensolve needs), 128-fibre
+// tiles (M = 128 TMEM lanes) taken dynamically from a global counter, warp-specialised:
+//   warp 0      TMEM owner + MMA issuer (one thread): per K-step (32 k) one MMA per F digit s
+//               (M = 128, N = NB x the U3 digits t paired with it, rounded up to 16; K = 32) into
+//               TMEM columns NB s ..: pair (s, t) accumulates in group s + t; the epilogue zeroes
+//               the accumulator before each tile;
+//   warp 1      F loader and tile schedule: two TMA boxes (16 k x 128 fibres, SWIZZLE_128B, zero
+//               fill past the edges) per K-step into a 5-stage ring (160 KB per SM), each stage
+//               converted in place into its K-step's digit tiles and freed by the MMAs' commit;
 //   warps 2-5   epilogue: tcgen05.ld of the 7 groups, Horner in FP64, T1 rows to HBM;
 //   warp 6      B loader: the U3 digit image of each 128-k block (6 NB rows x 128 B, pre-swizzled
 //               SWIZZLE_128B) by one cp.async.bulk into a 2-stage ring;
-//   warps 7-22  converters (each K-step over all 16 warps, 8 k of one fibre row per thread): a fibre row's 16 doubles from the F stage (conflict-free through the
-//               swizzle), one DFMA + byte permutes per element, digit words stored over the same
-//               stage in the SWIZZLE_128B K-major A layout (two 128 x 128 B tiles per K-step:
-//               digits 0-3 and 4-5 as the four 32-byte K chunks of a row).
+//   warps 7-22  converters: every K-step over all 16 warps (8 k of one fibre row per thread — every
+//               warp takes every stage in order, so its parity waits are exact), F from the stage
+//               through the swizzle (conflict-free), one DFMA + byte permutes per element, the
+//               digit words stored over the rows just read in the SWIZZLE_128B K-major A layout
+//               (two 128 x 128 B tiles per K-step: digits 0-3 and 4-5 as the 32-byte K chunks).
 // T1 is written transposed (T1t[j][i][c], n2 x n1 r3) so that TTM2 is ONE DMMA GEMM
 // U2^T (r2 x n2) T1t; TTM3 follows on T2 (0.3 % of the flops together).
 #include "common.cuh"
