@@ -223,9 +223,8 @@ TUCKER_API int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel*
  * it; nothing of F is re-read for the Grams): the row-maxima and residue passes are skipped, the
  * results are those tucker_hosvd computes on the shared layout.  A value outside the scheme's window
  * still trips the flag (TUCKER_ERR_INPUT with info, NaN without).  Same outputs and errors as
- * tucker_hosvd, plus UNSUPPORTED where tucker_fill_prepare is.  The call consumes the prepared
- * residue planes (the INT8 TTM of the core, TUCKER_TTM_AUTO, reuses their memory once the three
- * Grams are enqueued): every call needs its own tucker_fill_prepare (TUCKER_TTM_DMMA keeps them). */
+ * tucker_hosvd, plus UNSUPPORTED where tucker_fill_prepare is.  The prepared residue planes are
+ * only read: the workspace can serve further calls on the same F. */
 TUCKER_API int tucker_hosvd_prepared(const tucker_grid* grid, const int32_t r[3], const double* F, double* U1,
                           double* U2, double* U3, double* core, double* sigma1, double* sigma2, double* sigma3,
                           void* ws, size_t ws_bytes, void* stream, tucker_info* info);

@@ -141,6 +141,7 @@ Layout plan(const tucker_grid* g, const int32_t* rin) {
         for (int a = 0; a < 3; ++a) s = std::max(s, eig_ws_bytes(n[a], r[a]));
     s = std::max(s, ttm_ws_bytes(n, r));
     s = std::max(s, std::max(err_ws_bytes(n, r), err_i8_ws_bytes(n, r)));
+    s = std::max(s, ttm_i8_region_bytes(n, r));  // the INT8 TTM's T1 / digit image / TTM2 partials
     L.scratch_bytes = align_up(s, 256);
     off += L.scratch_bytes;
     L.outs = off;
@@ -246,10 +247,12 @@ int hosvd_impl(const tucker_grid* g, const int32_t* r, const double* F, double* 
             const uint32_t* gm = nullptr;
             void* reg = nullptr;
             size_t rb = 0;
+            // (its scratch is the general one, free here: the residue planes stay intact, so a prepared
+            // workspace can serve another tucker_hosvd_prepared call)
             if (ttm_engine() != TUCKER_TTM_DMMA && gram_i8_ttm_scratch(g->n, at(ws, L.i8), &gm, &reg, &rb))
                 // the mode-0 eigensolve runs beside it on side stream B: leave it its SMs (one CTA,
                 // or one thread-block cluster per iteration)
-                rc = launch_ttm12_i8(g->n, r, F, U[1], U[2], gm, T2, reg, rb, st,
+                rc = launch_ttm12_i8(g->n, r, F, U[1], U[2], gm, T2, scr, L.scratch_bytes, st,
                                      g->n[0] <= 112 ? 1 : (eig_cluster_supported(g->n[0]) ? eig_cluster_size(g->n[0]) : 0));
             if (rc == TUCKER_ERR_UNSUPPORTED)
                 rc = launch_ttm_core_impl(g->n, r, F, nullptr, nullptr, U[1], U[2], nullptr, scr, L.scratch_bytes, st,

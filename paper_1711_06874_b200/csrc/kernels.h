@@ -120,8 +120,8 @@ struct TtmI8 {
     size_t bytes;
 };
 bool gram_i8_fused_ttm_scratch(const int64_t n[3], void* ws, const uint32_t** gmax, void** region, size_t* bytes);
-// The INT8 shared route's global exponent word and its residue region (free once the three Grams
-// are enqueued): false when the materialised Grams do not use the shared layout.
+// The INT8 shared route's global exponent word (and its residue region): false when the
+// materialised Grams do not use the shared layout.
 // a-6 with the reconstruction W U3^T on the INT8 tensor cores (err_i8.cu, R23); UNSUPPORTED
 // when the shape does not apply or ws is too small (the caller then runs the DMMA error pass).
 bool err_i8_applies(const int64_t n[3], const int32_t r[3], const double* F);

@@ -102,3 +102,17 @@ def test_ttm_engine_flag(T):
     T.set_ttm_engine(T.TTM_AUTO)
     with pytest.raises(Exception):
         T.set_ttm_engine(7)
+
+
+def test_hosvd_prepared_twice_same_outputs(T):
+    """The INT8 TTM uses the general scratch, not the prepared residue planes: a second
+    tucker_hosvd_prepared call on the same prepared workspace gives bitwise the same results."""
+    g, k, r = GridSpec.cube(128, 1.0), MATERN32, (12, 12, 12)
+    ws = T.workspace(g, r)
+    F, ws = T.fill_prepare(g, k, r, ws=ws)
+    a = T.hosvd_prepared(g, r, F, ws)
+    b = T.hosvd_prepared(g, r, F, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(a.core), to_np(b.core))
+    for m in range(3):
+        assert np.array_equal(to_np(a.U[m]), to_np(b.U[m]))
