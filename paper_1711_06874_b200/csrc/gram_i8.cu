@@ -1487,7 +1487,7 @@ __global__ void __launch_bounds__(256) k_i8_gmax_eval(KParams kp, const double* 
 // Item = (i < h1, j < h2, 8-block t < n3/16): 8 consecutive k per thread -> one 64-byte run of F
 // and one 8-byte word per residue plane at each of the 8 mirrored positions (byte-reversed on the
 // k-mirror side).
-__global__ void __launch_bounds__(256) k_fill_octant_res(KParams kp, const double* __restrict__ cheb_g,
+__global__ void __launch_bounds__(256, 3) k_fill_octant_res(KParams kp, const double* __restrict__ cheb_g,
                                                          const double* __restrict__ x2, int64_t n1, int64_t n2,
                                                          int64_t n3, double* __restrict__ F, int8_t* __restrict__ R,
                                                          const uint32_t* __restrict__ gmax, int b,
