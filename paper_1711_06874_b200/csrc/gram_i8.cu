@@ -1023,11 +1023,12 @@ __device__ __forceinline__ double crt_value(const int32_t* __restrict__ Racc, in
     return u128_to_double_rn(neg ? (Pp - S) : S);
 }
 
-// nmod (device, nullptr: NMOD): the number of moduli the Grams were formed with (NMOD or NMOD - 1).
+// nmod (device, nullptr: NMOD): the number of moduli the Grams were formed with (NMOD - 2 .. NMOD);
+// bdev (device, nullptr: b): the integer width the residues were formed with.
 __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc, const uint32_t* __restrict__ mx,
                                                 int n, int nJ, int ntiles, int b, double* __restrict__ G,
                                                 const int* __restrict__ bad, int global_mx,
-                                                const int* __restrict__ nmod) {
+                                                const int* __restrict__ nmod, const int* __restrict__ bdev) {
     // block: 32 rows (i) x 8 columns (j) of the lower triangle; blockIdx.x -> i-block, y -> j-block
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -1040,7 +1041,10 @@ __global__ void __launch_bounds__(256) k_i8_crt(const int32_t* __restrict__ Racc
     const int64_t per = (int64_t)ntiles * PN * PM;
     const int64_t e = (int64_t)t * PN * PM + (int64_t)(j - J * PN) * PM + (i - I * PM);
     bool neg;
-    double d = (nmod && *nmod == NMOD - 1) ? crt_value<NMOD - 1>(Racc, per, e, neg) : crt_value<NMOD>(Racc, per, e, neg);
+    const int nm = nmod ? *nmod : NMOD;
+    double d = nm == NMOD - 2 ? crt_value<NMOD - 2>(Racc, per, e, neg)
+                              : (nm == NMOD - 1 ? crt_value<NMOD - 1>(Racc, per, e, neg) : crt_value<NMOD>(Racc, per, e, neg));
+    if (bdev) b = *bdev;
     // per-row exponents, or (shared layout) the one global exponent in mx[0]
     d = ldexp(d, row_exponent(mx[global_mx ? 0 : i]) + row_exponent(mx[global_mx ? 0 : j]) - 2 * b);
     if (neg) d = -d;
@@ -1202,7 +1206,7 @@ struct ModeGemm {
     int crt(double* G) {
         TK_PROF(TUCKER_PROF_I8_CRT, st);
         const dim3 cg((unsigned)ceil_div(p.rows, 32), (unsigned)ceil_div(p.rows, 8));
-        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad, 0, nullptr);
+        k_i8_crt<<<cg, 256, 0, st>>>(Racc, mxm, (int)p.rows, p.nJ, p.ntiles, p.b, G, bad, 0, nullptr, nullptr);
         TK_CHECK_LAUNCH();
         return TUCKER_OK;
     }
@@ -1496,11 +1500,12 @@ __global__ void __launch_bounds__(256, 3) k_fill_octant_res(KParams kp, const do
     if (kp.family == TUCKER_MATERN && kp.closed == 0)
         for (int t = threadIdx.x; t < kChebIntervals * kChebN; t += blockDim.x) cheb[t] = cheb_g[t];
     __syncthreads();
+    b = nmod[4];  // the width k_i8_nmod chose (b, or b - 1 / b - 2 with NMOD - 2 moduli)
     double sa, sbb;
     row_scale(*gmax, b, sa, sbb);
     const double lim = ldexp(1.0, b);
-    // residue planes a Gram reads: all NMOD unless every mode takes NMOD - 1 moduli (k_i8_nmod)
-    const int nplanes = (nmod[0] == NMOD - 1 && nmod[1] == NMOD - 1 && nmod[2] == NMOD - 1) ? NMOD - 1 : NMOD;
+    // residue planes a Gram reads: the most moduli any mode takes (k_i8_nmod)
+    const int nplanes = max(nmod[0], max(nmod[1], nmod[2]));
     const double* xa = x2;
     const double* xb = x2 + n1;
     const double* xc = x2 + n1 + n2;
@@ -1594,23 +1599,43 @@ __global__ void __launch_bounds__(256) k_i8_central_norms(KParams kp, const doub
 // partial sums (k_i8_central_norms) of a bound on max_i ||a_i||^2 of mode m (valid != 0), else
 // NMOD for every mode.  A NaN / Inf bound keeps NMOD.
 __global__ void k_i8_nmod(const double* __restrict__ rn, int64_t n1, int64_t n2, int64_t n3,
-                          const uint32_t* __restrict__ gmax, int b, int valid, int* __restrict__ nmod) {
+                          const uint32_t* __restrict__ gmax, int b, int valid, int* __restrict__ nmod, int nmin,
+                          int bfree, int* __restrict__ bout) {
     if (threadIdx.x != 0) return;
-    double P1 = 1.0;  // the product of the first NMOD - 1 moduli (rounded; the margins cover it)
-    for (int l = 0; l < NMOD - 1; ++l) P1 *= (double)kMod(l);
-    const double s = ldexp(1.0, b - row_exponent(*gmax));
+    // products of the first NMOD - 2 and NMOD - 1 moduli (rounded; the margins cover it)
+    double P2 = 1.0;
+    for (int l = 0; l < NMOD - 2; ++l) P2 *= (double)kMod(l);
+    const double P1 = P2 * (double)kMod(NMOD - 2);
     const int64_t nn[3] = {n1, n2, n3};
     const int64_t N = n1 * n2 * n3;
+    double A2[3];
     for (int a = 0; a < 3; ++a) {
-        double A2 = 0.0;
+        A2[a] = 0.0;
         if (valid) {
-            for (int z = 0; z < kNormBlocks; ++z) A2 += rn[a * kNormBlocks + z];
-            A2 *= 4.0;  // each octant entry stands for 4 entries of its row
+            for (int z = 0; z < kNormBlocks; ++z) A2[a] += rn[a * kNormBlocks + z];
+            A2[a] *= 4.0;  // each octant entry stands for 4 entries of its row
         }
-        const double nx = s * sqrt(A2 * (1.0 + 1e-9)) + 0.5 * sqrt((double)(N / nn[a]));
-        const bool fewer = valid && nx * nx * (1.0 + 1e-9) < 0.5 * P1 * (1.0 - 1e-9);  // false for NaN
-        nmod[a] = fewer ? NMOD - 1 : NMOD;
     }
+    // does mode a's exact Gram fit the product P with width bb (false for NaN)?
+    auto fits = [&](int a, int bb, double P) {
+        const double nx = ldexp(1.0, bb - row_exponent(*gmax)) * sqrt(A2[a] * (1.0 + 1e-9)) +
+                          0.5 * sqrt((double)(N / nn[a]));
+        return valid && nx * nx * (1.0 + 1e-9) < 0.5 * P * (1.0 - 1e-9);
+    };
+    // NMOD - 2 moduli for every mode at a width lowered by at most bfree bits: the input rounding
+    // would grow from 2^-(b+1) to at most 2^-(b-bfree+1) of the maximum (the routes pass bfree = 0:
+    // measured, it never reached the Target's modes and only broke the bitwise equality with the
+    // plain route elsewhere — DESIGN.md R21)
+    int bsel = b;
+    if (valid && nmin <= NMOD - 2 && !(fits(0, b, P2) && fits(1, b, P2) && fits(2, b, P2)))
+        for (int d = 1; d <= bfree; ++d)
+            if (fits(0, b - d, P2) && fits(1, b - d, P2) && fits(2, b - d, P2)) {
+                bsel = b - d;
+                break;
+            }
+    for (int a = 0; a < 3; ++a)
+        nmod[a] = (nmin <= NMOD - 2 && fits(a, bsel, P2)) ? NMOD - 2 : (fits(a, bsel, P1) ? NMOD - 1 : NMOD);
+    if (bout) *bout = bsel;
 }
 
 inline bool nmod_forced_full() {  // env TUCKER_I8_NMOD=16: always every modulus (test knob)
@@ -1623,9 +1648,10 @@ inline bool nmod_forced_full() {  // env TUCKER_I8_NMOD=16: always every modulus
 
 // k_i8_nmod on the plan's slots (valid: rn holds the three modes' row-norm bounds).
 int shared_nmod(const int64_t n[3], char* base, const SharedPlan& w, bool valid, cudaStream_t st) {
+    int* nm = reinterpret_cast<int*>(base + w.off_nmod);  // [0, 3): moduli per mode, [4]: the width b used
     k_i8_nmod<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(base + w.off_rn), n[0], n[1], n[2],
                                 reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
-                                (valid && !nmod_forced_full()) ? 1 : 0, reinterpret_cast<int*>(base + w.off_nmod));
+                                (valid && !nmod_forced_full()) ? 1 : 0, nm, NMOD - 2, 0, nm + 4);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
@@ -1688,12 +1714,12 @@ int shared_gemm(const int64_t c[3], int m, const int8_t* R, int8_t* P, int32_t* 
 
 // G_m (n_m x n_m, both triangles) from the folded residue sums, with the global exponent.
 int shared_crt(int64_t nm, const int32_t* Racc, const uint32_t* gmax, int b, const int* flag, double* G,
-               cudaStream_t st, const int* nmod = nullptr) {
+               cudaStream_t st, const int* nmod = nullptr, const int* bdev = nullptr) {
     TK_PROF(TUCKER_PROF_I8_CRT, st);
     int nJ;
     const int ntiles = count_tiles(nm, nJ);
     const dim3 cg((unsigned)ceil_div(nm, 32), (unsigned)ceil_div(nm, 8));
-    k_i8_crt<<<cg, 256, 0, st>>>(Racc, gmax, (int)nm, nJ, ntiles, b, G, flag, 1, nmod);
+    k_i8_crt<<<cg, 256, 0, st>>>(Racc, gmax, (int)nm, nJ, ntiles, b, G, flag, 1, nmod, bdev);
     TK_CHECK_LAUNCH();
     return TUCKER_OK;
 }
@@ -1706,7 +1732,8 @@ int shared_gram_mode(const int64_t n[3], int m, char* base, const SharedPlan& w,
     TK_RC(shared_gemm(n, m, reinterpret_cast<const int8_t*>(base + w.off_R), reinterpret_cast<int8_t*>(base + w.off_P),
                       Racc, reinterpret_cast<int2*>(base + w.off_utab), true, st, nmod));
     return shared_crt(n[m], Racc, reinterpret_cast<const uint32_t*>(base + w.off_gmax), w.b,
-                      reinterpret_cast<const int*>(base + w.off_flag), G, st, nmod);
+                      reinterpret_cast<const int*>(base + w.off_flag), G, st, nmod,
+                      reinterpret_cast<const int*>(base + w.off_nmod) + 4);
 }
 
 // ---- a-7 on the shared layout (F never stored): the residues of plane chunks generated straight
@@ -1855,7 +1882,7 @@ int launch_fused_shared(const int64_t n[3], const I8Gen& gen, double* G, char* b
         TK_CHECK_LAUNCH();
     }
     k_i8_nmod<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(base + w.off_rn), n[0], n[1], n[2], gw, w.b,
-                                cen ? 1 : 0, nmod);
+                                cen ? 1 : 0, nmod, NMOD - 1, 0, nullptr);
     TK_CHECK_LAUNCH();
     int8_t* R = reinterpret_cast<int8_t*>(base + w.off_R);
     int8_t* P = reinterpret_cast<int8_t*>(base + w.off_P);
