@@ -101,7 +101,7 @@ typedef struct {
     int32_t k_resolved[3]; /* #{k <= r_m : lambda_k >= 1e-12 lambda_1}: the resolved leading
                               eigenpairs (R14; past it the Gram route's noise)  */
     int32_t moduli[3];     /* INT8 Gram route: moduli the exact Gram of mode m was formed with
-                              (16, or 15 where the row-norm bound of DESIGN.md R21 allows it);
+                              (16, or 15 / 14 where the row-norm bound of DESIGN.md R21 allows it);
                               0 for the FP64 DMMA engine.  Set by tucker_hosvd,
                               tucker_hosvd_rowmax, tucker_hosvd_prepared (untouched elsewhere) */
 } tucker_info;
@@ -214,7 +214,8 @@ TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], 
  * and converts each to its residues once, storing value and residue bytes at the 8 mirrored
  * positions: the residue pass over F is gone.  Before the fill, the unfoldings' largest row norms
  * (the rows nearest the centre: C(r) is non-increasing in r) choose the moduli per mode (DESIGN.md
- * R21): 15 where (2^(b-E) max ||a_i|| + sqrt(K)/2)^2 < P_15 / 2 — the Gram is still exact — else
+ * R21): 14 where (2^(b-E) max ||a_i|| + sqrt(K)/2)^2 < P_14 / 2, else 15 where it is < P_15 / 2 — the
+ * Gram is still exact — else
  * 16; the 16th plane is not written when no mode reads it.  Follow it with tucker_hosvd_prepared
  * on the same F and ws. */
 TUCKER_API int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F,
