@@ -215,8 +215,7 @@ TUCKER_API int tucker_hosvd_rowmax(const tucker_grid* grid, const int32_t r[3], 
  * positions: the residue pass over F is gone.  Before the fill, the unfoldings' largest row norms
  * (the rows nearest the centre: C(r) is non-increasing in r) choose the moduli per mode (DESIGN.md
  * R21): 14 where (2^(b-E) max ||a_i|| + sqrt(K)/2)^2 < P_14 / 2, else 15 where it is < P_15 / 2 — the
- * Gram is still exact — else
- * 16; the 16th plane is not written when no mode reads it.  Follow it with tucker_hosvd_prepared
+ * Gram is still exact — else 16; planes no mode reads are not written.  Follow it with tucker_hosvd_prepared
  * on the same F and ws. */
 TUCKER_API int tucker_fill_prepare(const tucker_grid* grid, const tucker_kernel* kernel, const int32_t r[3], double* F,
                         void* ws, size_t ws_bytes, void* stream);
