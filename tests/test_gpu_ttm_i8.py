@@ -93,6 +93,9 @@ def test_ttm_i8_core_vs_oracle(T, orc, ci):
     assert np.all(np.abs(cdm - ref) <= bar), (ci, float(np.max(np.abs(cdm - ref) / bar)))
     # the bound is not vacuous: far below the core's scale
     assert np.max(bar) <= 1e-11 * np.max(np.abs(ref)), float(np.max(bar) / np.max(np.abs(ref)))
+    # and the INT8 path really ran (its rounding differs from the DMMA product's in the last bits)
+    if r[2] >= 8:
+        assert not np.array_equal(ci8, cdm)
 
 
 def test_ttm_engine_flag(T):
